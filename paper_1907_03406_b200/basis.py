@@ -1,0 +1,42 @@
+"""Polynomial basis Pi over vertex coordinates (reference `basis.py:15-62`).
+
+Columns [1, x, y, z (, x^2, y^2, z^2, xy, yz, zx)], replicated block
+diagonally per component under component-major unknown ordering, each
+column scaled to unit max-norm (zero columns left as they are).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+PI_COLS_SCALAR = {0: 1, 1: 4, 2: 10}
+
+
+@dataclass
+class PolyBasis:
+    Pi: np.ndarray
+    degree: int
+    pi_cols: int
+
+
+def build_polynomial_basis(coords, degree, components=1):
+    coords = np.asarray(coords, dtype=float)
+    if degree not in (0, 1, 2):
+        raise ValueError(f"degree must be 0, 1, or 2, got {degree}")
+    if components not in (1, 3):
+        raise ValueError(f"components must be 1 or 3, got {components}")
+    x, y, z = coords[:, 0], coords[:, 1], coords[:, 2]
+    mono = [np.ones(len(coords))]
+    if degree >= 1:
+        mono += [x, y, z]
+    if degree >= 2:
+        mono += [x * x, y * y, z * z, x * y, y * z, z * x]
+    S = np.column_stack(mono)
+    nv, ps = S.shape
+    Pi = np.zeros((components * nv, components * ps))
+    for c in range(components):
+        Pi[c * nv:(c + 1) * nv, c * ps:(c + 1) * ps] = S
+    scale = np.abs(Pi).max(axis=0)
+    scale[scale == 0] = 1.0
+    Pi = Pi / scale
+    return PolyBasis(Pi=Pi, degree=degree, pi_cols=Pi.shape[1])
