@@ -1,0 +1,145 @@
+/*
+ * sgf.h -- C ABI of the B200-native factorize -> apply -> PCG path of the
+ * polynomial-preserving hierarchical factorization (arXiv 1907.03406).
+ *
+ * Plain pointers and sizes only; no torch / CUDA C++ types cross the
+ * boundary (the stream is passed as an opaque pointer).  Every entry point
+ * returns an sgf_status; sgf_last_error() returns the message of the last
+ * failure on a context.  Status codes map one-to-one onto the reference's
+ * exception taxonomy (errors.py:4-50):
+ *   SGF_NOT_SPD       -> NotSPDError              (densela.py:106-110)
+ *   SGF_SHAPE         -> ShapeMismatchError       (factorization.py:235-239)
+ *   SGF_INDEFINITE    -> IndefiniteDetectedError  (krylov.py:62-63,71-72,90-91)
+ *   SGF_INVALID_ARG   -> ValueError               (factorization.py:427-440)
+ *   SGF_TRACE         -> RuntimeError (rank-trace divergence, factorization.py:497-509,543-549)
+ *   SGF_NON_SYMMETRIC -> NonSymmetricPatternError (blockmatrix.py:109-113)
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/polyprec/):
+ *   sgf_factorize          factorization.py:410-573  factorize(problem, scheme, degree, b,
+ *                                                    skip_levels, compression, mode, rank_tol,
+ *                                                    rank_trace)
+ *   sgf_apply              factorization.py:241-271  Preconditioner.apply_inverse /
+ *                                                    apply_half_inverse(_t) / apply_operator
+ *   sgf_pcg                krylov.py:34-102          pcg(matvec, b, precond, tol, maxit,
+ *                                                    true_residual_every)
+ *   sgf_precond_stats_json factorization.py:551-567  Preconditioner.stats
+ *   sgf_precond_rank_trace factorization.py:73-109   Preconditioner.rank_trace
+ *   sgf_precond_factor_*   factorization.py:112-213  factor attributes (.idx .L .Q .retained
+ *                                                    .node .couplings)
+ */
+#ifndef SGF_H
+#define SGF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SGF_OK = 0,
+  SGF_NOT_SPD = 1,
+  SGF_SHAPE = 2,
+  SGF_INDEFINITE = 3,
+  SGF_INVALID_ARG = 4,
+  SGF_TRACE = 5,
+  SGF_CUDA = 6,
+  SGF_OOM = 7,
+  SGF_NON_SYMMETRIC = 8
+} sgf_status;
+
+/* cell kinds (partition.py:17 KIND_NAMES, plus the general family) */
+enum { SGF_KIND_CELL0 = 0, SGF_KIND_CELL1 = 1, SGF_KIND_CELL2 = 2, SGF_KIND_CELL3 = 3, SGF_KIND_GENERAL = 4 };
+/* modes (factorization.py:33) */
+enum { SGF_MODE_POLYNOMIAL = 0, SGF_MODE_LOWRANK = 1, SGF_MODE_EXACT = 2 };
+/* apply operations (factorization.py:241-271) */
+enum { SGF_APPLY_INVERSE = 0, SGF_APPLY_HALF_INVERSE = 1, SGF_APPLY_HALF_INVERSE_T = 2, SGF_APPLY_OPERATOR = 3 };
+/* factor types (factorization.py:112-213) */
+enum { SGF_FACTOR_ELIMINATION = 0, SGF_FACTOR_COMPRESSION = 1, SGF_FACTOR_DENSE = 2 };
+
+typedef struct sgf_ctx sgf_ctx;
+typedef struct sgf_precond sgf_precond;
+typedef struct sgf_csr sgf_csr;
+
+typedef struct {
+  /* matrix: CSR pattern on the host, values on host or device */
+  int64_t n;
+  int64_t nnz;
+  const int64_t* indptr;    /* host, n+1 */
+  const int32_t* indices;   /* host, nnz */
+  const double* values;     /* nnz; device pointer when values_on_device != 0 */
+  int values_on_device;
+  /* polynomial basis Pi (host, n x pi_cols row-major), basis.py:38-62 */
+  int pi_cols;
+  const double* phi;
+  /* partition hierarchy (partition.py:179-217): nlevels levels */
+  int nlevels;
+  const int32_t* level_ncells;     /* [nlevels] */
+  const int8_t* cell_kind;         /* concatenated over levels, SGF_KIND_* */
+  const int8_t* cell_interior;     /* concatenated over levels, 1 = interior role */
+  const int64_t* father;           /* concatenated over levels 0..nlevels-2: child -> father */
+  const int64_t* l1_ptr;           /* [level_ncells[0]+1]: level-1 cell unknown lists */
+  const int64_t* l1_unknowns;      /* [n] component-major unknown ids per cell, ascending cell id */
+  /* options (factorization.py:410-412) */
+  int compress_kind_mask;          /* bit k: kind k is compressed (COMPRESS_KINDS :37-42) */
+  int raw_kind_mask;               /* bit k: couplings to kind k enter unfiltered (UNFILTERED_KINDS :47) */
+  int skip_levels;
+  int compression;
+  int mode;                        /* SGF_MODE_* */
+  double rank_tol;
+  /* low-rank replay: (level, node, rank) triples of a polynomial run */
+  int n_trace;
+  const int32_t* trace;
+  /* QR pivot replay (parity mode): one permutation per compression in
+     reference execution order; replay_ptr has n_replay+1 entries */
+  int n_replay;
+  const int64_t* replay_ptr;
+  const int32_t* replay_perm;
+} sgf_factor_args;
+
+typedef struct {
+  int iterations;
+  int converged;
+  double final_rel_residual;
+  double wall_time;          /* seconds, device-timed */
+  int history_len;
+} sgf_pcg_report;
+
+int sgf_create(sgf_ctx** ctx, int device);
+int sgf_destroy(sgf_ctx* ctx);
+const char* sgf_last_error(const sgf_ctx* ctx);
+/* the stream all work of the context runs on (cudaStream_t as void*) */
+void* sgf_stream(sgf_ctx* ctx);
+int sgf_sync(sgf_ctx* ctx);
+
+int sgf_factorize(sgf_ctx* ctx, const sgf_factor_args* args, sgf_precond** out);
+int sgf_precond_free(sgf_precond* p);
+int64_t sgf_precond_n(const sgf_precond* p);
+const char* sgf_precond_stats_json(const sgf_precond* p);
+int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap);  /* returns #entries */
+int sgf_precond_num_factors(const sgf_precond* p);
+/* info[0..7] = type, node, m (idx size), c (coupling rows), retained, level, reflectors, QR columns */
+int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info);
+/* what: 0 idx (int64 m), 1 L (m*m), 2 couplings E (c*m), 3 coupling idx (int64 c),
+         4 Q (m*m, compression), 5 inverse operator (m*m: L^-1, or Q^T L^-1), 6 QR perm (int64) */
+int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_out, int64_t cap_bytes);
+
+/* y = op(x); x,y device pointers when on_device != 0 else host.  Never
+   mutates x (factorization.py:235-239 copies). */
+int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device);
+
+int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                   const double* values, int on_device, sgf_csr** out);
+int sgf_csr_free(sgf_csr* a);
+int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device);
+
+/* PCG with the reference recurrence; precond may be NULL (identity).
+   history must hold maxit + 2 doubles. */
+int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x, double tol, int maxit,
+            int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,150 @@
+"""ctypes binding of the C ABI in include/sgf.h (libsgf.so, built in-tree).
+
+There is no CPU fallback: importing the package works without a GPU (so the
+host-side logic can be tested), but every compute entry point goes through
+`lib()` / `context()`, which raise `NativeUnavailable` when the shared
+library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsgf.so")
+
+SGF_OK, SGF_NOT_SPD, SGF_SHAPE, SGF_INDEFINITE, SGF_INVALID_ARG, SGF_TRACE, SGF_CUDA, SGF_OOM, SGF_NON_SYMMETRIC = range(9)
+MODE = {"polynomial": 0, "lowrank": 1, "exact": 2}
+APPLY_INVERSE, APPLY_HALF_INVERSE, APPLY_HALF_INVERSE_T, APPLY_OPERATOR = range(4)
+FACTOR_TYPES = {0: "EliminationFactor", 1: "CompressionFactor", 2: "DenseFactor"}
+
+# functions the header declares (checked by tests/test_native_abi.py)
+EXPORTS = (
+    "sgf_create", "sgf_destroy", "sgf_last_error", "sgf_stream", "sgf_sync", "sgf_factorize",
+    "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
+    "sgf_precond_num_factors", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
+    "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA implementation cannot run here (library or GPU missing)."""
+
+
+class FactorArgs(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("nnz", C.c_int64),
+        ("indptr", C.c_void_p), ("indices", C.c_void_p), ("values", C.c_void_p),
+        ("values_on_device", C.c_int),
+        ("pi_cols", C.c_int), ("phi", C.c_void_p),
+        ("nlevels", C.c_int), ("level_ncells", C.c_void_p), ("cell_kind", C.c_void_p),
+        ("cell_interior", C.c_void_p), ("father", C.c_void_p),
+        ("l1_ptr", C.c_void_p), ("l1_unknowns", C.c_void_p),
+        ("compress_kind_mask", C.c_int), ("raw_kind_mask", C.c_int), ("skip_levels", C.c_int),
+        ("compression", C.c_int), ("mode", C.c_int), ("rank_tol", C.c_double),
+        ("n_trace", C.c_int), ("trace", C.c_void_p),
+        ("n_replay", C.c_int), ("replay_ptr", C.c_void_p), ("replay_perm", C.c_void_p),
+    ]
+
+
+class PcgReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("final_rel_residual", C.c_double),
+                ("wall_time", C.c_double), ("history_len", C.c_int)]
+
+
+_lib = None
+_lock = threading.Lock()
+_ctx = {}
+
+
+def load_library(path=LIB_PATH):
+    """Load libsgf.so and declare signatures (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(path)
+        vp, i32, i64, d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+        sig = {
+            "sgf_create": (i32, [C.POINTER(vp), i32]),
+            "sgf_destroy": (i32, [vp]),
+            "sgf_last_error": (C.c_char_p, [vp]),
+            "sgf_stream": (vp, [vp]),
+            "sgf_sync": (i32, [vp]),
+            "sgf_factorize": (i32, [vp, C.POINTER(FactorArgs), C.POINTER(vp)]),
+            "sgf_precond_free": (i32, [vp]),
+            "sgf_precond_n": (i64, [vp]),
+            "sgf_precond_stats_json": (C.c_char_p, [vp]),
+            "sgf_precond_rank_trace": (i32, [vp, vp, i32]),
+            "sgf_precond_num_factors": (i32, [vp]),
+            "sgf_precond_factor_info": (i32, [vp, i32, vp]),
+            "sgf_precond_factor_copy": (i32, [vp, i32, i32, vp, i64]),
+            "sgf_apply": (i32, [vp, i32, vp, vp, i32]),
+            "sgf_csr_create": (i32, [vp, i64, i64, vp, vp, vp, i32, C.POINTER(vp)]),
+            "sgf_csr_free": (i32, [vp]),
+            "sgf_spmv": (i32, [vp, vp, vp, i32]),
+            "sgf_pcg": (i32, [vp, vp, vp, vp, vp, d, i32, i32, i32, C.POINTER(PcgReport), vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return L
+
+
+def lib():
+    return load_library()
+
+
+def raise_for(status, ctx=None, what=""):
+    if status == SGF_OK:
+        return
+    msg = lib().sgf_last_error(ctx).decode("utf-8", "replace") if ctx is not None else ""
+    if what:
+        msg = f"{what}: {msg}" if msg else what
+    cls = {
+        SGF_NOT_SPD: E.NotSPDError,
+        SGF_SHAPE: E.ShapeMismatchError,
+        SGF_INDEFINITE: E.IndefiniteDetectedError,
+        SGF_INVALID_ARG: ValueError,
+        SGF_TRACE: RuntimeError,
+        SGF_NON_SYMMETRIC: E.NonSymmetricPatternError,
+        SGF_OOM: MemoryError,
+    }.get(status, E.DeviceError)
+    raise cls(msg)
+
+
+def context(device=0):
+    """The per-device native context (created on first use)."""
+    with _lock:
+        if device in _ctx:
+            return _ctx[device]
+    L = lib()
+    h = C.c_void_p()
+    st = L.sgf_create(C.byref(h), int(device))
+    if st != SGF_OK:
+        msg = L.sgf_last_error(None).decode()
+        raise NativeUnavailable(f"cannot create a CUDA context on device {device}: {msg}")
+    with _lock:
+        _ctx[device] = h
+    return h
+
+
+def ptr(a):
+    """Data pointer of a contiguous numpy array or a torch tensor."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"], "array must be contiguous"
+        return a.ctypes.data
+    return a.data_ptr()

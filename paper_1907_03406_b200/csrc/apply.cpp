@@ -1,0 +1,354 @@
+// Level-batched preconditioner application and device PCG.
+//
+// apply_inverse = W^{-T} W^{-1} x (reference factorization.py:255-262).
+// Factors of one (level, kind) group touch disjoint node index sets and
+// commute inside the sweeps, so each group is one batched
+// phase: gathers of the group's unknowns, batched GEMVs over the stored
+// matrices, scatters back.  Elimination forward sweeps update shared
+// separator unknowns x_N -= E_N z_B; the plan's combine list applies those
+// in ascending factor order, exactly the reference's sequence.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+
+#include "precond.h"
+
+namespace sgf {
+
+namespace {
+constexpr int GN_ROWS = 64;   // rows per gemv_n CTA
+constexpr int GT_ROWS = 256;  // rows per gemv_t partial
+constexpr int GT_COLS = 256;  // columns per gemv_t CTA
+}  // namespace
+
+struct Group {
+  int type = 0;
+  long long nm = 0, nc = 0;  // sum of m, sum of c
+  int* idx = nullptr;
+  int* nidx = nullptr;
+  GemvTask* fwd1 = nullptr;
+  int nf1 = 0;
+  GemvTask* fwd2 = nullptr;
+  int nf2 = 0;
+  int* tgt = nullptr;
+  long long* tptr = nullptr;
+  long long* tpos = nullptr;
+  long long ntgt = 0;
+  GemvTask* bwd1 = nullptr;
+  int nb1 = 0;
+  RedSeg* red1 = nullptr;
+  int nred1 = 0, maxn1 = 0;
+  GemvTask* bwd2 = nullptr;
+  int nb2 = 0;
+  RedSeg* red2 = nullptr;
+  int nred2 = 0, maxn2 = 0;
+};
+
+struct ApplyPlan {
+  Arena mem;
+  std::vector<Group> groups;
+  double *xb = nullptr, *zb = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr, *acc = nullptr;
+  double* work = nullptr;  // n-vector (apply in place)
+  long long n = 0;
+  explicit ApplyPlan(cudaStream_t s) : mem(s, (size_t)64 << 20) {}
+};
+
+void destroy_plan(ApplyPlan* p) { delete p; }
+
+static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y, int rows,
+                       int cols, int tri) {
+  for (int r0 = 0; r0 < rows; r0 += GN_ROWS) {
+    GemvTask t;
+    t.A = A;
+    t.lda = lda;
+    t.x = x;
+    t.y = y;
+    t.r0 = r0;
+    t.r1 = std::min(rows, r0 + GN_ROWS);
+    t.c0 = 0;
+    t.c1 = cols;
+    t.tri = tri;
+    v.push_back(t);
+  }
+}
+
+// partials part[rb*cols + k] = sum_{i in rb} A[i,k] x[i]; returns #row blocks
+static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* part,
+                      int rows, int cols, int tri) {
+  int nrb = 0;
+  for (int r0 = 0; r0 < rows; r0 += GT_ROWS, ++nrb)
+    for (int c0 = 0; c0 < cols; c0 += GT_COLS) {
+      GemvTask t;
+      t.A = A;
+      t.lda = lda;
+      t.x = x;
+      t.y = part + (long long)nrb * cols;
+      t.r0 = r0;
+      t.r1 = std::min(rows, r0 + GT_ROWS);
+      t.c0 = c0;
+      t.c1 = std::min(cols, c0 + GT_COLS);
+      t.tri = tri;
+      v.push_back(t);
+    }
+  return nrb;
+}
+
+ApplyPlan* build_plan(Precond* P) {
+  cudaStream_t st = P->ctx->stream;
+  ApplyPlan* plan = new ApplyPlan(st);
+  plan->n = P->n;
+  // groups: consecutive factors of the same (level, type)
+  std::vector<std::pair<size_t, size_t>> ranges;
+  for (size_t i = 0; i < P->factors.size();) {
+    size_t j = i + 1;
+    while (j < P->factors.size() && P->factors[j].type == P->factors[i].type &&
+           P->factors[j].level == P->factors[i].level && P->factors[i].type != SGF_FACTOR_DENSE)
+      ++j;
+    ranges.push_back({i, j});
+    i = j;
+  }
+  long long max_m = 0, max_c = 0, max_part = 0;
+  for (auto& rg : ranges) {
+    long long sm = 0, sc = 0, sp = 0;
+    for (size_t i = rg.first; i < rg.second; ++i) {
+      const Factor& f = P->factors[i];
+      sm += f.m;
+      sc += f.c;
+      const long long rbE = (f.c + GT_ROWS - 1) / GT_ROWS, rbL = (f.m + GT_ROWS - 1) / GT_ROWS;
+      sp += std::max(rbE, rbL) * f.m;
+    }
+    max_m = std::max(max_m, sm);
+    max_c = std::max(max_c, sc);
+    max_part = std::max(max_part, sp);
+  }
+  plan->xb = plan->mem.alloc(std::max(max_m, 1LL));
+  plan->zb = plan->mem.alloc(std::max(max_m, 1LL));
+  plan->acc = plan->mem.alloc(std::max(max_m, 1LL));
+  plan->xn = plan->mem.alloc(std::max(max_c, 1LL));
+  plan->t = plan->mem.alloc(std::max(max_c, 1LL));
+  plan->part = plan->mem.alloc(std::max(max_part, 1LL));
+  plan->work = plan->mem.alloc(std::max<long long>(P->n, 1));
+
+  for (auto& rg : ranges) {
+    Group g;
+    g.type = P->factors[rg.first].type;
+    std::vector<int> idx, nidx;
+    std::vector<GemvTask> f1, f2, b1, b2;
+    std::vector<RedSeg> r1, r2;
+    long long om = 0, oc = 0, op = 0;
+    std::vector<std::pair<int64_t, long long>> contrib;  // (unknown, t position) in factor order
+    for (size_t i = rg.first; i < rg.second; ++i) {
+      const Factor& f = P->factors[i];
+      for (auto u : f.idx) idx.push_back((int)u);
+      const int tri = (g.type != SGF_FACTOR_COMPRESSION);
+      add_gemv_n(f1, f.inv, f.m, plan->xb + om, plan->zb + om, f.m, f.m, tri);
+      if (g.type == SGF_FACTOR_ELIMINATION) {
+        for (auto u : f.nidx) nidx.push_back((int)u);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.m, plan->zb + om, plan->t + oc, f.c, f.m, 0);
+        for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.m, plan->xn + oc, plan->part + op, f.c, f.m, 0) : 0;
+        r1.push_back(RedSeg{plan->part + op, plan->xb + om, plan->acc + om, f.m, nrb, f.m, -1.0});
+        // second stage reuses the partial buffer after red1 consumed it
+        int nrb2 = add_gemv_t(b2, f.inv, f.m, plan->acc + om, plan->part + op, f.m, f.m, 1);
+        r2.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb2, f.m, 1.0});
+        op += std::max<long long>(nrb, nrb2) * f.m;
+      } else {
+        int nrb = add_gemv_t(b1, f.inv, f.m, plan->xb + om, plan->part + op, f.m, f.m, tri);
+        r1.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb, f.m, 1.0});
+        op += (long long)nrb * f.m;
+      }
+      g.maxn1 = std::max(g.maxn1, f.m);
+      g.maxn2 = std::max(g.maxn2, f.m);
+      om += f.m;
+      oc += f.c;
+    }
+    g.nm = om;
+    g.nc = oc;
+    g.idx = plan->mem.upload(idx);
+    g.nidx = plan->mem.upload(nidx);
+    g.fwd1 = plan->mem.upload(f1);
+    g.nf1 = (int)f1.size();
+    g.fwd2 = plan->mem.upload(f2);
+    g.nf2 = (int)f2.size();
+    g.bwd1 = plan->mem.upload(b1);
+    g.nb1 = (int)b1.size();
+    g.bwd2 = plan->mem.upload(b2);
+    g.nb2 = (int)b2.size();
+    g.red1 = plan->mem.upload(r1);
+    g.nred1 = (int)r1.size();
+    g.red2 = plan->mem.upload(r2);
+    g.nred2 = (int)r2.size();
+    if (!contrib.empty()) {
+      std::stable_sort(contrib.begin(), contrib.end(),
+                       [](const std::pair<int64_t, long long>& x, const std::pair<int64_t, long long>& y) {
+                         return x.first < y.first;
+                       });
+      std::vector<int> tgt;
+      std::vector<long long> ptr, pos;
+      for (size_t i = 0; i < contrib.size(); ++i) {
+        if (i == 0 || contrib[i].first != contrib[i - 1].first) {
+          tgt.push_back((int)contrib[i].first);
+          ptr.push_back((long long)pos.size());
+        }
+        pos.push_back(contrib[i].second);
+      }
+      ptr.push_back((long long)pos.size());
+      g.ntgt = (long long)tgt.size();
+      g.tgt = plan->mem.upload(tgt);
+      g.tptr = plan->mem.upload(ptr);
+      g.tpos = plan->mem.upload(pos);
+    }
+    plan->groups.push_back(g);
+  }
+  return plan;
+}
+
+static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
+  SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
+  SGF_CUDA(launch_gemv(g.fwd1, g.nf1, 0, st));
+  if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_gemv(g.fwd2, g.nf2, 0, st));
+  SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
+  if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, pl->t, g.ntgt, st));
+}
+
+static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
+  SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
+  if (g.type == SGF_FACTOR_ELIMINATION) {
+    SGF_CUDA(launch_gather(y, g.nidx, pl->xn, g.nc, st));
+    SGF_CUDA(launch_gemv(g.bwd1, g.nb1, 1, st));
+    SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
+    SGF_CUDA(launch_gemv(g.bwd2, g.nb2, 1, st));
+    SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st));
+  } else {
+    SGF_CUDA(launch_gemv(g.bwd1, g.nb1, 1, st));
+    SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
+  }
+  SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
+}
+
+// y and x are device n-vectors; y may alias x
+void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
+  cudaStream_t st = P->ctx->stream;
+  ApplyPlan* pl = P->plan;
+  if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (op == SGF_APPLY_OPERATOR) fail(SGF_INVALID_ARG, "apply_operator is not available in this build");
+  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE)
+    for (auto& g : pl->groups) forward_group(pl, g, d_y, st);
+  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE_T)
+    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) backward_group(pl, *it, d_y, st);
+}
+
+// ---------------------------------------------------------------------------
+void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
+  SGF_CUDA(launch_spmv((int)A->n, A->rp, A->ci, A->v, d_x, d_y, d_b, A->tpr, A->ctx->stream));
+}
+
+// PCG with the reference recurrence (krylov.py:34-102): true-residual
+// replacement every `true_every` iterations, confirmation of a tentative
+// convergence with the true residual, history semantics identical.
+void pcg(Ctx& ctx, Csr* A, Precond* P, const double* d_b, double* d_x, double tol, int maxit, int true_every,
+         sgf_pcg_report* rep, double* history) {
+  cudaStream_t st = ctx.stream;
+  const long long n = A->n;
+  auto t0 = std::chrono::steady_clock::now();
+  Arena w(st, (size_t)8 * n * sizeof(double) + (1 << 20));
+  double* r = w.alloc(n);
+  double* z = w.alloc(n);
+  double* p = w.alloc(n);
+  double* q = w.alloc(n);
+  double* part = w.alloc(512);
+  double* sc = w.alloc(8);  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  double* hsc = nullptr;
+  SGF_CUDA(cudaMallocHost(&hsc, 8 * sizeof(double)));
+  struct HostFree {
+    double* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hsc};
+  auto readback = [&](int lo, int cnt) {
+    SGF_CUDA(cudaMemcpyAsync(hsc + lo, sc + lo, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+  };
+  auto precond = [&](const double* in, double* out) {
+    if (P) apply_op(P, SGF_APPLY_INVERSE, in, out);
+    else SGF_CUDA(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  };
+  int hl = 0;
+  SGF_CUDA(launch_dot(d_b, d_b, n, part, sc, 4, st));
+  readback(4, 1);
+  const double bnorm = std::sqrt(hsc[4]);
+  SGF_CUDA(cudaMemsetAsync(d_x, 0, n * sizeof(double), st));
+  if (bnorm == 0.0) {
+    history[hl++] = 0.0;
+    rep->iterations = 0;
+    rep->converged = 1;
+    rep->final_rel_residual = 0.0;
+    rep->history_len = hl;
+    SGF_CUDA(cudaStreamSynchronize(st));
+    rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return;
+  }
+  SGF_CUDA(cudaMemcpyAsync(r, d_b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  history[hl++] = 1.0;
+  precond(r, z);
+  SGF_CUDA(launch_dot(r, z, n, part, sc, 0, st));
+  readback(0, 1);
+  if (hsc[0] <= 0.0) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "initial r'Mr = %.3e is not positive", hsc[0]);
+    fail(SGF_INDEFINITE, buf);
+  }
+  SGF_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  bool converged = false;
+  int it = 0;
+  while (it < maxit) {
+    ++it;
+    spmv(A, p, q, nullptr);
+    SGF_CUDA(launch_dot(p, q, n, part, sc, 1, st));
+    SGF_CUDA(launch_xr_update(d_x, r, p, q, n, sc, part, sc, 3, st));
+    if (true_every > 0 && it % true_every == 0) {
+      spmv(A, d_x, r, d_b);
+      SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+    }
+    readback(1, 3);
+    if (hsc[1] <= 0.0) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "p'Ap = %.3e at iteration %d", hsc[1], it);
+      fail(SGF_INDEFINITE, buf);
+    }
+    double rel = std::sqrt(hsc[3]) / bnorm;
+    if (rel <= tol) {
+      spmv(A, d_x, r, d_b);
+      SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+      readback(3, 1);
+      rel = std::sqrt(hsc[3]) / bnorm;
+      history[hl++] = rel;
+      if (rel <= tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      history[hl++] = rel;
+    }
+    precond(r, z);
+    SGF_CUDA(launch_dot(r, z, n, part, sc, 2, st));
+    readback(2, 1);
+    if (hsc[2] <= 0.0) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "r'Mr = %.3e at iteration %d", hsc[2], it);
+      fail(SGF_INDEFINITE, buf);
+    }
+    SGF_CUDA(launch_p_update(p, z, n, sc, st));
+    SGF_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  spmv(A, d_x, r, d_b);
+  SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+  readback(3, 1);
+  const double fin = std::sqrt(hsc[3]) / bnorm;
+  rep->iterations = it;
+  rep->converged = (converged && fin <= tol) ? 1 : 0;
+  rep->final_rel_residual = fin;
+  rep->history_len = hl;
+  rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace sgf

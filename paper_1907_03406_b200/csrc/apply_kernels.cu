@@ -1,0 +1,253 @@
+// Preconditioner application and PCG vector kernels (HBM-bound paths).
+//
+// apply_inverse (reference factorization.py:255-262) runs, per factor group
+// (level, eliminations | compressions | final dense), batched GEMVs over the
+// stored factor matrices: row-major reads for y = A x, column-coalesced reads
+// with per-row-block partials for y = A^T x.  Every reduction has a fixed
+// order (partials are summed in row-block order, scatter-adds into shared
+// separator unknowns in ascending factor order), so results are bitwise
+// reproducible run to run.
+#include <cmath>
+
+#include "common.h"
+
+namespace sgf {
+
+// ---------------------------------------------------------------------------
+// y = A x for a row block (mode N).  One warp per row, lanes stride columns.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
+  const GemvTask T = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = T.r0 + warp; i < T.r1; i += 8) {
+    const double* a = T.A + (long long)i * T.lda;
+    const int ke = T.tri ? min(T.c1, i + 1) : T.c1;
+    double s0 = 0.0, s1 = 0.0;
+    int k = T.c0 + lane;
+    for (; k + 32 < ke; k += 64) {
+      s0 = fma(a[k], T.x[k], s0);
+      s1 = fma(a[k + 32], T.x[k + 32], s1);
+    }
+    if (k < ke) s0 = fma(a[k], T.x[k], s0);
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) T.y[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T) for 256 columns per CTA.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
+  const GemvTask T = tasks[blockIdx.x];
+  const int k = T.c0 + threadIdx.x;
+  if (k >= T.c1) return;
+  int i0 = T.r0;
+  if (T.tri) i0 = max(i0, k);
+  double s0 = 0.0, s1 = 0.0;
+  const double* a = T.A + k;
+  int i = i0;
+  for (; i + 1 < T.r1; i += 2) {
+    s0 = fma(a[(long long)i * T.lda], T.x[i], s0);
+    s1 = fma(a[(long long)(i + 1) * T.lda], T.x[i + 1], s1);
+  }
+  if (i < T.r1) s0 = fma(a[(long long)i * T.lda], T.x[i], s0);
+  T.y[k] = s0 + s1;
+}
+
+cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  if (mode == 0) gemv_n_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
+  else gemv_t_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// out[o] = sign_base*base[o] - sum_{q<nrb} part[poff + q*stride + k]  for the
+// flat segment layout described by RedSeg (one CTA-chunk per 256 entries).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const RedSeg* __restrict__ segs) {
+  const RedSeg R = segs[blockIdx.y];
+  const int k = blockIdx.x * 256 + threadIdx.x;
+  if (k >= R.n) return;
+  double s = 0.0;
+  for (int q = 0; q < R.nrb; ++q) s += R.part[(long long)q * R.stride + k];
+  const double b = R.base ? R.base[k] : 0.0;
+  R.out[k] = b + R.sign * s;
+}
+
+cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s) {
+  if (nseg <= 0 || max_n <= 0) return cudaSuccess;
+  dim3 grid((max_n + 255) / 256, nseg);
+  reduce_parts_kernel<<<grid, 256, 0, s>>>((const RedSeg*)d_segs);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// gathers / scatters over int32 index lists
+// ---------------------------------------------------------------------------
+__global__ void gather_kernel(const double* __restrict__ x, const int* __restrict__ idx, double* __restrict__ out,
+                              long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    out[e] = x[idx[e]];
+}
+__global__ void scatter_kernel(const double* __restrict__ v, const int* __restrict__ idx, double* __restrict__ x,
+                               long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    x[idx[e]] = v[e];
+}
+// x[tgt[u]] -= t[pos[j]] for j in [ptr[u], ptr[u+1]) in order (ascending factor)
+__global__ void combine_kernel(double* __restrict__ x, const int* __restrict__ tgt, const long long* __restrict__ ptr,
+                               const long long* __restrict__ pos, const double* __restrict__ t, long long nt) {
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < nt; u += (long long)gridDim.x * blockDim.x) {
+    double v = x[tgt[u]];
+    for (long long j = ptr[u]; j < ptr[u + 1]; ++j) v -= t[pos[j]];
+    x[tgt[u]] = v;
+  }
+}
+
+static inline unsigned grid_for(long long n) {
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  gather_kernel<<<grid_for(n), 256, 0, s>>>(x, idx, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  scatter_kernel<<<grid_for(n), 256, 0, s>>>(v, idx, x, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
+                           long long nt, cudaStream_t s) {
+  if (nt <= 0) return cudaSuccess;
+  combine_kernel<<<grid_for(nt), 256, 0, s>>>(x, tgt, ptr, pos, t, nt);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// PCG vector kernels (reference krylov.py:34-102).  Dots use a fixed grid and
+// a fixed-order final reduction: bitwise reproducible.
+// ---------------------------------------------------------------------------
+constexpr int RED_BLOCKS = 296;
+
+// CSR SpMV y = A x (mode 0) or y = b - A x (mode 1); `tpr` lanes per row.
+template <int TPR>
+__global__ void __launch_bounds__(256) spmv_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ ci,
+                                                   const double* __restrict__ v, const double* __restrict__ x,
+                                                   double* __restrict__ y, const double* __restrict__ b) {
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x % TPR;
+  const long long stride = (long long)gridDim.x * blockDim.x / TPR;
+  // warp-uniform trip count so the shuffles below always see full warps
+  const long long wbase = (gt - (threadIdx.x & 31)) / TPR;
+  for (long long rw = wbase, row = gt / TPR; rw < n; rw += stride, row += stride) {
+    double s = 0.0;
+    if (row < n)
+      for (long long e = rp[row] + sub; e < rp[row + 1]; e += TPR) s = fma(v[e], __ldg(x + ci[e]), s);
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
+    if (sub == 0 && row < n) y[row] = b ? b[row] - s : s;
+  }
+}
+
+cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double* v, const double* x, double* y,
+                        const double* b, int tpr, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long long threads = (long long)n * tpr;
+  long long blocks = (threads + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  switch (tpr) {
+    case 4: spmv_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    case 8: spmv_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    case 16: spmv_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    default: spmv_kernel<32><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+  }
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ void block_partial(double v, double* out) {
+  __shared__ double red[8];
+  v = wsum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    out[blockIdx.x] = s;
+  }
+}
+
+// partial dot products; op 0: a.b ; op 1: a.a
+__global__ void __launch_bounds__(256) dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                                                  double* __restrict__ part) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) s = fma(a[i], b[i], s);
+  block_partial(s, part);
+}
+
+// final reduction of RED_BLOCKS partials into out[slot]
+__global__ void finish_kernel(const double* __restrict__ part, double* __restrict__ out, int slot) {
+  __shared__ double red[RED_BLOCKS];
+  for (int i = threadIdx.x; i < RED_BLOCKS; i += blockDim.x) red[i] = part[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < RED_BLOCKS; ++i) s += red[i];
+    out[slot] = s;
+  }
+}
+
+// x += alpha p ; r -= alpha q ; partial ||r||^2  with alpha = sc[0]/sc[1]
+__global__ void __launch_bounds__(256) xr_update_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                        const double* __restrict__ p, const double* __restrict__ q,
+                                                        long long n, const double* __restrict__ sc,
+                                                        double* __restrict__ part) {
+  const double alpha = sc[0] / sc[1];
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  block_partial(s, part);
+}
+
+// p = z + beta p with beta = sc[2]/sc[0]
+__global__ void __launch_bounds__(256) p_update_kernel(double* __restrict__ p, const double* __restrict__ z, long long n,
+                                                       const double* __restrict__ sc) {
+  const double beta = sc[2] / sc[0];
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) p[i] = z[i] + beta * p[i];
+}
+
+cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
+                       cudaStream_t s) {
+  dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part);
+  finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+  return cudaGetLastError();
+}
+cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
+                             double* part, double* out, int slot, cudaStream_t s) {
+  xr_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(x, r, p, q, n, sc, part);
+  finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+  return cudaGetLastError();
+}
+cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s) {
+  p_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(p, z, n, sc);
+  return cudaGetLastError();
+}
+
+}  // namespace sgf

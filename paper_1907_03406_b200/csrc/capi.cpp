@@ -1,0 +1,296 @@
+// extern "C" boundary (include/sgf.h).  Every entry point converts internal
+// errors to an sgf_status and records the message on the context.
+#include <cstdio>
+
+#include "precond.h"
+
+using namespace sgf;
+
+struct sgf_ctx {
+  Ctx c;
+};
+struct sgf_precond {
+  Precond* p;
+  sgf_ctx* ctx;
+};
+struct sgf_csr {
+  Csr a;
+  sgf_ctx* ctx;
+};
+
+namespace {
+thread_local std::string g_orphan_error;
+
+template <class F>
+int guarded(sgf_ctx* ctx, F&& f) {
+  try {
+    f();
+    return SGF_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->c.last_error = e.msg;
+    else g_orphan_error = e.msg;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->c.last_error = "host out of memory";
+    return SGF_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.last_error = e.what();
+    return SGF_INVALID_ARG;
+  }
+}
+
+struct DevVec {
+  double* p = nullptr;
+  cudaStream_t s;
+  DevVec(size_t n, cudaStream_t st) : s(st) { SGF_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * 8, st)); }
+  ~DevVec() { cudaFreeAsync(p, s); }
+};
+}  // namespace
+
+extern "C" {
+
+int sgf_create(sgf_ctx** out, int device) {
+  if (!out) return SGF_INVALID_ARG;
+  *out = nullptr;
+  sgf_ctx* ctx = new sgf_ctx();
+  int st = guarded(ctx, [&] {
+    SGF_CUDA(cudaSetDevice(device));
+    ctx->c.device = device;
+    SGF_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    SGF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    SGF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  });
+  if (st != SGF_OK) {
+    g_orphan_error = ctx->c.last_error;
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return SGF_OK;
+}
+
+int sgf_destroy(sgf_ctx* ctx) {
+  if (!ctx) return SGF_OK;
+  if (ctx->c.stream) {
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStreamDestroy(ctx->c.stream);
+  }
+  delete ctx;
+  return SGF_OK;
+}
+
+const char* sgf_last_error(const sgf_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : g_orphan_error.c_str(); }
+
+void* sgf_stream(sgf_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+int sgf_sync(sgf_ctx* ctx) {
+  return guarded(ctx, [&] { SGF_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+int sgf_factorize(sgf_ctx* ctx, const sgf_factor_args* args, sgf_precond** out) {
+  if (!ctx || !args || !out) return SGF_INVALID_ARG;
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    SGF_CUDA(cudaSetDevice(ctx->c.device));
+    Precond* p = factorize(ctx->c, *args);
+    *out = new sgf_precond{p, ctx};
+  });
+}
+
+int sgf_precond_free(sgf_precond* p) {
+  if (!p) return SGF_OK;
+  cudaStreamSynchronize(p->ctx->c.stream);
+  delete p->p;
+  delete p;
+  return SGF_OK;
+}
+
+int64_t sgf_precond_n(const sgf_precond* p) { return p ? p->p->n : 0; }
+
+const char* sgf_precond_stats_json(const sgf_precond* p) { return p ? p->p->stats.c_str() : ""; }
+
+int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap) {
+  if (!p) return 0;
+  const int n = (int)p->p->trace.size() / 3;
+  if (out)
+    for (int i = 0; i < std::min(n * 3, cap * 3); ++i) out[i] = p->p->trace[i];
+  return n;
+}
+
+int sgf_precond_num_factors(const sgf_precond* p) { return p ? (int)p->p->factors.size() : 0; }
+
+int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info) {
+  if (!p || k < 0 || k >= (int)p->p->factors.size() || !info) return SGF_INVALID_ARG;
+  const Factor& f = p->p->factors[k];
+  info[0] = f.type;
+  info[1] = f.node;
+  info[2] = f.m;
+  info[3] = f.c;
+  info[4] = f.r;
+  info[5] = f.level;
+  info[6] = f.steps;
+  info[7] = f.ncols;
+  return SGF_OK;
+}
+
+int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_out, int64_t cap_bytes) {
+  if (!p || k < 0 || k >= (int)p->p->factors.size() || !host_out) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = p->ctx;
+  return guarded(ctx, [&] {
+    const Factor& f = p->p->factors[k];
+    cudaStream_t st = ctx->c.stream;
+    auto need = [&](int64_t bytes) {
+      if (bytes > cap_bytes) fail(SGF_SHAPE, "output buffer too small");
+    };
+    const long long mm = (long long)f.m * f.m;
+    switch (what) {
+      case 0:
+        need(8LL * f.m);
+        std::memcpy(host_out, f.idx.data(), 8LL * f.m);
+        break;
+      case 1:
+        need(8 * mm);
+        SGF_CUDA(cudaMemcpyAsync(host_out, f.L, 8 * mm, cudaMemcpyDeviceToHost, st));
+        break;
+      case 2:
+        need(8LL * f.c * f.m);
+        if (f.c) SGF_CUDA(cudaMemcpyAsync(host_out, f.E, 8LL * f.c * f.m, cudaMemcpyDeviceToHost, st));
+        break;
+      case 3:
+        need(8LL * f.c);
+        if (f.c) std::memcpy(host_out, f.nidx.data(), 8LL * f.c);
+        break;
+      case 4: {
+        // Q = I - V T V^T (m x m), formed on the host from the reflectors
+        need(8 * mm);
+        const int m = f.m, s = f.steps;
+        std::vector<double> V((size_t)m * s), T((size_t)s * s);
+        if (s) {
+          SGF_CUDA(cudaMemcpyAsync(V.data(), f.V, V.size() * 8, cudaMemcpyDeviceToHost, st));
+          SGF_CUDA(cudaMemcpyAsync(T.data(), f.Tw, T.size() * 8, cudaMemcpyDeviceToHost, st));
+        }
+        SGF_CUDA(cudaStreamSynchronize(st));
+        double* Q = (double*)host_out;
+        std::vector<double> VT((size_t)s * m, 0.0);  // (T V^T)[a][j]
+        for (int a = 0; a < s; ++a)
+          for (int b = a; b < s; ++b) {
+            const double tab = T[(size_t)a * s + b];
+            if (tab == 0.0) continue;
+            for (int j = 0; j < m; ++j) VT[(size_t)a * m + j] += tab * V[(size_t)b * m + j];
+          }
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) {
+            double acc = (i == j) ? 1.0 : 0.0;
+            for (int a = 0; a < s; ++a) acc -= V[(size_t)a * m + i] * VT[(size_t)a * m + j];
+            Q[(size_t)i * m + j] = acc;
+          }
+        break;
+      }
+      case 5:
+        need(8 * mm);
+        SGF_CUDA(cudaMemcpyAsync(host_out, f.inv, 8 * mm, cudaMemcpyDeviceToHost, st));
+        break;
+      case 6:
+        need(8LL * f.perm.size());
+        for (size_t i = 0; i < f.perm.size(); ++i) ((int64_t*)host_out)[i] = f.perm[i];
+        break;
+      default:
+        fail(SGF_INVALID_ARG, "unknown factor field");
+    }
+    SGF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device) {
+  if (!p || !x || !y) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = p->ctx;
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->c.stream;
+    const long long n = p->p->n;
+    if (on_device) {
+      apply_op(p->p, op, x, y);
+      SGF_CUDA(cudaStreamSynchronize(st));
+    } else {
+      DevVec d(n, st);
+      SGF_CUDA(cudaMemcpyAsync(d.p, x, n * 8, cudaMemcpyHostToDevice, st));
+      apply_op(p->p, op, d.p, d.p);
+      SGF_CUDA(cudaMemcpyAsync(y, d.p, n * 8, cudaMemcpyDeviceToHost, st));
+      SGF_CUDA(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                   const double* values, int on_device, sgf_csr** out) {
+  if (!ctx || !out) return SGF_INVALID_ARG;
+  *out = nullptr;
+  return guarded(ctx, [&] {
+    if (n > INT32_MAX) fail(SGF_INVALID_ARG, "n exceeds int32");
+    sgf_csr* A = new sgf_csr();
+    A->ctx = ctx;
+    A->a.ctx = &ctx->c;
+    A->a.mem.set_stream(ctx->c.stream);
+    A->a.n = n;
+    A->a.nnz = nnz;
+    cudaStream_t st = ctx->c.stream;
+    A->a.rp = A->a.mem.alloc_t<long long>(n + 1);
+    A->a.ci = A->a.mem.alloc_t<int>(std::max<int64_t>(nnz, 1));
+    A->a.v = A->a.mem.alloc(std::max<int64_t>(nnz, 1));
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    SGF_CUDA(cudaMemcpyAsync(A->a.rp, indptr, (n + 1) * 8, k, st));
+    SGF_CUDA(cudaMemcpyAsync(A->a.ci, indices, nnz * 4, k, st));
+    SGF_CUDA(cudaMemcpyAsync(A->a.v, values, nnz * 8, k, st));
+    const double avg = n ? (double)nnz / n : 0.0;
+    A->a.tpr = avg <= 6 ? 4 : avg <= 12 ? 8 : avg <= 24 ? 16 : 32;
+    SGF_CUDA(cudaStreamSynchronize(st));
+    *out = A;
+  });
+}
+
+int sgf_csr_free(sgf_csr* a) {
+  if (!a) return SGF_OK;
+  cudaStreamSynchronize(a->ctx->c.stream);
+  delete a;
+  return SGF_OK;
+}
+
+int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device) {
+  if (!a) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = a->ctx;
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->c.stream;
+    const long long n = a->a.n;
+    if (on_device) {
+      spmv(&a->a, x, y, nullptr);
+    } else {
+      DevVec dx(n, st), dy(n, st);
+      SGF_CUDA(cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, st));
+      spmv(&a->a, dx.p, dy.p, nullptr);
+      SGF_CUDA(cudaMemcpyAsync(y, dy.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    SGF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x, double tol, int maxit,
+            int true_residual_every, int on_device, sgf_pcg_report* rep, double* history) {
+  if (!ctx || !a || !b || !x || !rep || !history) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    if (p && p->p->n != a->a.n) fail(SGF_SHAPE, "preconditioner and matrix sizes differ");
+    cudaStream_t st = ctx->c.stream;
+    const long long n = a->a.n;
+    if (on_device) {
+      pcg(ctx->c, &a->a, p ? p->p : nullptr, b, x, tol, maxit, true_residual_every, rep, history);
+    } else {
+      DevVec db(n, st), dx(n, st);
+      SGF_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, st));
+      pcg(ctx->c, &a->a, p ? p->p : nullptr, db.p, dx.p, tol, maxit, true_residual_every, rep, history);
+      SGF_CUDA(cudaMemcpyAsync(x, dx.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    SGF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

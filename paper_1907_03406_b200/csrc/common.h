@@ -1,0 +1,132 @@
+// Shared definitions of the sgf native library (B200 / sm_100a).
+//
+// Data layout conventions
+//   * every dense block is row-major with an explicit leading dimension;
+//     kernels address operands through (row stride, col stride) pairs so a
+//     stored block (a,b) can be read as itself or as its transpose without
+//     a copy (the reference keeps only blocks i <= j, blockmatrix.py:14-83);
+//   * triangular matrices (L, L^{-1}) are stored as full squares with exact
+//     zeros in the unused triangle, so K-range limits are optimisations only.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgf {
+
+// ---- batched FP64 GEMM (DMMA) ------------------------------------------------
+// C(i,j) = beta*C(i,j) + alpha * sum_seg sum_{k in seg range} A(i,k) * B(j,k)
+// A(i,k) = A[i*a_rs + k*a_ks],  B(j,k) = B[j*b_rs + k*b_ks]
+enum : int {
+  SEG_KLIM_M = 1,    // k < m0 + BM   (A lower triangular in (i,k))
+  SEG_KLIM_N = 2,    // k < n0 + BN   (B lower triangular in (j,k))
+  SEG_KSTART_M = 4,  // k >= m0       (A upper triangular in (i,k))
+  SEG_KSTART_N = 8,  // k >= n0       (B upper triangular in (j,k))
+};
+
+struct GemmSeg {
+  const double* A;
+  const double* B;
+  long long a_rs, a_ks;
+  long long b_rs, b_ks;
+  int K;
+  int flags;
+};
+
+struct GemmTask {
+  double* C;
+  long long c_rs, c_cs;
+  int M, N;      // extents of C (bounds for the tile)
+  int m0, n0;    // tile origin
+  int seg0, nseg;
+  double alpha, beta;
+};
+
+// ---- Cholesky of diagonal tiles ------------------------------------------------
+// Factor the nb x nb (nb <= 64) diagonal tile W[k0:k1, k0:k1] (row-major,
+// ld) in place, write its inverse to Dinv (64x64, ld 64), and flag
+// breakdown (pivot <= floor or non-finite) into status[node].
+struct DiagTask {
+  double* W;        // node matrix base (row-major m x m, ld = m)
+  double* Dinv;     // 64 x 64 scratch for this node's current panel
+  int ld;
+  int k0, nb;
+  double floor;     // CHOL_PIVOT_RTOL * max(diag(A_BB), 0)
+  int node;         // index into the status array
+};
+
+// ---- 2-D block copies ------------------------------------------------------------
+struct CopyTask {
+  const double* src;
+  double* dst;
+  long long s_rs, s_cs;
+  long long d_rs, d_cs;
+  int rows, cols;
+};
+
+// ---- column-pivoted QR (truncated at the rank) ------------------------------------
+struct QrTask {
+  double* Nm;          // m x c column-major (ld = m); overwritten with R and reflectors
+  double* tau;         // >= min(m,c)
+  double* nrm2;        // c scratch
+  double* ref2;        // c scratch
+  int* perm;           // c, output permutation
+  const int* replay;   // optional: pivot column (original index) per step, or null
+  int nreplay;
+  int m, c;
+  int forced_rank;     // >= 0: low-rank mode (run exactly this many steps)
+  double tol;
+  int* out_rank;       // -> rank
+  int* out_steps;      // -> reflectors computed
+};
+
+// ---- apply / GEMV -----------------------------------------------------------------
+// mode 0 (N): y[i] = sum_{k in [kb,ke)} A[i*lda + k] * x[k]  for rows i in [r0, r1)
+// mode 1 (T): part[k] = sum_{i in [r0,r1)} A[i*lda + k] * x[i]  for k in [c0, c1)
+struct GemvTask {
+  const double* A;
+  long long lda;
+  const double* x;
+  double* y;
+  int r0, r1;
+  int c0, c1;
+  int tri;             // 1: lower-triangular A (row i uses k <= i)
+};
+
+struct TriTask { double* p; int m; int ld; };
+
+struct QrFinishTask {
+  const double* Nm;   // m x c panel holding the reflectors below the diagonal
+  const double* tau;
+  const int* steps;   // device scalar
+  const int* rank;    // device scalar
+  double* V;          // m x cap_s
+  double* Tm;         // cap_s x cap_s
+  double* Q1;         // m x cap_r
+  double* G;          // cap_s x cap_s scratch (reflector Gram matrix)
+  int m;
+};
+
+// out[k] = base[k] + sign * sum_{q<nrb} part[q*stride + k], k < n
+struct RedSeg {
+  const double* part;
+  const double* base;   // may be null (then 0)
+  double* out;
+  int n;
+  int nrb;
+  int stride;
+  double sign;
+};
+
+}  // namespace sgf
+
+// kernel launchers (defined in the .cu files)
+namespace sgf {
+cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, int big_tiles,
+                        cudaStream_t s);
+cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s);
+cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,
+                                  cudaStream_t s);
+cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s);
+cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, const int* d_ld, int n,
+                            double* d_out, cudaStream_t s);
+}  // namespace sgf

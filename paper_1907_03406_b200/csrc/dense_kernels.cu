@@ -1,0 +1,227 @@
+// Small dense kernels: diagonal-tile Cholesky + inverse, tiled block copies
+// (merge / gather / densify), CSR -> block scatter, identity blocks,
+// triangle zeroing, per-node max diagonal.
+#include <cmath>
+
+#include "common.h"
+
+namespace sgf {
+
+// ---------------------------------------------------------------------------
+// Diagonal tile Cholesky (nb <= 64).  Restates the reference pivot rule
+// (densela.py:106-110): breakdown when the pivot is <= floor (= 1e-14 x the
+// largest diagonal entry of the node's block) or not finite.  The factor
+// overwrites the tile; its inverse goes to Dinv (and optionally into the
+// diagonal tile of the node's L^{-1}).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) diag_chol_kernel(const DiagTask* __restrict__ tasks,
+                                                        int* __restrict__ status,
+                                                        double* __restrict__ pivval,
+                                                        double* const* __restrict__ xdiag,
+                                                        const int* __restrict__ ldx) {
+  __shared__ double S[64][65];
+  __shared__ int bad;
+  const DiagTask T = tasks[blockIdx.x];
+  const int nb = T.nb, tid = threadIdx.x;
+  double* W = T.W + (long long)T.k0 * T.ld + T.k0;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    int r = idx / nb, c = idx % nb;
+    S[r][c] = W[(long long)r * T.ld + c];
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      double d = S[j][j];
+      if (!(d > T.floor) || !isfinite(d)) {
+        bad = 1;
+        if (status[T.node] == 0) {
+          status[T.node] = T.k0 + j + 1;
+          pivval[T.node] = d;
+        }
+      } else {
+        S[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (bad) return;
+    const double djj = S[j][j];
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) S[i][j] /= djj;
+    __syncthreads();
+    const int rem = nb - j - 1;
+    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
+      int i = j + 1 + idx / rem, l = j + 1 + idx % rem;
+      if (l <= i) S[i][l] -= S[i][j] * S[l][j];
+    }
+    __syncthreads();
+  }
+  // inverse of the lower-triangular tile, one column per thread (the
+  // column lives in the thread's own slice of Dinv)
+  double* Dg = T.Dinv;
+  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) Dg[idx] = 0.0;
+  __syncthreads();
+  if (tid < nb) {
+    const int c = tid;
+    Dg[c * 64 + c] = 1.0 / S[c][c];
+    for (int i = c + 1; i < nb; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s = fma(S[i][k], Dg[k * 64 + c], s);
+      Dg[i * 64 + c] = -s / S[i][i];
+    }
+  }
+  __syncthreads();
+  double* X = xdiag ? xdiag[blockIdx.x] : nullptr;
+  const int lx = ldx ? ldx[blockIdx.x] : 0;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    int r = idx / nb, c = idx % nb;
+    W[(long long)r * T.ld + c] = (c <= r) ? S[r][c] : 0.0;
+    if (X) X[(long long)(T.k0 + r) * lx + T.k0 + c] = Dg[r * 64 + c];
+  }
+}
+
+cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
+                                double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  diag_chol_kernel<<<ntasks, 256, 0, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Tiled copies: one CTA per 32x32 tile; the task of a tile is found by binary
+// search over the per-task tile prefix.  The tile goes through shared memory
+// so both the read and the write are coalesced whatever the two layouts are.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int find_task(const long long* prefix, int ntasks, long long tile) {
+  int lo = 0, hi = ntasks - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) copy_kernel(const CopyTask* __restrict__ tasks,
+                                                   const long long* __restrict__ prefix, int ntasks,
+                                                   long long ntiles) {
+  __shared__ double buf[32][33];
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ti = find_task(prefix, ntasks, tile);
+    const CopyTask T = tasks[ti];
+    const long long local = tile - prefix[ti];
+    const int tcols = (T.cols + 31) / 32;
+    const int r0 = (int)(local / tcols) * 32, c0 = (int)(local % tcols) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const bool src_rowc = (T.s_cs == 1);  // columns contiguous in the source
+    for (int q = ty; q < 32; q += 8) {
+      int r = src_rowc ? q : tx, c = src_rowc ? tx : q;
+      int gr = r0 + r, gc = c0 + c;
+      if (gr < T.rows && gc < T.cols) buf[r][c] = T.src[(long long)gr * T.s_rs + (long long)gc * T.s_cs];
+    }
+    __syncthreads();
+    const bool dst_rowc = (T.d_cs == 1);
+    for (int q = ty; q < 32; q += 8) {
+      int r = dst_rowc ? q : tx, c = dst_rowc ? tx : q;
+      int gr = r0 + r, gc = c0 + c;
+      if (gr < T.rows && gc < T.cols) T.dst[(long long)gr * T.d_rs + (long long)gc * T.d_cs] = buf[r][c];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_copy_tiled(const CopyTask* d_tasks, const long long* d_prefix, int ntasks,
+                              long long ntiles, cudaStream_t s) {
+  if (ntasks <= 0 || ntiles <= 0) return cudaSuccess;
+  long long grid = ntiles < (1LL << 30) ? ntiles : (1LL << 30);
+  copy_kernel<<<(unsigned)grid, 256, 0, s>>>(d_tasks, d_prefix, ntasks, ntiles);
+  return cudaGetLastError();
+}
+
+// zero the strict upper triangle of square row-major matrices (tiles as copy)
+__global__ void __launch_bounds__(256) zero_upper_kernel(const TriTask* __restrict__ tasks,
+                                                         const long long* __restrict__ prefix,
+                                                         int ntasks, long long ntiles) {
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ti = find_task(prefix, ntasks, tile);
+    const TriTask T = tasks[ti];
+    const long long local = tile - prefix[ti];
+    const int tc = (T.m + 31) / 32;
+    const int r0 = (int)(local / tc) * 32, c0 = (int)(local % tc) * 32;
+    if (c0 + 31 <= r0) continue;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int q = ty; q < 32; q += 8) {
+      int r = r0 + q, c = c0 + tx;
+      if (r < T.m && c < T.m && c > r) T.p[(long long)r * T.ld + c] = 0.0;
+    }
+  }
+}
+
+cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, int ntasks, long long ntiles,
+                              cudaStream_t s) {
+  if (ntasks <= 0 || ntiles <= 0) return cudaSuccess;
+  long long grid = ntiles < (1LL << 30) ? ntiles : (1LL << 30);
+  zero_upper_kernel<<<(unsigned)grid, 256, 0, s>>>((const TriTask*)d_tasks, d_prefix, ntasks, ntiles);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+__global__ void scatter_values_kernel(const double* __restrict__ vals, const long long* __restrict__ dst,
+                                      long long nnz, double* __restrict__ base) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long d = dst[e];
+    if (d >= 0) base[d] = vals[e];
+  }
+}
+
+cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,
+                                  cudaStream_t s) {
+  if (nnz <= 0) return cudaSuccess;
+  long long blocks = (nnz + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  scatter_values_kernel<<<(unsigned)blocks, 256, 0, s>>>(vals, dst, nnz, base);
+  return cudaGetLastError();
+}
+
+// r x r identity blocks (compressed node diagonal, factorization.py:345-346)
+__global__ void identity_kernel(double* const* __restrict__ ptrs, const int* __restrict__ sizes) {
+  double* p = ptrs[blockIdx.x];
+  const int r = sizes[blockIdx.x];
+  for (long long i = threadIdx.x; i < (long long)r * r; i += blockDim.x) p[i] = (i / r == i % r) ? 1.0 : 0.0;
+}
+
+cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  identity_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes);
+  return cudaGetLastError();
+}
+
+// floor[i] = 1e-14 * max(max_j A_i[j,j], 0)   (densela.py:105)
+__global__ void max_diag_kernel(const double* const* __restrict__ ptrs, const int* __restrict__ sizes,
+                                const int* __restrict__ ld, double* __restrict__ out) {
+  __shared__ double red[256];
+  const double* p = ptrs[blockIdx.x];
+  const int m = sizes[blockIdx.x], l = ld[blockIdx.x];
+  double mx = 0.0;
+  bool any = false;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double v = p[(long long)i * l + i];
+    mx = any ? fmax(mx, v) : v;
+    any = true;
+  }
+  red[threadIdx.x] = any ? mx : -INFINITY;
+  __syncthreads();
+  for (int s2 = 128; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s2]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = 1e-14 * fmax(red[0], 0.0);
+}
+
+cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, const int* d_ld, int n,
+                            double* d_out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  max_diag_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes, d_ld, d_out);
+  return cudaGetLastError();
+}
+
+}  // namespace sgf

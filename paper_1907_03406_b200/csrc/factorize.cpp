@@ -1,0 +1,926 @@
+// Level-synchronous driver of the hierarchical factorization (reference
+// factorization.py:410-573, the paper's Alg. 4.1) on the device.
+//
+// Per level, host work is symbolic only (block table, neighbour lists, task
+// lists); every floating-point operation runs in batched sm_100a kernels:
+//   eliminations  all interiors of the level at once (they never touch each
+//                 other): blocked POTRF + inverse, E = A_NB L^{-T} as one
+//                 triangular DMMA GEMM, target-centric Schur GEMM with the
+//                 contributors of a target block accumulated in ascending
+//                 interior order (factorization.py:277-299, 485-489);
+//   compressions  DAG wavefronts: a node waits for already-compressed adjacent
+//                 nodes of lower id, non-adjacent compressions touch disjoint
+//                 blocks, so the result equals the reference's ascending-id
+//                 sequence (factorization.py:302-353, 490-519);
+//   merge         one tiled copy launch per level (factorization.py:356-407);
+//   final dense   one blocked POTRF (factorization.py:535-541).
+// The analytic flop tally (densela.py:24-40) and the live/peak block-byte
+// accounting (blockmatrix.py:25-43) are recomputed on the host in the
+// reference's operation order, so the stats dict matches exactly.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+
+#include "precond.h"
+
+namespace sgf {
+
+namespace {
+
+struct Node {
+  std::vector<int64_t> active;
+  double* phi = nullptr;  // device, active.size() x pi, row-major
+  int kind = 0;
+  bool interior = false;
+};
+
+struct LevelStats {
+  int level, nodes, eliminated = 0, compressed = 0;
+  std::vector<int> ranks;
+};
+
+struct State {
+  Ctx* ctx;
+  cudaStream_t st;
+  const sgf_factor_args* a;
+  int pi;
+  BlockTable M;
+  std::vector<Node> nodes;
+  std::unique_ptr<Arena> lvl;  // blocks + phi of the current level
+  Arena scratch;
+  long long flops = 0;
+  long long peak = 0;
+  int comp_counter = 0;  // compressions so far (reference execution order)
+  Precond* P;
+  explicit State(cudaStream_t s) : scratch(s) {}
+};
+
+inline bool kind_in(int mask, int kind) { return (mask >> kind) & 1; }
+
+// ---------------------------------------------------------------------------
+// level 1: nodes, basis rows, and the CSR -> block scatter (blockmatrix.py:97-144)
+// ---------------------------------------------------------------------------
+void setup_level1(State& S) {
+  const sgf_factor_args& a = *S.a;
+  const int nc = a.level_ncells[0];
+  const int64_t n = a.n;
+  std::vector<int32_t> owner(n, -1), local(n, 0);
+  std::vector<int> sizes(nc);
+  S.nodes.assign(nc, Node());
+  for (int c = 0; c < nc; ++c) {
+    const int64_t b = a.l1_ptr[c], e = a.l1_ptr[c + 1];
+    sizes[c] = (int)(e - b);
+    Node& nd = S.nodes[c];
+    nd.active.assign(a.l1_unknowns + b, a.l1_unknowns + e);
+    nd.kind = a.cell_kind[c];
+    nd.interior = a.cell_interior[c] != 0;
+    for (int64_t i = b; i < e; ++i) {
+      const int64_t u = a.l1_unknowns[i];
+      if (u < 0 || u >= n || owner[u] != -1) fail(SGF_INVALID_ARG, "level-1 cells do not partition the unknowns");
+      owner[u] = c;
+      local[u] = (int32_t)(i - b);
+    }
+  }
+  for (int64_t u = 0; u < n; ++u)
+    if (owner[u] < 0) fail(SGF_INVALID_ARG, "node unknown lists do not cover all unknowns");
+
+  // symmetry of pattern and values (blockmatrix.py:107-113), indices sorted per row
+  {
+    double scale = 0.0;
+    if (!a.values_on_device)
+      for (int64_t e = 0; e < a.nnz; ++e) scale = std::max(scale, std::fabs(a.values[e]));
+    for (int64_t r = 0; r < n; ++r) {
+      for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
+        const int32_t c = a.indices[e];
+        if (c <= r) continue;
+        const int32_t* b0 = a.indices + a.indptr[c];
+        const int32_t* b1 = a.indices + a.indptr[c + 1];
+        const int32_t* f = std::lower_bound(b0, b1, (int32_t)r);
+        bool found = (f != b1 && *f == r);
+        if (!found) {
+          if (!a.values_on_device && a.values[e] == 0.0) continue;
+          fail(SGF_NON_SYMMETRIC, "matrix is not symmetric (pattern)");
+        }
+        if (!a.values_on_device) {
+          const double d = std::fabs(a.values[e] - a.values[a.indptr[c] + (f - b0)]);
+          if (d > 1e-12 * std::max(scale, 1e-300)) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "matrix is not symmetric (max asymmetry %.2e)", d);
+            fail(SGF_NON_SYMMETRIC, buf);
+          }
+        }
+      }
+    }
+  }
+
+  // block discovery: per cell the sorted list of coupled cells (b > a)
+  std::vector<std::vector<int>> up(nc);
+  std::vector<char> has_diag(nc, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    const int ca = owner[r];
+    for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
+      const int cb = owner[a.indices[e]];
+      if (cb == ca) { has_diag[ca] = 1; continue; }
+      const int lo = std::min(ca, cb), hi = std::max(ca, cb);
+      auto& v = up[lo];
+      if (std::find(v.begin(), v.end(), hi) == v.end()) v.push_back(hi);
+    }
+  }
+  S.M.init(sizes);
+  long long total = 0;
+  for (int c = 0; c < nc; ++c) {
+    std::sort(up[c].begin(), up[c].end());
+    if (has_diag[c]) total += (long long)sizes[c] * sizes[c];
+    for (int b : up[c]) total += (long long)sizes[c] * sizes[b];
+  }
+  S.lvl.reset(new Arena(S.st));
+  double* base = S.lvl->alloc(std::max<long long>(total, 1));
+  SGF_CUDA(cudaMemsetAsync(base, 0, std::max<long long>(total, 1) * sizeof(double), S.st));
+  // blocks in lexicographic (a, b) order: the reference's insertion order
+  std::vector<long long> diag_off(nc, -1);
+  std::vector<std::vector<long long>> up_off(nc);
+  long long off = 0;
+  for (int c = 0; c < nc; ++c) {
+    if (has_diag[c]) {
+      diag_off[c] = off;
+      S.M.insert(c, c, Blk{base + off, sizes[c], sizes[c]});
+      off += (long long)sizes[c] * sizes[c];
+    }
+    for (int b : up[c]) {
+      up_off[c].push_back(off);
+      S.M.insert(c, b, Blk{base + off, sizes[c], sizes[b]});
+      off += (long long)sizes[c] * sizes[b];
+    }
+  }
+  // per-nnz destination offsets (entries stored once: the (min,max) orientation)
+  std::vector<long long> dst(a.nnz);
+  for (int64_t r = 0; r < n; ++r) {
+    const int ca = owner[r];
+    for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
+      const int32_t col = a.indices[e];
+      const int cb = owner[col];
+      if (cb == ca) {
+        dst[e] = diag_off[ca] + (long long)local[r] * sizes[ca] + local[col];
+      } else if (ca < cb) {
+        const auto& v = up[ca];
+        const size_t j = std::lower_bound(v.begin(), v.end(), cb) - v.begin();
+        dst[e] = up_off[ca][j] + (long long)local[r] * sizes[cb] + local[col];
+      } else {
+        dst[e] = -1;  // written by the symmetric partner
+      }
+    }
+  }
+  long long* d_dst = S.scratch.upload(dst);
+  const double* d_vals = a.values;
+  if (!a.values_on_device) {
+    double* dv = S.scratch.alloc(a.nnz);
+    SGF_CUDA(cudaMemcpyAsync(dv, a.values, a.nnz * sizeof(double), cudaMemcpyHostToDevice, S.st));
+    d_vals = dv;
+  }
+  SGF_CUDA(launch_scatter_values(d_vals, d_dst, a.nnz, base, S.st));
+
+  // basis rows of every node: Pi[active] in cell order
+  const int pi = S.pi;
+  std::vector<double> phi_perm((size_t)n * pi);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t u = a.l1_unknowns[i];
+    std::memcpy(&phi_perm[(size_t)i * pi], a.phi + (size_t)u * pi, pi * sizeof(double));
+  }
+  double* d_phi = S.lvl->upload(phi_perm);
+  for (int c = 0; c < nc; ++c) S.nodes[c].phi = d_phi ? d_phi + (size_t)a.l1_ptr[c] * pi : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// eliminations of one level (factorization.py:277-299)
+// ---------------------------------------------------------------------------
+void eliminate_level(State& S, const std::vector<int>& elim, int level) {
+  if (elim.empty()) return;
+  cudaStream_t st = S.st;
+  BlockTable& M = S.M;
+  Precond* P = S.P;
+  struct EI {
+    int x, m, c;
+    std::vector<int> nb;
+    std::vector<int> off;
+    double *W, *X, *E;
+  };
+  std::vector<EI> info(elim.size());
+  CopyBatch cp;
+  std::vector<CholJob> jobs;
+  for (size_t q = 0; q < elim.size(); ++q) {
+    EI& e = info[q];
+    e.x = elim[q];
+    e.m = M.size[e.x];
+    e.nb = M.nbrs(e.x);
+    e.c = 0;
+    for (int j : e.nb) {
+      e.off.push_back(e.c);
+      e.c += M.size[j];
+    }
+    const size_t mm = (size_t)e.m * e.m;
+    e.W = P->store.alloc(mm);
+    e.X = P->store.alloc(mm);
+    SGF_CUDA(cudaMemsetAsync(e.X, 0, mm * sizeof(double), st));
+    e.E = e.c ? P->store.alloc((size_t)e.c * e.m) : nullptr;
+    Blk* d = M.find(e.x, e.x);
+    if (!d) fail(SGF_NOT_SPD, "interior node without a diagonal block");
+    cp.add(d->p, d->cols, 1, e.W, e.m, 1, e.m, e.m);
+    jobs.push_back(CholJob{e.W, e.X, e.m, e.x});
+  }
+  cp.launch(S.scratch, st);
+  chol_inv_batch(*S.ctx, S.scratch, jobs);
+
+  GemmBatch ge;
+  for (auto& e : info) {
+    long long f = (long long)e.m * e.m * e.m / 3;
+    for (size_t q = 0; q < e.nb.size(); ++q) {
+      View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
+      ge.add(e.E + (long long)e.off[q] * e.m, e.m, 1, v.rows, e.m, 1.0, 0.0,
+             {seg(v.p, v.rs, v.cs, e.X, e.m, 1, e.m, SEG_KLIM_N)});
+      f += (long long)e.m * e.m * v.rows;
+    }
+    for (size_t p = 0; p < e.nb.size(); ++p)
+      for (size_t q = p; q < e.nb.size(); ++q) f += 2LL * M.size[e.nb[p]] * e.m * M.size[e.nb[q]];
+    S.flops += f;
+  }
+  ge.launch(S.scratch, st);
+
+  // Schur targets in the reference's insertion order (ascending interior id,
+  // neighbour pairs a <= b); fill blocks are created zero (blockmatrix.py:65-72)
+  struct Target {
+    int a, b;
+    std::vector<std::pair<int, std::pair<int, int>>> contrib;
+  };
+  std::unordered_map<uint64_t, int> tix;
+  std::vector<Target> targets;
+  long long fill_elems = 0;
+  std::vector<std::pair<uint64_t, long long>> fills;  // key -> elems, in creation order
+  {
+    std::unordered_map<uint64_t, char> created;
+    for (size_t q = 0; q < info.size(); ++q) {
+      const EI& e = info[q];
+      for (size_t p = 0; p < e.nb.size(); ++p)
+        for (size_t r = p; r < e.nb.size(); ++r) {
+          const int A = e.nb[p], B = e.nb[r];
+          const uint64_t k = bkey(A, B);
+          if (!M.find(A, B) && !created.count(k)) {
+            created[k] = 1;
+            const long long el = (long long)M.size[A] * M.size[B];
+            fills.push_back({k, el});
+            fill_elems += el;
+          }
+          auto it = tix.find(k);
+          if (it == tix.end()) {
+            tix[k] = (int)targets.size();
+            targets.push_back(Target{A, B, {}});
+            it = tix.find(k);
+          }
+          targets[it->second].contrib.push_back({(int)q, {(int)p, (int)r}});
+        }
+    }
+  }
+  double* fill_base = nullptr;
+  if (fill_elems > 0) {
+    fill_base = S.lvl->alloc(fill_elems);
+    SGF_CUDA(cudaMemsetAsync(fill_base, 0, fill_elems * sizeof(double), st));
+  }
+  {
+    std::unordered_map<uint64_t, double*> fill_ptr;
+    long long off = 0;
+    for (auto& f : fills) {
+      fill_ptr[f.first] = fill_base + off;
+      off += f.second;
+    }
+    // replay the reference sequence for the table and its byte accounting
+    for (size_t q = 0; q < info.size(); ++q) {
+      const EI& e = info[q];
+      for (size_t p = 0; p < e.nb.size(); ++p)
+        for (size_t r = p; r < e.nb.size(); ++r) {
+          const int A = e.nb[p], B = e.nb[r];
+          if (!M.find(A, B)) {
+            auto it = fill_ptr.find(bkey(A, B));
+            M.insert(A, B, Blk{it->second, M.size[A], M.size[B]});
+          }
+        }
+      // factor record (before the node's actives are cleared)
+      Factor f;
+      f.type = SGF_FACTOR_ELIMINATION;
+      f.node = e.x;
+      f.level = level;
+      f.m = e.m;
+      f.c = e.c;
+      f.idx = S.nodes[e.x].active;
+      for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
+      f.L = e.W;
+      f.inv = e.X;
+      f.E = e.E;
+      P->factors.push_back(std::move(f));
+      M.drop(e.x);
+      M.size[e.x] = 0;
+      S.nodes[e.x].active.clear();
+      S.nodes[e.x].phi = nullptr;
+    }
+  }
+  GemmBatch gs;
+  for (auto& T : targets) {
+    Blk* blk = M.find(T.a, T.b);  // T.a <= T.b: rows in a
+    std::vector<GemmSeg> sg;
+    for (auto& c : T.contrib) {
+      const EI& e = info[c.first];
+      sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.m, e.m, 1,
+                       e.E + (long long)e.off[c.second.second] * e.m, e.m, 1, e.m));
+    }
+    gs.add(blk->p, blk->cols, 1, blk->rows, blk->cols, -1.0, 1.0, sg);
+  }
+  gs.launch(S.scratch, st);
+}
+
+// ---------------------------------------------------------------------------
+// compressions of one level in DAG wavefronts (factorization.py:302-353)
+// ---------------------------------------------------------------------------
+struct CompOut {
+  int node;
+  Factor f;
+  int rank;
+};
+
+void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int>& seqno,
+                   const std::vector<int>& forced, int level, std::vector<CompOut>& out) {
+  cudaStream_t st = S.st;
+  BlockTable& M = S.M;
+  Precond* P = S.P;
+  const sgf_factor_args& a = *S.a;
+  const int pi = S.pi;
+  const bool lowrank = a.mode == SGF_MODE_LOWRANK;
+  struct CI {
+    int c, m, cN;
+    std::vector<int> nb;
+    std::vector<char> raw;
+    std::vector<int> col;  // column offset in N of each neighbour's block
+    double *L, *X, *LP, *N, *tau, *nrm2, *ref2;
+    int* perm;
+    std::vector<double*> Z;
+  };
+  const int nw = (int)wave.size();
+  std::vector<CI> ci(nw);
+  CopyBatch cp;
+  std::vector<CholJob> jobs;
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    c.c = wave[w];
+    c.m = M.size[c.c];
+    c.nb = M.nbrs(c.c);
+    c.cN = lowrank ? 0 : pi;
+    for (int j : c.nb) {
+      const bool raw = lowrank || kind_in(a.raw_kind_mask, S.nodes[j].kind);
+      c.raw.push_back(raw);
+      c.col.push_back(c.cN);
+      c.cN += raw ? M.size[j] : pi;
+    }
+    const size_t mm = (size_t)c.m * c.m;
+    c.L = P->store.alloc(mm);
+    c.X = P->store.alloc(mm);
+    SGF_CUDA(cudaMemsetAsync(c.X, 0, mm * sizeof(double), st));
+    c.LP = S.scratch.alloc((size_t)c.m * pi);
+    c.N = S.scratch.alloc((size_t)c.m * std::max(c.cN, 1));
+    const int kmax = std::max(std::min(c.m, c.cN), 1);
+    c.tau = S.scratch.alloc(kmax);
+    c.nrm2 = S.scratch.alloc(std::max(c.cN, 1));
+    c.ref2 = S.scratch.alloc(std::max(c.cN, 1));
+    c.perm = S.scratch.alloc_t<int>(std::max(c.cN, 1));
+    Blk* d = M.find(c.c, c.c);
+    if (!d) fail(SGF_NOT_SPD, "compressed node without a diagonal block");
+    cp.add(d->p, d->cols, 1, c.L, c.m, 1, c.m, c.m);
+    jobs.push_back(CholJob{c.L, c.X, c.m, c.c});
+  }
+  cp.launch(S.scratch, st);
+  chol_inv_batch(*S.ctx, S.scratch, jobs);
+
+  // L^T Phi_B and the filtered products M_BN Phi_N
+  GemmBatch g1;
+  for (auto& c : ci) {
+    g1.add(c.LP, pi, 1, c.m, pi, 1.0, 0.0,
+           {seg(c.L, 1, c.m, S.nodes[c.c].phi, 1, pi, c.m, SEG_KSTART_M)});
+    c.Z.assign(c.nb.size(), nullptr);
+    for (size_t q = 0; q < c.nb.size(); ++q) {
+      if (c.raw[q]) continue;
+      View v = view_of(M, c.c, c.nb[q]);  // m x |N|
+      c.Z[q] = S.scratch.alloc((size_t)c.m * pi);
+      g1.add(c.Z[q], pi, 1, c.m, pi, 1.0, 0.0, {seg(v.p, v.rs, v.cs, S.nodes[c.nb[q]].phi, 1, pi, v.cols)});
+    }
+  }
+  g1.launch(S.scratch, st);
+  // assemble N (column major): [L^T Phi_B | L^{-1} M_BN Phi_N or L^{-1} M_BN]
+  GemmBatch g2;
+  CopyBatch cn;
+  for (auto& c : ci) {
+    if (!lowrank) cn.add(c.LP, pi, 1, c.N, 1, c.m, c.m, pi);
+    for (size_t q = 0; q < c.nb.size(); ++q) {
+      double* dstc = c.N + (long long)c.col[q] * c.m;
+      if (c.raw[q]) {
+        View v = view_of(M, c.c, c.nb[q]);
+        g2.add(dstc, 1, c.m, c.m, v.cols, 1.0, 0.0, {seg(c.X, c.m, 1, v.p, v.cs, v.rs, c.m, SEG_KLIM_M)});
+      } else {
+        g2.add(dstc, 1, c.m, c.m, pi, 1.0, 0.0, {seg(c.X, c.m, 1, c.Z[q], 1, pi, c.m, SEG_KLIM_M)});
+      }
+    }
+  }
+  cn.launch(S.scratch, st);
+  g2.launch(S.scratch, st);
+
+  // pivoted QR (truncated at the rank), ranks read back
+  std::vector<QrTask> qt(nw);
+  int* d_out = S.scratch.alloc_t<int>(2 * nw);
+  int max_m = 1;
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    QrTask& t = qt[w];
+    t.Nm = c.N;
+    t.tau = c.tau;
+    t.nrm2 = c.nrm2;
+    t.ref2 = c.ref2;
+    t.perm = c.perm;
+    t.replay = nullptr;
+    t.nreplay = 0;
+    if (a.replay_ptr && seqno[w] < a.n_replay) {
+      const int64_t b = a.replay_ptr[seqno[w]], e = a.replay_ptr[seqno[w] + 1];
+      std::vector<int> rp(a.replay_perm + b, a.replay_perm + e);
+      t.replay = S.scratch.upload(rp);
+      t.nreplay = (int)rp.size();
+    }
+    t.m = c.m;
+    t.c = c.cN;
+    t.forced_rank = lowrank ? forced[w] : -1;
+    t.tol = a.rank_tol;
+    t.out_rank = d_out + w;
+    t.out_steps = d_out + nw + w;
+    max_m = std::max(max_m, c.m);
+  }
+  {
+    QrTask* d_qt = S.scratch.upload(qt);
+    SGF_CUDA(launch_qrcp(d_qt, nw, max_m, st));
+  }
+  std::vector<int> rs(2 * nw);
+  SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaStreamSynchronize(st));
+
+  // reflectors, compact-WY T, Q1
+  std::vector<QrFinishTask> ft(nw);
+  std::vector<double*> V(nw), Tw(nw), Q1(nw);
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    const int r = rs[w], s = rs[nw + w];
+    V[w] = s ? P->store.alloc((size_t)c.m * s) : nullptr;
+    Tw[w] = s ? P->store.alloc((size_t)s * s) : nullptr;
+    Q1[w] = r ? S.scratch.alloc((size_t)c.m * r) : nullptr;
+    QrFinishTask& f = ft[w];
+    f.Nm = c.N;
+    f.tau = c.tau;
+    f.steps = d_out + nw + w;
+    f.rank = d_out + w;
+    f.V = V[w];
+    f.Tm = Tw[w];
+    f.Q1 = Q1[w];
+    f.G = s ? S.scratch.alloc((size_t)s * s) : nullptr;
+    f.m = c.m;
+  }
+  {
+    QrFinishTask* d_ft = S.scratch.upload(ft);
+    SGF_CUDA(launch_qr_finish(d_ft, nw, st));
+  }
+  // inv = Q^T L^{-1} = L^{-1} - V T^T V^T L^{-1}
+  std::vector<double*> inv(nw), Y(nw), Y2(nw);
+  CopyBatch ci0;
+  GemmBatch gy, gy2, gin;
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    const int s = rs[nw + w];
+    inv[w] = P->store.alloc((size_t)c.m * c.m);
+    ci0.add(c.X, c.m, 1, inv[w], c.m, 1, c.m, c.m);
+    if (!s) continue;
+    Y[w] = S.scratch.alloc((size_t)s * c.m);
+    Y2[w] = S.scratch.alloc((size_t)s * c.m);
+    gy.add(Y[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(V[w], c.m, 1, c.X, 1, c.m, c.m, SEG_KSTART_N)});
+    gy2.add(Y2[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(Tw[w], 1, s, Y[w], 1, c.m, s, SEG_KLIM_M)});
+    gin.add(inv[w], c.m, 1, c.m, c.m, -1.0, 1.0, {seg(V[w], 1, c.m, Y2[w], 1, c.m, s)});
+  }
+  ci0.launch(S.scratch, st);
+  gy.launch(S.scratch, st);
+  gy2.launch(S.scratch, st);
+  gin.launch(S.scratch, st);
+
+  // new couplings Q1^T L^{-1} M_BN, basis update Q1^T L^T Phi_B, identity diagonal
+  GemmBatch gn;
+  std::vector<double*> id_ptr;
+  std::vector<int> id_sz;
+  std::vector<std::vector<Blk>> newblk(nw);
+  std::vector<double*> newphi(nw, nullptr);
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    const int r = rs[w];
+    if (r <= 0) continue;
+    for (size_t q = 0; q < c.nb.size(); ++q) {
+      const int j = c.nb[q];
+      View v = view_of(M, c.c, j);  // m x |N|
+      const int nj = v.cols;
+      double* p = S.lvl->alloc((size_t)r * nj);
+      if (c.c < j) {
+        newblk[w].push_back(Blk{p, r, nj});
+        gn.add(p, nj, 1, r, nj, 1.0, 0.0, {seg(inv[w], c.m, 1, v.p, v.cs, v.rs, c.m)});
+      } else {
+        newblk[w].push_back(Blk{p, nj, r});
+        gn.add(p, 1, r, r, nj, 1.0, 0.0, {seg(inv[w], c.m, 1, v.p, v.cs, v.rs, c.m)});
+      }
+    }
+    newphi[w] = S.lvl->alloc((size_t)r * pi);
+    gn.add(newphi[w], pi, 1, r, pi, 1.0, 0.0, {seg(Q1[w], c.m, 1, c.LP, 1, pi, c.m)});
+    double* I = S.lvl->alloc((size_t)r * r);
+    id_ptr.push_back(I);
+    id_sz.push_back(r);
+    newblk[w].push_back(Blk{I, r, r});  // last: diagonal
+  }
+  gn.launch(S.scratch, st);
+  if (!id_ptr.empty()) {
+    double** d_p = S.scratch.upload(id_ptr);
+    int* d_s = S.scratch.upload(id_sz);
+    SGF_CUDA(launch_fill_identity(d_p, d_s, (int)id_ptr.size(), st));
+  }
+  // perms back (information / parity)
+  std::vector<std::vector<int32_t>> perms(nw);
+  for (int w = 0; w < nw; ++w) {
+    perms[w].resize(std::max(ci[w].cN, 0));
+    if (ci[w].cN > 0)
+      SGF_CUDA(cudaMemcpyAsync(perms[w].data(), ci[w].perm, ci[w].cN * sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  SGF_CUDA(cudaStreamSynchronize(st));
+
+  // host structure updates and factor records
+  for (int w = 0; w < nw; ++w) {
+    CI& c = ci[w];
+    const int r = rs[w], s = rs[nw + w];
+    long long f = (long long)c.m * c.m * c.m / 3;
+    for (int j : c.nb) f += (long long)c.m * c.m * M.size[j];
+    f += 2LL * c.m * c.m * pi;
+    for (size_t q = 0; q < c.nb.size(); ++q)
+      if (!lowrank && !c.raw[q]) f += 2LL * c.m * M.size[c.nb[q]] * pi;
+    f += 2LL * c.m * c.cN * c.cN;
+    for (int j : c.nb) f += 2LL * r * c.m * M.size[j];
+    f += 2LL * r * c.m * pi;
+    S.flops += f;
+
+    CompOut o;
+    o.node = c.c;
+    o.rank = r;
+    o.f.type = SGF_FACTOR_COMPRESSION;
+    o.f.node = c.c;
+    o.f.level = level;
+    o.f.m = c.m;
+    o.f.r = r;
+    o.f.steps = s;
+    o.f.idx = S.nodes[c.c].active;
+    o.f.L = c.L;
+    o.f.inv = inv[w];
+    o.f.V = V[w];
+    o.f.Tw = Tw[w];
+    o.f.perm = perms[w];
+    o.f.ncols = c.cN;
+    out.push_back(std::move(o));
+
+    M.drop(c.c);
+    M.size[c.c] = r;
+    if (r > 0) {
+      M.insert(c.c, c.c, newblk[w].back());
+      for (size_t q = 0; q < c.nb.size(); ++q) M.insert(c.c, c.nb[q], newblk[w][q]);
+    }
+    S.nodes[c.c].active.resize(r);
+    S.nodes[c.c].phi = newphi[w];
+  }
+}
+
+void compress_level(State& S, const std::vector<int>& comp, int level, LevelStats& ls) {
+  if (comp.empty()) return;
+  const sgf_factor_args& a = *S.a;
+  BlockTable& M = S.M;
+  const int nc = (int)comp.size();
+  // rank-trace replay checks in reference order (factorization.py:492-509)
+  std::vector<int> forced(nc, -1);
+  if (a.mode == SGF_MODE_LOWRANK) {
+    for (int i = 0; i < nc; ++i) {
+      const int k = S.comp_counter + i;
+      char buf[256];
+      if (k >= a.n_trace) {
+        snprintf(buf, sizeof buf, "rank trace exhausted; structural divergence at level %d, node %d", level,
+                 comp[i]);
+        fail(SGF_TRACE, buf);
+      }
+      const int lv = a.trace[3 * k], nd = a.trace[3 * k + 1], r = a.trace[3 * k + 2];
+      if (lv != level || nd != comp[i]) {
+        snprintf(buf, sizeof buf, "rank trace divergence: expected [%d, %d], reached [%d, %d]", lv, nd, level,
+                 comp[i]);
+        fail(SGF_TRACE, buf);
+      }
+      forced[i] = r;
+    }
+  }
+  std::unordered_map<int, int> pos;
+  for (int i = 0; i < nc; ++i) pos[comp[i]] = i;
+  std::vector<int> wv(nc, 0);
+  int nwaves = 0;
+  for (int i = 0; i < nc; ++i) {
+    int w = 0;
+    for (int b : M.adj[comp[i]]) {
+      auto it = pos.find(b);
+      if (it != pos.end() && it->second < i) w = std::max(w, wv[it->second] + 1);
+    }
+    wv[i] = w;
+    nwaves = std::max(nwaves, w + 1);
+  }
+  std::vector<CompOut> outs;
+  for (int w = 0; w < nwaves; ++w) {
+    std::vector<int> nodes, seqno, fr;
+    for (int i = 0; i < nc; ++i)
+      if (wv[i] == w) {
+        nodes.push_back(comp[i]);
+        seqno.push_back(S.comp_counter + i);
+        int r = forced[i];
+        if (r > M.size[comp[i]]) {
+          fprintf(stderr, "warning: forced rank %d exceeds node size %d; clipping\n", r, M.size[comp[i]]);
+          r = M.size[comp[i]];
+        }
+        fr.push_back(r);
+      }
+    compress_wave(S, nodes, seqno, fr, level, outs);
+    S.scratch.release();
+  }
+  std::sort(outs.begin(), outs.end(), [](const CompOut& x, const CompOut& y) { return x.node < y.node; });
+  for (auto& o : outs) {
+    S.P->trace.push_back(level);
+    S.P->trace.push_back(o.node);
+    S.P->trace.push_back(o.rank);
+    ls.ranks.push_back(o.rank);
+    ls.compressed++;
+    S.P->factors.push_back(std::move(o.f));
+  }
+  S.comp_counter += nc;
+}
+
+// ---------------------------------------------------------------------------
+// merge into the next level (factorization.py:356-407)
+// ---------------------------------------------------------------------------
+void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kinds, const int8_t* interior) {
+  cudaStream_t st = S.st;
+  BlockTable& M = S.M;
+  const int nc = (int)S.nodes.size();
+  const int pi = S.pi;
+  std::vector<std::vector<int>> kids(next_nc);
+  for (int c = 0; c < nc; ++c) {
+    const int64_t f = father[c];
+    if (f < 0 || f >= next_nc) fail(SGF_INVALID_ARG, "bad father map");
+    kids[f].push_back(c);
+  }
+  std::vector<int> fof(nc), oof(nc), nsize(next_nc, 0);
+  std::vector<Node> nn(next_nc);
+  long long phi_rows = 0;
+  for (int f = 0; f < next_nc; ++f) {
+    int pos = 0;
+    for (int c : kids[f]) {  // ascending child id
+      fof[c] = f;
+      oof[c] = pos;
+      pos += (int)S.nodes[c].active.size();
+      nn[f].active.insert(nn[f].active.end(), S.nodes[c].active.begin(), S.nodes[c].active.end());
+    }
+    nsize[f] = pos;
+    nn[f].kind = kinds[f];
+    nn[f].interior = interior[f] != 0;
+    phi_rows += pos;
+  }
+  std::unique_ptr<Arena> nl(new Arena(st));
+  CopyBatch cp;
+  double* phi = nl->alloc(std::max<long long>(phi_rows * pi, 1));
+  {
+    long long off = 0;
+    for (int f = 0; f < next_nc; ++f) {
+      nn[f].phi = phi + off * pi;
+      for (int c : kids[f]) {
+        const int rows = (int)S.nodes[c].active.size();
+        if (rows) cp.add(S.nodes[c].phi, pi, 1, phi + (off + oof[c]) * pi, pi, 1, rows, pi);
+      }
+      off += nsize[f];
+    }
+  }
+  // father blocks in the reference's creation order (sorted old keys)
+  std::vector<uint64_t> keys;
+  keys.reserve(M.map.size());
+  for (auto& kv : M.map) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());
+  BlockTable N;
+  N.init(nsize);
+  std::vector<std::pair<uint64_t, long long>> order;
+  std::unordered_map<uint64_t, long long> newoff;
+  long long tot = 0;
+  for (uint64_t k : keys) {
+    const Blk& b = M.map[k];
+    if ((long long)b.rows * b.cols == 0) continue;
+    const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
+    const uint64_t fk = bkey(fof[a0], fof[b0]);
+    if (!newoff.count(fk)) {
+      const int fa = (int)(fk >> 32), fb = (int)(fk & 0xffffffffu);
+      newoff[fk] = tot;
+      order.push_back({fk, tot});
+      tot += (long long)nsize[fa] * nsize[fb];
+    }
+  }
+  double* base = nl->alloc(std::max<long long>(tot, 1));
+  if (tot) SGF_CUDA(cudaMemsetAsync(base, 0, tot * sizeof(double), st));
+  for (auto& o : order) {
+    const int fa = (int)(o.first >> 32), fb = (int)(o.first & 0xffffffffu);
+    N.insert(fa, fb, Blk{base + o.second, nsize[fa], nsize[fb]});
+  }
+  for (uint64_t k : keys) {
+    const Blk& b = M.map[k];
+    if ((long long)b.rows * b.cols == 0) continue;
+    const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
+    const int fa = fof[a0], fb = fof[b0], oa = oof[a0], ob = oof[b0];
+    if (fa == fb) {
+      Blk* t = N.find(fa, fa);
+      cp.add(b.p, b.cols, 1, t->p + (long long)oa * t->cols + ob, t->cols, 1, b.rows, b.cols);
+      if (a0 != b0) cp.add(b.p, 1, b.cols, t->p + (long long)ob * t->cols + oa, t->cols, 1, b.cols, b.rows);
+    } else if (fa < fb) {
+      Blk* t = N.find(fa, fb);
+      cp.add(b.p, b.cols, 1, t->p + (long long)oa * t->cols + ob, t->cols, 1, b.rows, b.cols);
+    } else {
+      Blk* t = N.find(fb, fa);
+      cp.add(b.p, 1, b.cols, t->p + (long long)ob * t->cols + oa, t->cols, 1, b.cols, b.rows);
+    }
+  }
+  cp.launch(S.scratch, st);
+  SGF_CUDA(cudaStreamSynchronize(st));
+  S.scratch.release();
+  S.lvl = std::move(nl);  // frees the old level (stream ordered)
+  S.M = std::move(N);
+  S.nodes = std::move(nn);
+}
+
+// ---------------------------------------------------------------------------
+// final dense factor (factorization.py:535-541, blockmatrix.py:148-170)
+// ---------------------------------------------------------------------------
+void final_dense(State& S) {
+  cudaStream_t st = S.st;
+  BlockTable& M = S.M;
+  std::vector<int> rem;
+  for (int c = 0; c < (int)S.nodes.size(); ++c)
+    if (!S.nodes[c].active.empty()) rem.push_back(c);
+  if (rem.empty()) return;
+  std::unordered_map<int, int> off;
+  int tot = 0;
+  for (int c : rem) {
+    off[c] = tot;
+    tot += M.size[c];
+  }
+  Precond* P = S.P;
+  const size_t tt = (size_t)tot * tot;
+  double* D = P->store.alloc(tt);
+  double* X = P->store.alloc(tt);
+  SGF_CUDA(cudaMemsetAsync(D, 0, tt * sizeof(double), st));
+  SGF_CUDA(cudaMemsetAsync(X, 0, tt * sizeof(double), st));
+  CopyBatch cp;
+  for (auto& kv : M.map) {
+    const int a0 = (int)(kv.first >> 32), b0 = (int)(kv.first & 0xffffffffu);
+    auto ia = off.find(a0), ib = off.find(b0);
+    if (ia == off.end() || ib == off.end()) continue;
+    const Blk& b = kv.second;
+    cp.add(b.p, b.cols, 1, D + (long long)ia->second * tot + ib->second, tot, 1, b.rows, b.cols);
+    if (a0 != b0) cp.add(b.p, 1, b.cols, D + (long long)ib->second * tot + ia->second, tot, 1, b.cols, b.rows);
+  }
+  cp.launch(S.scratch, st);
+  std::vector<CholJob> jobs{CholJob{D, X, tot, -1}};
+  chol_inv_batch(*S.ctx, S.scratch, jobs);
+  S.flops += (long long)tot * tot * tot / 3;
+  Factor f;
+  f.type = SGF_FACTOR_DENSE;
+  f.node = -1;
+  f.m = tot;
+  for (int c : rem) f.idx.insert(f.idx.end(), S.nodes[c].active.begin(), S.nodes[c].active.end());
+  f.L = D;
+  f.inv = X;
+  P->factors.push_back(std::move(f));
+}
+
+std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<LevelStats>& lv, int max_after,
+                       int max_seen, int final_dense, long long flops, long long flops_apply, long long peak,
+                       int nfactors, int b_used, const char* scheme_unused) {
+  (void)scheme_unused;
+  std::ostringstream o;
+  o << "{\"n\": " << n << ", \"levels\": " << lv.size() << ", \"per_level\": [";
+  for (size_t i = 0; i < lv.size(); ++i) {
+    if (i) o << ", ";
+    o << "{\"level\": " << lv[i].level << ", \"nodes\": " << lv[i].nodes << ", \"eliminated\": " << lv[i].eliminated
+      << ", \"compressed\": " << lv[i].compressed << ", \"ranks\": [";
+    for (size_t k = 0; k < lv[i].ranks.size(); ++k) o << (k ? ", " : "") << lv[i].ranks[k];
+    o << "]}";
+  }
+  o << "], \"max_node_size\": " << max_after << ", \"max_node_seen\": " << max_seen
+    << ", \"final_dense_size\": " << final_dense << ", \"flops_factorize\": " << flops
+    << ", \"flops_apply\": " << flops_apply << ", \"peak_blocks_bytes\": " << peak << ", \"factors\": " << nfactors
+    << "}";
+  (void)b_used;
+  (void)a;
+  return o.str();
+}
+
+}  // namespace
+
+Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
+  if (a.n <= 0 || a.nlevels <= 0 || !a.indptr || !a.indices || !a.values || !a.l1_ptr || !a.l1_unknowns)
+    fail(SGF_INVALID_ARG, "incomplete factorization arguments");
+  if (a.pi_cols <= 0 || !a.phi) fail(SGF_INVALID_ARG, "missing polynomial basis");
+  if (a.n > (int64_t)INT32_MAX) fail(SGF_INVALID_ARG, "n exceeds int32 index range");
+  std::unique_ptr<Precond> P(new Precond());
+  P->ctx = &ctx;
+  P->n = a.n;
+  P->store.set_stream(ctx.stream);
+  State S(ctx.stream);
+  S.ctx = &ctx;
+  S.st = ctx.stream;
+  S.a = &a;
+  S.pi = a.pi_cols;
+  S.P = P.get();
+  const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
+
+  setup_level1(S);
+  S.peak = 0;
+  std::vector<LevelStats> per_level;
+  int max_seen = 0, max_after = 0;
+  long long cell_off = 0, father_off = 0;
+  for (int t = 0; t < a.nlevels; ++t) {
+    const int ncell = a.level_ncells[t];
+    long long remaining = 0;
+    int maxsz = 0;
+    for (auto& nd : S.nodes) {
+      remaining += (long long)nd.active.size();
+      maxsz = std::max(maxsz, (int)nd.active.size());
+    }
+    if (remaining == 0) break;
+    if (t > 0 && remaining < max_seen) break;
+    if (ncell == 1) break;
+    max_seen = std::max(max_seen, maxsz);
+    LevelStats ls;
+    ls.level = t + 1;
+    ls.nodes = ncell;
+    std::vector<int> elim;
+    for (int c = 0; c < (int)S.nodes.size(); ++c)
+      if (S.nodes[c].interior && !S.nodes[c].active.empty()) elim.push_back(c);
+    eliminate_level(S, elim, t + 1);
+    ls.eliminated = (int)elim.size();
+    SGF_CUDA(cudaStreamSynchronize(S.st));
+    S.scratch.release();
+    if (compression && (t + 1) > a.skip_levels) {
+      std::vector<int> comp;
+      for (int c = 0; c < (int)S.nodes.size(); ++c)
+        if (kind_in(a.compress_kind_mask, S.nodes[c].kind) && !S.nodes[c].active.empty()) comp.push_back(c);
+      compress_level(S, comp, t + 1, ls);
+    }
+    for (auto& nd : S.nodes) max_after = std::max(max_after, (int)nd.active.size());
+    per_level.push_back(ls);
+    S.peak = std::max(S.peak, S.M.peak);
+    if (t + 1 < a.nlevels) {
+      const long long old_live = S.M.live;
+      cell_off += ncell;
+      merge_level(S, a.father + father_off, a.level_ncells[t + 1], a.cell_kind + cell_off,
+                  a.cell_interior + cell_off);
+      father_off += ncell;
+      S.peak = std::max(S.peak, old_live + S.M.live);
+    } else {
+      break;
+    }
+  }
+  size_t before = P->factors.size();
+  final_dense(S);
+  int final_size = 0;
+  if (P->factors.size() > before) {
+    final_size = P->factors.back().m;
+    S.peak = std::max(S.peak, S.M.peak);
+  }
+  if (a.mode == SGF_MODE_LOWRANK && S.comp_counter < a.n_trace) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "rank trace has %d unreplayed entries; first: [%d, %d, %d]", a.n_trace - S.comp_counter,
+             a.trace[3 * S.comp_counter], a.trace[3 * S.comp_counter + 1], a.trace[3 * S.comp_counter + 2]);
+    fail(SGF_TRACE, buf);
+  }
+  SGF_CUDA(cudaStreamSynchronize(S.st));
+  S.scratch.release();
+  S.lvl.reset();
+  long long fa = 0;
+  for (auto& f : P->factors) {
+    const long long m = f.m;
+    fa += (f.type == SGF_FACTOR_ELIMINATION) ? 4 * m * m + 4 * m * f.c : 4 * m * m;
+  }
+  P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
+                        (int)P->factors.size(), 0, nullptr);
+  P->plan = build_plan(P.get());
+  SGF_CUDA(cudaStreamSynchronize(S.st));
+  return P.release();
+}
+
+}  // namespace sgf

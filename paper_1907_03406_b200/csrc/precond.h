@@ -1,0 +1,60 @@
+// Device-resident preconditioner: the ordered elementary factors of the
+// reference (factorization.py:112-213) plus the level-batched apply plan.
+#pragma once
+#include <memory>
+
+#include "runtime.h"
+
+namespace sgf {
+
+struct Factor {
+  int type = 0;   // SGF_FACTOR_*
+  int node = -1;
+  int level = 0;  // 1-based level of the factorization pass (dense: levels+1)
+  int m = 0, c = 0, r = 0, steps = 0;
+  std::vector<int64_t> idx;   // node actives at factor time
+  std::vector<int64_t> nidx;  // elimination: stacked neighbour actives (sorted neighbour order)
+  double* L = nullptr;        // m x m lower (row-major)
+  double* inv = nullptr;      // m x m: L^{-1} (elim/dense) or Q^T L^{-1} (compression)
+  double* E = nullptr;        // c x m couplings E_N = A_NB L^{-T}, stacked
+  double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
+  double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
+  std::vector<int32_t> perm;  // compression: QR column permutation (first `steps` meaningful)
+  int ncols = 0;              // compression: columns of the rank basis N
+};
+
+struct ApplyPlan;
+void destroy_plan(ApplyPlan* p);
+ApplyPlan* build_plan(class Precond* P);
+
+class Precond {
+ public:
+  Ctx* ctx = nullptr;
+  int64_t n = 0;
+  std::vector<Factor> factors;
+  std::string stats;
+  std::vector<int32_t> trace;  // (level, node, rank) triples
+  Arena store;
+  ApplyPlan* plan = nullptr;
+  ~Precond() {
+    if (plan) destroy_plan(plan);
+  }
+};
+
+Precond* factorize(Ctx& ctx, const sgf_factor_args& a);
+void apply_op(Precond* P, int op, const double* d_x, double* d_y);
+
+struct Csr {
+  Ctx* ctx = nullptr;
+  int64_t n = 0, nnz = 0;
+  long long* rp = nullptr;
+  int* ci = nullptr;
+  double* v = nullptr;
+  int tpr = 8;
+  Arena mem;
+};
+void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b);
+void pcg(Ctx& ctx, Csr* A, Precond* P, const double* d_b, double* d_x, double tol, int maxit, int true_every,
+         sgf_pcg_report* rep, double* history);
+
+}  // namespace sgf

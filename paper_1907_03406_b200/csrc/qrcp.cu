@@ -1,0 +1,289 @@
+// Householder QR with column-norm pivoting, truncated at the numerical rank.
+//
+// Restates the pivot/reflector rules of the reference `pivoted_qr`
+// (densela.py:149-217):
+//   pivot      = first argmax of the downdated squared column norms (lowest
+//                index on exact ties), or the replayed column (parity mode);
+//   stop       when the pivot norm^2 <= floor^2 or ||x|| <= floor,
+//                floor = eps * max(max|A|, 1);
+//   reflector  sign = -sign(x0) (-1 for x0 == 0), u1 = x0 - sign*||x||,
+//              w = x / u1 (w0 = 1), tau = -sign*u1/||x||, R_kk = sign*||x||;
+//   downdate   norm2_j = max(norm2_j - R_kj^2, 0), recomputed from the
+//              column below row k when norm2_j <= eps * ref2_j.
+// The reference runs every step and counts rank = #{|R_ii| > tol |R_00|};
+// the first r steps of a pivoted QR do not depend on later ones, and
+// |R_ii| is non-increasing, so stopping at the first |R_kk| <= tol |R_00|
+// yields the same rank, pivots, R_1 and Q_1 while skipping min(m,c) - r steps.
+// Low-rank mode (forced rank r, factorization.py:331-339) runs exactly r steps.
+//
+// One CTA per compressed node; the m x c panel (column major) stays in
+// global memory / L2, the current reflector lives in shared memory.
+#include <cfloat>
+#include <cmath>
+
+#include "common.h"
+
+namespace sgf {
+
+constexpr int QR_THREADS = 512;
+constexpr int QR_WARPS = QR_THREADS / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double s = (l < QR_WARPS) ? red[l] : 0.0;
+    s = warp_sum(s);
+    if (l == 0) red[QR_WARPS] = s;
+  }
+  __syncthreads();
+  return red[QR_WARPS];
+}
+
+__device__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double s = (l < QR_WARPS) ? red[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (l == 0) red[QR_WARPS] = s;
+  }
+  __syncthreads();
+  return red[QR_WARPS];
+}
+
+// first index of the maximum of nrm2[k..c)
+__device__ int block_argmax(const double* nrm2, int k, int c, double* redv, int* redi) {
+  double bv = -1.0;
+  int bi = c;
+  for (int j = k + threadIdx.x; j < c; j += blockDim.x) {
+    double v = nrm2[j];
+    if (v > bv) { bv = v; bi = j; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { redv[w] = bv; redi[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    bv = (l < QR_WARPS) ? redv[l] : -1.0;
+    bi = (l < QR_WARPS) ? redi[l] : c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (l == 0) redi[QR_WARPS] = bi;
+  }
+  __syncthreads();
+  return redi[QR_WARPS];
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restrict__ tasks) {
+  extern __shared__ double v[];  // m
+  __shared__ double red[QR_WARPS + 1];
+  __shared__ double redv[QR_WARPS + 1];
+  __shared__ int redi[QR_WARPS + 1];
+  __shared__ int s_piv;
+  const QrTask T = tasks[blockIdx.x];
+  const int m = T.m, c = T.c, kmax = min(m, c);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* N = T.Nm;
+  const double eps = DBL_EPSILON;
+
+  for (int j = warp; j < c; j += QR_WARPS) {
+    const double* col = N + (long long)j * m;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(col[i], col[i], s);
+    s = warp_sum(s);
+    if (lane == 0) { T.nrm2[j] = s; T.ref2[j] = s; T.perm[j] = j; }
+  }
+  double amax = 0.0;
+  for (long long e = tid; e < (long long)m * c; e += QR_THREADS) amax = fmax(amax, fabs(N[e]));
+  amax = block_max(amax, red);
+  const double floor_ = eps * fmax(amax, 1.0);
+  const double floor2 = floor_ * floor_;
+  __syncthreads();
+
+  const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
+  int steps = 0, rank = 0;
+  double r00 = 0.0;
+  for (int k = 0; k < limit; ++k) {
+    int piv;
+    if (T.replay && k < T.nreplay) {
+      if (tid == 0) s_piv = -1;
+      __syncthreads();
+      const int want = T.replay[k];
+      for (int j = k + tid; j < c; j += QR_THREADS)
+        if (T.perm[j] == want) s_piv = j;
+      __syncthreads();
+      piv = s_piv;
+      if (piv < 0) piv = block_argmax(T.nrm2, k, c, redv, redi);  // malformed replay: fall back
+    } else {
+      piv = block_argmax(T.nrm2, k, c, redv, redi);
+    }
+    if (T.nrm2[piv] <= floor2) break;
+    if (piv != k) {
+      double* a = N + (long long)k * m;
+      double* b = N + (long long)piv * m;
+      for (int i = tid; i < m; i += QR_THREADS) { double tmp = a[i]; a[i] = b[i]; b[i] = tmp; }
+      __syncthreads();
+      if (tid == 0) {
+        double t2 = T.nrm2[k]; T.nrm2[k] = T.nrm2[piv]; T.nrm2[piv] = t2;
+        t2 = T.ref2[k]; T.ref2[k] = T.ref2[piv]; T.ref2[piv] = t2;
+        int ti = T.perm[k]; T.perm[k] = T.perm[piv]; T.perm[piv] = ti;
+      }
+    }
+    __syncthreads();
+    double* xk = N + (long long)k * m;
+    double ss = 0.0;
+    for (int i = k + tid; i < m; i += QR_THREADS) ss = fma(xk[i], xk[i], ss);
+    const double xn = sqrt(block_sum(ss, red));
+    if (xn <= floor_) break;
+    if (k == 0) r00 = xn;
+    if (T.forced_rank < 0 && !(xn > T.tol * r00)) break;  // rank reached
+    const double x0 = xk[k];
+    const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
+    const double u1 = x0 - sgn * xn;
+    const double tau = -sgn * u1 / xn;
+    for (int i = k + tid; i < m; i += QR_THREADS) v[i - k] = (i == k) ? 1.0 : xk[i] / u1;
+    __syncthreads();
+    const int len = m - k;
+    for (int j = k + 1 + warp; j < c; j += QR_WARPS) {
+      double* col = N + (long long)j * m + k;
+      double s = 0.0;
+      for (int i = lane; i < len; i += 32) s = fma(v[i], col[i], s);
+      s = warp_sum(s);
+      const double ts = tau * s;
+      double fresh = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        double nv = fma(-ts, v[i], col[i]);
+        col[i] = nv;
+        if (i > 0) fresh = fma(nv, nv, fresh);
+      }
+      fresh = warp_sum(fresh);
+      if (lane == 0) {
+        const double rkj = col[0];
+        double nn = fmax(T.nrm2[j] - rkj * rkj, 0.0);
+        if (nn <= eps * T.ref2[j]) {
+          nn = fresh;
+          T.ref2[j] = fmax(fresh, floor2);
+        }
+        T.nrm2[j] = nn;
+      }
+    }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < m; i += QR_THREADS) xk[i] = v[i - k];
+    if (tid == 0) { xk[k] = sgn * xn; T.tau[k] = tau; }
+    __syncthreads();
+    steps = k + 1;
+  }
+  if (T.forced_rank >= 0) rank = min(T.forced_rank, m);
+  else rank = steps;
+  if (tid == 0) { *T.out_rank = rank; *T.out_steps = steps; }
+}
+
+cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  size_t smem = (size_t)max_m * sizeof(double);
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Finish: explicit reflectors V (m x s, unit lower trapezoid, column major),
+// the compact-WY factor T (s x s upper, row major) with
+// H_0 ... H_{s-1} = I - V T V^T, and Q1 = H_0...H_{s-1} [I_r; 0] (m x r,
+// column major).  Q = H_0 ... H_{s-1} is the orthogonal completion used for
+// the compression factor; its first r columns are the reference's Q_1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(QR_THREADS) qr_finish_kernel(const QrFinishTask* __restrict__ tasks) {
+  const QrFinishTask F = tasks[blockIdx.x];
+  const int m = F.m, s = *F.steps, r = *F.rank;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // V
+  for (long long e = tid; e < (long long)m * s; e += QR_THREADS) {
+    const int k = (int)(e / m), i = (int)(e % m);
+    F.V[e] = (i < k) ? 0.0 : (i == k ? 1.0 : F.Nm[(long long)k * m + i]);
+  }
+  __syncthreads();
+  // gram G[a][b] = V[:,a] . V[:,b] for a < b (only rows >= b contribute)
+  double* G = F.G;  // s*s
+  for (int p = warp; p < s * s; p += QR_WARPS) {
+    const int a = p / s, b = p % s;
+    if (a >= b) continue;
+    const double* va = F.V + (long long)a * m;
+    const double* vb = F.V + (long long)b * m;
+    double acc = 0.0;
+    for (int i = b + lane; i < m; i += 32) acc = fma(va[i], vb[i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) G[a * s + b] = acc;
+  }
+  __syncthreads();
+  // T recurrence (LAPACK larft, forward, columnwise)
+  for (int k = 0; k < s; ++k) {
+    const double tk = F.tau[k];
+    // w[a] = sum_{b<k} T[a][b] * G[b][k], a < k   (T upper)
+    for (int a = tid; a < k; a += QR_THREADS) {
+      double acc = 0.0;
+      for (int b = a; b < k; ++b) acc = fma(F.Tm[(long long)a * s + b], G[b * s + k], acc);
+      F.Tm[(long long)a * s + k] = -tk * acc;
+    }
+    if (tid == 0) F.Tm[(long long)k * s + k] = tk;
+    for (int a = k + 1 + tid; a < s; a += QR_THREADS) F.Tm[(long long)a * s + k] = 0.0;
+    __syncthreads();
+  }
+  // Q1: start from [I_r; 0], apply H_k for k = min(s,r)-1 .. 0
+  for (long long e = tid; e < (long long)m * r; e += QR_THREADS) {
+    const int j = (int)(e / m), i = (int)(e % m);
+    F.Q1[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int sr = min(s, r);
+  for (int k = sr - 1; k >= 0; --k) {
+    const double* vk = F.V + (long long)k * m;
+    const double tk = F.tau[k];
+    for (int j = k + warp; j < r; j += QR_WARPS) {
+      double* q = F.Q1 + (long long)j * m;
+      double acc = 0.0;
+      for (int i = k + lane; i < m; i += 32) acc = fma(vk[i], q[i], acc);
+      acc = warp_sum(acc) * tk;
+      for (int i = k + lane; i < m; i += 32) q[i] = fma(-acc, vk[i], q[i]);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  qr_finish_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  return cudaGetLastError();
+}
+
+}  // namespace sgf

@@ -1,0 +1,188 @@
+// Runtime utilities: arena allocator, batched launch builders, and the
+// batched blocked Cholesky + explicit inverse used by elimination,
+// compression and the final dense factor.
+#include "runtime.h"
+
+#include <cstdio>
+
+namespace sgf {
+
+void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  int st = (e == cudaErrorMemoryAllocation) ? SGF_OOM : SGF_CUDA;
+  fail(st, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what);
+}
+
+void* Arena::alloc_bytes(size_t bytes) {
+  bytes = (bytes + 255) & ~(size_t)255;
+  if (bytes == 0) bytes = 256;
+  for (auto& c : chunks_) {
+    if (c.cap - c.off >= bytes) {
+      void* p = c.base + c.off;
+      c.off += bytes;
+      used_ += bytes;
+      return p;
+    }
+  }
+  size_t cap = std::max(bytes, chunk_);
+  void* p = nullptr;
+  SGF_CUDA(cudaMallocAsync(&p, cap, s_));
+  chunks_.push_back(Chunk{(char*)p, cap, bytes});
+  used_ += bytes;
+  return p;
+}
+
+void Arena::release() {
+  for (auto& c : chunks_) cudaFreeAsync(c.base, s_);
+  chunks_.clear();
+  used_ = 0;
+}
+
+void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
+  if (empty()) return;
+  GemmSeg* d_segs = scratch.upload(segs);
+  if (!big.empty()) {
+    GemmTask* d = scratch.upload(big);
+    SGF_CUDA(launch_gemm(d, (int)big.size(), d_segs, 1, st));
+  }
+  if (!small.empty()) {
+    GemmTask* d = scratch.upload(small);
+    SGF_CUDA(launch_gemm(d, (int)small.size(), d_segs, 0, st));
+  }
+}
+
+void CopyBatch::launch(Arena& scratch, cudaStream_t st) {
+  if (tasks.empty()) return;
+  std::vector<long long> prefix(tasks.size());
+  long long tot = 0;
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    prefix[i] = tot;
+    tot += (long long)((tasks[i].rows + 31) / 32) * ((tasks[i].cols + 31) / 32);
+  }
+  CopyTask* d_t = scratch.upload(tasks);
+  long long* d_p = scratch.upload(prefix);
+  SGF_CUDA(launch_copy_tiled(d_t, d_p, (int)tasks.size(), tot, st));
+}
+
+void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tasks) {
+  if (tasks.empty()) return;
+  std::vector<long long> prefix(tasks.size());
+  long long tot = 0;
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    prefix[i] = tot;
+    long long t = (tasks[i].m + 31) / 32;
+    tot += t * t;
+  }
+  TriTask* d_t = scratch.upload(tasks);
+  long long* d_p = scratch.upload(prefix);
+  SGF_CUDA(launch_zero_upper(d_t, d_p, (int)tasks.size(), tot, st));
+}
+
+// ---------------------------------------------------------------------------
+// Blocked left-looking Cholesky with the inverse built alongside.
+// Per 64-column panel k (all jobs with m > k0 batched in each launch):
+//   A: W[k0:, k]   -= L[k0:, :k0] L[k, :k0]^T            (panel update)
+//      T_k          = L[k, :k0] X[:k0, :k0]               (inverse, part 1)
+//   B: L_kk = chol(W_kk), D_k = L_kk^{-1}, X_kk = D_k    (diag tile, pivot check)
+//   C: L[k1:, k]    = W[k1:, k] D_k^T                     (panel solve)
+//      X[k, :k0]    = -D_k T_k                            (inverse, part 2)
+// The breakdown rule is the reference's (densela.py:105-110).
+// ---------------------------------------------------------------------------
+void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
+  if (jobs.empty()) return;
+  cudaStream_t st = ctx.stream;
+  const int nj = (int)jobs.size();
+  std::vector<const double*> wp(nj);
+  std::vector<int> ms(nj);
+  int mmax = 0;
+  for (int i = 0; i < nj; ++i) {
+    wp[i] = jobs[i].W;
+    ms[i] = jobs[i].m;
+    mmax = std::max(mmax, jobs[i].m);
+  }
+  double* d_floor = scratch.alloc(nj);
+  {
+    const double** d_wp = scratch.upload(wp);
+    int* d_m = scratch.upload(ms);
+    SGF_CUDA(launch_max_diag(d_wp, d_m, d_m, nj, d_floor, st));
+  }
+  std::vector<double> floors(nj);
+  SGF_CUDA(cudaMemcpyAsync(floors.data(), d_floor, nj * sizeof(double), cudaMemcpyDeviceToHost, st));
+  int* d_status = scratch.alloc_t<int>(nj);
+  double* d_piv = scratch.alloc(nj);
+  SGF_CUDA(cudaMemsetAsync(d_status, 0, nj * sizeof(int), st));
+  std::vector<double*> dinv(nj), tk(nj);
+  for (int i = 0; i < nj; ++i) {
+    dinv[i] = scratch.alloc(64 * 64);
+    tk[i] = scratch.alloc((size_t)64 * std::max(jobs[i].m, 1));
+  }
+  SGF_CUDA(cudaStreamSynchronize(st));  // floors
+
+  for (int k0 = 0; k0 < mmax; k0 += 64) {
+    GemmBatch ga, gc;
+    std::vector<DiagTask> dt;
+    std::vector<double*> xd;
+    std::vector<int> xl;
+    for (int i = 0; i < nj; ++i) {
+      const int m = jobs[i].m;
+      if (m <= k0) continue;
+      double* W = jobs[i].W;
+      double* X = jobs[i].X;
+      const int nb = std::min(64, m - k0), k1 = k0 + nb;
+      if (k0 > 0) {
+        // A: panel update and T_k
+        ga.add(W + (long long)k0 * m + k0, m, 1, m - k0, nb, -1.0, 1.0,
+               {seg(W + (long long)k0 * m, m, 1, W + (long long)k0 * m, m, 1, k0)});
+        ga.add(tk[i], m, 1, nb, k0, 1.0, 0.0,
+               {seg(W + (long long)k0 * m, m, 1, X, 1, m, k0, SEG_KSTART_N)}, 0);
+      }
+      DiagTask d;
+      d.W = W;
+      d.Dinv = dinv[i];
+      d.ld = m;
+      d.k0 = k0;
+      d.nb = nb;
+      d.floor = floors[i];
+      d.node = i;
+      dt.push_back(d);
+      xd.push_back(X);
+      xl.push_back(m);
+      if (m > k1)
+        gc.add(W + (long long)k1 * m + k0, m, 1, m - k1, nb, 1.0, 0.0,
+               {seg(W + (long long)k1 * m + k0, m, 1, dinv[i], 64, 1, nb, SEG_KLIM_N)}, 0);
+      if (k0 > 0)
+        gc.add(X + (long long)k0 * m, m, 1, nb, k0, -1.0, 0.0,
+               {seg(dinv[i], 64, 1, tk[i], 1, m, nb, SEG_KLIM_M)}, 0);
+    }
+    ga.launch(scratch, st);
+    {
+      DiagTask* d_dt = scratch.upload(dt);
+      double** d_xd = scratch.upload(xd);
+      int* d_xl = scratch.upload(xl);
+      SGF_CUDA(launch_diag_chol_ex(d_dt, (int)dt.size(), d_status, d_piv, d_xd, d_xl, st));
+    }
+    gc.launch(scratch, st);
+  }
+  std::vector<TriTask> tri;
+  for (auto& j : jobs) tri.push_back(TriTask{j.W, j.m, j.m});
+  zero_upper(scratch, st, tri);
+
+  std::vector<int> status(nj);
+  std::vector<double> piv(nj);
+  SGF_CUDA(cudaMemcpyAsync(status.data(), d_status, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaMemcpyAsync(piv.data(), d_piv, nj * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaStreamSynchronize(st));
+  int worst = -1;
+  for (int i = 0; i < nj; ++i)
+    if (status[i] != 0 && (worst < 0 || jobs[i].node < jobs[worst].node)) worst = i;
+  if (worst >= 0) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "non-positive pivot %.3e at index %d (node %d)", piv[worst], status[worst] - 1,
+             jobs[worst].node);
+    fail(SGF_NOT_SPD, buf);
+  }
+}
+
+}  // namespace sgf

@@ -1,0 +1,255 @@
+// Host runtime of the sgf library: context, device arenas, block table,
+// batched-launch builders.  The factorization driver (factorize.cpp), the
+// apply plan (apply.cpp) and the C ABI (capi.cpp) build on this.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "common.h"
+#include "sgf.h"
+
+namespace sgf {
+
+struct Error {
+  int status;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int status, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define SGF_CUDA(x) ::sgf::cuda_check((x), #x)
+
+// extra launchers (defined in .cu files, not in common.h)
+cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
+                                double* const* d_xdiag, const int* d_ldx, cudaStream_t s);
+cudaError_t launch_copy_tiled(const CopyTask* d_tasks, const long long* d_prefix, int ntasks, long long ntiles,
+                              cudaStream_t s);
+cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, int ntasks, long long ntiles,
+                              cudaStream_t s);
+cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
+cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, cudaStream_t s);
+cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s);
+cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
+cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s);
+cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
+                           long long nt, cudaStream_t s);
+cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double* v, const double* x, double* y,
+                        const double* b, int tpr, cudaStream_t s);
+cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
+                       cudaStream_t s);
+cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
+                             double* part, double* out, int slot, cudaStream_t s);
+cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s);
+
+
+// ---------------------------------------------------------------------------
+// Device bump arena (stream-ordered chunks from the CUDA memory pool).
+// ---------------------------------------------------------------------------
+class Arena {
+ public:
+  explicit Arena(cudaStream_t s = nullptr, size_t chunk = (size_t)256 << 20) : s_(s), chunk_(chunk) {}
+  ~Arena() { release(); }
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  void set_stream(cudaStream_t s) { s_ = s; }
+  void* alloc_bytes(size_t bytes);
+  double* alloc(size_t n) { return (double*)alloc_bytes(n * sizeof(double)); }
+  template <class T>
+  T* alloc_t(size_t n) { return (T*)alloc_bytes(n * sizeof(T)); }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    T* d = alloc_t<T>(v.size());
+    SGF_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s_));
+    return d;
+  }
+  void release();
+  size_t used() const { return used_; }
+
+ private:
+  struct Chunk { char* base; size_t cap; size_t off; };
+  cudaStream_t s_;
+  size_t chunk_;
+  std::vector<Chunk> chunks_;
+  size_t used_ = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+};
+
+// ---------------------------------------------------------------------------
+// Block table: symmetric block-sparse trailing matrix, blocks (a,b) a <= b,
+// row-major rows = size[a], cols = size[b] (reference blockmatrix.py:14-83,
+// including its live/peak byte accounting :25-43).
+// ---------------------------------------------------------------------------
+struct Blk {
+  double* p;
+  int rows, cols;
+};
+
+inline uint64_t bkey(int a, int b) {
+  if (a > b) std::swap(a, b);
+  return ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
+}
+
+struct BlockTable {
+  std::unordered_map<uint64_t, Blk> map;
+  std::vector<std::vector<int>> adj;
+  std::vector<int> size;
+  long long live = 0, peak = 0;
+
+  void init(const std::vector<int>& sizes) {
+    size = sizes;
+    adj.assign(sizes.size(), {});
+    map.clear();
+    map.reserve(sizes.size() * 8);
+    live = peak = 0;
+  }
+  static long long nbytes(const Blk& b) { return 8LL * b.rows * b.cols; }
+  Blk* find(int a, int b) {
+    auto it = map.find(bkey(a, b));
+    return it == map.end() ? nullptr : &it->second;
+  }
+  void insert(int a, int b, Blk blk) {
+    uint64_t k = bkey(a, b);
+    auto it = map.find(k);
+    if (it != map.end()) live -= nbytes(it->second);
+    map[k] = blk;
+    live += nbytes(blk);
+    peak = std::max(peak, live);
+    if (a != b) {
+      add_adj(a, b);
+      add_adj(b, a);
+    }
+  }
+  void add_adj(int a, int b) {
+    auto& v = adj[a];
+    if (std::find(v.begin(), v.end(), b) == v.end()) v.push_back(b);
+  }
+  void drop(int a) {
+    for (int b : adj[a]) {
+      auto it = map.find(bkey(a, b));
+      if (it != map.end()) {
+        live -= nbytes(it->second);
+        map.erase(it);
+      }
+      auto& v = adj[b];
+      v.erase(std::remove(v.begin(), v.end(), a), v.end());
+    }
+    adj[a].clear();
+    auto it = map.find(bkey(a, a));
+    if (it != map.end()) {
+      live -= nbytes(it->second);
+      map.erase(it);
+    }
+  }
+  std::vector<int> nbrs(int a) const {
+    std::vector<int> v = adj[a];
+    std::sort(v.begin(), v.end());
+    return v;
+  }
+};
+
+// operand view of block (a,b) as the matrix with rows in a, cols in b
+struct View {
+  const double* p;
+  long long rs, cs;
+  int rows, cols;
+};
+inline View view_of(BlockTable& M, int a, int b) {
+  Blk* blk = M.find(a, b);
+  if (!blk) fail(SGF_INVALID_ARG, "internal: missing block");
+  if (a <= b) return View{blk->p, (long long)blk->cols, 1, blk->rows, blk->cols};
+  return View{blk->p, 1, (long long)blk->cols, blk->cols, blk->rows};
+}
+
+// ---------------------------------------------------------------------------
+// Batched launch builders
+// ---------------------------------------------------------------------------
+struct GemmBatch {
+  std::vector<GemmTask> big, small;
+  std::vector<GemmSeg> segs;
+  long long flops = 0;  // executed flops (information)
+
+  // add all tiles of C(MxN) = beta*C + alpha * sum(segs)
+  void add(double* C, long long c_rs, long long c_cs, int M, int N, double alpha, double beta,
+           const std::vector<GemmSeg>& sg, int force = -1) {
+    if (M <= 0 || N <= 0) return;
+    int seg0 = (int)segs.size();
+    for (auto& s : sg) segs.push_back(s);
+    bool use_big = force >= 0 ? force == 1 : (M >= 96 && N >= 96);
+    int bm = use_big ? 128 : 64, bn = bm;
+    auto& dst = use_big ? big : small;
+    for (int m0 = 0; m0 < M; m0 += bm)
+      for (int n0 = 0; n0 < N; n0 += bn) {
+        GemmTask t;
+        t.C = C;
+        t.c_rs = c_rs;
+        t.c_cs = c_cs;
+        t.M = M;
+        t.N = N;
+        t.m0 = m0;
+        t.n0 = n0;
+        t.seg0 = seg0;
+        t.nseg = (int)sg.size();
+        t.alpha = alpha;
+        t.beta = beta;
+        dst.push_back(t);
+      }
+    for (auto& s : sg) flops += 2LL * M * N * s.K;
+  }
+  bool empty() const { return big.empty() && small.empty(); }
+  void launch(Arena& scratch, cudaStream_t st);
+  void clear() {
+    big.clear();
+    small.clear();
+    segs.clear();
+  }
+};
+
+inline GemmSeg seg(const double* A, long long a_rs, long long a_ks, const double* B, long long b_rs, long long b_ks,
+                   int K, int flags = 0) {
+  GemmSeg s;
+  s.A = A;
+  s.B = B;
+  s.a_rs = a_rs;
+  s.a_ks = a_ks;
+  s.b_rs = b_rs;
+  s.b_ks = b_ks;
+  s.K = K;
+  s.flags = flags;
+  return s;
+}
+
+struct CopyBatch {
+  std::vector<CopyTask> tasks;
+  void add(const double* src, long long s_rs, long long s_cs, double* dst, long long d_rs, long long d_cs, int rows,
+           int cols) {
+    if (rows <= 0 || cols <= 0) return;
+    CopyTask t{src, dst, s_rs, s_cs, d_rs, d_cs, rows, cols};
+    tasks.push_back(t);
+  }
+  void launch(Arena& scratch, cudaStream_t st);
+};
+
+void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tasks);
+
+// Cholesky + explicit inverse of a batch of SPD matrices (W holds A on entry
+// and L on exit; X must be zero on entry and holds L^{-1} on exit).
+struct CholJob {
+  double* W;
+  double* X;
+  int m;
+  int node;  // for error messages
+};
+void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs);
+
+}  // namespace sgf

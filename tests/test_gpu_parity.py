@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden fixtures and the CPU oracle.  Gates:
+  bit-exact   hierarchy (host, test_partition_host.py), rank trace, stats
+              (flop tally, per-level ranks, peak bytes), factor index sets;
+  <= 1e-10    factor entries, apply_inverse, PCG residual history (all but
+              the final rounding-floor entry) under QR pivot replay;
+  +-1         PCG iterations free-running."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import Golden, golden_names
+
+pytestmark = pytest.mark.gpu
+
+sgf = pytest.importorskip("paper_1907_03406_b200")
+
+FULL = [n for n in golden_names(full=False)]
+WITH_FACTORS = ["p3d9_exact", "p3d12_b3", "p3d10_deg2", "p2d32_b5", "elast3", "p3d9_gen_d1"]
+TOL = 1e-10
+
+
+def run(g, replay=True, **kw):
+    opts = dict(g.opts)
+    opts.update(kw)
+    return sgf.factorize(g.problem(), replay_perms=g.perms() if replay else None, **opts)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_structure_stats_apply(name):
+    g = Golden(name)
+    P = run(g)
+    assert P.stats == g.stats
+    assert [tuple(e) for e in P.rank_trace.entries] == g.trace()
+    y = P.apply_inverse(g["rhs"])
+    assert rel(y, g["apply_inverse"]) <= TOL, rel(y, g["apply_inverse"])
+
+
+@pytest.mark.parametrize("name", WITH_FACTORS)
+def test_factor_entries(name):
+    g = Golden(name)
+    P = run(g)
+    assert len(P.factors) == int(g["nfactors"])
+    for k, f in enumerate(P.factors):
+        assert f.kind == str(g[f"f{k}_type"])
+        assert np.array_equal(f.idx, g[f"f{k}_idx"])
+        L = g[f"f{k}_L"]
+        assert np.abs(f.L - L).max() <= TOL * max(np.abs(L).max(), 1.0)
+        if f.kind == "EliminationFactor" and len(g[f"f{k}_Eidx"]):
+            (nidx, E), = f.couplings
+            assert np.array_equal(nidx, g[f"f{k}_Eidx"])
+            assert np.abs(E - g[f"f{k}_E"]).max() <= TOL * max(np.abs(E).max(), 1.0)
+        if f.kind == "CompressionFactor":
+            r = f.retained
+            assert r == int(g[f"f{k}_r"])
+            Q = f.Q
+            assert np.abs(Q.T @ Q - np.eye(len(Q))).max() <= 1e-12
+            assert np.abs(Q[:, :r] - g[f"f{k}_Q"][:, :r]).max() <= TOL
+
+
+@pytest.mark.parametrize("name", [n for n in FULL if n not in ("p3d40_b9",)])
+def test_pcg_history(name):
+    g = Golden(name)
+    P = run(g)
+    x, rep = sgf.pcg(g.matrix(), g["rhs"], precond=P.apply_inverse, tol=1e-12)
+    assert abs(rep.iterations - int(g["pcg_iters"])) <= 1
+    h = np.array(rep.residual_history)
+    ref = g["pcg_hist"]
+    k = min(len(h), len(ref)) - 1
+    assert np.all(np.abs(h[:k] - ref[:k]) <= TOL * ref[:k] + 1e-15), np.abs(h[:k] - ref[:k]) / ref[:k]
+    assert rep.converged and rep.final_rel_residual <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["cfg1", "p3d12_b3", "aniso14", "tpfa12", "p3d40_b9"])
+def test_free_running_iterations(name):
+    g = Golden(name)
+    P = run(g, replay=False)
+    assert [tuple(e) for e in P.rank_trace.entries] == g.trace()
+    x, rep = sgf.pcg(g.matrix(), g["rhs"], precond=P, tol=1e-12)
+    assert abs(rep.iterations - int(g["pcg_iters"])) <= 1
+
+
+def test_cfg2_full_size():
+    """BASELINE config 2 (3-D Poisson 64^3, b = 9, rank_tol 1e-2)."""
+    from paper_1907_03406_b200.problems import CONFIGS, config_rhs
+    g = Golden("cfg2")
+    prob = CONFIGS[2]["make"]()
+    P = sgf.factorize(prob, replay_perms=g.perms(), **g.opts)
+    assert P.stats == g.stats
+    assert [tuple(e) for e in P.rank_trace.entries] == g.trace()
+    rhs = config_rhs(prob.n, 1)
+    assert np.array_equal(rhs, g["rhs"])
+    assert rel(P.apply_inverse(rhs), g["apply_inverse"]) <= TOL
+    x, rep = sgf.pcg(prob.matrix, rhs, precond=P, tol=1e-12)
+    assert rep.iterations == int(g["pcg_iters"])
+    Pf = sgf.factorize(prob, **g.opts)
+    x, rep = sgf.pcg(prob.matrix, rhs, precond=Pf, tol=1e-12)
+    assert abs(rep.iterations - int(g["pcg_iters"])) <= 1
+
+
+def test_determinism_bitwise():
+    g = Golden("p3d12_b3")
+    P1, P2 = run(g, replay=False), run(g, replay=False)
+    x = np.random.default_rng(4).standard_normal(g.n)
+    assert np.array_equal(P1.apply_inverse(x), P2.apply_inverse(x))
+    x1, r1 = sgf.pcg(g.matrix(), g["rhs"], precond=P1, tol=1e-12)
+    x2, r2 = sgf.pcg(g.matrix(), g["rhs"], precond=P2, tol=1e-12)
+    assert r1.residual_history == r2.residual_history and np.array_equal(x1, x2)
+
+
+def test_lowrank_replay():
+    g = Golden("p3d9_gen")
+    P = run(g)
+    L = sgf.factorize(g.problem(), mode="lowrank", rank_trace=P.rank_trace,
+                      **{k: v for k, v in g.opts.items() if k != "mode"})
+    assert rel(L.apply_inverse(g["rhs"]), g["lowrank_apply_inverse"]) <= 1e-8
+    bad = sgf.RankTrace(P.rank_trace.entries[:-1])
+    with pytest.raises(RuntimeError):
+        sgf.factorize(g.problem(), mode="lowrank", rank_trace=bad, **{k: v for k, v in g.opts.items() if k != "mode"})
+
+
+def test_errors_map_to_reference_exceptions():
+    prob = sgf.poisson7(6)
+    neg = sgf.ProblemInstance(-prob.matrix, prob.coords, prob.grid, 1, prob.rhs, "neg")
+    with pytest.raises(sgf.NotSPDError):
+        sgf.factorize(neg)
+    P = sgf.factorize(prob)
+    with pytest.raises(sgf.ShapeMismatchError):
+        P.apply_inverse(np.ones(prob.n + 1))
+    with pytest.raises(ValueError):
+        sgf.factorize(prob, scheme="bogus")
+    with pytest.raises(ValueError):
+        sgf.factorize(prob, mode="lowrank")
+    with pytest.raises(sgf.IndefiniteDetectedError):
+        sgf.pcg(-prob.matrix, np.ones(prob.n), precond=None, tol=1e-10)
+
+
+def test_pcg_edge_cases():
+    prob = sgf.poisson7(7)
+    P = sgf.factorize(prob, mode="exact")
+    x, rep = sgf.pcg(prob.matrix, np.zeros(prob.n), precond=P)
+    assert rep.iterations == 0 and rep.residual_history == [0.0] and not x.any()
+    b = np.random.default_rng(1).uniform(-1, 1, prob.n)
+    x, rep = sgf.pcg(prob.matrix, b, precond=P, tol=1e-10)
+    assert rep.iterations <= 2
+    assert np.linalg.norm(x - sp.linalg.spsolve(prob.matrix.tocsc(), b)) <= 1e-8 * np.linalg.norm(x)
+    x, rep = sgf.pcg(sp.identity(50, format="csr"), np.ones(50), tol=1e-12)
+    assert rep.iterations == 1
+    x, rep = sgf.pcg(prob.matrix, b, tol=1e-14, maxit=3)
+    assert rep.iterations == 3 and not rep.converged and len(rep.residual_history) == 4
+
+
+def test_device_tensor_apply():
+    import torch
+    g = Golden("p2d32_b5")
+    P = run(g)
+    x = torch.tensor(g["rhs"], device="cuda")
+    y = P.apply_inverse(x)
+    assert y.is_cuda
+    assert rel(y.cpu().numpy(), g["apply_inverse"]) <= TOL
