@@ -190,7 +190,11 @@ def run_case(name, prob, opts, store_factors=False, pcg_tol=1e-12, rhs_seed=0, l
                 "indptr", "indices", "data", "coords", "apply_operator", "half_inverse", "pcg_x"]:
             d.pop(k, None)
     if lowrank:
+        _perms.clear()
         Pl = pp.factorize(prob, **dict(opts, mode="lowrank"), rank_trace=P.rank_trace)
+        lp = list(_perms)
+        d["lowrank_perm_ptr"] = np.cumsum([0] + [len(p) for p in lp]).astype(np.int64)
+        d["lowrank_perm_all"] = np.concatenate(lp) if lp else np.zeros(0, np.int64)
         d["lowrank_apply_inverse"] = Pl.apply_inverse(rhs)
         d["lowrank_stats"] = json.dumps(Pl.stats)
     path = os.path.join(HERE, f"{name}.npz")
