@@ -139,6 +139,14 @@ int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device);
 int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x, double tol, int maxit,
             int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
 
+/* instrumentation (no reference counterpart): kernels launched so far, and
+   per-kernel-class CUDA-event timing.  Classes: 0 GEMM (work = flops),
+   1 GEMV (bytes), 2 SpMV (bytes), 3 QR, 4 diagonal Cholesky, 5 copies (bytes),
+   6 vector ops.  out[3*cls + 0..2] = milliseconds, work, launches. */
+uint64_t sgf_kernel_launches(void);
+int sgf_profile_enable(int on);
+int sgf_profile_read(double* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,9 @@ EXPORTS = (
     "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
     "sgf_precond_num_factors", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg",
+    "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read",
 )
+PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec")
 
 
 class NativeUnavailable(RuntimeError):
@@ -93,6 +95,9 @@ def load_library(path=LIB_PATH):
             "sgf_csr_free": (i32, [vp]),
             "sgf_spmv": (i32, [vp, vp, vp, i32]),
             "sgf_pcg": (i32, [vp, vp, vp, vp, vp, d, i32, i32, i32, C.POINTER(PcgReport), vp]),
+            "sgf_kernel_launches": (C.c_uint64, []),
+            "sgf_profile_enable": (i32, [i32]),
+            "sgf_profile_read": (i32, [vp, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -138,6 +143,22 @@ def context(device=0):
     with _lock:
         _ctx[device] = h
     return h
+
+
+def kernel_launches():
+    return int(lib().sgf_kernel_launches())
+
+
+def profile_enable(on=True):
+    lib().sgf_profile_enable(1 if on else 0)
+
+
+def profile_read():
+    """{class: (ms, work, launches)} accumulated since profile_enable()."""
+    out = np.zeros(3 * len(PROF_CLASSES))
+    st = lib().sgf_profile_read(out.ctypes.data, len(out))
+    raise_for(st, None)
+    return {c: tuple(out[3 * i:3 * i + 3]) for i, c in enumerate(PROF_CLASSES)}
 
 
 def ptr(a):

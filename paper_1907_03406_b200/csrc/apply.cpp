@@ -42,7 +42,23 @@ struct Group {
   int nb2 = 0;
   RedSeg* red2 = nullptr;
   int nred2 = 0, maxn2 = 0;
+  double bytes_f1 = 0, bytes_f2 = 0, bytes_b1 = 0, bytes_b2 = 0;  // matrix bytes streamed
 };
+
+// algorithmic bytes of the matrix entries a GEMV task list reads
+static double gemv_bytes(const std::vector<GemvTask>& v, int mode) {
+  double b = 0.0;
+  for (const auto& t : v) {
+    if (!t.tri) {
+      b += 8.0 * (t.r1 - t.r0) * (t.c1 - t.c0);
+    } else if (mode == 0) {
+      for (int i = t.r0; i < t.r1; ++i) b += 8.0 * std::max(0, std::min(t.c1, i + 1) - t.c0);
+    } else {
+      for (int k = t.c0; k < t.c1; ++k) b += 8.0 * std::max(0, t.r1 - std::max(t.r0, k));
+    }
+  }
+  return b;
+}
 
 struct ApplyPlan {
   Arena mem;
@@ -166,6 +182,10 @@ ApplyPlan* build_plan(Precond* P) {
     g.nc = oc;
     g.idx = plan->mem.upload(idx);
     g.nidx = plan->mem.upload(nidx);
+    g.bytes_f1 = gemv_bytes(f1, 0);
+    g.bytes_f2 = gemv_bytes(f2, 0);
+    g.bytes_b1 = gemv_bytes(b1, 1);
+    g.bytes_b2 = gemv_bytes(b2, 1);
     g.fwd1 = plan->mem.upload(f1);
     g.nf1 = (int)f1.size();
     g.fwd2 = plan->mem.upload(f2);
@@ -203,10 +223,15 @@ ApplyPlan* build_plan(Precond* P) {
   return plan;
 }
 
+static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t st) {
+  ProfScope ps(st, PROF_GEMV, bytes);
+  SGF_CUDA(launch_gemv(t, nt, mode, st));
+}
+
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
   SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
-  SGF_CUDA(launch_gemv(g.fwd1, g.nf1, 0, st));
-  if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_gemv(g.fwd2, g.nf2, 0, st));
+  gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st);
+  if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, 0, g.bytes_f2, st);
   SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, pl->t, g.ntgt, st));
 }
@@ -215,12 +240,12 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
   SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) {
     SGF_CUDA(launch_gather(y, g.nidx, pl->xn, g.nc, st));
-    SGF_CUDA(launch_gemv(g.bwd1, g.nb1, 1, st));
+    gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
-    SGF_CUDA(launch_gemv(g.bwd2, g.nb2, 1, st));
+    gemv(g.bwd2, g.nb2, 1, g.bytes_b2, st);
     SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st));
   } else {
-    SGF_CUDA(launch_gemv(g.bwd1, g.nb1, 1, st));
+    gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
   }
   SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
@@ -240,6 +265,8 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
 
 // ---------------------------------------------------------------------------
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
+  // values + int32 columns + int64 row pointers + x + y (+ b)
+  ProfScope ps(A->ctx->stream, PROF_SPMV, 12.0 * A->nnz + 8.0 * (A->n + 1) + (d_b ? 24.0 : 16.0) * A->n);
   SGF_CUDA(launch_spmv((int)A->n, A->rp, A->ci, A->v, d_x, d_y, d_b, A->tpr, A->ctx->stream));
 }
 

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) gemv_t_kernel(const GemvTask* __restrict_
 
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
+  count_launch();
   if (mode == 0) gemv_n_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
   else gemv_t_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
   return cudaGetLastError();
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const RedSeg* __restr
 cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s) {
   if (nseg <= 0 || max_n <= 0) return cudaSuccess;
   dim3 grid((max_n + 255) / 256, nseg);
-  reduce_parts_kernel<<<grid, 256, 0, s>>>((const RedSeg*)d_segs);
+  count_launch(); reduce_parts_kernel<<<grid, 256, 0, s>>>((const RedSeg*)d_segs);
   return cudaGetLastError();
 }
 
@@ -116,18 +117,18 @@ static inline unsigned grid_for(long long n) {
 
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  gather_kernel<<<grid_for(n), 256, 0, s>>>(x, idx, out, n);
+  count_launch(); gather_kernel<<<grid_for(n), 256, 0, s>>>(x, idx, out, n);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  scatter_kernel<<<grid_for(n), 256, 0, s>>>(v, idx, x, n);
+  count_launch(); scatter_kernel<<<grid_for(n), 256, 0, s>>>(v, idx, x, n);
   return cudaGetLastError();
 }
 cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
                            long long nt, cudaStream_t s) {
   if (nt <= 0) return cudaSuccess;
-  combine_kernel<<<grid_for(nt), 256, 0, s>>>(x, tgt, ptr, pos, t, nt);
+  count_launch(); combine_kernel<<<grid_for(nt), 256, 0, s>>>(x, tgt, ptr, pos, t, nt);
   return cudaGetLastError();
 }
 
@@ -164,10 +165,10 @@ cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double*
   long long blocks = (threads + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   switch (tpr) {
-    case 4: spmv_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    case 8: spmv_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    case 16: spmv_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    default: spmv_kernel<32><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    case 4: count_launch(); spmv_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    case 8: count_launch(); spmv_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    case 16: count_launch(); spmv_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
+    default: count_launch(); spmv_kernel<32><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
   }
   return cudaGetLastError();
 }
@@ -235,18 +236,18 @@ __global__ void __launch_bounds__(256) p_update_kernel(double* __restrict__ p, c
 
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s) {
-  dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part);
-  finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+  count_launch(); dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part);
+  count_launch(); finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
   return cudaGetLastError();
 }
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
                              double* part, double* out, int slot, cudaStream_t s) {
-  xr_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(x, r, p, q, n, sc, part);
-  finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+  count_launch(); xr_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(x, r, p, q, n, sc, part);
+  count_launch(); finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
   return cudaGetLastError();
 }
 cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s) {
-  p_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(p, z, n, sc);
+  count_launch(); p_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(p, z, n, sc);
   return cudaGetLastError();
 }
 

@@ -222,6 +222,20 @@ int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device)
   });
 }
 
+uint64_t sgf_kernel_launches(void) { return g_kernel_launches; }
+
+int sgf_profile_enable(int on) {
+  g_prof.reset();
+  g_prof.on = on != 0;
+  return SGF_OK;
+}
+
+int sgf_profile_read(double* out, int cap) {
+  if (!out || cap < 3 * PROF_NCLS) return SGF_INVALID_ARG;
+  g_prof.read(out);
+  return SGF_OK;
+}
+
 int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                    const double* values, int on_device, sgf_csr** out) {
   if (!ctx || !out) return SGF_INVALID_ARG;

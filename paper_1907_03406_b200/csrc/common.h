@@ -121,6 +121,10 @@ struct RedSeg {
 
 // kernel launchers (defined in the .cu files)
 namespace sgf {
+// number of kernels launched by the library (all launchers increment it)
+extern unsigned long long g_kernel_launches;
+inline void count_launch(unsigned long long k = 1) { g_kernel_launches += k; }
+
 cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, int big_tiles,
                         cudaStream_t s);
 cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s);

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) diag_chol_kernel(const DiagTask* __restri
 cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
                                 double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  diag_chol_kernel<<<ntasks, 256, 0, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
+  count_launch(); diag_chol_kernel<<<ntasks, 256, 0, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
   return cudaGetLastError();
 }
 
@@ -132,7 +132,7 @@ cudaError_t launch_copy_tiled(const CopyTask* d_tasks, const long long* d_prefix
                               long long ntiles, cudaStream_t s) {
   if (ntasks <= 0 || ntiles <= 0) return cudaSuccess;
   long long grid = ntiles < (1LL << 30) ? ntiles : (1LL << 30);
-  copy_kernel<<<(unsigned)grid, 256, 0, s>>>(d_tasks, d_prefix, ntasks, ntiles);
+  count_launch(); copy_kernel<<<(unsigned)grid, 256, 0, s>>>(d_tasks, d_prefix, ntasks, ntiles);
   return cudaGetLastError();
 }
 
@@ -159,7 +159,7 @@ cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, in
                               cudaStream_t s) {
   if (ntasks <= 0 || ntiles <= 0) return cudaSuccess;
   long long grid = ntiles < (1LL << 30) ? ntiles : (1LL << 30);
-  zero_upper_kernel<<<(unsigned)grid, 256, 0, s>>>((const TriTask*)d_tasks, d_prefix, ntasks, ntiles);
+  count_launch(); zero_upper_kernel<<<(unsigned)grid, 256, 0, s>>>((const TriTask*)d_tasks, d_prefix, ntasks, ntiles);
   return cudaGetLastError();
 }
 
@@ -178,7 +178,7 @@ cudaError_t launch_scatter_values(const double* vals, const long long* dst, long
   if (nnz <= 0) return cudaSuccess;
   long long blocks = (nnz + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  scatter_values_kernel<<<(unsigned)blocks, 256, 0, s>>>(vals, dst, nnz, base);
+  count_launch(); scatter_values_kernel<<<(unsigned)blocks, 256, 0, s>>>(vals, dst, nnz, base);
   return cudaGetLastError();
 }
 
@@ -191,7 +191,7 @@ __global__ void identity_kernel(double* const* __restrict__ ptrs, const int* __r
 
 cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  identity_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes);
+  count_launch(); identity_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes);
   return cudaGetLastError();
 }
 
@@ -220,7 +220,7 @@ __global__ void max_diag_kernel(const double* const* __restrict__ ptrs, const in
 cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, const int* d_ld, int n,
                             double* d_out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  max_diag_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes, d_ld, d_out);
+  count_launch(); max_diag_kernel<<<n, 256, 0, s>>>(d_ptrs, d_sizes, d_ld, d_out);
   return cudaGetLastError();
 }
 

@@ -459,6 +459,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   }
   {
     QrTask* d_qt = S.scratch.upload(qt);
+    ProfScope ps(st, PROF_QR, 0.0);
     SGF_CUDA(launch_qrcp(d_qt, nw, max_m, st));
   }
   std::vector<int> rs(2 * nw);
@@ -487,6 +488,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   }
   {
     QrFinishTask* d_ft = S.scratch.upload(ft);
+    ProfScope ps(st, PROF_QR, 0.0);
     SGF_CUDA(launch_qr_finish(d_ft, nw, st));
   }
   // inv = Q^T L^{-1} = L^{-1} - V T^T V^T L^{-1}

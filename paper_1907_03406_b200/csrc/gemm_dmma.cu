@@ -195,7 +195,7 @@ static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg
   // gridDim.x is limited to 2^31-1; tasks are launched in chunks of 1<<30
   for (int off = 0; off < ntasks; off += (1 << 30)) {
     int cnt = ntasks - off < (1 << 30) ? ntasks - off : (1 << 30);
-    kern<<<cnt, NT, smem, s>>>(d_tasks + off, d_segs);
+    count_launch(); kern<<<cnt, NT, smem, s>>>(d_tasks + off, d_segs);
   }
   return cudaGetLastError();
 }

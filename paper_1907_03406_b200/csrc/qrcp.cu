@@ -212,7 +212,7 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
+  count_launch(); qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
   return cudaGetLastError();
 }
 
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_finish_kernel(const QrFinishTas
 
 cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  qr_finish_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  count_launch(); qr_finish_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
   return cudaGetLastError();
 }
 

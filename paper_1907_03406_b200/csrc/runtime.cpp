@@ -7,6 +7,49 @@
 
 namespace sgf {
 
+unsigned long long g_kernel_launches = 0;
+Profiler g_prof;
+
+void Profiler::reset() {
+  for (auto& r : recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  recs.clear();
+}
+
+void Profiler::read(double* out) {
+  for (int i = 0; i < 3 * PROF_NCLS; ++i) out[i] = 0.0;
+  for (auto& r : recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    out[3 * r.cls] += ms;
+    out[3 * r.cls + 1] += r.work;
+    out[3 * r.cls + 2] += (double)r.launches;
+  }
+}
+
+ProfScope::ProfScope(cudaStream_t st, int cls, double work) : s(st) {
+  if (!g_prof.on) return;
+  Profiler::Rec r;
+  r.cls = cls;
+  r.work = work;
+  r.launches = (long long)g_kernel_launches;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  idx = (int)g_prof.recs.size();
+  g_prof.recs.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (idx < 0) return;
+  auto& r = g_prof.recs[idx];
+  cudaEventRecord(r.b, s);
+  r.launches = (long long)g_kernel_launches - r.launches;
+}
+
 void fail(int status, const std::string& msg) { throw Error{status, msg}; }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -40,15 +83,36 @@ void Arena::release() {
   used_ = 0;
 }
 
+// flops the tiles actually multiply (k range per segment after the
+// triangular limits), for the roofline accounting
+static double useful_flops(const std::vector<GemmTask>& ts, const std::vector<GemmSeg>& segs, int bm) {
+  double f = 0.0;
+  for (const auto& t : ts) {
+    const int rows = std::min(bm, t.M - t.m0), cols = std::min(bm, t.N - t.n0);
+    for (int s = 0; s < t.nseg; ++s) {
+      const GemmSeg& g = segs[t.seg0 + s];
+      int kb = 0, ke = g.K;
+      if (g.flags & SEG_KLIM_M) ke = std::min(ke, t.m0 + bm);
+      if (g.flags & SEG_KLIM_N) ke = std::min(ke, t.n0 + bm);
+      if (g.flags & SEG_KSTART_M) kb = std::max(kb, t.m0);
+      if (g.flags & SEG_KSTART_N) kb = std::max(kb, t.n0);
+      if (ke > kb) f += 2.0 * rows * cols * (ke - kb);
+    }
+  }
+  return f;
+}
+
 void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
   if (empty()) return;
   GemmSeg* d_segs = scratch.upload(segs);
   if (!big.empty()) {
     GemmTask* d = scratch.upload(big);
+    ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(big, segs, 128) : 0.0);
     SGF_CUDA(launch_gemm(d, (int)big.size(), d_segs, 1, st));
   }
   if (!small.empty()) {
     GemmTask* d = scratch.upload(small);
+    ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(small, segs, 64) : 0.0);
     SGF_CUDA(launch_gemm(d, (int)small.size(), d_segs, 0, st));
   }
 }
@@ -63,6 +127,10 @@ void CopyBatch::launch(Arena& scratch, cudaStream_t st) {
   }
   CopyTask* d_t = scratch.upload(tasks);
   long long* d_p = scratch.upload(prefix);
+  double bytes = 0.0;
+  if (g_prof.on)
+    for (auto& t : tasks) bytes += 16.0 * t.rows * t.cols;
+  ProfScope ps(st, PROF_MOVE, bytes);
   SGF_CUDA(launch_copy_tiled(d_t, d_p, (int)tasks.size(), tot, st));
 }
 
@@ -161,6 +229,7 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
       DiagTask* d_dt = scratch.upload(dt);
       double** d_xd = scratch.upload(xd);
       int* d_xl = scratch.upload(xl);
+      ProfScope ps(st, PROF_CHOL, 0.0);
       SGF_CUDA(launch_diag_chol_ex(d_dt, (int)dt.size(), d_status, d_piv, d_xd, d_xl, st));
     }
     gc.launch(scratch, st);

@@ -48,6 +48,27 @@ cudaError_t launch_p_update(double* p, const double* z, long long n, const doubl
 
 
 // ---------------------------------------------------------------------------
+// Optional per-kernel-class timing with CUDA events on the launching stream
+// (bench.py's roofline numbers).  Classes: see PROF_* below.
+// ---------------------------------------------------------------------------
+enum { PROF_GEMM = 0, PROF_GEMV = 1, PROF_SPMV = 2, PROF_QR = 3, PROF_CHOL = 4, PROF_MOVE = 5, PROF_VEC = 6,
+       PROF_NCLS = 7 };
+struct Profiler {
+  bool on = false;
+  struct Rec { int cls; cudaEvent_t a, b; double work; long long launches; };
+  std::vector<Rec> recs;
+  void reset();
+  void read(double* out);  // out[3*cls + 0..2] = ms, work, launches
+};
+extern Profiler g_prof;
+struct ProfScope {
+  cudaStream_t s;
+  int idx = -1;
+  ProfScope(cudaStream_t st, int cls, double work);
+  ~ProfScope();
+};
+
+// ---------------------------------------------------------------------------
 // Device bump arena (stream-ordered chunks from the CUDA memory pool).
 // ---------------------------------------------------------------------------
 class Arena {

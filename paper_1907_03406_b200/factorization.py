@@ -235,11 +235,14 @@ def _kind_mask(names):
 
 def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
               compression=True, mode="polynomial", rank_tol=DEFAULT_RANK_TOL,
-              rank_trace=None, *, replay_perms=None, device=0):
+              rank_trace=None, *, replay_perms=None, device=0, device_values=None):
     """Build the hierarchical preconditioner on the GPU (reference
     factorization.py:410-573).  `replay_perms` (parity mode) is a list of QR
     column permutations, one per compression in the reference's execution
-    order, that the device QR follows instead of its own argmax."""
+    order, that the device QR follows instead of its own argmax.
+    `device_values` optionally supplies the CSR values (in the order of
+    problem.matrix.tocsr() with sorted indices) as a float64 CUDA tensor
+    already resident in HBM; the host matrix then only provides the pattern."""
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}; expected one of {SCHEMES}")
     if mode not in MODES:
@@ -281,6 +284,10 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
     args.n, args.nnz = n, A.nnz
     args.indptr, args.indices, args.values = indptr.ctypes.data, indices.ctypes.data, values.ctypes.data
     args.values_on_device = 0
+    if device_values is not None:
+        if tuple(device_values.shape) != (A.nnz,) or not device_values.is_cuda:
+            raise ShapeMismatchError("device_values must be a CUDA vector with one entry per nonzero")
+        args.values, args.values_on_device = device_values.data_ptr(), 1
     args.pi_cols, args.phi = basis.pi_cols, phi.ctypes.data
     args.nlevels = len(hl)
     args.level_ncells = level_ncells.ctypes.data

@@ -33,18 +33,26 @@ class SolveReport:
 class DeviceCSR(object):
     """A CSR matrix resident in HBM (int32 column indices, int64 row pointer)."""
 
-    def __init__(self, A, device=0):
-        A = sp.csr_matrix(A)
-        self.shape = A.shape
-        self.n = A.shape[0]
-        self.nnz = A.nnz
-        ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
-        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
-        dv = np.ascontiguousarray(A.data, dtype=np.float64)
+    def __init__(self, A=None, device=0, *, indptr=None, indices=None, values=None, n=None):
+        """From a scipy matrix (host), or from CUDA tensors indptr (int64),
+        indices (int32) and values (float64) already resident in HBM."""
         self._ctx = N.context(device)
         h = C.c_void_p()
-        st = N.lib().sgf_csr_create(self._ctx, self.n, self.nnz, ip.ctypes.data, ix.ctypes.data,
-                                    dv.ctypes.data, 0, C.byref(h))
+        if A is not None:
+            A = sp.csr_matrix(A)
+            self.shape = A.shape
+            self.n = A.shape[0]
+            self.nnz = A.nnz
+            ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
+            ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+            dv = np.ascontiguousarray(A.data, dtype=np.float64)
+            ptrs, on_dev = (ip.ctypes.data, ix.ctypes.data, dv.ctypes.data), 0
+        else:
+            self.n = int(n)
+            self.shape = (self.n, self.n)
+            self.nnz = int(values.shape[0])
+            ptrs, on_dev = (indptr.data_ptr(), indices.data_ptr(), values.data_ptr()), 1
+        st = N.lib().sgf_csr_create(self._ctx, self.n, self.nnz, ptrs[0], ptrs[1], ptrs[2], on_dev, C.byref(h))
         N.raise_for(st, self._ctx)
         self._h = h
 
@@ -100,7 +108,27 @@ def _as_device_precond(precond):
 
 
 def pcg(matvec, b, precond=None, tol=1e-10, maxit=5000, true_residual_every=50):
-    """Conjugate gradients (reference krylov.py:34-102) on the GPU."""
+    """Conjugate gradients (reference krylov.py:34-102) on the GPU.  With a
+    float64 CUDA tensor `b` the solve stays on the device and x is returned
+    as a CUDA tensor."""
+    if not isinstance(b, np.ndarray) and getattr(b, "is_cuda", False):
+        import torch
+
+        A = _as_device_matrix(matvec)
+        P = _as_device_precond(precond)
+        if b.dim() != 1 or b.shape[0] != A.n or b.dtype != torch.float64:
+            raise ShapeMismatchError(f"right-hand side must be a float64 vector of length {A.n}")
+        b = b.contiguous()
+        x = torch.empty_like(b)
+        hist = np.empty(int(maxit) + 2)
+        rep = N.PcgReport()
+        st = N.lib().sgf_pcg(A._ctx, A._h, P._h if P is not None else None, b.data_ptr(), x.data_ptr(),
+                             float(tol), int(maxit), int(true_residual_every), 1, C.byref(rep),
+                             hist.ctypes.data)
+        N.raise_for(st, A._ctx)
+        return x, SolveReport(iterations=rep.iterations, residual_history=hist[:rep.history_len].tolist(),
+                              converged=bool(rep.converged), wall_time=rep.wall_time,
+                              final_rel_residual=rep.final_rel_residual)
     b = np.asarray(b, dtype=float)
     if b.ndim != 1:
         raise ShapeMismatchError(f"right-hand side must be a vector, got {b.shape}")
