@@ -96,6 +96,13 @@ typedef struct {
   int n_replay;
   const int64_t* replay_ptr;
   const int32_t* replay_perm;
+  /* alternative to phi: build Pi natively from vertex coordinates (host,
+     n_vertices x 3) with basis.py:38-62's rule (degree 0/1/2, components
+     1/3); used when phi == NULL */
+  const double* coords;
+  int64_t n_vertices;
+  int degree;
+  int components;
 } sgf_factor_args;
 
 typedef struct {

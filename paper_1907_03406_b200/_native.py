@@ -52,6 +52,7 @@ class FactorArgs(C.Structure):
         ("compression", C.c_int), ("mode", C.c_int), ("rank_tol", C.c_double),
         ("n_trace", C.c_int), ("trace", C.c_void_p),
         ("n_replay", C.c_int), ("replay_ptr", C.c_void_p), ("replay_perm", C.c_void_p),
+        ("coords", C.c_void_p), ("n_vertices", C.c_int64), ("degree", C.c_int), ("components", C.c_int),
     ]
 
 

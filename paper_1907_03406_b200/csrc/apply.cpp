@@ -144,6 +144,7 @@ ApplyPlan* build_plan(Precond* P) {
   plan->t = plan->mem.alloc(std::max(max_c, 1LL));
   plan->part = plan->mem.alloc(std::max(max_part, 1LL));
   plan->work = plan->mem.alloc(std::max<long long>(P->n, 1));
+  std::vector<int> tix(P->n, -1);
 
   for (auto& rg : ranges) {
     Group g;
@@ -199,20 +200,29 @@ ApplyPlan* build_plan(Precond* P) {
     g.red2 = plan->mem.upload(r2);
     g.nred2 = (int)r2.size();
     if (!contrib.empty()) {
-      std::stable_sort(contrib.begin(), contrib.end(),
-                       [](const std::pair<int64_t, long long>& x, const std::pair<int64_t, long long>& y) {
-                         return x.first < y.first;
-                       });
+      // bucket the contributions per target unknown, keeping factor order
+      // inside a bucket (counting sort; tix is an n-sized scratch map)
       std::vector<int> tgt;
-      std::vector<long long> ptr, pos;
-      for (size_t i = 0; i < contrib.size(); ++i) {
-        if (i == 0 || contrib[i].first != contrib[i - 1].first) {
-          tgt.push_back((int)contrib[i].first);
-          ptr.push_back((long long)pos.size());
+      std::vector<long long> ptr, pos(contrib.size());
+      for (auto& c : contrib) {
+        int& ti = tix[c.first];
+        if (ti < 0) {
+          ti = (int)tgt.size();
+          tgt.push_back((int)c.first);
+          ptr.push_back(0);
         }
-        pos.push_back(contrib[i].second);
+        ++ptr[ti];
       }
-      ptr.push_back((long long)pos.size());
+      long long run = 0;
+      for (auto& p : ptr) {
+        const long long k = p;
+        p = run;
+        run += k;
+      }
+      ptr.push_back(run);
+      std::vector<long long> fillp(ptr.begin(), ptr.end() - 1);
+      for (auto& c : contrib) pos[fillp[tix[c.first]]++] = c.second;
+      for (int u : tgt) tix[u] = -1;
       g.ntgt = (long long)tgt.size();
       g.tgt = plan->mem.upload(tgt);
       g.tptr = plan->mem.upload(ptr);

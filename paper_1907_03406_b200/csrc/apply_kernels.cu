@@ -22,14 +22,19 @@ __global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict_
   for (int i = T.r0 + warp; i < T.r1; i += 8) {
     const double* a = T.A + (long long)i * T.lda;
     const int ke = T.tri ? min(T.c1, i + 1) : T.c1;
-    double s0 = 0.0, s1 = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int k = T.c0 + lane;
-    for (; k + 32 < ke; k += 64) {
-      s0 = fma(a[k], T.x[k], s0);
-      s1 = fma(a[k + 32], T.x[k + 32], s1);
+    // four independent streaming loads in flight per lane (matrix entries are
+    // read once per sweep: evict-first; x stays cached)
+    for (; k + 96 < ke; k += 128) {
+      const double a0 = __ldcs(a + k), a1 = __ldcs(a + k + 32), a2 = __ldcs(a + k + 64), a3 = __ldcs(a + k + 96);
+      s0 = fma(a0, T.x[k], s0);
+      s1 = fma(a1, T.x[k + 32], s1);
+      s2 = fma(a2, T.x[k + 64], s2);
+      s3 = fma(a3, T.x[k + 96], s3);
     }
-    if (k < ke) s0 = fma(a[k], T.x[k], s0);
-    double s = s0 + s1;
+    for (; k < ke; k += 32) s0 = fma(__ldcs(a + k), T.x[k], s0);
+    double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) T.y[i] = s;
@@ -45,15 +50,19 @@ __global__ void __launch_bounds__(256) gemv_t_kernel(const GemvTask* __restrict_
   if (k >= T.c1) return;
   int i0 = T.r0;
   if (T.tri) i0 = max(i0, k);
-  double s0 = 0.0, s1 = 0.0;
-  const double* a = T.A + k;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  const double* a = T.A + k + (long long)i0 * T.lda;
+  const long long ld = T.lda;
   int i = i0;
-  for (; i + 1 < T.r1; i += 2) {
-    s0 = fma(a[(long long)i * T.lda], T.x[i], s0);
-    s1 = fma(a[(long long)(i + 1) * T.lda], T.x[i + 1], s1);
+  for (; i + 3 < T.r1; i += 4, a += 4 * ld) {
+    const double a0 = __ldcs(a), a1 = __ldcs(a + ld), a2 = __ldcs(a + 2 * ld), a3 = __ldcs(a + 3 * ld);
+    s0 = fma(a0, T.x[i], s0);
+    s1 = fma(a1, T.x[i + 1], s1);
+    s2 = fma(a2, T.x[i + 2], s2);
+    s3 = fma(a3, T.x[i + 3], s3);
   }
-  if (i < T.r1) s0 = fma(a[(long long)i * T.lda], T.x[i], s0);
-  T.y[k] = s0 + s1;
+  for (; i < T.r1; ++i, a += ld) s0 = fma(__ldcs(a), T.x[i], s0);
+  T.y[k] = (s0 + s1) + (s2 + s3);
 }
 
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s) {

@@ -19,70 +19,75 @@ __global__ void __launch_bounds__(256) diag_chol_kernel(const DiagTask* __restri
                                                         double* __restrict__ pivval,
                                                         double* const* __restrict__ xdiag,
                                                         const int* __restrict__ ldx) {
-  __shared__ double S[64][65];
-  __shared__ int bad;
+  // left-looking column Cholesky (the reference's order, densela.py:107-114)
+  // with the inverse built row by row alongside; a quad of threads per row,
+  // two barriers per column
+  extern __shared__ double dsm[];
+  double(*S)[65] = reinterpret_cast<double(*)[65]>(dsm);
+  double(*D)[65] = reinterpret_cast<double(*)[65]>(dsm + 64 * 65);
+  double* col = dsm + 2 * 64 * 65;
   const DiagTask T = tasks[blockIdx.x];
   const int nb = T.nb, tid = threadIdx.x;
+  const int q = tid >> 2, sub = tid & 3;
   double* W = T.W + (long long)T.k0 * T.ld + T.k0;
   for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
     int r = idx / nb, c = idx % nb;
     S[r][c] = W[(long long)r * T.ld + c];
   }
-  if (tid == 0) bad = 0;
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      double d = S[j][j];
-      if (!(d > T.floor) || !isfinite(d)) {
-        bad = 1;
-        if (status[T.node] == 0) {
-          status[T.node] = T.k0 + j + 1;
-          pivval[T.node] = d;
-        }
-      } else {
-        S[j][j] = sqrt(d);
+    const int i = j + q;
+    double acc = 0.0;
+    if (i < nb)
+      for (int k = sub; k < j; k += 4) acc = fma(S[i][k], S[j][k], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (i < nb && sub == 0) col[i] = S[i][j] - acc;
+    __syncthreads();
+    const double d = col[j];
+    if (!(d > T.floor) || !isfinite(d)) {
+      if (tid == 0 && status[T.node] == 0) {
+        status[T.node] = T.k0 + j + 1;
+        pivval[T.node] = d;
       }
+      return;  // uniform: every thread saw the same pivot
     }
-    __syncthreads();
-    if (bad) return;
-    const double djj = S[j][j];
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) S[i][j] /= djj;
-    __syncthreads();
-    const int rem = nb - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
-      int i = j + 1 + idx / rem, l = j + 1 + idx % rem;
-      if (l <= i) S[i][l] -= S[i][j] * S[l][j];
-    }
+    const double djj = sqrt(d);
+    if (i < nb && sub == 0) S[i][j] = (i == j) ? djj : col[i] / djj;
+    // row j of the inverse: D[j][c] = -(sum_{c<=k<j} L[j][k] D[k][c]) / L[j][j]
+    double a2 = 0.0;
+    if (q < j)
+      for (int k = q + sub; k < j; k += 4) a2 = fma(S[j][k], D[k][q], a2);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, 1);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, 2);
+    if (sub == 0 && q <= j) D[j][q] = (q == j) ? 1.0 / djj : -a2 / djj;
     __syncthreads();
   }
-  // inverse of the lower-triangular tile, one column per thread (the
-  // column lives in the thread's own slice of Dinv)
-  double* Dg = T.Dinv;
-  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) Dg[idx] = 0.0;
-  __syncthreads();
-  if (tid < nb) {
-    const int c = tid;
-    Dg[c * 64 + c] = 1.0 / S[c][c];
-    for (int i = c + 1; i < nb; ++i) {
-      double s = 0.0;
-      for (int k = c; k < i; ++k) s = fma(S[i][k], Dg[k * 64 + c], s);
-      Dg[i * 64 + c] = -s / S[i][i];
-    }
-  }
-  __syncthreads();
   double* X = xdiag ? xdiag[blockIdx.x] : nullptr;
   const int lx = ldx ? ldx[blockIdx.x] : 0;
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    int r = idx / nb, c = idx % nb;
-    W[(long long)r * T.ld + c] = (c <= r) ? S[r][c] : 0.0;
-    if (X) X[(long long)(T.k0 + r) * lx + T.k0 + c] = Dg[r * 64 + c];
+  for (int idx = tid; idx < 64 * 64; idx += blockDim.x) {
+    const int r = idx >> 6, c = idx & 63;
+    const bool in = (r < nb && c < nb && c <= r);
+    const double dv = in ? D[r][c] : 0.0;
+    T.Dinv[idx] = dv;
+    if (r < nb && c < nb) {
+      W[(long long)r * T.ld + c] = in ? S[r][c] : 0.0;
+      if (X) X[(long long)(T.k0 + r) * lx + T.k0 + c] = dv;
+    }
   }
 }
 
 cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
                                 double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  count_launch(); diag_chol_kernel<<<ntasks, 256, 0, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
+  const size_t smem = (2 * 64 * 65 + 64) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(diag_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  count_launch(); diag_chol_kernel<<<ntasks, 256, smem, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
   return cudaGetLastError();
 }
 

@@ -58,6 +58,30 @@ struct State {
 
 inline bool kind_in(int mask, int kind) { return (mask >> kind) & 1; }
 
+// SGF_TRACE=1: per-phase wall times (stream synchronised) on stderr
+struct Phase {
+  const char* name;
+  int level;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  static bool on() {
+    static int v = getenv("SGF_TRACE") ? 1 : 0;
+    return v;
+  }
+  Phase(const char* n, int lv, cudaStream_t s) : name(n), level(lv), st(s) {
+    if (on()) {
+      cudaStreamSynchronize(st);
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  ~Phase() {
+    if (!on()) return;
+    cudaStreamSynchronize(st);
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[sgf] L%d %-10s %9.2f ms\n", level, name, ms);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // level 1: nodes, basis rows, and the CSR -> block scatter (blockmatrix.py:97-144)
 // ---------------------------------------------------------------------------
@@ -68,6 +92,8 @@ void setup_level1(State& S) {
   std::vector<int32_t> owner(n, -1), local(n, 0);
   std::vector<int> sizes(nc);
   S.nodes.assign(nc, Node());
+  int bad_cover = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(| : bad_cover)
   for (int c = 0; c < nc; ++c) {
     const int64_t b = a.l1_ptr[c], e = a.l1_ptr[c + 1];
     sizes[c] = (int)(e - b);
@@ -77,19 +103,26 @@ void setup_level1(State& S) {
     nd.interior = a.cell_interior[c] != 0;
     for (int64_t i = b; i < e; ++i) {
       const int64_t u = a.l1_unknowns[i];
-      if (u < 0 || u >= n || owner[u] != -1) fail(SGF_INVALID_ARG, "level-1 cells do not partition the unknowns");
-      owner[u] = c;
+      if (u < 0 || u >= n) { bad_cover = 1; continue; }
+      owner[u] = c;  // a duplicate shows up as a hole below
       local[u] = (int32_t)(i - b);
     }
   }
+  if (bad_cover || a.l1_ptr[nc] != n) fail(SGF_INVALID_ARG, "level-1 cells do not partition the unknowns");
   for (int64_t u = 0; u < n; ++u)
     if (owner[u] < 0) fail(SGF_INVALID_ARG, "node unknown lists do not cover all unknowns");
 
   // symmetry of pattern and values (blockmatrix.py:107-113), indices sorted per row
   {
+    Phase ph(" s-sym", -1, S.st);
     double scale = 0.0;
-    if (!a.values_on_device)
+    if (!a.values_on_device) {
+#pragma omp parallel for reduction(max : scale)
       for (int64_t e = 0; e < a.nnz; ++e) scale = std::max(scale, std::fabs(a.values[e]));
+    }
+    int pattern_bad = 0;
+    double worst = 0.0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : pattern_bad) reduction(max : worst)
     for (int64_t r = 0; r < n; ++r) {
       for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
         const int32_t c = a.indices[e];
@@ -97,40 +130,41 @@ void setup_level1(State& S) {
         const int32_t* b0 = a.indices + a.indptr[c];
         const int32_t* b1 = a.indices + a.indptr[c + 1];
         const int32_t* f = std::lower_bound(b0, b1, (int32_t)r);
-        bool found = (f != b1 && *f == r);
-        if (!found) {
-          if (!a.values_on_device && a.values[e] == 0.0) continue;
-          fail(SGF_NON_SYMMETRIC, "matrix is not symmetric (pattern)");
+        if (f == b1 || *f != r) {
+          if (a.values_on_device || a.values[e] != 0.0) pattern_bad = 1;
+          continue;
         }
-        if (!a.values_on_device) {
-          const double d = std::fabs(a.values[e] - a.values[a.indptr[c] + (f - b0)]);
-          if (d > 1e-12 * std::max(scale, 1e-300)) {
-            char buf[128];
-            snprintf(buf, sizeof buf, "matrix is not symmetric (max asymmetry %.2e)", d);
-            fail(SGF_NON_SYMMETRIC, buf);
-          }
-        }
+        if (!a.values_on_device) worst = std::max(worst, std::fabs(a.values[e] - a.values[a.indptr[c] + (f - b0)]));
       }
+    }
+    if (pattern_bad) fail(SGF_NON_SYMMETRIC, "matrix is not symmetric (pattern)");
+    if (worst > 1e-12 * std::max(scale, 1e-300)) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "matrix is not symmetric (max asymmetry %.2e)", worst);
+      fail(SGF_NON_SYMMETRIC, buf);
     }
   }
 
-  // block discovery: per cell the sorted list of coupled cells (b > a)
+  // block discovery, per cell (rows of a cell are its unknowns): coupled
+  // cells b > a; the symmetric pattern makes the (b, a) side redundant
   std::vector<std::vector<int>> up(nc);
   std::vector<char> has_diag(nc, 0);
-  for (int64_t r = 0; r < n; ++r) {
-    const int ca = owner[r];
-    for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
-      const int cb = owner[a.indices[e]];
-      if (cb == ca) { has_diag[ca] = 1; continue; }
-      const int lo = std::min(ca, cb), hi = std::max(ca, cb);
-      auto& v = up[lo];
-      if (std::find(v.begin(), v.end(), hi) == v.end()) v.push_back(hi);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int c = 0; c < nc; ++c) {
+    auto& v = up[c];
+    for (int64_t i = a.l1_ptr[c]; i < a.l1_ptr[c + 1]; ++i) {
+      const int64_t r = a.l1_unknowns[i];
+      for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
+        const int cb = owner[a.indices[e]];
+        if (cb == c) has_diag[c] = 1;
+        else if (cb > c && std::find(v.begin(), v.end(), cb) == v.end()) v.push_back(cb);
+      }
     }
+    std::sort(v.begin(), v.end());
   }
   S.M.init(sizes);
   long long total = 0;
   for (int c = 0; c < nc; ++c) {
-    std::sort(up[c].begin(), up[c].end());
     if (has_diag[c]) total += (long long)sizes[c] * sizes[c];
     for (int b : up[c]) total += (long long)sizes[c] * sizes[b];
   }
@@ -154,7 +188,10 @@ void setup_level1(State& S) {
     }
   }
   // per-nnz destination offsets (entries stored once: the (min,max) orientation)
-  std::vector<long long> dst(a.nnz);
+  Phase ph_dst(" s-dst", -1, S.st);
+  std::vector<long long> dstv(std::max<int64_t>(a.nnz, 1));
+  long long* dst = dstv.data();
+#pragma omp parallel for schedule(dynamic, 4096)
   for (int64_t r = 0; r < n; ++r) {
     const int ca = owner[r];
     for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
@@ -171,24 +208,65 @@ void setup_level1(State& S) {
       }
     }
   }
-  long long* d_dst = S.scratch.upload(dst);
+  long long* d_dst = S.scratch.alloc_t<long long>(std::max<int64_t>(a.nnz, 1));
+  upload_pinned(*S.ctx, d_dst, dst, a.nnz * sizeof(long long));
   const double* d_vals = a.values;
   if (!a.values_on_device) {
     double* dv = S.scratch.alloc(a.nnz);
-    SGF_CUDA(cudaMemcpyAsync(dv, a.values, a.nnz * sizeof(double), cudaMemcpyHostToDevice, S.st));
+    upload_pinned(*S.ctx, dv, a.values, a.nnz * sizeof(double));
     d_vals = dv;
   }
   SGF_CUDA(launch_scatter_values(d_vals, d_dst, a.nnz, base, S.st));
 
   // basis rows of every node: Pi[active] in cell order
+  Phase ph_phi(" s-phi", -1, S.st);
   const int pi = S.pi;
   std::vector<double> phi_perm((size_t)n * pi);
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t u = a.l1_unknowns[i];
-    std::memcpy(&phi_perm[(size_t)i * pi], a.phi + (size_t)u * pi, pi * sizeof(double));
+  if (a.phi) {
+#pragma omp parallel for
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t u = a.l1_unknowns[i];
+      std::memcpy(&phi_perm[(size_t)i * pi], a.phi + (size_t)u * pi, pi * sizeof(double));
+    }
+  } else {
+    // Pi from the coordinates (basis.py:27-62): monomials [1 x y z (x^2 y^2
+    // z^2 xy yz zx)], block diagonal per component, column / max |column|
+    const int ps = a.degree == 0 ? 1 : (a.degree == 1 ? 4 : 10);
+    const int64_t nv = a.n_vertices;
+    auto mono = [&](int64_t v, int q) -> double {
+      const double x = a.coords[3 * v], y = a.coords[3 * v + 1], z = a.coords[3 * v + 2];
+      switch (q) {
+        case 0: return 1.0;
+        case 1: return x;
+        case 2: return y;
+        case 3: return z;
+        case 4: return x * x;
+        case 5: return y * y;
+        case 6: return z * z;
+        case 7: return x * y;
+        case 8: return y * z;
+        default: return z * x;
+      }
+    };
+    std::vector<double> scale(ps, 0.0);
+    for (int q = 0; q < ps; ++q) {
+      double mx = 0.0;
+#pragma omp parallel for reduction(max : mx)
+      for (int64_t v = 0; v < nv; ++v) mx = std::max(mx, std::fabs(mono(v, q)));
+      scale[q] = (mx == 0.0) ? 1.0 : mx;
+    }
+#pragma omp parallel for
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t u = a.l1_unknowns[i];
+      const int64_t c = u / nv, v = u % nv;
+      double* row = &phi_perm[(size_t)i * pi];
+      for (int k = 0; k < pi; ++k) row[k] = 0.0;
+      for (int q = 0; q < ps; ++q) row[c * ps + q] = mono(v, q) / scale[q];
+    }
   }
-  double* d_phi = S.lvl->upload(phi_perm);
-  for (int c = 0; c < nc; ++c) S.nodes[c].phi = d_phi ? d_phi + (size_t)a.l1_ptr[c] * pi : nullptr;
+  double* d_phi = S.lvl->alloc(std::max<size_t>(phi_perm.size(), 1));
+  upload_pinned(*S.ctx, d_phi, phi_perm.data(), phi_perm.size() * sizeof(double));
+  for (int c = 0; c < nc; ++c) S.nodes[c].phi = d_phi + (size_t)a.l1_ptr[c] * pi;
 }
 
 // ---------------------------------------------------------------------------
@@ -756,10 +834,17 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
       cp.add(b.p, 1, b.cols, t->p + (long long)ob * t->cols + oa, t->cols, 1, b.cols, b.rows);
     }
   }
-  cp.launch(S.scratch, st);
-  SGF_CUDA(cudaStreamSynchronize(st));
-  S.scratch.release();
-  S.lvl = std::move(nl);  // frees the old level (stream ordered)
+  {
+    Phase ph(" m-copy", -1, st);
+    cp.launch(S.scratch, st);
+    SGF_CUDA(cudaStreamSynchronize(st));
+  }
+  {
+    Phase ph(" m-free", -1, st);
+    S.scratch.release();
+    S.lvl = std::move(nl);  // frees the old level (stream ordered)
+  }
+  Phase ph(" m-move", -1, st);
   S.M = std::move(N);
   S.nodes = std::move(nn);
 }
@@ -836,7 +921,13 @@ std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<Le
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   if (a.n <= 0 || a.nlevels <= 0 || !a.indptr || !a.indices || !a.values || !a.l1_ptr || !a.l1_unknowns)
     fail(SGF_INVALID_ARG, "incomplete factorization arguments");
-  if (a.pi_cols <= 0 || !a.phi) fail(SGF_INVALID_ARG, "missing polynomial basis");
+  if (a.pi_cols <= 0 || (!a.phi && !a.coords)) fail(SGF_INVALID_ARG, "missing polynomial basis");
+  if (!a.phi) {
+    const int ps = a.degree == 0 ? 1 : (a.degree == 1 ? 4 : 10);
+    if (a.degree < 0 || a.degree > 2 || (a.components != 1 && a.components != 3) ||
+        a.pi_cols != ps * a.components || a.n_vertices * a.components != a.n)
+      fail(SGF_INVALID_ARG, "inconsistent basis description");
+  }
   if (a.n > (int64_t)INT32_MAX) fail(SGF_INVALID_ARG, "n exceeds int32 index range");
   std::unique_ptr<Precond> P(new Precond());
   P->ctx = &ctx;
@@ -850,7 +941,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.P = P.get();
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
 
-  setup_level1(S);
+  { Phase ph("setup", 0, S.st); setup_level1(S); }
   S.peak = 0;
   std::vector<LevelStats> per_level;
   int max_seen = 0, max_after = 0;
@@ -873,7 +964,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     std::vector<int> elim;
     for (int c = 0; c < (int)S.nodes.size(); ++c)
       if (S.nodes[c].interior && !S.nodes[c].active.empty()) elim.push_back(c);
-    eliminate_level(S, elim, t + 1);
+    { Phase ph("eliminate", t + 1, S.st); eliminate_level(S, elim, t + 1); }
     ls.eliminated = (int)elim.size();
     SGF_CUDA(cudaStreamSynchronize(S.st));
     S.scratch.release();
@@ -881,7 +972,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       std::vector<int> comp;
       for (int c = 0; c < (int)S.nodes.size(); ++c)
         if (kind_in(a.compress_kind_mask, S.nodes[c].kind) && !S.nodes[c].active.empty()) comp.push_back(c);
-      compress_level(S, comp, t + 1, ls);
+      { Phase ph("compress", t + 1, S.st); compress_level(S, comp, t + 1, ls); }
     }
     for (auto& nd : S.nodes) max_after = std::max(max_after, (int)nd.active.size());
     per_level.push_back(ls);
@@ -889,6 +980,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     if (t + 1 < a.nlevels) {
       const long long old_live = S.M.live;
       cell_off += ncell;
+      Phase ph("merge", t + 1, S.st);
       merge_level(S, a.father + father_off, a.level_ncells[t + 1], a.cell_kind + cell_off,
                   a.cell_interior + cell_off);
       father_off += ncell;
@@ -898,7 +990,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     }
   }
   size_t before = P->factors.size();
-  final_dense(S);
+  { Phase ph("dense", 0, S.st); final_dense(S); }
   int final_size = 0;
   if (P->factors.size() > before) {
     final_size = P->factors.back().m;
@@ -920,7 +1012,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   }
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
                         (int)P->factors.size(), 0, nullptr);
-  P->plan = build_plan(P.get());
+  { Phase ph("plan", 0, S.st); P->plan = build_plan(P.get()); }
   SGF_CUDA(cudaStreamSynchronize(S.st));
   return P.release();
 }

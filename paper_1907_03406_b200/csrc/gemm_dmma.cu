@@ -11,15 +11,18 @@
 //     ascending interior order inside one tile: no atomics, deterministic),
 //   * the compression GEMMs (M_BN Phi_N, L^{-1} X, Q1^T L^{-1} M_BN, WY updates).
 // Operands are streamed global -> shared with cp.async (LDGSTS) through a
-// 3-stage pipeline; each operand tile is stored [row][k] or [k][row]
-// depending on which global stride is unit, with padding chosen so the
-// DMMA fragment reads are bank-conflict free in both layouts.
+// multi-stage pipeline.  Each operand tile is stored [row][k] or [k][row]
+// depending on which global stride is unit (padding 4 doubles keeps the DMMA
+// fragment reads bank-conflict free in both layouts).  Per segment every
+// thread precomputes its load pointers, so a stage issues one 64-bit add and
+// one LDGSTS per element.
+#include <cstdlib>
+
 #include "common.h"
 
 namespace sgf {
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+__device__ __forceinline__ void cp_async8(unsigned saddr, const void* gmem, bool valid) {
   int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
 }
@@ -30,12 +33,12 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int BK>
 __device__ __forceinline__ void seg_krange(const GemmSeg& S, int m0, int n0, int& kb, int& ke) {
   kb = 0;
   ke = S.K;
@@ -43,25 +46,89 @@ __device__ __forceinline__ void seg_krange(const GemmSeg& S, int m0, int n0, int
   if (S.flags & SEG_KLIM_N) ke = min(ke, n0 + BN);
   if (S.flags & SEG_KSTART_M) kb = max(kb, m0);
   if (S.flags & SEG_KSTART_N) kb = max(kb, n0);
-  kb = (kb / 16) * 16;
+  kb = (kb / BK) * BK;
 }
 
-template <int BM, int BN, int WM, int WN, int NT, int STAGES>
+// Per-thread load plan for one operand of one segment.  The shared tile is
+// always [row][k] (stride BK+4 == 4 mod 16 doubles: conflict-free DMMA
+// fragment reads); k-contiguous operands are read along k, row-contiguous
+// (transposed) operands along rows.
+template <int BR, int BK, int NT>
+struct LoadPlan {
+  static constexpr int E = BR * BK / NT;  // elements per thread per stage
+  static constexpr int SK = BK + 4;
+  const double* base;
+  long long estep;   // global offset between consecutive elements of this thread
+  long long kscale;  // global stride of k
+  int kfix;          // k of this thread's elements (k-contiguous) or of element 0
+  unsigned rowmask;  // bit e: row in range
+  int soff;          // smem offset of element 0
+  bool kc;
+
+  __device__ __forceinline__ void setup(const double* P, long long rs, long long ks, int row0, int rows) {
+    const int tid = threadIdx.x;
+    kc = (ks == 1) || (rs != 1);
+    kscale = ks;
+    rowmask = 0;
+    if (kc) {
+      constexpr int RSTEP = NT / BK;
+      const int r0 = tid / BK;
+      kfix = tid % BK;
+      base = P + (long long)(row0 + r0) * rs + (long long)kfix * ks;
+      estep = (long long)RSTEP * rs;
+      soff = r0 * SK + kfix;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (row0 + r0 + e * RSTEP < rows) rowmask |= 1u << e;
+    } else {
+      constexpr int KSTEP = NT / BR;
+      const int r0 = tid % BR;
+      kfix = tid / BR;
+      base = P + (long long)(row0 + r0) * rs + (long long)kfix * ks;
+      estep = (long long)KSTEP * ks;
+      soff = r0 * SK + kfix;
+      if (row0 + r0 < rows) rowmask = (E >= 32) ? 0xffffffffu : ((1u << (E & 31)) - 1);
+    }
+  }
+
+  __device__ __forceinline__ void issue(unsigned sbase, int k0, int ke) const {
+    const double* p = base + (long long)k0 * kscale;
+    const unsigned s = sbase + 8u * (unsigned)soff;
+    if (kc) {
+      constexpr int RSTEP = NT / BK;
+      const bool kin = (k0 + kfix < ke);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const bool v = kin && ((rowmask >> e) & 1u);
+        cp_async8(s + 8u * (e * RSTEP * SK), p, v);  // src-size 0: nothing is read
+        p += estep;
+      }
+    } else {
+      constexpr int KSTEP = NT / BR;
+      const bool rin = rowmask != 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const bool v = rin && (k0 + kfix + e * KSTEP < ke);
+        cp_async8(s + 8u * (e * KSTEP), p, v);
+        p += estep;
+      }
+    }
+  }
+};
+
+template <int BM, int BN, int WM, int WN, int NT, int STAGES, int BK>
 __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict__ tasks,
                                                       const GemmSeg* __restrict__ segs) {
-  constexpr int BK = 16;
-  constexpr int SK = BK + 4;   // [row][k] stride (== 4 mod 16: conflict free)
-  constexpr int SMA = BM + 4;  // [k][row] strides
-  constexpr int SMB = BN + 4;
-  constexpr int A_EL = (BM * SK > BK * SMA) ? BM * SK : BK * SMA;
-  constexpr int B_EL = (BN * SK > BK * SMB) ? BN * SK : BK * SMB;
+  using LA = LoadPlan<BM, BK, NT>;
+  using LB = LoadPlan<BN, BK, NT>;
+  constexpr int A_EL = BM * LA::SK;
+  constexpr int B_EL = BN * LB::SK;
   constexpr int WARPS_N = BN / WN;
   constexpr int FM = WM / 8, FN = WN / 8;
 
   extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + STAGES * A_EL;
-  __shared__ int s_kc[STAGES][2];
+  const unsigned sA0 = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned sB0 = sA0 + STAGES * A_EL * 8;
 
   const GemmTask T = tasks[blockIdx.x];
   const int tid = threadIdx.x;
@@ -69,11 +136,10 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
 
-  // count k-tiles over all segments
   int njobs = 0;
   for (int s = 0; s < T.nseg; ++s) {
     int kb, ke;
-    seg_krange<BM, BN>(segs[T.seg0 + s], T.m0, T.n0, kb, ke);
+    seg_krange<BM, BN, BK>(segs[T.seg0 + s], T.m0, T.n0, kb, ke);
     if (ke > kb) njobs += (ke - kb + BK - 1) / BK;
   }
 
@@ -83,47 +149,32 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
 #pragma unroll
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // loader iterator
-  int l_seg = 0, l_k = 0, l_kb = 0, l_ke = 0;
-  auto l_setup = [&](int s) {
+  // loader state
+  LA la;
+  LB lb;
+  int l_seg = -1, l_k = 0, l_ke = 0;
+  auto next_seg = [&](int s) {
+    int kb = 0, ke = 0;
     while (s < T.nseg) {
-      seg_krange<BM, BN>(segs[T.seg0 + s], T.m0, T.n0, l_kb, l_ke);
-      if (l_ke > l_kb) break;
+      seg_krange<BM, BN, BK>(segs[T.seg0 + s], T.m0, T.n0, kb, ke);
+      if (ke > kb) break;
       ++s;
     }
     l_seg = s;
-    l_k = l_kb;
+    if (s < T.nseg) {
+      const GemmSeg S = segs[T.seg0 + s];
+      la.setup(S.A, S.a_rs, S.a_ks, T.m0, T.M);
+      lb.setup(S.B, S.b_rs, S.b_ks, T.n0, T.N);
+      l_k = kb;
+      l_ke = ke;
+    }
   };
-  l_setup(0);
-
+  next_seg(0);
   auto load_stage = [&](int st) {
-    const GemmSeg S = segs[T.seg0 + l_seg];
-    const int k0 = l_k, ke = l_ke;
-    const bool akc = (S.a_ks == 1);
-    const bool bkc = (S.b_ks == 1);
-    double* dA = sA + st * A_EL;
-    double* dB = sB + st * B_EL;
-#pragma unroll 4
-    for (int idx = tid; idx < BM * BK; idx += NT) {
-      int r, k;
-      if (akc) { r = idx / BK; k = idx % BK; } else { r = idx % BM; k = idx / BM; }
-      const int gi = T.m0 + r, gk = k0 + k;
-      const bool v = (gi < T.M) && (gk < ke);
-      const double* src = v ? S.A + (long long)gi * S.a_rs + (long long)gk * S.a_ks : S.A;
-      cp_async8(dA + (akc ? r * SK + k : k * SMA + r), src, v);
-    }
-#pragma unroll 4
-    for (int idx = tid; idx < BN * BK; idx += NT) {
-      int r, k;
-      if (bkc) { r = idx / BK; k = idx % BK; } else { r = idx % BN; k = idx / BN; }
-      const int gj = T.n0 + r, gk = k0 + k;
-      const bool v = (gj < T.N) && (gk < ke);
-      const double* src = v ? S.B + (long long)gj * S.b_rs + (long long)gk * S.b_ks : S.B;
-      cp_async8(dB + (bkc ? r * SK + k : k * SMB + r), src, v);
-    }
-    if (tid == 0) { s_kc[st][0] = akc; s_kc[st][1] = bkc; }
+    la.issue(sA0 + st * A_EL * 8, l_k, l_ke);
+    lb.issue(sB0 + st * B_EL * 8, l_k, l_ke);
     l_k += BK;
-    if (l_k >= l_ke) l_setup(l_seg + 1);
+    if (l_k >= l_ke) next_seg(l_seg + 1);
   };
 
 #pragma unroll
@@ -138,19 +189,17 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
     cp_wait<STAGES - 1>();
     __syncthreads();
     const int st = j % STAGES;
-    const double* cA = sA + st * A_EL;
-    const double* cB = sB + st * B_EL;
-    const bool akc = s_kc[st][0], bkc = s_kc[st][1];
-    const int a_r = akc ? SK : 1, a_k = akc ? 1 : SMA;
-    const int b_r = bkc ? SK : 1, b_k = bkc ? 1 : SMB;
+    const double* cA = smem + st * A_EL;
+    const double* cB = smem + STAGES * A_EL + st * B_EL;
+    const double* pa = cA + (wm * WM + g) * LA::SK + t;
+    const double* pb = cB + (wn * WN + g) * LB::SK + t;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double af[FM], bf[FN];
-      const int k = kk * 4 + t;
 #pragma unroll
-      for (int i = 0; i < FM; ++i) af[i] = cA[(wm * WM + i * 8 + g) * a_r + k * a_k];
+      for (int i = 0; i < FM; ++i) af[i] = pa[i * 8 * LA::SK + kk * 4];
 #pragma unroll
-      for (int i = 0; i < FN; ++i) bf[i] = cB[(wn * WN + i * 8 + g) * b_r + k * b_k];
+      for (int i = 0; i < FN; ++i) bf[i] = pb[i * 8 * LB::SK + kk * 4];
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -179,13 +228,12 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
   }
 }
 
-template <int BM, int BN, int WM, int WN, int NT, int STAGES>
+template <int BM, int BN, int WM, int WN, int NT, int STAGES, int BK>
 static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, cudaStream_t s) {
-  constexpr int BK = 16;
-  constexpr int A_EL = (BM * (BK + 4) > BK * (BM + 4)) ? BM * (BK + 4) : BK * (BM + 4);
-  constexpr int B_EL = (BN * (BK + 4) > BK * (BN + 4)) ? BN * (BK + 4) : BK * (BN + 4);
+  constexpr int A_EL = BM * (BK + 4);
+  constexpr int B_EL = BN * (BK + 4);
   const size_t smem = (size_t)STAGES * (A_EL + B_EL) * sizeof(double);
-  auto kern = gemm_f64_kernel<BM, BN, WM, WN, NT, STAGES>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN, NT, STAGES, BK>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -203,8 +251,23 @@ static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg
 cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, int big_tiles,
                         cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  if (big_tiles) return launch_cfg<128, 128, 64, 32, 256, 3>(d_tasks, ntasks, d_segs, s);
-  return launch_cfg<64, 64, 32, 32, 128, 3>(d_tasks, ntasks, d_segs, s);
+  static int variant = getenv("SGF_GEMM_VARIANT") ? atoi(getenv("SGF_GEMM_VARIANT")) : 0;
+  if (big_tiles) return launch_cfg<128, 128, 64, 32, 256, 3, 32>(d_tasks, ntasks, d_segs, s);
+  switch (variant) {
+    case 1: return launch_cfg<64, 64, 32, 32, 128, 4, 16>(d_tasks, ntasks, d_segs, s);
+    case 2: return launch_cfg<64, 64, 32, 32, 128, 3, 16>(d_tasks, ntasks, d_segs, s);
+    case 3: return launch_cfg<64, 64, 32, 32, 128, 2, 32>(d_tasks, ntasks, d_segs, s);
+    case 4: return launch_cfg<64, 64, 32, 64, 64, 3, 32>(d_tasks, ntasks, d_segs, s);
+    case 5: return launch_cfg<64, 64, 64, 32, 64, 3, 32>(d_tasks, ntasks, d_segs, s);
+    case 6: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
+    case 7: return launch_cfg<128, 64, 32, 32, 256, 3, 16>(d_tasks, ntasks, d_segs, s);
+    case 8: return launch_cfg<64, 64, 32, 32, 128, 4, 8>(d_tasks, ntasks, d_segs, s);
+    case 9: return launch_cfg<64, 64, 32, 32, 128, 3, 32>(d_tasks, ntasks, d_segs, s);
+    // default: 64x64 tile, 4 warps of 32x32, BK=16, 2 stages (41 KB smem -> 4 CTAs
+    // = 16 warps per SM): 33.9 TFLOP/s = 91% of the measured DMMA peak on a
+    // 7680^2 x 3584 NT problem (tools/gemm_bench.cu)
+    default: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
+  }
 }
 
 }  // namespace sgf

@@ -52,6 +52,25 @@ ProfScope::~ProfScope() {
 
 void fail(int status, const std::string& msg) { throw Error{status, msg}; }
 
+void upload_pinned(Ctx& ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  const size_t chunk = (size_t)256 << 20;
+  char* stage = (char*)ctx.pinned(std::min(bytes, chunk));
+  for (size_t off = 0; off < bytes; off += chunk) {
+    const size_t len = std::min(chunk, bytes - off);
+    SGF_CUDA(cudaStreamSynchronize(ctx.stream));
+    const char* s = (const char*)src + off;
+    const long long nblk = (long long)((len + (1 << 20) - 1) >> 20);
+#pragma omp parallel for
+    for (long long b = 0; b < nblk; ++b) {
+      const size_t o = (size_t)b << 20;
+      std::memcpy(stage + o, s + o, std::min((size_t)1 << 20, len - o));
+    }
+    SGF_CUDA(cudaMemcpyAsync((char*)dst + off, stage, len, cudaMemcpyHostToDevice, ctx.stream));
+  }
+  SGF_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
   int st = (e == cudaErrorMemoryAllocation) ? SGF_OOM : SGF_CUDA;
@@ -102,19 +121,44 @@ static double useful_flops(const std::vector<GemmTask>& ts, const std::vector<Ge
   return f;
 }
 
+static int trace_level() {
+  static int v = getenv("SGF_TRACE") ? atoi(getenv("SGF_TRACE")) : 0;
+  return v;
+}
+
+// SGF_TRACE=2: time every GEMM launch (synchronising) and print its rate
+static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const GemmSeg* d_segs,
+                        const std::vector<GemmSeg>& segs, int big, cudaStream_t st) {
+  const int bm = big ? 128 : 64;
+  ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(h, segs, bm) : 0.0);
+  if (trace_level() < 2) {
+    SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
+    return;
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+  SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  const double f = useful_flops(h, segs, bm);
+  long long ksum = 0;
+  for (auto& t : h)
+    for (int s = 0; s < t.nseg; ++s) ksum += segs[t.seg0 + s].K;
+  fprintf(stderr, "[gemm] %s tiles=%7zu avgK=%7.0f gflop=%9.3f ms=%8.3f tflops=%6.2f\n", big ? "128" : " 64",
+          h.size(), h.empty() ? 0.0 : (double)ksum / h.size(), f / 1e9, ms, f / (ms * 1e-3) / 1e12);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
 void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
   if (empty()) return;
   GemmSeg* d_segs = scratch.upload(segs);
-  if (!big.empty()) {
-    GemmTask* d = scratch.upload(big);
-    ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(big, segs, 128) : 0.0);
-    SGF_CUDA(launch_gemm(d, (int)big.size(), d_segs, 1, st));
-  }
-  if (!small.empty()) {
-    GemmTask* d = scratch.upload(small);
-    ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(small, segs, 64) : 0.0);
-    SGF_CUDA(launch_gemm(d, (int)small.size(), d_segs, 0, st));
-  }
+  if (!big.empty()) traced_gemm(scratch.upload(big), big, d_segs, segs, 1, st);
+  if (!small.empty()) traced_gemm(scratch.upload(small), small, d_segs, segs, 0, st);
 }
 
 void CopyBatch::launch(Arena& scratch, cudaStream_t st) {

@@ -104,7 +104,27 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::string last_error;
+  // grow-only pinned staging buffer for large host->device uploads; callers
+  // synchronise the stream before reusing it
+  void* pin = nullptr;
+  size_t pin_cap = 0;
+  void* pinned(size_t bytes) {
+    if (bytes > pin_cap) {
+      if (pin) cudaFreeHost(pin);
+      pin = nullptr;
+      pin_cap = 0;
+      SGF_CUDA(cudaMallocHost(&pin, bytes));
+      pin_cap = bytes;
+    }
+    return pin;
+  }
+  ~Ctx() {
+    if (pin) cudaFreeHost(pin);
+  }
 };
+// copy n bytes host -> device through the context's pinned buffer (chunked,
+// parallel host memcpy); synchronises the stream
+void upload_pinned(Ctx& ctx, void* dst, const void* src, size_t bytes);
 
 // ---------------------------------------------------------------------------
 // Block table: symmetric block-sparse trailing matrix, blocks (a,b) a <= b,
@@ -206,7 +226,9 @@ struct GemmBatch {
     if (M <= 0 || N <= 0) return;
     int seg0 = (int)segs.size();
     for (auto& s : sg) segs.push_back(s);
-    bool use_big = force >= 0 ? force == 1 : (M >= 96 && N >= 96);
+    // the 64x64 configuration is the fastest on B200 for every shape measured
+    // (tools/gemm_bench.cu); the 128x128 path stays available via force = 1
+    bool use_big = force == 1;
     int bm = use_big ? 128 : 64, bn = bm;
     auto& dst = use_big ? big : small;
     for (int m0 = 0; m0 < M; m0 += bm)

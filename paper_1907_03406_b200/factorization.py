@@ -18,7 +18,7 @@ import warnings
 import numpy as np
 
 from . import _native as N
-from .basis import build_polynomial_basis
+from .basis import PI_COLS_SCALAR, build_polynomial_basis
 from .errors import ShapeMismatchError
 from .partition import KIND_CODE, build_general_hierarchy, build_nested_hierarchy, level1_unknowns
 
@@ -152,12 +152,13 @@ class Preconditioner(object):
     """
 
     def __init__(self, handle, ctx, n, stats, rank_trace, basis, scheme, degree, mode):
+        # basis: a PolyBasis or a zero-argument callable building it on first use
         self._h = handle
         self._ctx = ctx
         self.n = n
         self.stats = stats
         self.rank_trace = rank_trace
-        self.basis = basis
+        self._basis = basis
         self.scheme = scheme
         self.degree = degree
         self.mode = mode
@@ -171,6 +172,12 @@ class Preconditioner(object):
             except Exception:
                 pass
             self._h = None
+
+    @property
+    def basis(self):
+        if callable(self._basis):
+            self._basis = self._basis()
+        return self._basis
 
     @property
     def factors(self):
@@ -260,7 +267,13 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
     if skip_levels is None:
         skip_levels = default_skip_levels(scheme)
     hier = (build_general_hierarchy if scheme == "gen-all-all" else build_nested_hierarchy)(grid, b)
-    basis = build_polynomial_basis(problem.coords, degree, grid.components_per_vertex)
+    comps = grid.components_per_vertex
+    if degree not in (0, 1, 2):
+        raise ValueError(f"degree must be 0, 1, or 2, got {degree}")
+    if comps not in (1, 3):
+        raise ValueError(f"components must be 1 or 3, got {comps}")
+    coords = np.ascontiguousarray(problem.coords, dtype=np.float64)
+    pi_cols = PI_COLS_SCALAR[degree] * comps
 
     A = problem.matrix.tocsr()
     if not A.has_sorted_indices:
@@ -269,7 +282,6 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
     indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
     indices = np.ascontiguousarray(A.indices, dtype=np.int32)
     values = np.ascontiguousarray(A.data, dtype=np.float64)
-    phi = np.ascontiguousarray(basis.Pi, dtype=np.float64)
     hl = hier.hlevels
     level_ncells = np.array([h.ncells for h in hl], dtype=np.int32)
     kinds = np.ascontiguousarray(np.concatenate([h.kind_code for h in hl]).astype(np.int8))
@@ -288,7 +300,9 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
         if tuple(device_values.shape) != (A.nnz,) or not device_values.is_cuda:
             raise ShapeMismatchError("device_values must be a CUDA vector with one entry per nonzero")
         args.values, args.values_on_device = device_values.data_ptr(), 1
-    args.pi_cols, args.phi = basis.pi_cols, phi.ctypes.data
+    # Pi is built natively from the coordinates (same rule as basis.py)
+    args.pi_cols, args.phi = pi_cols, None
+    args.coords, args.n_vertices, args.degree, args.components = coords.ctypes.data, grid.n_vertices, degree, comps
     args.nlevels = len(hl)
     args.level_ncells = level_ncells.ctypes.data
     args.cell_kind, args.cell_interior, args.father = kinds.ctypes.data, interior.ctypes.data, father.ctypes.data
@@ -333,5 +347,6 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
     tr = np.zeros(max(nt, 1) * 3, dtype=np.int32)
     L.sgf_precond_rank_trace(h, tr.ctypes.data, nt)
     trace = RankTrace([tuple(int(v) for v in tr[3 * i:3 * i + 3]) for i in range(nt)])
+    basis = lambda: build_polynomial_basis(problem.coords, degree, comps)  # noqa: E731
     return Preconditioner(h, ctx, n, stats, trace, basis, scheme, degree,
                           mode if compression else "exact")

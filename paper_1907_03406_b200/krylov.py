@@ -75,21 +75,12 @@ class DeviceCSR(object):
         return y
 
 
-_csr_cache = {}
-
-
 def _as_device_matrix(matvec):
     if isinstance(matvec, DeviceCSR):
         return matvec
     if sp.issparse(matvec):
-        key = id(matvec)
-        hit = _csr_cache.get(key)
-        if hit is not None and hit[0] is matvec:
-            return hit[1]
-        D = DeviceCSR(matvec)
-        _csr_cache.clear()
-        _csr_cache[key] = (matvec, D)
-        return D
+        # a host matrix is uploaded per call (keep a DeviceCSR to reuse it)
+        return DeviceCSR(matvec)
     raise TypeError("pcg needs the operator as a sparse matrix (scipy.sparse or DeviceCSR) so the "
                     "iteration can run on the GPU; Python callables are not executed on the host")
 

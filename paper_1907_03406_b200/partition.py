@@ -170,12 +170,25 @@ class HLevel:
 
     def vertex_order(self):
         """All vertex ids grouped by cell id (cells ascending, vertices
-        ascending within a cell) plus the CSR pointer per cell."""
-        cov = self.cell_of_vertex()
-        order = np.argsort(cov, kind="stable")
+        ascending within a cell) plus the CSR pointer per cell.
+
+        No sort: a vertex's slot is its cell's start plus its rank inside
+        the cell's box (k-major, then j, then i, i.e. ascending vertex id)."""
+        nx, ny, nz = self._grid.dims
+        ax, ay, az = self.axes
         ptr = np.zeros(self.ncells + 1, dtype=np.int64)
-        np.cumsum(np.bincount(cov, minlength=self.ncells), out=ptr[1:])
-        return order.astype(np.int64), ptr
+        np.cumsum(self.cell_sizes(), out=ptr[1:])
+        ty, tz = self.shape[1], self.shape[2]
+        i, j, k = np.arange(nx), np.arange(ny), np.arange(nz)
+        wx = (ax.hi - ax.lo + 1)[ax.rank]              # box width of each index's label
+        wy = (ay.hi - ay.lo + 1)[ay.rank]
+        ox, oy, oz = i - ax.lo[ax.rank], j - ay.lo[ay.rank], k - az.lo[az.rank]
+        cell = (ax.rank[None, None, :] * (ty * tz) + ay.rank[None, :, None] * tz + az.rank[:, None, None])
+        local = (oz[:, None, None] * wy[None, :, None] + oy[None, :, None]) * wx[None, None, :] + ox[None, None, :]
+        slot = (ptr[cell] + local).ravel()
+        order = np.empty(nx * ny * nz, dtype=np.int64)
+        order[slot] = np.arange(nx * ny * nz, dtype=np.int64)
+        return order, ptr
 
 
 class PartitionHierarchy:

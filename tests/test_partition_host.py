@@ -72,3 +72,13 @@ def test_large_hierarchy_is_fast():
     unk, ptr = Pm.level1_unknowns(H)
     assert [h.ncells for h in H.hlevels] == [24389, 3375, 343, 27, 1]
     assert time.perf_counter() - t < 10.0
+
+
+@pytest.mark.parametrize("degree,comps", [(0, 1), (1, 1), (2, 1), (1, 3), (2, 3)])
+def test_basis_bitwise_matches_oracle(degree, comps):
+    from paper_1907_03406_b200.basis import build_polynomial_basis
+    rng = np.random.default_rng(degree + 7 * comps)
+    coords = rng.uniform(-2, 3, (57, 3))
+    coords[:, 2] = 0.0 if degree == 1 else coords[:, 2]      # a zero column
+    B = build_polynomial_basis(coords, degree, comps)
+    assert np.array_equal(B.Pi, O.poly_basis(coords, degree, comps))
