@@ -208,6 +208,8 @@ void setup_level1(State& S) {
       }
     }
   }
+  if (Phase::on()) fprintf(stderr, "[sgf]  s-dst host loop done\n");
+  Phase ph_up(" s-upload", -1, S.st);
   long long* d_dst = S.scratch.alloc_t<long long>(std::max<int64_t>(a.nnz, 1));
   upload_pinned(*S.ctx, d_dst, dst, a.nnz * sizeof(long long));
   const double* d_vals = a.values;

@@ -20,6 +20,8 @@
 // global memory / L2, the current reflector lives in shared memory.
 #include <cfloat>
 #include <cmath>
+#include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -203,16 +205,216 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
   if (tid == 0) { *T.out_rank = rank; *T.out_steps = steps; }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant: one thread-block cluster of QC CTAs per node.  CTA q owns
+// the panel columns at positions j == q (mod QC) (norms, updates); every CTA
+// recomputes the reflector from the pivot column redundantly (identical
+// arithmetic => identical results), so per step the only exchange is the
+// pivot candidates through distributed shared memory and three cluster
+// barriers.  Same arithmetic rules as qrcp_kernel above.
+// ---------------------------------------------------------------------------
+constexpr int QC = 8;             // CTAs per cluster
+constexpr int QCT = 256;          // threads per CTA
+constexpr int QCW = QCT / 32;
+
+__device__ double cblock_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < QCW; ++i) s += red[i];  // fixed order, same in every CTA
+  return s;
+}
+
+__global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
+    qrcp_cluster_kernel(const QrTask* __restrict__ tasks) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double v[];  // m
+  __shared__ double red[QCW];
+  __shared__ double cand_v;
+  __shared__ int cand_i;
+  __shared__ double s_amax;
+  const int q = (int)cluster.block_rank();
+  const QrTask T = tasks[blockIdx.x / QC];
+  const int m = T.m, c = T.c, kmax = min(m, c);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* N = T.Nm;
+  const double eps = DBL_EPSILON;
+
+  // initial norms of owned columns, local max |A|
+  double amax = 0.0;
+  for (int j = q + QC * warp; j < c; j += QC * QCW) {
+    const double* col = N + (long long)j * m;
+    double s = 0.0, mx = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      s = fma(col[i], col[i], s);
+      mx = fmax(mx, fabs(col[i]));
+    }
+    s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    amax = fmax(amax, mx);
+    if (lane == 0) { T.nrm2[j] = s; T.ref2[j] = s; T.perm[j] = j; }
+  }
+  if (lane == 0) red[warp] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < QCW; ++i) mx = fmax(mx, red[i]);
+    s_amax = mx;
+  }
+  cluster.sync();
+  {
+    double mx = 0.0;
+    for (int r = 0; r < QC; ++r) mx = fmax(mx, *cluster.map_shared_rank(&s_amax, r));
+    amax = mx;
+  }
+  const double floor_ = eps * fmax(amax, 1.0);
+  const double floor2 = floor_ * floor_;
+
+  const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
+  int steps = 0;
+  double r00 = 0.0;
+  int pend_k = -1;       // column whose final values (R_kk, v) this CTA still has to store
+  double pend_r = 0.0;
+  for (int k = 0; k < limit; ++k) {
+    // store the previous step's pivot column (everyone has read it)
+    if (pend_k >= 0) {
+      double* col = N + (long long)pend_k * m;
+      for (int i = pend_k + 1 + tid; i < m; i += QCT) col[i] = v[i - pend_k];
+      if (tid == 0) col[pend_k] = pend_r;
+      pend_k = -1;
+    }
+    // local candidate (first max; or the replayed column)
+    const bool rep = T.replay && k < T.nreplay;
+    double bv = rep ? 0.0 : -1.0;
+    int bi = c;
+    for (int j = k + ((q - k) % QC + QC) % QC + QC * tid; j < c; j += QC * QCT) {
+      if (rep) {
+        if (T.perm[j] == T.replay[k]) { bi = j; bv = 1.0; }
+      } else {
+        const double x = T.nrm2[j];
+        if (x > bv) { bv = x; bi = j; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    __shared__ double wv[QCW];
+    __shared__ int wi[QCW];
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = wv[0];
+      int i0 = wi[0];
+      for (int w = 1; w < QCW; ++w)
+        if (wv[w] > b || (wv[w] == b && wi[w] < i0)) { b = wv[w]; i0 = wi[w]; }
+      cand_v = b;
+      cand_i = i0;
+    }
+    cluster.sync();  // B1: candidates visible
+    int piv = c;
+    {
+      double b = -2.0;
+      for (int r = 0; r < QC; ++r) {
+        const double ov = *cluster.map_shared_rank(&cand_v, r);
+        const int oi = *cluster.map_shared_rank(&cand_i, r);
+        if (oi >= c) continue;
+        if (ov > b || (ov == b && oi < piv)) { b = ov; piv = oi; }
+      }
+    }
+    if (piv >= c) break;  // malformed replay
+    if (T.nrm2[piv] <= floor2) break;
+    if (piv != k && q == 0) {
+      double* a = N + (long long)k * m;
+      double* b = N + (long long)piv * m;
+      for (int i = tid; i < m; i += QCT) { const double t2 = a[i]; a[i] = b[i]; b[i] = t2; }
+      if (tid == 0) {
+        double t2 = T.nrm2[k]; T.nrm2[k] = T.nrm2[piv]; T.nrm2[piv] = t2;
+        t2 = T.ref2[k]; T.ref2[k] = T.ref2[piv]; T.ref2[piv] = t2;
+        int ti = T.perm[k]; T.perm[k] = T.perm[piv]; T.perm[piv] = ti;
+      }
+    }
+    cluster.sync();  // B2: pivot column in place
+    const double* xk = N + (long long)k * m;
+    double ss = 0.0;
+    for (int i = k + tid; i < m; i += QCT) ss = fma(xk[i], xk[i], ss);
+    const double xn = sqrt(cblock_sum(ss, red));
+    if (xn <= floor_) break;
+    if (k == 0) r00 = xn;
+    if (T.forced_rank < 0 && !(xn > T.tol * r00)) break;
+    const double x0 = xk[k];
+    const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
+    const double u1 = x0 - sgn * xn;
+    const double tau = -sgn * u1 / xn;
+    for (int i = k + tid; i < m; i += QCT) v[i - k] = (i == k) ? 1.0 : xk[i] / u1;
+    __syncthreads();
+    const int len = m - k;
+    for (int j = k + 1 + ((q - k - 1) % QC + QC) % QC + QC * warp; j < c; j += QC * QCW) {
+      double* col = N + (long long)j * m + k;
+      double s = 0.0;
+      for (int i = lane; i < len; i += 32) s = fma(v[i], col[i], s);
+      s = warp_sum(s);
+      const double ts = tau * s;
+      double fresh = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        const double nv = fma(-ts, v[i], col[i]);
+        col[i] = nv;
+        if (i > 0) fresh = fma(nv, nv, fresh);
+      }
+      fresh = warp_sum(fresh);
+      if (lane == 0) {
+        const double rkj = col[0];
+        double nn = fmax(T.nrm2[j] - rkj * rkj, 0.0);
+        if (nn <= eps * T.ref2[j]) {
+          nn = fresh;
+          T.ref2[j] = fmax(fresh, floor2);
+        }
+        T.nrm2[j] = nn;
+      }
+    }
+    if (k % QC == q) {
+      pend_k = k;
+      pend_r = sgn * xn;
+      if (tid == 0) T.tau[k] = tau;
+    }
+    steps = k + 1;
+    cluster.sync();  // B3: updates and norms visible; column k read by all
+  }
+  if (pend_k >= 0) {
+    double* col = N + (long long)pend_k * m;
+    for (int i = pend_k + 1 + tid; i < m; i += QCT) col[i] = v[i - pend_k];
+    if (tid == 0) col[pend_k] = pend_r;
+  }
+  if (q == 0 && tid == 0) {
+    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : steps;
+    *T.out_steps = steps;
+  }
+  cluster.sync();  // keep every CTA's shared memory alive for remote reads
+}
+
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = (size_t)max_m * sizeof(double);
   static size_t configured = 48 * 1024;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  count_launch(); qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
+  static int single = getenv("SGF_QR_SINGLE_CTA") ? 1 : 0;
+  count_launch();
+  if (single) qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
+  else qrcp_cluster_kernel<<<ntasks * QC, QCT, smem, s>>>(d_tasks);
   return cudaGetLastError();
 }
 

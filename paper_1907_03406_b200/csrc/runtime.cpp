@@ -3,7 +3,10 @@
 // compression and the final dense factor.
 #include "runtime.h"
 
+#include <chrono>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 namespace sgf {
 
@@ -89,17 +92,69 @@ void* Arena::alloc_bytes(size_t bytes) {
     }
   }
   size_t cap = std::max(bytes, chunk_);
-  void* p = nullptr;
-  SGF_CUDA(cudaMallocAsync(&p, cap, s_));
+  void* p = chunk_get(cap, &cap);
   chunks_.push_back(Chunk{(char*)p, cap, bytes});
   used_ += bytes;
   return p;
 }
 
 void Arena::release() {
-  for (auto& c : chunks_) cudaFreeAsync(c.base, s_);
+  for (auto& c : chunks_) chunk_put(c.base, c.cap);
   chunks_.clear();
   used_ = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Process-wide cache of device chunks.  All library work of a context runs on
+// one stream, so a chunk handed back by a finished phase can be reused by
+// work enqueued later without synchronisation.  Repeated factorizations of
+// the same problem then allocate nothing (cudaMalloc only when growing; the
+// cache is emptied and the allocation retried on out-of-memory).
+// ---------------------------------------------------------------------------
+namespace {
+std::mutex g_cache_mu;
+std::multimap<size_t, void*> g_cache;  // cap -> chunk
+}  // namespace
+
+void* chunk_get(size_t bytes, size_t* cap) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.lower_bound(bytes);
+    if (it != g_cache.end() && it->first <= 2 * bytes + ((size_t)64 << 20)) {
+      void* p = it->second;
+      *cap = it->first;
+      g_cache.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  static const bool trace = getenv("SGF_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    chunk_trim();
+    e = cudaMalloc(&p, bytes);
+  }
+  SGF_CUDA(e);
+  if (trace) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 1.0) fprintf(stderr, "[alloc] %.1f MB took %.2f ms\n", bytes / 1048576.0, ms);
+  }
+  *cap = bytes;
+  return p;
+}
+
+void chunk_put(void* p, size_t cap) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.emplace(cap, p);
+}
+
+void chunk_trim() {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& kv : g_cache) cudaFree(kv.second);
+  g_cache.clear();
 }
 
 // flops the tiles actually multiply (k range per segment after the

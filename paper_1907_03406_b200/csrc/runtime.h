@@ -68,8 +68,13 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// process-wide device chunk cache (runtime.cpp)
+void* chunk_get(size_t bytes, size_t* cap);
+void chunk_put(void* p, size_t cap);
+void chunk_trim();
+
 // ---------------------------------------------------------------------------
-// Device bump arena (stream-ordered chunks from the CUDA memory pool).
+// Device bump arena (chunks from the process-wide cache).
 // ---------------------------------------------------------------------------
 class Arena {
  public:
