@@ -66,7 +66,14 @@ struct ApplyPlan {
   double *xb = nullptr, *zb = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr, *acc = nullptr;
   double* work = nullptr;  // n-vector (apply in place)
   long long n = 0;
+  // CUDA graphs of the sweeps on `work` (index = op), captured on first use
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  unsigned long long graph_launches[3] = {0, 0, 0};
   explicit ApplyPlan(cudaStream_t s) : mem(s, (size_t)64 << 20) {}
+  ~ApplyPlan() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+  }
 };
 
 void destroy_plan(ApplyPlan* p) { delete p; }
@@ -262,15 +269,40 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
 }
 
 // y and x are device n-vectors; y may alias x
+static void sweeps(ApplyPlan* pl, int op, double* y, cudaStream_t st) {
+  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE)
+    for (auto& g : pl->groups) forward_group(pl, g, y, st);
+  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE_T)
+    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) backward_group(pl, *it, y, st);
+}
+
 void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   cudaStream_t st = P->ctx->stream;
   ApplyPlan* pl = P->plan;
-  if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (op == SGF_APPLY_OPERATOR) fail(SGF_INVALID_ARG, "apply_operator is not available in this build");
-  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE)
-    for (auto& g : pl->groups) forward_group(pl, g, d_y, st);
-  if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE_T)
-    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) backward_group(pl, *it, d_y, st);
+  if (op < 0 || op > 2) fail(SGF_INVALID_ARG, "unknown apply operation");
+  static const bool no_graph = getenv("SGF_NO_GRAPH") != nullptr;
+  if (g_prof.on || no_graph) {  // per-kernel timing needs eager launches
+    if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    sweeps(pl, op, d_y, st);
+    return;
+  }
+  // the whole sweep sequence (~100 launches) replays as one CUDA graph on
+  // the plan's work vector
+  if (!pl->graph[op]) {
+    cudaGraph_t g;
+    SGF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const unsigned long long before = g_kernel_launches;
+    sweeps(pl, op, pl->work, st);
+    SGF_CUDA(cudaStreamEndCapture(st, &g));
+    pl->graph_launches[op] = g_kernel_launches - before;
+    SGF_CUDA(cudaGraphInstantiate(&pl->graph[op], g, 0));
+    cudaGraphDestroy(g);
+  }
+  SGF_CUDA(cudaMemcpyAsync(pl->work, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  SGF_CUDA(cudaGraphLaunch(pl->graph[op], st));
+  count_launch(pl->graph_launches[op]);
+  SGF_CUDA(cudaMemcpyAsync(d_y, pl->work, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
 
 // ---------------------------------------------------------------------------

@@ -50,7 +50,7 @@ struct DiagTask {
   double* Dinv;     // 64 x 64 scratch for this node's current panel
   int ld;
   int k0, nb;
-  double floor;     // CHOL_PIVOT_RTOL * max(diag(A_BB), 0)
+  const double* floor;  // device: CHOL_PIVOT_RTOL * max(diag(A_BB), 0)
   int node;         // index into the status array
 };
 
@@ -104,6 +104,22 @@ struct QrFinishTask {
   double* Q1;         // m x cap_r
   double* G;          // cap_s x cap_s scratch (reflector Gram matrix)
   int m;
+};
+
+// CSR -> level-1 block scatter parameters (dense_kernels.cu)
+struct CsrScatter {
+  const long long* indptr;
+  const int* indices;
+  const double* values;
+  const int* owner;
+  const int* local;
+  const int* size;           // per cell
+  const long long* diag_off;
+  const int* up_ptr;         // per cell: coupled cells b > a, ascending
+  const int* up_cell;
+  const long long* up_off;
+  double* base;
+  long long n;
 };
 
 // out[k] = base[k] + sign * sum_{q<nrb} part[q*stride + k], k < n

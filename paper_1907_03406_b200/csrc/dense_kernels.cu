@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) diag_chol_kernel(const DiagTask* __restri
     if (i < nb && sub == 0) col[i] = S[i][j] - acc;
     __syncthreads();
     const double d = col[j];
-    if (!(d > T.floor) || !isfinite(d)) {
+    if (!(d > *T.floor) || !isfinite(d)) {
       if (tid == 0 && status[T.node] == 0) {
         status[T.node] = T.k0 + j + 1;
         pivval[T.node] = d;
@@ -184,6 +184,37 @@ cudaError_t launch_scatter_values(const double* vals, const long long* dst, long
   long long blocks = (nnz + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   count_launch(); scatter_values_kernel<<<(unsigned)blocks, 256, 0, s>>>(vals, dst, nnz, base);
+  return cudaGetLastError();
+}
+
+// CSR -> level-1 blocks (blockmatrix.py:97-144): one thread per row; an entry
+// (r, col) goes to block (owner[r], owner[col]) when owner[r] <= owner[col]
+// (the other orientation is written by its symmetric partner).
+__global__ void __launch_bounds__(256) csr_scatter_kernel(const CsrScatter P) {
+  for (long long r = blockIdx.x * 256LL + threadIdx.x; r < P.n; r += (long long)gridDim.x * 256) {
+    const int ca = P.owner[r];
+    const long long lr = P.local[r];
+    const int u0 = P.up_ptr[ca], u1 = P.up_ptr[ca + 1];
+    for (long long e = P.indptr[r]; e < P.indptr[r + 1]; ++e) {
+      const int col = P.indices[e];
+      const int cb = P.owner[col];
+      if (cb == ca) {
+        P.base[P.diag_off[ca] + lr * P.size[ca] + P.local[col]] = P.values[e];
+      } else if (cb > ca) {
+        int j = u0;
+        while (j < u1 && P.up_cell[j] != cb) ++j;
+        if (j < u1) P.base[P.up_off[j] + lr * P.size[cb] + P.local[col]] = P.values[e];
+      }
+    }
+  }
+}
+
+cudaError_t launch_csr_scatter(const void* params, cudaStream_t s) {
+  const CsrScatter& P = *(const CsrScatter*)params;
+  if (P.n <= 0) return cudaSuccess;
+  long long blocks = (P.n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  count_launch(); csr_scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(P);
   return cudaGetLastError();
 }
 

@@ -49,11 +49,13 @@ struct State {
   std::vector<Node> nodes;
   std::unique_ptr<Arena> lvl;  // blocks + phi of the current level
   Arena scratch;
+  Arena persist;   // lives for the whole factorization (deferred status buffers)
+  CholCheck chk;   // Cholesky breakdowns, verified at host sync points
   long long flops = 0;
   long long peak = 0;
   int comp_counter = 0;  // compressions so far (reference execution order)
   Precond* P;
-  explicit State(cudaStream_t s) : scratch(s) {}
+  explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
 };
 
 inline bool kind_in(int mask, int kind) { return (mask >> kind) & 1; }
@@ -187,38 +189,46 @@ void setup_level1(State& S) {
       off += (long long)sizes[c] * sizes[b];
     }
   }
-  // per-nnz destination offsets (entries stored once: the (min,max) orientation)
-  Phase ph_dst(" s-dst", -1, S.st);
-  std::vector<long long> dstv(std::max<int64_t>(a.nnz, 1));
-  long long* dst = dstv.data();
-#pragma omp parallel for schedule(dynamic, 4096)
-  for (int64_t r = 0; r < n; ++r) {
-    const int ca = owner[r];
-    for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
-      const int32_t col = a.indices[e];
-      const int cb = owner[col];
-      if (cb == ca) {
-        dst[e] = diag_off[ca] + (long long)local[r] * sizes[ca] + local[col];
-      } else if (ca < cb) {
-        const auto& v = up[ca];
-        const size_t j = std::lower_bound(v.begin(), v.end(), cb) - v.begin();
-        dst[e] = up_off[ca][j] + (long long)local[r] * sizes[cb] + local[col];
-      } else {
-        dst[e] = -1;  // written by the symmetric partner
-      }
+  // scatter the CSR entries into the blocks on the device (entries stored
+  // once, in the (min,max) orientation)
+  Phase ph_dst(" s-scatter", -1, S.st);
+  {
+    std::vector<int> up_ptr(nc + 1, 0), up_cell;
+    std::vector<long long> up_o;
+    for (int c = 0; c < nc; ++c) {
+      up_ptr[c + 1] = up_ptr[c] + (int)up[c].size();
+      up_cell.insert(up_cell.end(), up[c].begin(), up[c].end());
+      up_o.insert(up_o.end(), up_off[c].begin(), up_off[c].end());
     }
+    CsrScatter P;
+    long long* d_ip = S.scratch.alloc_t<long long>(n + 1);
+    int* d_ix = S.scratch.alloc_t<int>(std::max<int64_t>(a.nnz, 1));
+    int* d_own = S.scratch.alloc_t<int>(n);
+    int* d_loc = S.scratch.alloc_t<int>(n);
+    upload_pinned(*S.ctx, d_ip, a.indptr, (n + 1) * sizeof(long long));
+    upload_pinned(*S.ctx, d_ix, a.indices, a.nnz * sizeof(int));
+    upload_pinned(*S.ctx, d_own, owner.data(), n * sizeof(int));
+    upload_pinned(*S.ctx, d_loc, local.data(), n * sizeof(int));
+    const double* d_vals = a.values;
+    if (!a.values_on_device) {
+      double* dv = S.scratch.alloc(std::max<int64_t>(a.nnz, 1));
+      upload_pinned(*S.ctx, dv, a.values, a.nnz * sizeof(double));
+      d_vals = dv;
+    }
+    P.indptr = d_ip;
+    P.indices = d_ix;
+    P.values = d_vals;
+    P.owner = d_own;
+    P.local = d_loc;
+    P.size = S.scratch.upload(sizes);
+    P.diag_off = S.scratch.upload(diag_off);
+    P.up_ptr = S.scratch.upload(up_ptr);
+    P.up_cell = up_cell.empty() ? d_own : S.scratch.upload(up_cell);
+    P.up_off = up_o.empty() ? d_ip : S.scratch.upload(up_o);
+    P.base = base;
+    P.n = n;
+    SGF_CUDA(launch_csr_scatter(&P, S.st));
   }
-  if (Phase::on()) fprintf(stderr, "[sgf]  s-dst host loop done\n");
-  Phase ph_up(" s-upload", -1, S.st);
-  long long* d_dst = S.scratch.alloc_t<long long>(std::max<int64_t>(a.nnz, 1));
-  upload_pinned(*S.ctx, d_dst, dst, a.nnz * sizeof(long long));
-  const double* d_vals = a.values;
-  if (!a.values_on_device) {
-    double* dv = S.scratch.alloc(a.nnz);
-    upload_pinned(*S.ctx, dv, a.values, a.nnz * sizeof(double));
-    d_vals = dv;
-  }
-  SGF_CUDA(launch_scatter_values(d_vals, d_dst, a.nnz, base, S.st));
 
   // basis rows of every node: Pi[active] in cell order
   Phase ph_phi(" s-phi", -1, S.st);
@@ -309,7 +319,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     jobs.push_back(CholJob{e.W, e.X, e.m, e.x});
   }
   cp.launch(S.scratch, st);
-  chol_inv_batch(*S.ctx, S.scratch, jobs);
+  chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
 
   GemmBatch ge;
   for (auto& e : info) {
@@ -411,7 +421,9 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.m, e.m, 1,
                        e.E + (long long)e.off[c.second.second] * e.m, e.m, 1, e.m));
     }
-    gs.add(blk->p, blk->cols, 1, blk->rows, blk->cols, -1.0, 1.0, sg);
+    // diagonal blocks are kept valid in their lower triangle only: every
+    // consumer (Cholesky of the node, densify + Cholesky) reads only that
+    gs.add(blk->p, blk->cols, 1, blk->rows, blk->cols, -1.0, 1.0, sg, -1, T.a == T.b);
   }
   gs.launch(S.scratch, st);
 }
@@ -475,7 +487,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     jobs.push_back(CholJob{c.L, c.X, c.m, c.c});
   }
   cp.launch(S.scratch, st);
-  chol_inv_batch(*S.ctx, S.scratch, jobs);
+  chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
 
   // L^T Phi_B and the filtered products M_BN Phi_N
   GemmBatch g1;
@@ -545,6 +557,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   std::vector<int> rs(2 * nw);
   SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));
   SGF_CUDA(cudaStreamSynchronize(st));
+  S.chk.verify(st);  // a breakdown upstream must surface before ranks are used
 
   // reflectors, compact-WY T, Q1
   std::vector<QrFinishTask> ft(nw);
@@ -839,7 +852,6 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
   {
     Phase ph(" m-copy", -1, st);
     cp.launch(S.scratch, st);
-    SGF_CUDA(cudaStreamSynchronize(st));
   }
   {
     Phase ph(" m-free", -1, st);
@@ -884,7 +896,7 @@ void final_dense(State& S) {
   }
   cp.launch(S.scratch, st);
   std::vector<CholJob> jobs{CholJob{D, X, tot, -1}};
-  chol_inv_batch(*S.ctx, S.scratch, jobs);
+  chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
   S.flops += (long long)tot * tot * tot / 3;
   Factor f;
   f.type = SGF_FACTOR_DENSE;
@@ -968,8 +980,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       if (S.nodes[c].interior && !S.nodes[c].active.empty()) elim.push_back(c);
     { Phase ph("eliminate", t + 1, S.st); eliminate_level(S, elim, t + 1); }
     ls.eliminated = (int)elim.size();
-    SGF_CUDA(cudaStreamSynchronize(S.st));
-    S.scratch.release();
+    S.scratch.release();  // chunks are reused in stream order: no sync needed
     if (compression && (t + 1) > a.skip_levels) {
       std::vector<int> comp;
       for (int c = 0; c < (int)S.nodes.size(); ++c)
@@ -1004,7 +1015,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
              a.trace[3 * S.comp_counter], a.trace[3 * S.comp_counter + 1], a.trace[3 * S.comp_counter + 2]);
     fail(SGF_TRACE, buf);
   }
-  SGF_CUDA(cudaStreamSynchronize(S.st));
+  S.chk.verify(S.st);
   S.scratch.release();
   S.lvl.reset();
   long long fa = 0;

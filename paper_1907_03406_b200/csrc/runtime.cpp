@@ -113,17 +113,52 @@ void Arena::release() {
 // ---------------------------------------------------------------------------
 namespace {
 std::mutex g_cache_mu;
-std::multimap<size_t, void*> g_cache;  // cap -> chunk
+std::map<int, std::multimap<size_t, void*>> g_cache;  // device -> (cap -> chunk)
+
+struct Stager {
+  char* buf = nullptr;
+  size_t cap = 0, off = 0;
+};
+std::mutex g_stage_mu;
+std::map<cudaStream_t, Stager> g_stage;
 }  // namespace
 
+void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Stager& s = g_stage[st];
+  const size_t need = (bytes + 255) & ~(size_t)255;
+  if (s.off + need > s.cap) {
+    SGF_CUDA(cudaStreamSynchronize(st));  // every staged copy has landed
+    s.off = 0;
+    if (need > s.cap) {
+      if (s.buf) cudaFreeHost(s.buf);
+      s.cap = std::max(need, (size_t)256 << 20);
+      SGF_CUDA(cudaMallocHost((void**)&s.buf, s.cap));
+    }
+  }
+  char* p = s.buf + s.off;
+  s.off += need;
+  std::memcpy(p, src, bytes);
+  SGF_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));
+}
+
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
 void* chunk_get(size_t bytes, size_t* cap) {
+  const int dev = cur_device();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.lower_bound(bytes);
-    if (it != g_cache.end() && it->first <= 2 * bytes + ((size_t)64 << 20)) {
+    auto& cache = g_cache[dev];
+    auto it = cache.lower_bound(bytes);
+    if (it != cache.end() && it->first <= 2 * bytes + ((size_t)64 << 20)) {
       void* p = it->second;
       *cap = it->first;
-      g_cache.erase(it);
+      cache.erase(it);
       return p;
     }
   }
@@ -146,15 +181,17 @@ void* chunk_get(size_t bytes, size_t* cap) {
 }
 
 void chunk_put(void* p, size_t cap) {
+  const int dev = cur_device();
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  g_cache.emplace(cap, p);
+  g_cache[dev].emplace(cap, p);
 }
 
 void chunk_trim() {
   cudaDeviceSynchronize();
+  const int dev = cur_device();
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto& kv : g_cache) cudaFree(kv.second);
-  g_cache.clear();
+  for (auto& kv : g_cache[dev]) cudaFree(kv.second);
+  g_cache[dev].clear();
 }
 
 // flops the tiles actually multiply (k range per segment after the
@@ -257,7 +294,30 @@ void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tas
 //      X[k, :k0]    = -D_k T_k                            (inverse, part 2)
 // The breakdown rule is the reference's (densela.py:105-110).
 // ---------------------------------------------------------------------------
-void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
+void CholCheck::verify(cudaStream_t st) {
+  if (pend.empty()) return;
+  SGF_CUDA(cudaStreamSynchronize(st));
+  for (auto& p : pend) {
+    const int nj = (int)p.nodes.size();
+    std::vector<int> status(nj);
+    std::vector<double> piv(nj);
+    SGF_CUDA(cudaMemcpy(status.data(), p.status, nj * sizeof(int), cudaMemcpyDeviceToHost));
+    SGF_CUDA(cudaMemcpy(piv.data(), p.piv, nj * sizeof(double), cudaMemcpyDeviceToHost));
+    int worst = -1;
+    for (int i = 0; i < nj; ++i)
+      if (status[i] != 0 && (worst < 0 || p.nodes[i] < p.nodes[worst])) worst = i;
+    if (worst >= 0) {
+      char buf[256];
+      snprintf(buf, sizeof buf, "non-positive pivot %.3e at index %d (node %d)", piv[worst], status[worst] - 1,
+               p.nodes[worst]);
+      pend.clear();
+      fail(SGF_NOT_SPD, buf);
+    }
+  }
+  pend.clear();
+}
+
+void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check) {
   if (jobs.empty()) return;
   cudaStream_t st = ctx.stream;
   const int nj = (int)jobs.size();
@@ -269,23 +329,22 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
     ms[i] = jobs[i].m;
     mmax = std::max(mmax, jobs[i].m);
   }
+  // breakdown status lives as long as the check that will read it
+  Arena& keep = check ? *check->arena : scratch;
   double* d_floor = scratch.alloc(nj);
   {
     const double** d_wp = scratch.upload(wp);
     int* d_m = scratch.upload(ms);
     SGF_CUDA(launch_max_diag(d_wp, d_m, d_m, nj, d_floor, st));
   }
-  std::vector<double> floors(nj);
-  SGF_CUDA(cudaMemcpyAsync(floors.data(), d_floor, nj * sizeof(double), cudaMemcpyDeviceToHost, st));
-  int* d_status = scratch.alloc_t<int>(nj);
-  double* d_piv = scratch.alloc(nj);
+  int* d_status = keep.alloc_t<int>(nj);
+  double* d_piv = keep.alloc(nj);
   SGF_CUDA(cudaMemsetAsync(d_status, 0, nj * sizeof(int), st));
   std::vector<double*> dinv(nj), tk(nj);
   for (int i = 0; i < nj; ++i) {
     dinv[i] = scratch.alloc(64 * 64);
     tk[i] = scratch.alloc((size_t)64 * std::max(jobs[i].m, 1));
   }
-  SGF_CUDA(cudaStreamSynchronize(st));  // floors
 
   for (int k0 = 0; k0 < mmax; k0 += 64) {
     GemmBatch ga, gc;
@@ -311,7 +370,7 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
       d.ld = m;
       d.k0 = k0;
       d.nb = nb;
-      d.floor = floors[i];
+      d.floor = d_floor + i;
       d.node = i;
       dt.push_back(d);
       xd.push_back(X);
@@ -337,20 +396,14 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs) {
   for (auto& j : jobs) tri.push_back(TriTask{j.W, j.m, j.m});
   zero_upper(scratch, st, tri);
 
-  std::vector<int> status(nj);
-  std::vector<double> piv(nj);
-  SGF_CUDA(cudaMemcpyAsync(status.data(), d_status, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
-  SGF_CUDA(cudaMemcpyAsync(piv.data(), d_piv, nj * sizeof(double), cudaMemcpyDeviceToHost, st));
-  SGF_CUDA(cudaStreamSynchronize(st));
-  int worst = -1;
-  for (int i = 0; i < nj; ++i)
-    if (status[i] != 0 && (worst < 0 || jobs[i].node < jobs[worst].node)) worst = i;
-  if (worst >= 0) {
-    char buf[256];
-    snprintf(buf, sizeof buf, "non-positive pivot %.3e at index %d (node %d)", piv[worst], status[worst] - 1,
-             jobs[worst].node);
-    fail(SGF_NOT_SPD, buf);
-  }
+  CholCheck local;
+  CholCheck& chk = check ? *check : local;
+  CholCheck::Pending p;
+  p.status = d_status;
+  p.piv = d_piv;
+  for (auto& j : jobs) p.nodes.push_back(j.node);
+  chk.pend.push_back(std::move(p));
+  if (!check) chk.verify(st);
 }
 
 }  // namespace sgf

@@ -32,6 +32,7 @@ cudaError_t launch_copy_tiled(const CopyTask* d_tasks, const long long* d_prefix
 cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, int ntasks, long long ntiles,
                               cudaStream_t s);
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
+cudaError_t launch_csr_scatter(const void* params, cudaStream_t s);
 cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, cudaStream_t s);
 cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s);
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
@@ -68,10 +69,16 @@ struct ProfScope {
   ~ProfScope();
 };
 
-// process-wide device chunk cache (runtime.cpp)
+// process-wide device chunk cache (runtime.cpp), per device
 void* chunk_get(size_t bytes, size_t* cap);
 void chunk_put(void* p, size_t cap);
 void chunk_trim();
+
+// Asynchronous small host->device upload through a pinned staging ring (a
+// cudaMemcpyAsync from pageable memory would synchronise the stream first
+// and serialise host planning with device execution).  The ring is recycled
+// with a stream synchronisation only when it is full.
+void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes);
 
 // ---------------------------------------------------------------------------
 // Device bump arena (chunks from the process-wide cache).
@@ -91,7 +98,7 @@ class Arena {
   T* upload(const std::vector<T>& v) {
     if (v.empty()) return nullptr;
     T* d = alloc_t<T>(v.size());
-    SGF_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s_));
+    stage_upload(s_, d, v.data(), v.size() * sizeof(T));
     return d;
   }
   void release();
@@ -226,8 +233,10 @@ struct GemmBatch {
   long long flops = 0;  // executed flops (information)
 
   // add all tiles of C(MxN) = beta*C + alpha * sum(segs)
+  // lower_only: C is a symmetric diagonal block kept valid in its lower
+  // triangle only; tiles strictly above the diagonal are skipped
   void add(double* C, long long c_rs, long long c_cs, int M, int N, double alpha, double beta,
-           const std::vector<GemmSeg>& sg, int force = -1) {
+           const std::vector<GemmSeg>& sg, int force = -1, bool lower_only = false) {
     if (M <= 0 || N <= 0) return;
     int seg0 = (int)segs.size();
     for (auto& s : sg) segs.push_back(s);
@@ -238,6 +247,7 @@ struct GemmBatch {
     auto& dst = use_big ? big : small;
     for (int m0 = 0; m0 < M; m0 += bm)
       for (int n0 = 0; n0 < N; n0 += bn) {
+        if (lower_only && n0 >= m0 + bm) continue;
         GemmTask t;
         t.C = C;
         t.c_rs = c_rs;
@@ -298,6 +308,19 @@ struct CholJob {
   int m;
   int node;  // for error messages
 };
-void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs);
+// Breakdown statuses of Cholesky batches whose check is deferred (no host
+// synchronisation per batch); verify() syncs and raises NotSPD for the
+// earliest failing batch, lowest node id first (densela.py:106-110).
+struct CholCheck {
+  Arena* arena = nullptr;  // owns the status buffers until verify()
+  struct Pending {
+    int* status;
+    double* piv;
+    std::vector<int> nodes;
+  };
+  std::vector<Pending> pend;
+  void verify(cudaStream_t st);
+};
+void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check = nullptr);
 
 }  // namespace sgf
