@@ -437,8 +437,16 @@ struct CompOut {
   int rank;
 };
 
+// per compressed node, prepared for the whole level before the wavefronts:
+// the node's diagonal block and basis rows do not change until its own
+// compression, so every Cholesky + inverse and L^T Phi runs in one batch
+struct CompPre {
+  double *L, *X, *LP;
+};
+
 void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int>& seqno,
-                   const std::vector<int>& forced, int level, std::vector<CompOut>& out) {
+                   const std::vector<int>& forced, int level, std::vector<CompOut>& out,
+                   std::unordered_map<int, CompPre>& pre) {
   cudaStream_t st = S.st;
   BlockTable& M = S.M;
   Precond* P = S.P;
@@ -456,8 +464,6 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   };
   const int nw = (int)wave.size();
   std::vector<CI> ci(nw);
-  CopyBatch cp;
-  std::vector<CholJob> jobs;
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
     c.c = wave[w];
@@ -470,30 +476,21 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
       c.col.push_back(c.cN);
       c.cN += raw ? M.size[j] : pi;
     }
-    const size_t mm = (size_t)c.m * c.m;
-    c.L = P->store.alloc(mm);
-    c.X = P->store.alloc(mm);
-    SGF_CUDA(cudaMemsetAsync(c.X, 0, mm * sizeof(double), st));
-    c.LP = S.scratch.alloc((size_t)c.m * pi);
+    const CompPre& pr = pre.at(c.c);
+    c.L = pr.L;
+    c.X = pr.X;
+    c.LP = pr.LP;
     c.N = S.scratch.alloc((size_t)c.m * std::max(c.cN, 1));
     const int kmax = std::max(std::min(c.m, c.cN), 1);
     c.tau = S.scratch.alloc(kmax);
     c.nrm2 = S.scratch.alloc(std::max(c.cN, 1));
     c.ref2 = S.scratch.alloc(std::max(c.cN, 1));
     c.perm = S.scratch.alloc_t<int>(std::max(c.cN, 1));
-    Blk* d = M.find(c.c, c.c);
-    if (!d) fail(SGF_NOT_SPD, "compressed node without a diagonal block");
-    cp.add(d->p, d->cols, 1, c.L, c.m, 1, c.m, c.m);
-    jobs.push_back(CholJob{c.L, c.X, c.m, c.c});
   }
-  cp.launch(S.scratch, st);
-  chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
 
-  // L^T Phi_B and the filtered products M_BN Phi_N
+  // the filtered products M_BN Phi_N
   GemmBatch g1;
   for (auto& c : ci) {
-    g1.add(c.LP, pi, 1, c.m, pi, 1.0, 0.0,
-           {seg(c.L, 1, c.m, S.nodes[c.c].phi, 1, pi, c.m, SEG_KSTART_M)});
     c.Z.assign(c.nb.size(), nullptr);
     for (size_t q = 0; q < c.nb.size(); ++q) {
       if (c.raw[q]) continue;
@@ -559,15 +556,16 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   SGF_CUDA(cudaStreamSynchronize(st));
   S.chk.verify(st);  // a breakdown upstream must surface before ranks are used
 
-  // reflectors, compact-WY T, Q1
+  // reflectors V and the compact-WY T (Q = H_0...H_{s-1} = I - V T V^T)
   std::vector<QrFinishTask> ft(nw);
-  std::vector<double*> V(nw), Tw(nw), Q1(nw);
+  std::vector<double*> V(nw), Tw(nw), G(nw);
+  GemmBatch gg;
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
-    const int r = rs[w], s = rs[nw + w];
+    const int s = rs[nw + w];
     V[w] = s ? P->store.alloc((size_t)c.m * s) : nullptr;
     Tw[w] = s ? P->store.alloc((size_t)s * s) : nullptr;
-    Q1[w] = r ? S.scratch.alloc((size_t)c.m * r) : nullptr;
+    G[w] = s ? S.scratch.alloc((size_t)s * s) : nullptr;
     QrFinishTask& f = ft[w];
     f.Nm = c.N;
     f.tau = c.tau;
@@ -575,42 +573,55 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     f.rank = d_out + w;
     f.V = V[w];
     f.Tm = Tw[w];
-    f.Q1 = Q1[w];
-    f.G = s ? S.scratch.alloc((size_t)s * s) : nullptr;
+    f.Q1 = nullptr;
+    f.G = G[w];
     f.m = c.m;
+    if (s) gg.add(G[w], s, 1, s, s, 1.0, 0.0, {seg(V[w], c.m, 1, V[w], c.m, 1, c.m)});
   }
   {
     QrFinishTask* d_ft = S.scratch.upload(ft);
     ProfScope ps(st, PROF_QR, 0.0);
-    SGF_CUDA(launch_qr_finish(d_ft, nw, st));
+    SGF_CUDA(launch_qr_finish(d_ft, nw, 0, st));
+    gg.launch(S.scratch, st);
+    SGF_CUDA(launch_qr_finish(d_ft, nw, 1, st));
   }
-  // inv = Q^T L^{-1} = L^{-1} - V T^T V^T L^{-1}
-  std::vector<double*> inv(nw), Y(nw), Y2(nw);
+  // inv = Q^T L^{-1} = L^{-1} - V T^T (V^T L^{-1}) and the basis update
+  // Q1^T L^T Phi = first r rows of (L^T Phi - V T^T (V^T L^T Phi))
+  std::vector<double*> inv(nw), Y(nw), Y2(nw), Zp(nw), Zp2(nw);
+  std::vector<double*> newphi(nw, nullptr);
   CopyBatch ci0;
   GemmBatch gy, gy2, gin;
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
-    const int s = rs[nw + w];
+    const int r = rs[w], s = rs[nw + w];
     inv[w] = P->store.alloc((size_t)c.m * c.m);
     ci0.add(c.X, c.m, 1, inv[w], c.m, 1, c.m, c.m);
+    if (r > 0) {
+      newphi[w] = S.lvl->alloc((size_t)r * pi);
+      ci0.add(c.LP, pi, 1, newphi[w], pi, 1, r, pi);
+    }
     if (!s) continue;
     Y[w] = S.scratch.alloc((size_t)s * c.m);
     Y2[w] = S.scratch.alloc((size_t)s * c.m);
+    Zp[w] = S.scratch.alloc((size_t)s * pi);
+    Zp2[w] = S.scratch.alloc((size_t)s * pi);
     gy.add(Y[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(V[w], c.m, 1, c.X, 1, c.m, c.m, SEG_KSTART_N)});
+    gy.add(Zp[w], pi, 1, s, pi, 1.0, 0.0, {seg(V[w], c.m, 1, c.LP, 1, pi, c.m)});
     gy2.add(Y2[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(Tw[w], 1, s, Y[w], 1, c.m, s, SEG_KLIM_M)});
+    gy2.add(Zp2[w], pi, 1, s, pi, 1.0, 0.0, {seg(Tw[w], 1, s, Zp[w], 1, pi, s, SEG_KLIM_M)});
     gin.add(inv[w], c.m, 1, c.m, c.m, -1.0, 1.0, {seg(V[w], 1, c.m, Y2[w], 1, c.m, s)});
+    if (r > 0) gin.add(newphi[w], pi, 1, r, pi, -1.0, 1.0, {seg(V[w], 1, c.m, Zp2[w], 1, pi, s)});
   }
   ci0.launch(S.scratch, st);
   gy.launch(S.scratch, st);
   gy2.launch(S.scratch, st);
   gin.launch(S.scratch, st);
 
-  // new couplings Q1^T L^{-1} M_BN, basis update Q1^T L^T Phi_B, identity diagonal
+  // new couplings Q1^T L^{-1} M_BN (rows of inv), identity diagonal
   GemmBatch gn;
   std::vector<double*> id_ptr;
   std::vector<int> id_sz;
   std::vector<std::vector<Blk>> newblk(nw);
-  std::vector<double*> newphi(nw, nullptr);
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
     const int r = rs[w];
@@ -628,8 +639,6 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
         gn.add(p, 1, r, r, nj, 1.0, 0.0, {seg(inv[w], c.m, 1, v.p, v.cs, v.rs, c.m)});
       }
     }
-    newphi[w] = S.lvl->alloc((size_t)r * pi);
-    gn.add(newphi[w], pi, 1, r, pi, 1.0, 0.0, {seg(Q1[w], c.m, 1, c.LP, 1, pi, c.m)});
     double* I = S.lvl->alloc((size_t)r * r);
     id_ptr.push_back(I);
     id_sz.push_back(r);
@@ -641,14 +650,14 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     int* d_s = S.scratch.upload(id_sz);
     SGF_CUDA(launch_fill_identity(d_p, d_s, (int)id_ptr.size(), st));
   }
-  // perms back (information / parity)
-  std::vector<std::vector<int32_t>> perms(nw);
-  for (int w = 0; w < nw; ++w) {
-    perms[w].resize(std::max(ci[w].cN, 0));
-    if (ci[w].cN > 0)
-      SGF_CUDA(cudaMemcpyAsync(perms[w].data(), ci[w].perm, ci[w].cN * sizeof(int), cudaMemcpyDeviceToHost, st));
-  }
-  SGF_CUDA(cudaStreamSynchronize(st));
+  // QR permutations (information / parity): kept on the device and read
+  // back once at the end of the factorization (no per-wave synchronisation)
+  std::vector<int*> perm_dev(nw, nullptr);
+  for (int w = 0; w < nw; ++w)
+    if (ci[w].cN > 0) {
+      perm_dev[w] = S.persist.alloc_t<int>(ci[w].cN);
+      SGF_CUDA(cudaMemcpyAsync(perm_dev[w], ci[w].perm, ci[w].cN * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
 
   // host structure updates and factor records
   for (int w = 0; w < nw; ++w) {
@@ -678,7 +687,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     o.f.inv = inv[w];
     o.f.V = V[w];
     o.f.Tw = Tw[w];
-    o.f.perm = perms[w];
+    o.f.perm_dev = perm_dev[w];
     o.f.ncols = c.cN;
     out.push_back(std::move(o));
 
@@ -731,6 +740,38 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
     wv[i] = w;
     nwaves = std::max(nwaves, w + 1);
   }
+  // Cholesky + inverse of every compressed node's diagonal block and L^T Phi,
+  // one batch for the level (factorization.py:317, 320)
+  std::unordered_map<int, CompPre> pre;
+  {
+    cudaStream_t st = S.st;
+    const int pi = S.pi;
+    CopyBatch cp;
+    GemmBatch glp;
+    std::vector<CholJob> jobs;
+    for (int c : comp) {
+      const int m = M.size[c];
+      const size_t mm = (size_t)m * m;
+      CompPre p;
+      p.L = S.P->store.alloc(mm);
+      p.X = S.P->store.alloc(mm);
+      SGF_CUDA(cudaMemsetAsync(p.X, 0, mm * sizeof(double), st));
+      p.LP = S.lvl->alloc((size_t)m * pi);
+      Blk* d = M.find(c, c);
+      if (!d) fail(SGF_NOT_SPD, "compressed node without a diagonal block");
+      cp.add(d->p, d->cols, 1, p.L, m, 1, m, m);
+      jobs.push_back(CholJob{p.L, p.X, m, c});
+      pre[c] = p;
+    }
+    cp.launch(S.scratch, st);
+    chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
+    for (int c : comp) {
+      const CompPre& p = pre[c];
+      const int m = M.size[c];
+      glp.add(p.LP, pi, 1, m, pi, 1.0, 0.0, {seg(p.L, 1, m, S.nodes[c].phi, 1, pi, m, SEG_KSTART_M)});
+    }
+    glp.launch(S.scratch, st);
+  }
   std::vector<CompOut> outs;
   for (int w = 0; w < nwaves; ++w) {
     std::vector<int> nodes, seqno, fr;
@@ -745,7 +786,7 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
         }
         fr.push_back(r);
       }
-    compress_wave(S, nodes, seqno, fr, level, outs);
+    compress_wave(S, nodes, seqno, fr, level, outs, pre);
     S.scratch.release();
   }
   std::sort(outs.begin(), outs.end(), [](const CompOut& x, const CompOut& y) { return x.node < y.node; });
@@ -1016,6 +1057,13 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     fail(SGF_TRACE, buf);
   }
   S.chk.verify(S.st);
+  SGF_CUDA(cudaStreamSynchronize(S.st));
+  for (auto& f : P->factors)
+    if (f.perm_dev) {
+      f.perm.resize(f.ncols);
+      SGF_CUDA(cudaMemcpy(f.perm.data(), f.perm_dev, f.ncols * sizeof(int), cudaMemcpyDeviceToHost));
+      f.perm_dev = nullptr;
+    }
   S.scratch.release();
   S.lvl.reset();
   long long fa = 0;

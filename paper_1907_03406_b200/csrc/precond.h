@@ -20,6 +20,7 @@ struct Factor {
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   std::vector<int32_t> perm;  // compression: QR column permutation (first `steps` meaningful)
+  int* perm_dev = nullptr;    // device copy until the end-of-factorization readback
   int ncols = 0;              // compression: columns of the rank basis N
 };
 

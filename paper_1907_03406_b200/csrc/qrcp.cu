@@ -425,29 +425,24 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
 // column major).  Q = H_0 ... H_{s-1} is the orthogonal completion used for
 // the compression factor; its first r columns are the reference's Q_1.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(QR_THREADS) qr_finish_kernel(const QrFinishTask* __restrict__ tasks) {
-  const QrFinishTask F = tasks[blockIdx.x];
-  const int m = F.m, s = *F.steps, r = *F.rank;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // V
-  for (long long e = tid; e < (long long)m * s; e += QR_THREADS) {
+// phase 0: V (one CTA-stripe per node); phase 1: T from G = V^T V (computed by
+// the GEMM kernel between the two phases).  Q1 is never formed: every
+// product with Q (inverse operator, basis update) goes through V and T.
+__global__ void __launch_bounds__(QR_THREADS) qr_extract_v_kernel(const QrFinishTask* __restrict__ tasks) {
+  const QrFinishTask F = tasks[blockIdx.y];
+  const int m = F.m, s = *F.steps;
+  for (long long e = blockIdx.x * (long long)QR_THREADS + threadIdx.x; e < (long long)m * s;
+       e += (long long)gridDim.x * QR_THREADS) {
     const int k = (int)(e / m), i = (int)(e % m);
     F.V[e] = (i < k) ? 0.0 : (i == k ? 1.0 : F.Nm[(long long)k * m + i]);
   }
-  __syncthreads();
-  // gram G[a][b] = V[:,a] . V[:,b] for a < b (only rows >= b contribute)
-  double* G = F.G;  // s*s
-  for (int p = warp; p < s * s; p += QR_WARPS) {
-    const int a = p / s, b = p % s;
-    if (a >= b) continue;
-    const double* va = F.V + (long long)a * m;
-    const double* vb = F.V + (long long)b * m;
-    double acc = 0.0;
-    for (int i = b + lane; i < m; i += 32) acc = fma(va[i], vb[i], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) G[a * s + b] = acc;
-  }
-  __syncthreads();
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qr_larft_kernel(const QrFinishTask* __restrict__ tasks) {
+  const QrFinishTask F = tasks[blockIdx.x];
+  const int s = *F.steps;
+  const int tid = threadIdx.x;
+  const double* G = F.G;  // s x s, G[a][b] = v_a . v_b
   // T recurrence (LAPACK larft, forward, columnwise)
   for (int k = 0; k < s; ++k) {
     const double tk = F.tau[k];
@@ -461,30 +456,13 @@ __global__ void __launch_bounds__(QR_THREADS) qr_finish_kernel(const QrFinishTas
     for (int a = k + 1 + tid; a < s; a += QR_THREADS) F.Tm[(long long)a * s + k] = 0.0;
     __syncthreads();
   }
-  // Q1: start from [I_r; 0], apply H_k for k = min(s,r)-1 .. 0
-  for (long long e = tid; e < (long long)m * r; e += QR_THREADS) {
-    const int j = (int)(e / m), i = (int)(e % m);
-    F.Q1[e] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  const int sr = min(s, r);
-  for (int k = sr - 1; k >= 0; --k) {
-    const double* vk = F.V + (long long)k * m;
-    const double tk = F.tau[k];
-    for (int j = k + warp; j < r; j += QR_WARPS) {
-      double* q = F.Q1 + (long long)j * m;
-      double acc = 0.0;
-      for (int i = k + lane; i < m; i += 32) acc = fma(vk[i], q[i], acc);
-      acc = warp_sum(acc) * tk;
-      for (int i = k + lane; i < m; i += 32) q[i] = fma(-acc, vk[i], q[i]);
-    }
-    __syncthreads();
-  }
 }
 
-cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, cudaStream_t s) {
+cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  count_launch(); qr_finish_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  count_launch();
+  if (phase == 0) qr_extract_v_kernel<<<dim3(16, ntasks), QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  else qr_larft_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
   return cudaGetLastError();
 }
 
