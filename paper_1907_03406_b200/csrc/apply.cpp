@@ -18,7 +18,7 @@ namespace sgf {
 namespace {
 constexpr int GN_ROWS = 64;   // rows per gemv_n CTA
 constexpr int GT_ROWS = 256;  // rows per gemv_t partial
-constexpr int GT_COLS = 256;  // columns per gemv_t CTA
+constexpr int GT_COLS = 512;  // columns per gemv_t CTA (2 per thread)
 }  // namespace
 
 struct Group {
@@ -165,19 +165,19 @@ ApplyPlan* build_plan(Precond* P) {
       const Factor& f = P->factors[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
-      add_gemv_n(f1, f.inv, f.m, plan->xb + om, plan->zb + om, f.m, f.m, tri);
+      add_gemv_n(f1, f.inv, f.ld, plan->xb + om, plan->zb + om, f.m, f.m, tri);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
-        if (f.c > 0) add_gemv_n(f2, f.E, f.m, plan->zb + om, plan->t + oc, f.c, f.m, 0);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, plan->zb + om, plan->t + oc, f.c, f.m, 0);
         for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
-        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.m, plan->xn + oc, plan->part + op, f.c, f.m, 0) : 0;
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, plan->xn + oc, plan->part + op, f.c, f.m, 0) : 0;
         r1.push_back(RedSeg{plan->part + op, plan->xb + om, plan->acc + om, f.m, nrb, f.m, -1.0});
         // second stage reuses the partial buffer after red1 consumed it
-        int nrb2 = add_gemv_t(b2, f.inv, f.m, plan->acc + om, plan->part + op, f.m, f.m, 1);
+        int nrb2 = add_gemv_t(b2, f.inv, f.ld, plan->acc + om, plan->part + op, f.m, f.m, 1);
         r2.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb2, f.m, 1.0});
         op += std::max<long long>(nrb, nrb2) * f.m;
       } else {
-        int nrb = add_gemv_t(b1, f.inv, f.m, plan->xb + om, plan->part + op, f.m, f.m, tri);
+        int nrb = add_gemv_t(b1, f.inv, f.ld, plan->xb + om, plan->part + op, f.m, f.m, tri);
         r1.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb, f.m, 1.0});
         op += (long long)nrb * f.m;
       }

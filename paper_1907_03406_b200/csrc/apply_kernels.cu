@@ -16,24 +16,32 @@ namespace sgf {
 // ---------------------------------------------------------------------------
 // y = A x for a row block (mode N).  One warp per row, lanes stride columns.
 // ---------------------------------------------------------------------------
+// Matrices have an even leading dimension and 16-byte aligned bases
+// (pad_ld), so rows are streamed with 128-bit loads: 4 x 16 B in flight per
+// lane, evict-first (each entry is read once per sweep); x stays cached.
 __global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = T.r0 + warp; i < T.r1; i += 8) {
-    const double* a = T.A + (long long)i * T.lda;
-    const int ke = T.tri ? min(T.c1, i + 1) : T.c1;
+    const double* arow = T.A + (long long)i * T.lda;
+    const double2* a = reinterpret_cast<const double2*>(arow);
+    const int ke = T.tri ? min(T.c1, i + 1) : T.c1;  // c0 == 0 for every task
+    const int k2 = ke >> 1;
+    const double* x = T.x;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int k = T.c0 + lane;
-    // four independent streaming loads in flight per lane (matrix entries are
-    // read once per sweep: evict-first; x stays cached)
-    for (; k + 96 < ke; k += 128) {
-      const double a0 = __ldcs(a + k), a1 = __ldcs(a + k + 32), a2 = __ldcs(a + k + 64), a3 = __ldcs(a + k + 96);
-      s0 = fma(a0, T.x[k], s0);
-      s1 = fma(a1, T.x[k + 32], s1);
-      s2 = fma(a2, T.x[k + 64], s2);
-      s3 = fma(a3, T.x[k + 96], s3);
+    int k = lane;
+    for (; k + 96 < k2; k += 128) {
+      const double2 a0 = __ldcs(a + k), a1 = __ldcs(a + k + 32), a2 = __ldcs(a + k + 64), a3 = __ldcs(a + k + 96);
+      s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
+      s1 = fma(a1.x, x[2 * k + 64], fma(a1.y, x[2 * k + 65], s1));
+      s2 = fma(a2.x, x[2 * k + 128], fma(a2.y, x[2 * k + 129], s2));
+      s3 = fma(a3.x, x[2 * k + 192], fma(a3.y, x[2 * k + 193], s3));
     }
-    for (; k < ke; k += 32) s0 = fma(__ldcs(a + k), T.x[k], s0);
+    for (; k < k2; k += 32) {
+      const double2 a0 = __ldcs(a + k);
+      s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
+    }
+    if ((ke & 1) && lane == 0) s0 = fma(arow[ke - 1], x[ke - 1], s0);
     double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -42,27 +50,36 @@ __global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T) for 256 columns per CTA.
+// part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T): each thread owns two
+// adjacent columns (one 16-byte load per row), 512 columns per CTA.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
-  const int k = T.c0 + threadIdx.x;
+  const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
   if (k >= T.c1) return;
   int i0 = T.r0;
+  // lower triangular: column k starts at row k; A[k][k+1] is a stored zero
   if (T.tri) i0 = max(i0, k);
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  const double* a = T.A + k + (long long)i0 * T.lda;
   const long long ld = T.lda;
+  const double2* a = reinterpret_cast<const double2*>(T.A + k + (long long)i0 * ld);
+  const long long ld2 = ld >> 1;
+  double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
   int i = i0;
-  for (; i + 3 < T.r1; i += 4, a += 4 * ld) {
-    const double a0 = __ldcs(a), a1 = __ldcs(a + ld), a2 = __ldcs(a + 2 * ld), a3 = __ldcs(a + 3 * ld);
-    s0 = fma(a0, T.x[i], s0);
-    s1 = fma(a1, T.x[i + 1], s1);
-    s2 = fma(a2, T.x[i + 2], s2);
-    s3 = fma(a3, T.x[i + 3], s3);
+  for (; i + 3 < T.r1; i += 4, a += 4 * ld2) {
+    const double2 a0 = __ldcs(a), a1 = __ldcs(a + ld2), a2 = __ldcs(a + 2 * ld2), a3 = __ldcs(a + 3 * ld2);
+    const double x0 = T.x[i], x1 = T.x[i + 1], x2 = T.x[i + 2], x3 = T.x[i + 3];
+    s0 = fma(a0.x, x0, fma(a1.x, x1, s0));
+    t0 = fma(a0.y, x0, fma(a1.y, x1, t0));
+    s1 = fma(a2.x, x2, fma(a3.x, x3, s1));
+    t1 = fma(a2.y, x2, fma(a3.y, x3, t1));
   }
-  for (; i < T.r1; ++i, a += ld) s0 = fma(__ldcs(a), T.x[i], s0);
-  T.y[k] = (s0 + s1) + (s2 + s3);
+  for (; i < T.r1; ++i, a += ld2) {
+    const double2 a0 = __ldcs(a);
+    s0 = fma(a0.x, T.x[i], s0);
+    t0 = fma(a0.y, T.x[i], t0);
+  }
+  T.y[k] = s0 + s1;
+  if (k + 1 < T.c1) T.y[k + 1] = t0 + t1;
 }
 
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s) {

@@ -152,11 +152,12 @@ int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_ou
         break;
       case 1:
         need(8 * mm);
-        SGF_CUDA(cudaMemcpyAsync(host_out, f.L, 8 * mm, cudaMemcpyDeviceToHost, st));
+        SGF_CUDA(cudaMemcpy2DAsync(host_out, 8 * f.m, f.L, 8 * f.ld, 8 * f.m, f.m, cudaMemcpyDeviceToHost, st));
         break;
       case 2:
         need(8LL * f.c * f.m);
-        if (f.c) SGF_CUDA(cudaMemcpyAsync(host_out, f.E, 8LL * f.c * f.m, cudaMemcpyDeviceToHost, st));
+        if (f.c)
+          SGF_CUDA(cudaMemcpy2DAsync(host_out, 8 * f.m, f.E, 8 * f.ld, 8 * f.m, f.c, cudaMemcpyDeviceToHost, st));
         break;
       case 3:
         need(8LL * f.c);
@@ -190,7 +191,7 @@ int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_ou
       }
       case 5:
         need(8 * mm);
-        SGF_CUDA(cudaMemcpyAsync(host_out, f.inv, 8 * mm, cudaMemcpyDeviceToHost, st));
+        SGF_CUDA(cudaMemcpy2DAsync(host_out, 8 * f.m, f.inv, 8 * f.ld, 8 * f.m, f.m, cudaMemcpyDeviceToHost, st));
         break;
       case 6:
         need(8LL * f.perm.size());

@@ -290,7 +290,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   BlockTable& M = S.M;
   Precond* P = S.P;
   struct EI {
-    int x, m, c;
+    int x, m, c, ld;
     std::vector<int> nb;
     std::vector<int> off;
     double *W, *X, *E;
@@ -308,15 +308,16 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       e.off.push_back(e.c);
       e.c += M.size[j];
     }
-    const size_t mm = (size_t)e.m * e.m;
+    e.ld = pad_ld(e.m);
+    const size_t mm = (size_t)e.m * e.ld;
     e.W = P->store.alloc(mm);
     e.X = P->store.alloc(mm);
     SGF_CUDA(cudaMemsetAsync(e.X, 0, mm * sizeof(double), st));
-    e.E = e.c ? P->store.alloc((size_t)e.c * e.m) : nullptr;
+    e.E = e.c ? P->store.alloc((size_t)e.c * e.ld) : nullptr;
     Blk* d = M.find(e.x, e.x);
     if (!d) fail(SGF_NOT_SPD, "interior node without a diagonal block");
-    cp.add(d->p, d->cols, 1, e.W, e.m, 1, e.m, e.m);
-    jobs.push_back(CholJob{e.W, e.X, e.m, e.x});
+    cp.add(d->p, d->cols, 1, e.W, e.ld, 1, e.m, e.m);
+    jobs.push_back(CholJob{e.W, e.X, e.m, e.x, e.ld});
   }
   cp.launch(S.scratch, st);
   chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
@@ -326,8 +327,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     long long f = (long long)e.m * e.m * e.m / 3;
     for (size_t q = 0; q < e.nb.size(); ++q) {
       View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
-      ge.add(e.E + (long long)e.off[q] * e.m, e.m, 1, v.rows, e.m, 1.0, 0.0,
-             {seg(v.p, v.rs, v.cs, e.X, e.m, 1, e.m, SEG_KLIM_N)});
+      ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
+             {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
       f += (long long)e.m * e.m * v.rows;
     }
     for (size_t p = 0; p < e.nb.size(); ++p)
@@ -399,6 +400,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       f.node = e.x;
       f.level = level;
       f.m = e.m;
+      f.ld = e.ld;
       f.c = e.c;
       f.idx = S.nodes[e.x].active;
       for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
@@ -418,8 +420,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     std::vector<GemmSeg> sg;
     for (auto& c : T.contrib) {
       const EI& e = info[c.first];
-      sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.m, e.m, 1,
-                       e.E + (long long)e.off[c.second.second] * e.m, e.m, 1, e.m));
+      sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.ld, e.ld, 1,
+                       e.E + (long long)e.off[c.second.second] * e.ld, e.ld, 1, e.m));
     }
     // diagonal blocks are kept valid in their lower triangle only: every
     // consumer (Cholesky of the node, densify + Cholesky) reads only that
@@ -442,6 +444,7 @@ struct CompOut {
 // compression, so every Cholesky + inverse and L^T Phi runs in one batch
 struct CompPre {
   double *L, *X, *LP;
+  int ld;
 };
 
 void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int>& seqno,
@@ -454,7 +457,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   const int pi = S.pi;
   const bool lowrank = a.mode == SGF_MODE_LOWRANK;
   struct CI {
-    int c, m, cN;
+    int c, m, cN, ld;
     std::vector<int> nb;
     std::vector<char> raw;
     std::vector<int> col;  // column offset in N of each neighbour's block
@@ -480,6 +483,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     c.L = pr.L;
     c.X = pr.X;
     c.LP = pr.LP;
+    c.ld = pr.ld;
     c.N = S.scratch.alloc((size_t)c.m * std::max(c.cN, 1));
     const int kmax = std::max(std::min(c.m, c.cN), 1);
     c.tau = S.scratch.alloc(kmax);
@@ -509,9 +513,9 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
       double* dstc = c.N + (long long)c.col[q] * c.m;
       if (c.raw[q]) {
         View v = view_of(M, c.c, c.nb[q]);
-        g2.add(dstc, 1, c.m, c.m, v.cols, 1.0, 0.0, {seg(c.X, c.m, 1, v.p, v.cs, v.rs, c.m, SEG_KLIM_M)});
+        g2.add(dstc, 1, c.m, c.m, v.cols, 1.0, 0.0, {seg(c.X, c.ld, 1, v.p, v.cs, v.rs, c.m, SEG_KLIM_M)});
       } else {
-        g2.add(dstc, 1, c.m, c.m, pi, 1.0, 0.0, {seg(c.X, c.m, 1, c.Z[q], 1, pi, c.m, SEG_KLIM_M)});
+        g2.add(dstc, 1, c.m, c.m, pi, 1.0, 0.0, {seg(c.X, c.ld, 1, c.Z[q], 1, pi, c.m, SEG_KLIM_M)});
       }
     }
   }
@@ -594,8 +598,8 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
     const int r = rs[w], s = rs[nw + w];
-    inv[w] = P->store.alloc((size_t)c.m * c.m);
-    ci0.add(c.X, c.m, 1, inv[w], c.m, 1, c.m, c.m);
+    inv[w] = P->store.alloc((size_t)c.m * c.ld);
+    ci0.add(c.X, c.ld, 1, inv[w], c.ld, 1, c.m, c.m);
     if (r > 0) {
       newphi[w] = S.lvl->alloc((size_t)r * pi);
       ci0.add(c.LP, pi, 1, newphi[w], pi, 1, r, pi);
@@ -605,11 +609,11 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     Y2[w] = S.scratch.alloc((size_t)s * c.m);
     Zp[w] = S.scratch.alloc((size_t)s * pi);
     Zp2[w] = S.scratch.alloc((size_t)s * pi);
-    gy.add(Y[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(V[w], c.m, 1, c.X, 1, c.m, c.m, SEG_KSTART_N)});
+    gy.add(Y[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(V[w], c.m, 1, c.X, 1, c.ld, c.m, SEG_KSTART_N)});
     gy.add(Zp[w], pi, 1, s, pi, 1.0, 0.0, {seg(V[w], c.m, 1, c.LP, 1, pi, c.m)});
     gy2.add(Y2[w], c.m, 1, s, c.m, 1.0, 0.0, {seg(Tw[w], 1, s, Y[w], 1, c.m, s, SEG_KLIM_M)});
     gy2.add(Zp2[w], pi, 1, s, pi, 1.0, 0.0, {seg(Tw[w], 1, s, Zp[w], 1, pi, s, SEG_KLIM_M)});
-    gin.add(inv[w], c.m, 1, c.m, c.m, -1.0, 1.0, {seg(V[w], 1, c.m, Y2[w], 1, c.m, s)});
+    gin.add(inv[w], c.ld, 1, c.m, c.m, -1.0, 1.0, {seg(V[w], 1, c.m, Y2[w], 1, c.m, s)});
     if (r > 0) gin.add(newphi[w], pi, 1, r, pi, -1.0, 1.0, {seg(V[w], 1, c.m, Zp2[w], 1, pi, s)});
   }
   ci0.launch(S.scratch, st);
@@ -633,10 +637,10 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
       double* p = S.lvl->alloc((size_t)r * nj);
       if (c.c < j) {
         newblk[w].push_back(Blk{p, r, nj});
-        gn.add(p, nj, 1, r, nj, 1.0, 0.0, {seg(inv[w], c.m, 1, v.p, v.cs, v.rs, c.m)});
+        gn.add(p, nj, 1, r, nj, 1.0, 0.0, {seg(inv[w], c.ld, 1, v.p, v.cs, v.rs, c.m)});
       } else {
         newblk[w].push_back(Blk{p, nj, r});
-        gn.add(p, 1, r, r, nj, 1.0, 0.0, {seg(inv[w], c.m, 1, v.p, v.cs, v.rs, c.m)});
+        gn.add(p, 1, r, r, nj, 1.0, 0.0, {seg(inv[w], c.ld, 1, v.p, v.cs, v.rs, c.m)});
       }
     }
     double* I = S.lvl->alloc((size_t)r * r);
@@ -680,6 +684,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     o.f.node = c.c;
     o.f.level = level;
     o.f.m = c.m;
+    o.f.ld = c.ld;
     o.f.r = r;
     o.f.steps = s;
     o.f.idx = S.nodes[c.c].active;
@@ -751,16 +756,17 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
     std::vector<CholJob> jobs;
     for (int c : comp) {
       const int m = M.size[c];
-      const size_t mm = (size_t)m * m;
       CompPre p;
+      p.ld = pad_ld(m);
+      const size_t mm = (size_t)m * p.ld;
       p.L = S.P->store.alloc(mm);
       p.X = S.P->store.alloc(mm);
       SGF_CUDA(cudaMemsetAsync(p.X, 0, mm * sizeof(double), st));
       p.LP = S.lvl->alloc((size_t)m * pi);
       Blk* d = M.find(c, c);
       if (!d) fail(SGF_NOT_SPD, "compressed node without a diagonal block");
-      cp.add(d->p, d->cols, 1, p.L, m, 1, m, m);
-      jobs.push_back(CholJob{p.L, p.X, m, c});
+      cp.add(d->p, d->cols, 1, p.L, p.ld, 1, m, m);
+      jobs.push_back(CholJob{p.L, p.X, m, c, p.ld});
       pre[c] = p;
     }
     cp.launch(S.scratch, st);
@@ -768,7 +774,7 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
     for (int c : comp) {
       const CompPre& p = pre[c];
       const int m = M.size[c];
-      glp.add(p.LP, pi, 1, m, pi, 1.0, 0.0, {seg(p.L, 1, m, S.nodes[c].phi, 1, pi, m, SEG_KSTART_M)});
+      glp.add(p.LP, pi, 1, m, pi, 1.0, 0.0, {seg(p.L, 1, p.ld, S.nodes[c].phi, 1, pi, m, SEG_KSTART_M)});
     }
     glp.launch(S.scratch, st);
   }
@@ -921,7 +927,8 @@ void final_dense(State& S) {
     tot += M.size[c];
   }
   Precond* P = S.P;
-  const size_t tt = (size_t)tot * tot;
+  const int ldt = pad_ld(tot);
+  const size_t tt = (size_t)tot * ldt;
   double* D = P->store.alloc(tt);
   double* X = P->store.alloc(tt);
   SGF_CUDA(cudaMemsetAsync(D, 0, tt * sizeof(double), st));
@@ -932,17 +939,18 @@ void final_dense(State& S) {
     auto ia = off.find(a0), ib = off.find(b0);
     if (ia == off.end() || ib == off.end()) continue;
     const Blk& b = kv.second;
-    cp.add(b.p, b.cols, 1, D + (long long)ia->second * tot + ib->second, tot, 1, b.rows, b.cols);
-    if (a0 != b0) cp.add(b.p, 1, b.cols, D + (long long)ib->second * tot + ia->second, tot, 1, b.cols, b.rows);
+    cp.add(b.p, b.cols, 1, D + (long long)ia->second * ldt + ib->second, ldt, 1, b.rows, b.cols);
+    if (a0 != b0) cp.add(b.p, 1, b.cols, D + (long long)ib->second * ldt + ia->second, ldt, 1, b.cols, b.rows);
   }
   cp.launch(S.scratch, st);
-  std::vector<CholJob> jobs{CholJob{D, X, tot, -1}};
+  std::vector<CholJob> jobs{CholJob{D, X, tot, -1, ldt}};
   chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
   S.flops += (long long)tot * tot * tot / 3;
   Factor f;
   f.type = SGF_FACTOR_DENSE;
   f.node = -1;
   f.m = tot;
+  f.ld = ldt;
   for (int c : rem) f.idx.insert(f.idx.end(), S.nodes[c].active.begin(), S.nodes[c].active.end());
   f.L = D;
   f.inv = X;

@@ -12,6 +12,7 @@ struct Factor {
   int node = -1;
   int level = 0;  // 1-based level of the factorization pass (dense: levels+1)
   int m = 0, c = 0, r = 0, steps = 0;
+  int ld = 0;                 // leading dimension of L, inv and E (pad_ld(m))
   std::vector<int64_t> idx;   // node actives at factor time
   std::vector<int64_t> nidx;  // elimination: stacked neighbour actives (sorted neighbour order)
   double* L = nullptr;        // m x m lower (row-major)

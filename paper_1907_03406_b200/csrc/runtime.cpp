@@ -322,11 +322,12 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
   cudaStream_t st = ctx.stream;
   const int nj = (int)jobs.size();
   std::vector<const double*> wp(nj);
-  std::vector<int> ms(nj);
+  std::vector<int> ms(nj), lds(nj);
   int mmax = 0;
   for (int i = 0; i < nj; ++i) {
     wp[i] = jobs[i].W;
     ms[i] = jobs[i].m;
+    lds[i] = jobs[i].ld;
     mmax = std::max(mmax, jobs[i].m);
   }
   // breakdown status lives as long as the check that will read it
@@ -335,7 +336,8 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
   {
     const double** d_wp = scratch.upload(wp);
     int* d_m = scratch.upload(ms);
-    SGF_CUDA(launch_max_diag(d_wp, d_m, d_m, nj, d_floor, st));
+    int* d_ld = scratch.upload(lds);
+    SGF_CUDA(launch_max_diag(d_wp, d_m, d_ld, nj, d_floor, st));
   }
   int* d_status = keep.alloc_t<int>(nj);
   double* d_piv = keep.alloc(nj);
@@ -353,34 +355,33 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
     std::vector<int> xl;
     for (int i = 0; i < nj; ++i) {
       const int m = jobs[i].m;
+      const long long ld = jobs[i].ld;
       if (m <= k0) continue;
       double* W = jobs[i].W;
       double* X = jobs[i].X;
       const int nb = std::min(64, m - k0), k1 = k0 + nb;
       if (k0 > 0) {
-        // A: panel update and T_k
-        ga.add(W + (long long)k0 * m + k0, m, 1, m - k0, nb, -1.0, 1.0,
-               {seg(W + (long long)k0 * m, m, 1, W + (long long)k0 * m, m, 1, k0)});
-        ga.add(tk[i], m, 1, nb, k0, 1.0, 0.0,
-               {seg(W + (long long)k0 * m, m, 1, X, 1, m, k0, SEG_KSTART_N)}, 0);
+        // A: panel update and T_k (T_k is nb x k0 with leading dimension m)
+        ga.add(W + k0 * ld + k0, ld, 1, m - k0, nb, -1.0, 1.0,
+               {seg(W + k0 * ld, ld, 1, W + k0 * ld, ld, 1, k0)});
+        ga.add(tk[i], m, 1, nb, k0, 1.0, 0.0, {seg(W + k0 * ld, ld, 1, X, 1, ld, k0, SEG_KSTART_N)}, 0);
       }
       DiagTask d;
       d.W = W;
       d.Dinv = dinv[i];
-      d.ld = m;
+      d.ld = (int)ld;
       d.k0 = k0;
       d.nb = nb;
       d.floor = d_floor + i;
       d.node = i;
       dt.push_back(d);
       xd.push_back(X);
-      xl.push_back(m);
+      xl.push_back((int)ld);
       if (m > k1)
-        gc.add(W + (long long)k1 * m + k0, m, 1, m - k1, nb, 1.0, 0.0,
-               {seg(W + (long long)k1 * m + k0, m, 1, dinv[i], 64, 1, nb, SEG_KLIM_N)}, 0);
+        gc.add(W + k1 * ld + k0, ld, 1, m - k1, nb, 1.0, 0.0,
+               {seg(W + k1 * ld + k0, ld, 1, dinv[i], 64, 1, nb, SEG_KLIM_N)}, 0);
       if (k0 > 0)
-        gc.add(X + (long long)k0 * m, m, 1, nb, k0, -1.0, 0.0,
-               {seg(dinv[i], 64, 1, tk[i], 1, m, nb, SEG_KLIM_M)}, 0);
+        gc.add(X + k0 * ld, ld, 1, nb, k0, -1.0, 0.0, {seg(dinv[i], 64, 1, tk[i], 1, m, nb, SEG_KLIM_M)}, 0);
     }
     ga.launch(scratch, st);
     {
@@ -393,7 +394,7 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
     gc.launch(scratch, st);
   }
   std::vector<TriTask> tri;
-  for (auto& j : jobs) tri.push_back(TriTask{j.W, j.m, j.m});
+  for (auto& j : jobs) tri.push_back(TriTask{j.W, j.m, j.ld});
   zero_upper(scratch, st, tri);
 
   CholCheck local;

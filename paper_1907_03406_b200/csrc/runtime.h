@@ -307,7 +307,12 @@ struct CholJob {
   double* X;
   int m;
   int node;  // for error messages
+  int ld;    // leading dimension of W and X (>= m; even so rows are 16-byte aligned)
 };
+
+// leading dimension of stored factor matrices: even, so every row starts
+// 16-byte aligned and the apply GEMVs can use 128-bit loads
+inline int pad_ld(int m) { return (m + 1) & ~1; }
 // Breakdown statuses of Cholesky batches whose check is deferred (no host
 // synchronisation per batch); verify() syncs and raises NotSPD for the
 // earliest failing batch, lowest node id first (densela.py:106-110).
