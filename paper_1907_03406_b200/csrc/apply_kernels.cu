@@ -19,7 +19,9 @@ namespace sgf {
 // Matrices have an even leading dimension and 16-byte aligned bases
 // (pad_ld), so rows are streamed with 128-bit loads: 4 x 16 B in flight per
 // lane, evict-first (each entry is read once per sweep); x stays cached.
-__global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
+// (256, 8): at most 32 registers so 8 CTAs = 64 warps fit per SM (the
+// register limit capped residency at 4 CTAs and left HBM latency exposed)
+__global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = T.r0 + warp; i < T.r1; i += 8) {
@@ -53,7 +55,7 @@ __global__ void __launch_bounds__(256) gemv_n_kernel(const GemvTask* __restrict_
 // part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T): each thread owns two
 // adjacent columns (one 16-byte load per row), 512 columns per CTA.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
   const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
   if (k >= T.c1) return;
