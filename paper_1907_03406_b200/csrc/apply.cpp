@@ -43,6 +43,7 @@ struct Group {
   RedSeg* red2 = nullptr;
   int nred2 = 0, maxn2 = 0;
   double bytes_f1 = 0, bytes_f2 = 0, bytes_b1 = 0, bytes_b2 = 0;  // matrix bytes streamed
+  double *xb = nullptr, *zb = nullptr, *acc = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr;  // workspaces
 };
 
 // algorithmic bytes of the matrix entries a GEMV task list reads
@@ -63,8 +64,8 @@ static double gemv_bytes(const std::vector<GemvTask>& v, int mode) {
 struct ApplyPlan {
   Arena mem;
   std::vector<Group> groups;
-  double *xb = nullptr, *zb = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr, *acc = nullptr;
   double* work = nullptr;  // n-vector (apply in place)
+  std::vector<int> tix;    // host scratch of the plan builder (released by plan_finish)
   long long n = 0;
   // CUDA graphs of the sweeps on `work` (index = op), captured on first use
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
@@ -116,22 +117,33 @@ static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, 
   return nrb;
 }
 
-ApplyPlan* build_plan(Precond* P) {
+// Extend the plan with the groups of factors [begin, end).  Called by the
+// factorization driver right after each level's kernels are enqueued, so this
+// host work overlaps the device execution of the level.  Every group owns its
+// workspace slices.
+void plan_extend(Precond* P, size_t begin, size_t end) {
   cudaStream_t st = P->ctx->stream;
-  ApplyPlan* plan = new ApplyPlan(st);
-  plan->n = P->n;
+  if (!P->plan) {
+    P->plan = new ApplyPlan(st);
+    P->plan->n = P->n;
+    P->plan->work = P->plan->mem.alloc(std::max<long long>(P->n, 1));
+    P->plan->tix.assign(P->n, -1);
+  }
+  ApplyPlan* plan = P->plan;
+  std::vector<int>& tix = plan->tix;
   // groups: consecutive factors of the same (level, type)
   std::vector<std::pair<size_t, size_t>> ranges;
-  for (size_t i = 0; i < P->factors.size();) {
+  for (size_t i = begin; i < end;) {
     size_t j = i + 1;
-    while (j < P->factors.size() && P->factors[j].type == P->factors[i].type &&
-           P->factors[j].level == P->factors[i].level && P->factors[i].type != SGF_FACTOR_DENSE)
+    while (j < end && P->factors[j].type == P->factors[i].type && P->factors[j].level == P->factors[i].level &&
+           P->factors[i].type != SGF_FACTOR_DENSE)
       ++j;
     ranges.push_back({i, j});
     i = j;
   }
-  long long max_m = 0, max_c = 0, max_part = 0;
   for (auto& rg : ranges) {
+    Group g;
+    g.type = P->factors[rg.first].type;
     long long sm = 0, sc = 0, sp = 0;
     for (size_t i = rg.first; i < rg.second; ++i) {
       const Factor& f = P->factors[i];
@@ -140,22 +152,12 @@ ApplyPlan* build_plan(Precond* P) {
       const long long rbE = (f.c + GT_ROWS - 1) / GT_ROWS, rbL = (f.m + GT_ROWS - 1) / GT_ROWS;
       sp += std::max(rbE, rbL) * f.m;
     }
-    max_m = std::max(max_m, sm);
-    max_c = std::max(max_c, sc);
-    max_part = std::max(max_part, sp);
-  }
-  plan->xb = plan->mem.alloc(std::max(max_m, 1LL));
-  plan->zb = plan->mem.alloc(std::max(max_m, 1LL));
-  plan->acc = plan->mem.alloc(std::max(max_m, 1LL));
-  plan->xn = plan->mem.alloc(std::max(max_c, 1LL));
-  plan->t = plan->mem.alloc(std::max(max_c, 1LL));
-  plan->part = plan->mem.alloc(std::max(max_part, 1LL));
-  plan->work = plan->mem.alloc(std::max<long long>(P->n, 1));
-  std::vector<int> tix(P->n, -1);
-
-  for (auto& rg : ranges) {
-    Group g;
-    g.type = P->factors[rg.first].type;
+    g.xb = plan->mem.alloc(std::max(sm, 1LL));
+    g.zb = plan->mem.alloc(std::max(sm, 1LL));
+    g.acc = plan->mem.alloc(std::max(sm, 1LL));
+    g.xn = plan->mem.alloc(std::max(sc, 1LL));
+    g.t = plan->mem.alloc(std::max(sc, 1LL));
+    g.part = plan->mem.alloc(std::max(sp, 1LL));
     std::vector<int> idx, nidx;
     std::vector<GemvTask> f1, f2, b1, b2;
     std::vector<RedSeg> r1, r2;
@@ -165,20 +167,20 @@ ApplyPlan* build_plan(Precond* P) {
       const Factor& f = P->factors[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
-      add_gemv_n(f1, f.inv, f.ld, plan->xb + om, plan->zb + om, f.m, f.m, tri);
+      add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
-        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, plan->zb + om, plan->t + oc, f.c, f.m, 0);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0);
         for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
-        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, plan->xn + oc, plan->part + op, f.c, f.m, 0) : 0;
-        r1.push_back(RedSeg{plan->part + op, plan->xb + om, plan->acc + om, f.m, nrb, f.m, -1.0});
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0) : 0;
+        r1.push_back(RedSeg{g.part + op, g.xb + om, g.acc + om, f.m, nrb, f.m, -1.0});
         // second stage reuses the partial buffer after red1 consumed it
-        int nrb2 = add_gemv_t(b2, f.inv, f.ld, plan->acc + om, plan->part + op, f.m, f.m, 1);
-        r2.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb2, f.m, 1.0});
+        int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1);
+        r2.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb2, f.m, 1.0});
         op += std::max<long long>(nrb, nrb2) * f.m;
       } else {
-        int nrb = add_gemv_t(b1, f.inv, f.ld, plan->xb + om, plan->part + op, f.m, f.m, tri);
-        r1.push_back(RedSeg{plan->part + op, nullptr, plan->zb + om, f.m, nrb, f.m, 1.0});
+        int nrb = add_gemv_t(b1, f.inv, f.ld, g.xb + om, g.part + op, f.m, f.m, tri);
+        r1.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb, f.m, 1.0});
         op += (long long)nrb * f.m;
       }
       g.maxn1 = std::max(g.maxn1, f.m);
@@ -237,7 +239,15 @@ ApplyPlan* build_plan(Precond* P) {
     }
     plan->groups.push_back(g);
   }
-  return plan;
+}
+
+ApplyPlan* build_plan(Precond* P) {
+  plan_extend(P, 0, P->factors.size());
+  return P->plan;
+}
+
+void plan_finish(Precond* P) {
+  if (P->plan) std::vector<int>().swap(P->plan->tix);
 }
 
 static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t st) {
@@ -246,17 +256,19 @@ static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t
 }
 
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
-  SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
+  (void)pl;
+  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
   gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st);
   if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, 0, g.bytes_f2, st);
-  SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
-  if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, pl->t, g.ntgt, st));
+  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, g.t, g.ntgt, st));
 }
 
 static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
-  SGF_CUDA(launch_gather(y, g.idx, pl->xb, g.nm, st));
+  (void)pl;
+  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) {
-    SGF_CUDA(launch_gather(y, g.nidx, pl->xn, g.nc, st));
+    SGF_CUDA(launch_gather(y, g.nidx, g.xn, g.nc, st));
     gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
     gemv(g.bwd2, g.nb2, 1, g.bytes_b2, st);
@@ -265,7 +277,7 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
     gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
   }
-  SGF_CUDA(launch_scatter(pl->zb, g.idx, y, g.nm, st));
+  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
 }
 
 // y and x are device n-vectors; y may alias x

@@ -1027,14 +1027,24 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     std::vector<int> elim;
     for (int c = 0; c < (int)S.nodes.size(); ++c)
       if (S.nodes[c].interior && !S.nodes[c].active.empty()) elim.push_back(c);
-    { Phase ph("eliminate", t + 1, S.st); eliminate_level(S, elim, t + 1); }
+    {
+      Phase ph("eliminate", t + 1, S.st);
+      const size_t f0 = P->factors.size();
+      eliminate_level(S, elim, t + 1);
+      plan_extend(P.get(), f0, P->factors.size());  // host work overlapping the level's kernels
+    }
     ls.eliminated = (int)elim.size();
     S.scratch.release();  // chunks are reused in stream order: no sync needed
     if (compression && (t + 1) > a.skip_levels) {
       std::vector<int> comp;
       for (int c = 0; c < (int)S.nodes.size(); ++c)
         if (kind_in(a.compress_kind_mask, S.nodes[c].kind) && !S.nodes[c].active.empty()) comp.push_back(c);
-      { Phase ph("compress", t + 1, S.st); compress_level(S, comp, t + 1, ls); }
+      {
+        Phase ph("compress", t + 1, S.st);
+        const size_t f0 = P->factors.size();
+        compress_level(S, comp, t + 1, ls);
+        plan_extend(P.get(), f0, P->factors.size());
+      }
     }
     for (auto& nd : S.nodes) max_after = std::max(max_after, (int)nd.active.size());
     per_level.push_back(ls);
@@ -1052,7 +1062,12 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     }
   }
   size_t before = P->factors.size();
-  { Phase ph("dense", 0, S.st); final_dense(S); }
+  {
+    Phase ph("dense", 0, S.st);
+    const size_t f0 = P->factors.size();
+    final_dense(S);
+    plan_extend(P.get(), f0, P->factors.size());
+  }
   int final_size = 0;
   if (P->factors.size() > before) {
     final_size = P->factors.back().m;
@@ -1081,7 +1096,8 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   }
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
                         (int)P->factors.size(), 0, nullptr);
-  { Phase ph("plan", 0, S.st); P->plan = build_plan(P.get()); }
+  if (!P->plan) plan_extend(P.get(), 0, 0);
+  plan_finish(P.get());
   SGF_CUDA(cudaStreamSynchronize(S.st));
   return P.release();
 }

@@ -28,6 +28,8 @@ struct Factor {
 struct ApplyPlan;
 void destroy_plan(ApplyPlan* p);
 ApplyPlan* build_plan(class Precond* P);
+void plan_extend(class Precond* P, size_t begin, size_t end);  // add groups of factors [begin, end)
+void plan_finish(class Precond* P);
 
 class Precond {
  public:
