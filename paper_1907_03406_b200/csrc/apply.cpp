@@ -44,6 +44,13 @@ struct Group {
   int nred2 = 0, maxn2 = 0;
   double bytes_f1 = 0, bytes_f2 = 0, bytes_b1 = 0, bytes_b2 = 0;  // matrix bytes streamed
   double *xb = nullptr, *zb = nullptr, *acc = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr;  // workspaces
+  size_t f0 = 0, f1 = 0;  // factor range
+  // apply_operator task lists (built on first use)
+  GemvTask *oT = nullptr, *oE = nullptr, *oL = nullptr;
+  int noT = 0, noE = 0, noL = 0;
+  RedSeg* oRed = nullptr;
+  int noRed = 0;
+  double bytes_oT = 0, bytes_oE = 0, bytes_oL = 0;
 };
 
 // algorithmic bytes of the matrix entries a GEMV task list reads
@@ -66,6 +73,7 @@ struct ApplyPlan {
   std::vector<Group> groups;
   double* work = nullptr;  // n-vector (apply in place)
   std::vector<int> tix;    // host scratch of the plan builder (released by plan_finish)
+  bool op_ready = false;   // apply_operator tasks built
   long long n = 0;
   // CUDA graphs of the sweeps on `work` (index = op), captured on first use
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
@@ -144,13 +152,15 @@ void plan_extend(Precond* P, size_t begin, size_t end) {
   for (auto& rg : ranges) {
     Group g;
     g.type = P->factors[rg.first].type;
+    g.f0 = rg.first;
+    g.f1 = rg.second;
     long long sm = 0, sc = 0, sp = 0;
     for (size_t i = rg.first; i < rg.second; ++i) {
       const Factor& f = P->factors[i];
       sm += f.m;
       sc += f.c;
       const long long rbE = (f.c + GT_ROWS - 1) / GT_ROWS, rbL = (f.m + GT_ROWS - 1) / GT_ROWS;
-      sp += std::max(rbE, rbL) * f.m;
+      sp += (rbE + rbL) * f.m;  // apply_operator stacks both partial sets
     }
     g.xb = plan->mem.alloc(std::max(sm, 1LL));
     g.zb = plan->mem.alloc(std::max(sm, 1LL));
@@ -288,11 +298,101 @@ static void sweeps(ApplyPlan* pl, int op, double* y, cudaStream_t st) {
     for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) backward_group(pl, *it, y, st);
 }
 
+// ---------------------------------------------------------------------------
+// apply_operator = W W^T x (reference factorization.py:264-271): the
+// mult_transpose sweep over the factors in order, then mult_forward in
+// reverse (:144-148, 179-183, 205-209).  Compression factors need L Q, formed
+// once on first use as L - (L V) T V^T.
+// ---------------------------------------------------------------------------
+static void prepare_operator(Precond* P) {
+  ApplyPlan* pl = P->plan;
+  if (pl->op_ready) return;
+  cudaStream_t st = P->ctx->stream;
+  Arena scratch(st);
+  GemmBatch g1, g2, g3;
+  CopyBatch cp;
+  for (auto& f : P->factors) {
+    if (f.type != SGF_FACTOR_COMPRESSION) continue;
+    const int m = f.m, s = f.steps;
+    f.LQ = P->store.alloc((size_t)m * f.ld);
+    cp.add(f.L, f.ld, 1, f.LQ, f.ld, 1, m, m);
+    if (!s) continue;
+    double* P1 = scratch.alloc((size_t)m * s);
+    double* P2 = scratch.alloc((size_t)m * s);
+    g1.add(P1, s, 1, m, s, 1.0, 0.0, {seg(f.L, f.ld, 1, f.V, m, 1, m, SEG_KLIM_M)});
+    g2.add(P2, s, 1, m, s, 1.0, 0.0, {seg(P1, s, 1, f.Tw, 1, s, s, SEG_KLIM_N)});  // T upper
+    g3.add(f.LQ, f.ld, 1, m, m, -1.0, 1.0, {seg(P2, s, 1, f.V, 1, m, s)});
+  }
+  cp.launch(scratch, st);
+  g1.launch(scratch, st);
+  g2.launch(scratch, st);
+  g3.launch(scratch, st);
+  for (auto& g : pl->groups) {
+    std::vector<GemvTask> t1, te, tl;
+    std::vector<RedSeg> rr;
+    long long om = 0, oc = 0, op = 0;
+    for (size_t i = g.f0; i < g.f1; ++i) {
+      const Factor& f = P->factors[i];
+      const double* M = (f.type == SGF_FACTOR_COMPRESSION) ? f.LQ : f.L;
+      const int tri = (f.type != SGF_FACTOR_COMPRESSION);
+      // transpose pass: [L^T | (LQ)^T] x_B (+ E^T x_N), partial row blocks stacked
+      int nrb = add_gemv_t(t1, M, f.ld, g.xb + om, g.part + op, f.m, f.m, tri);
+      if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0)
+        nrb += add_gemv_t(t1, f.E, f.ld, g.xn + oc, g.part + op + (long long)nrb * f.m, f.c, f.m, 0);
+      rr.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb, f.m, 1.0});
+      op += (long long)nrb * f.m;
+      // forward pass: x_N += E x_B, x_B = [L | LQ] x_B
+      if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0) add_gemv_n(te, f.E, f.ld, g.xb + om, g.t + oc, f.c, f.m, 0);
+      add_gemv_n(tl, M, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri);
+      om += f.m;
+      oc += f.c;
+    }
+    g.oT = pl->mem.upload(t1);
+    g.noT = (int)t1.size();
+    g.oRed = pl->mem.upload(rr);
+    g.noRed = (int)rr.size();
+    g.oE = pl->mem.upload(te);
+    g.noE = (int)te.size();
+    g.oL = pl->mem.upload(tl);
+    g.noL = (int)tl.size();
+    g.bytes_oT = gemv_bytes(t1, 1);
+    g.bytes_oE = gemv_bytes(te, 0);
+    g.bytes_oL = gemv_bytes(tl, 0);
+  }
+  SGF_CUDA(cudaStreamSynchronize(st));
+  pl->op_ready = true;
+}
+
+static void operator_sweeps(ApplyPlan* pl, double* y, cudaStream_t st) {
+  for (auto& g : pl->groups) {  // mult_transpose, factor order
+    SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+    if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_gather(y, g.nidx, g.xn, g.nc, st));
+    gemv(g.oT, g.noT, 1, g.bytes_oT, st);
+    SGF_CUDA(launch_reduce_parts(g.oRed, g.noRed, g.maxn1, st));
+    SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  }
+  for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) {  // mult_forward, reverse order
+    const Group& g = *it;
+    SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+    if (g.type == SGF_FACTOR_ELIMINATION) {
+      gemv(g.oE, g.noE, 0, g.bytes_oE, st);
+      SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, g.t, g.ntgt, st, 1));
+    }
+    gemv(g.oL, g.noL, 0, g.bytes_oL, st);
+    SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  }
+}
+
 void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   cudaStream_t st = P->ctx->stream;
   ApplyPlan* pl = P->plan;
-  if (op == SGF_APPLY_OPERATOR) fail(SGF_INVALID_ARG, "apply_operator is not available in this build");
-  if (op < 0 || op > 2) fail(SGF_INVALID_ARG, "unknown apply operation");
+  if (op < 0 || op > 3) fail(SGF_INVALID_ARG, "unknown apply operation");
+  if (op == SGF_APPLY_OPERATOR) {
+    prepare_operator(P);
+    if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    operator_sweeps(pl, d_y, st);
+    return;
+  }
   static const bool no_graph = getenv("SGF_NO_GRAPH") != nullptr;
   if (g_prof.on || no_graph) {  // per-kernel timing needs eager launches
     if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));

@@ -126,12 +126,17 @@ __global__ void scatter_kernel(const double* __restrict__ v, const int* __restri
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     x[idx[e]] = v[e];
 }
-// x[tgt[u]] -= t[pos[j]] for j in [ptr[u], ptr[u+1]) in order (ascending factor)
+// x[tgt[u]] -= t[pos[j]] (add = 0) or += (add = 1) for j in [ptr[u], ptr[u+1])
+// in order (ascending factor)
 __global__ void combine_kernel(double* __restrict__ x, const int* __restrict__ tgt, const long long* __restrict__ ptr,
-                               const long long* __restrict__ pos, const double* __restrict__ t, long long nt) {
+                               const long long* __restrict__ pos, const double* __restrict__ t, long long nt,
+                               int add) {
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < nt; u += (long long)gridDim.x * blockDim.x) {
     double v = x[tgt[u]];
-    for (long long j = ptr[u]; j < ptr[u + 1]; ++j) v -= t[pos[j]];
+    if (add)
+      for (long long j = ptr[u]; j < ptr[u + 1]; ++j) v += t[pos[j]];
+    else
+      for (long long j = ptr[u]; j < ptr[u + 1]; ++j) v -= t[pos[j]];
     x[tgt[u]] = v;
   }
 }
@@ -154,9 +159,9 @@ cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long
   return cudaGetLastError();
 }
 cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
-                           long long nt, cudaStream_t s) {
+                           long long nt, cudaStream_t s, int add) {
   if (nt <= 0) return cudaSuccess;
-  count_launch(); combine_kernel<<<grid_for(nt), 256, 0, s>>>(x, tgt, ptr, pos, t, nt);
+  count_launch(); combine_kernel<<<grid_for(nt), 256, 0, s>>>(x, tgt, ptr, pos, t, nt, add);
   return cudaGetLastError();
 }
 

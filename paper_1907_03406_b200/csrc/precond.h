@@ -20,6 +20,7 @@ struct Factor {
   double* E = nullptr;        // c x m couplings E_N = A_NB L^{-T}, stacked
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
+  double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator
   std::vector<int32_t> perm;  // compression: QR column permutation (first `steps` meaningful)
   int* perm_dev = nullptr;    // device copy until the end-of-factorization readback
   int ncols = 0;              // compression: columns of the rank basis N

@@ -38,7 +38,7 @@ cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStr
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
 cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s);
 cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
-                           long long nt, cudaStream_t s);
+                           long long nt, cudaStream_t s, int add = 0);
 cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double* v, const double* x, double* y,
                         const double* b, int tpr, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,

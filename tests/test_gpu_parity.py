@@ -168,3 +168,31 @@ def test_device_tensor_apply():
     y = P.apply_inverse(x)
     assert y.is_cuda
     assert rel(y.cpu().numpy(), g["apply_inverse"]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["p3d12_b3", "p2d32_b5", "elast8", "p3d9_gen_d1", "aniso14", "cfg1"])
+def test_apply_operator(name):
+    """W W^T x (factorization.py:264-271) against the reference's value."""
+    g = Golden(name)
+    P = run(g)
+    w = P.apply_operator(g["rhs"])
+    assert rel(w, g["apply_operator"]) <= TOL, rel(w, g["apply_operator"])
+    x = np.random.default_rng(3).standard_normal(g.n)
+    assert rel(P.apply_inverse(P.apply_operator(x)), x) <= 1e-9
+
+
+@pytest.mark.parametrize("scheme,degree", [("nest-2-2", 1), ("nest-2-2", 2), ("nest-all-all", 1), ("gen-all-all", 1)])
+def test_polynomial_preservation_and_spd(scheme, degree):
+    """Reference acceptance C02/C03 (test_acceptance.py:81-111) on the device
+    factorization: A_l Pi = A Pi to 1e-8 at rank_tol 1e-10; x^T A_l x > 0."""
+    prob = sgf.poisson7(12)
+    P = sgf.factorize(prob, scheme=scheme, degree=degree)
+    Pi = P.basis.Pi
+    AlPi = np.column_stack([P.apply_operator(Pi[:, c]) for c in range(Pi.shape[1])])
+    APi = prob.matrix @ Pi
+    assert np.linalg.norm(AlPi - APi) <= 1e-8 * np.linalg.norm(APi)
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        x = rng.standard_normal(prob.n)
+        assert x @ P.apply_operator(x) > 0
+        assert x @ P.apply_inverse(x) > 0
