@@ -130,33 +130,42 @@ static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, 
 // host work overlaps the device execution of the level.  Every group owns its
 // workspace slices.
 void plan_extend(Precond* P, size_t begin, size_t end) {
-  cudaStream_t st = P->ctx->stream;
-  if (!P->plan) {
-    P->plan = new ApplyPlan(st);
-    P->plan->n = P->n;
-    P->plan->work = P->plan->mem.alloc(std::max<long long>(P->n, 1));
-    P->plan->tix.assign(P->n, -1);
-  }
+  std::vector<const Factor*> fs;
+  for (size_t i = begin; i < end; ++i) fs.push_back(&P->factors[i]);
+  plan_extend_ptrs(P, begin, fs);
+}
+
+void plan_init(Precond* P) {
+  if (P->plan) return;
+  P->plan = new ApplyPlan(P->ctx->stream);
+  P->plan->n = P->n;
+  P->plan->work = P->plan->mem.alloc(std::max<long long>(P->n, 1));
+  P->plan->tix.assign(P->n, -1);
+}
+
+void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>& fs) {
+  HostTimer ht("plan_extend");
+  plan_init(P);
   ApplyPlan* plan = P->plan;
   std::vector<int>& tix = plan->tix;
-  // groups: consecutive factors of the same (level, type)
+  // groups: consecutive factors of the same (level, type); indices local to fs
   std::vector<std::pair<size_t, size_t>> ranges;
-  for (size_t i = begin; i < end;) {
+  for (size_t i = 0; i < fs.size();) {
     size_t j = i + 1;
-    while (j < end && P->factors[j].type == P->factors[i].type && P->factors[j].level == P->factors[i].level &&
-           P->factors[i].type != SGF_FACTOR_DENSE)
+    while (j < fs.size() && fs[j]->type == fs[i]->type && fs[j]->level == fs[i]->level &&
+           fs[i]->type != SGF_FACTOR_DENSE)
       ++j;
     ranges.push_back({i, j});
     i = j;
   }
   for (auto& rg : ranges) {
     Group g;
-    g.type = P->factors[rg.first].type;
-    g.f0 = rg.first;
-    g.f1 = rg.second;
+    g.type = fs[rg.first]->type;
+    g.f0 = begin + rg.first;
+    g.f1 = begin + rg.second;
     long long sm = 0, sc = 0, sp = 0;
     for (size_t i = rg.first; i < rg.second; ++i) {
-      const Factor& f = P->factors[i];
+      const Factor& f = *fs[i];
       sm += f.m;
       sc += f.c;
       const long long rbE = (f.c + GT_ROWS - 1) / GT_ROWS, rbL = (f.m + GT_ROWS - 1) / GT_ROWS;
@@ -174,7 +183,7 @@ void plan_extend(Precond* P, size_t begin, size_t end) {
     long long om = 0, oc = 0, op = 0;
     std::vector<std::pair<int64_t, long long>> contrib;  // (unknown, t position) in factor order
     for (size_t i = rg.first; i < rg.second; ++i) {
-      const Factor& f = P->factors[i];
+      const Factor& f = *fs[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
       add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri);

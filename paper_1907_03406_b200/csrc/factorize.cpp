@@ -19,8 +19,12 @@
 // reference's operation order, so the stats dict matches exactly.
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
+#include <exception>
+#include <mutex>
 #include <sstream>
+#include <thread>
 
 #include "precond.h"
 
@@ -60,29 +64,84 @@ struct State {
 
 inline bool kind_in(int mask, int kind) { return (mask >> kind) & 1; }
 
-// SGF_TRACE=1: per-phase wall times (stream synchronised) on stderr
+// SGF_TRACE=1: per-phase wall times (stream synchronised) on stderr.
+// SGF_TRACE=3: asynchronous timeline (no synchronisation): host and device
+// start/end of every phase, printed at the end of the factorization.
+struct Timeline {
+  struct Rec {
+    std::string name;
+    double h0, h1;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Rec> recs;
+  std::chrono::steady_clock::time_point origin = std::chrono::steady_clock::now();
+  cudaEvent_t eorigin = nullptr;
+  double now() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - origin).count();
+  }
+};
+Timeline* g_tl = nullptr;
+
 struct Phase {
   const char* name;
   int level;
   cudaStream_t st;
   std::chrono::steady_clock::time_point t0;
-  static bool on() {
-    static int v = getenv("SGF_TRACE") ? 1 : 0;
+  int rec = -1;
+  static int mode() {
+    static int v = getenv("SGF_TRACE") ? atoi(getenv("SGF_TRACE")) : 0;
     return v;
   }
+  static bool on() { return mode() == 1 || mode() == 2; }
   Phase(const char* n, int lv, cudaStream_t s) : name(n), level(lv), st(s) {
     if (on()) {
       cudaStreamSynchronize(st);
       t0 = std::chrono::steady_clock::now();
+    } else if (mode() == 3 && g_tl) {
+      Timeline::Rec r;
+      r.name = std::string(n) + " L" + std::to_string(lv);
+      r.h0 = g_tl->now();
+      cudaEventCreate(&r.e0);
+      cudaEventCreate(&r.e1);
+      cudaEventRecord(r.e0, st);
+      rec = (int)g_tl->recs.size();
+      g_tl->recs.push_back(r);
     }
   }
   ~Phase() {
+    if (rec >= 0 && g_tl) {
+      cudaEventRecord(g_tl->recs[rec].e1, st);
+      g_tl->recs[rec].h1 = g_tl->now();
+      return;
+    }
     if (!on()) return;
     cudaStreamSynchronize(st);
     double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     fprintf(stderr, "[sgf] L%d %-10s %9.2f ms\n", level, name, ms);
   }
 };
+
+void timeline_begin(cudaStream_t st) {
+  if (Phase::mode() != 3) return;
+  g_tl = new Timeline();
+  cudaEventCreate(&g_tl->eorigin);
+  cudaEventRecord(g_tl->eorigin, st);
+}
+
+void timeline_end(cudaStream_t st) {
+  if (!g_tl) return;
+  cudaStreamSynchronize(st);
+  fprintf(stderr, "[timeline] %-16s %9s %9s | %9s %9s\n", "phase", "host0", "host1", "dev0", "dev1");
+  for (auto& r : g_tl->recs) {
+    float d0 = 0, d1 = 0;
+    cudaEventElapsedTime(&d0, g_tl->eorigin, r.e0);
+    cudaEventElapsedTime(&d1, g_tl->eorigin, r.e1);
+    fprintf(stderr, "[timeline] %-16s %9.2f %9.2f | %9.2f %9.2f\n", r.name.c_str(), r.h0, r.h1, d0, d1);
+  }
+  fprintf(stderr, "[timeline] total host %.2f ms\n", g_tl->now());
+  delete g_tl;
+  g_tl = nullptr;
+}
 
 // ---------------------------------------------------------------------------
 // level 1: nodes, basis rows, and the CSR -> block scatter (blockmatrix.py:97-144)
@@ -233,51 +292,75 @@ void setup_level1(State& S) {
   // basis rows of every node: Pi[active] in cell order
   Phase ph_phi(" s-phi", -1, S.st);
   const int pi = S.pi;
-  std::vector<double> phi_perm((size_t)n * pi);
-  if (a.phi) {
-#pragma omp parallel for
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t u = a.l1_unknowns[i];
-      std::memcpy(&phi_perm[(size_t)i * pi], a.phi + (size_t)u * pi, pi * sizeof(double));
+  // rows are generated straight into the context's pinned buffer, in chunks,
+  // each chunk's DMA overlapping the generation of the next
+  double* d_phi = S.lvl->alloc(std::max<size_t>((size_t)n * pi, 1));
+  const int64_t chunk_rows = std::max<int64_t>(1, ((int64_t)64 << 20) / (pi * (int64_t)sizeof(double)));
+  double* hp_buf[2] = {nullptr, nullptr};
+  {
+    const size_t half = (size_t)std::min<int64_t>(chunk_rows, std::max<int64_t>(n, 1)) * pi;
+    double* hp = (double*)S.ctx->pinned(2 * half * sizeof(double));
+    hp_buf[0] = hp;
+    hp_buf[1] = hp + half;
+  }
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  SGF_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+  SGF_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+  const int ps = a.degree == 0 ? 1 : (a.degree == 1 ? 4 : 10);
+  const int64_t nv = a.n_vertices;
+  auto mono = [&](int64_t v, int q) -> double {
+    const double x = a.coords[3 * v], y = a.coords[3 * v + 1], z = a.coords[3 * v + 2];
+    switch (q) {
+      case 0: return 1.0;
+      case 1: return x;
+      case 2: return y;
+      case 3: return z;
+      case 4: return x * x;
+      case 5: return y * y;
+      case 6: return z * z;
+      case 7: return x * y;
+      case 8: return y * z;
+      default: return z * x;
     }
-  } else {
-    // Pi from the coordinates (basis.py:27-62): monomials [1 x y z (x^2 y^2
-    // z^2 xy yz zx)], block diagonal per component, column / max |column|
-    const int ps = a.degree == 0 ? 1 : (a.degree == 1 ? 4 : 10);
-    const int64_t nv = a.n_vertices;
-    auto mono = [&](int64_t v, int q) -> double {
-      const double x = a.coords[3 * v], y = a.coords[3 * v + 1], z = a.coords[3 * v + 2];
-      switch (q) {
-        case 0: return 1.0;
-        case 1: return x;
-        case 2: return y;
-        case 3: return z;
-        case 4: return x * x;
-        case 5: return y * y;
-        case 6: return z * z;
-        case 7: return x * y;
-        case 8: return y * z;
-        default: return z * x;
-      }
-    };
-    std::vector<double> scale(ps, 0.0);
+  };
+  // Pi from the coordinates (basis.py:27-62): monomials [1 x y z (x^2 y^2
+  // z^2 xy yz zx)], block diagonal per component, column / max |column|
+  std::vector<double> scale(ps, 1.0);
+  if (!a.phi) {
     for (int q = 0; q < ps; ++q) {
       double mx = 0.0;
 #pragma omp parallel for reduction(max : mx)
       for (int64_t v = 0; v < nv; ++v) mx = std::max(mx, std::fabs(mono(v, q)));
       scale[q] = (mx == 0.0) ? 1.0 : mx;
     }
-#pragma omp parallel for
-    for (int64_t i = 0; i < n; ++i) {
-      const int64_t u = a.l1_unknowns[i];
-      const int64_t c = u / nv, v = u % nv;
-      double* row = &phi_perm[(size_t)i * pi];
-      for (int k = 0; k < pi; ++k) row[k] = 0.0;
-      for (int q = 0; q < ps; ++q) row[c * ps + q] = mono(v, q) / scale[q];
-    }
   }
-  double* d_phi = S.lvl->alloc(std::max<size_t>(phi_perm.size(), 1));
-  upload_pinned(*S.ctx, d_phi, phi_perm.data(), phi_perm.size() * sizeof(double));
+  int k = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += chunk_rows, k ^= 1) {
+    const int64_t r1 = std::min<int64_t>(n, r0 + chunk_rows);
+    SGF_CUDA(cudaEventSynchronize(done[k]));  // the copy that last used this half has landed
+    double* hp = hp_buf[k];
+    if (a.phi) {
+#pragma omp parallel for
+      for (int64_t i = r0; i < r1; ++i)
+        std::memcpy(hp + (size_t)(i - r0) * pi, a.phi + (size_t)a.l1_unknowns[i] * pi, pi * sizeof(double));
+    } else {
+#pragma omp parallel for
+      for (int64_t i = r0; i < r1; ++i) {
+        const int64_t u = a.l1_unknowns[i];
+        const int64_t c = u / nv, v = u % nv;
+        double* row = hp + (size_t)(i - r0) * pi;
+        for (int q = 0; q < pi; ++q) row[q] = 0.0;
+        for (int q = 0; q < ps; ++q) row[c * ps + q] = mono(v, q) / scale[q];
+      }
+    }
+    SGF_CUDA(cudaMemcpyAsync(d_phi + (size_t)r0 * pi, hp, (size_t)(r1 - r0) * pi * sizeof(double),
+                             cudaMemcpyHostToDevice, S.st));
+    SGF_CUDA(cudaEventRecord(done[k], S.st));
+  }
+  // the pinned buffer is reused only after a stream synchronisation
+  // (upload_pinned); the events can go once their copies are enqueued
+  cudaEventDestroy(done[0]);
+  cudaEventDestroy(done[1]);
   for (int c = 0; c < nc; ++c) S.nodes[c].phi = d_phi + (size_t)a.l1_ptr[c] * pi;
 }
 
@@ -298,6 +381,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   std::vector<EI> info(elim.size());
   CopyBatch cp;
   std::vector<CholJob> jobs;
+  HostTimer ht0("elim setup+chol");
+  size_t tot_w = 0, tot_e = 0;
   for (size_t q = 0; q < elim.size(); ++q) {
     EI& e = info[q];
     e.x = elim[q];
@@ -309,19 +394,35 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       e.c += M.size[j];
     }
     e.ld = pad_ld(e.m);
+    tot_w += (size_t)e.m * e.ld;
+    tot_e += (size_t)e.c * e.ld;
+  }
+  // one region per kind for the whole level: L, L^{-1} (zeroed once: the
+  // inverse kernel writes the lower triangle only) and the couplings E
+  double* Wall = P->store.alloc(std::max<size_t>(tot_w, 1));
+  double* Xall = P->store.alloc(std::max<size_t>(tot_w, 1));
+  double* Eall = tot_e ? P->store.alloc(tot_e) : nullptr;
+  SGF_CUDA(cudaMemsetAsync(Xall, 0, tot_w * sizeof(double), st));
+  size_t ow = 0, oe = 0;
+  for (size_t q = 0; q < elim.size(); ++q) {
+    EI& e = info[q];
     const size_t mm = (size_t)e.m * e.ld;
-    e.W = P->store.alloc(mm);
-    e.X = P->store.alloc(mm);
-    SGF_CUDA(cudaMemsetAsync(e.X, 0, mm * sizeof(double), st));
-    e.E = e.c ? P->store.alloc((size_t)e.c * e.ld) : nullptr;
+    e.W = Wall + ow;
+    e.X = Xall + ow;
+    ow += mm;
+    e.E = e.c ? Eall + oe : nullptr;
+    oe += (size_t)e.c * e.ld;
     Blk* d = M.find(e.x, e.x);
     if (!d) fail(SGF_NOT_SPD, "interior node without a diagonal block");
     cp.add(d->p, d->cols, 1, e.W, e.ld, 1, e.m, e.m);
     jobs.push_back(CholJob{e.W, e.X, e.m, e.x, e.ld});
   }
   cp.launch(S.scratch, st);
-  chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
-
+  {
+    HostTimer htc("elim chol_inv_batch");
+    chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
+  }
+  HostTimer hte("elim E gemm");
   GemmBatch ge;
   for (auto& e : info) {
     long long f = (long long)e.m * e.m * e.m / 3;
@@ -338,36 +439,38 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   ge.launch(S.scratch, st);
 
   // Schur targets in the reference's insertion order (ascending interior id,
-  // neighbour pairs a <= b); fill blocks are created zero (blockmatrix.py:65-72)
+  // neighbour pairs a <= b); a target first seen without a block is a fill,
+  // created zero (blockmatrix.py:65-72) when its first contributor runs
   struct Target {
     int a, b;
+    int q0;                 // first contributing interior (creation point of a fill)
+    long long fill = -1;    // offset in the fill region, -1: existing block
     std::vector<std::pair<int, std::pair<int, int>>> contrib;
   };
-  std::unordered_map<uint64_t, int> tix;
+  HostTimer ht1("elim targets");
   std::vector<Target> targets;
+  std::vector<int> fills;  // target ids of fills, in creation order
   long long fill_elems = 0;
-  std::vector<std::pair<uint64_t, long long>> fills;  // key -> elems, in creation order
   {
-    std::unordered_map<uint64_t, char> created;
+    size_t pairs = 0;
+    for (auto& e : info) pairs += e.nb.size() * (e.nb.size() + 1) / 2;
+    FlatMap<int> tix(pairs / 4 + 16);
     for (size_t q = 0; q < info.size(); ++q) {
       const EI& e = info[q];
       for (size_t p = 0; p < e.nb.size(); ++p)
         for (size_t r = p; r < e.nb.size(); ++r) {
           const int A = e.nb[p], B = e.nb[r];
-          const uint64_t k = bkey(A, B);
-          if (!M.find(A, B) && !created.count(k)) {
-            created[k] = 1;
-            const long long el = (long long)M.size[A] * M.size[B];
-            fills.push_back({k, el});
-            fill_elems += el;
+          auto ins = tix.emplace(bkey(A, B));
+          if (ins.second) {
+            *ins.first = (int)targets.size();
+            targets.push_back(Target{A, B, (int)q, -1, {}});
+            if (!M.find(A, B)) {
+              targets.back().fill = fill_elems;
+              fills.push_back(*ins.first);
+              fill_elems += (long long)M.size[A] * M.size[B];
+            }
           }
-          auto it = tix.find(k);
-          if (it == tix.end()) {
-            tix[k] = (int)targets.size();
-            targets.push_back(Target{A, B, {}});
-            it = tix.find(k);
-          }
-          targets[it->second].contrib.push_back({(int)q, {(int)p, (int)r}});
+          targets[*ins.first].contrib.push_back({(int)q, {(int)p, (int)r}});
         }
     }
   }
@@ -376,24 +479,48 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     fill_base = S.lvl->alloc(fill_elems);
     SGF_CUDA(cudaMemsetAsync(fill_base, 0, fill_elems * sizeof(double), st));
   }
+  // Schur GEMMs first (the level's largest device work), table bookkeeping after
   {
-    std::unordered_map<uint64_t, double*> fill_ptr;
-    long long off = 0;
-    for (auto& f : fills) {
-      fill_ptr[f.first] = fill_base + off;
-      off += f.second;
+    HostTimer ht("schur tasks");
+    GemmBatch gs;
+    std::vector<GemmSeg> sg;
+    for (auto& T : targets) {
+      double* bp;
+      int br, bc;
+      if (T.fill < 0) {
+        Blk* blk = M.find(T.a, T.b);  // T.a <= T.b: rows in a
+        bp = blk->p;
+        br = blk->rows;
+        bc = blk->cols;
+      } else {
+        bp = fill_base + T.fill;
+        br = M.size[T.a];
+        bc = M.size[T.b];
+      }
+      sg.clear();
+      for (auto& c : T.contrib) {
+        const EI& e = info[c.first];
+        sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.ld, e.ld, 1,
+                         e.E + (long long)e.off[c.second.second] * e.ld, e.ld, 1, e.m));
+      }
+      // diagonal blocks are kept valid in their lower triangle only: every
+      // consumer (Cholesky of the node, densify + Cholesky) reads only that
+      gs.add(bp, bc, 1, br, bc, -1.0, 1.0, sg, -1, T.a == T.b);
     }
-    // replay the reference sequence for the table and its byte accounting
+    HostTimer ht2("schur launch");
+    gs.launch(S.scratch, st);
+  }
+  {
+    HostTimer ht("elim bookkeeping");
+    // replay the reference sequence for the table and its byte accounting:
+    // interior q creates the fills it touches first, then is dropped
+    size_t fi = 0;
     for (size_t q = 0; q < info.size(); ++q) {
       const EI& e = info[q];
-      for (size_t p = 0; p < e.nb.size(); ++p)
-        for (size_t r = p; r < e.nb.size(); ++r) {
-          const int A = e.nb[p], B = e.nb[r];
-          if (!M.find(A, B)) {
-            auto it = fill_ptr.find(bkey(A, B));
-            M.insert(A, B, Blk{it->second, M.size[A], M.size[B]});
-          }
-        }
+      for (; fi < fills.size() && targets[fills[fi]].q0 == (int)q; ++fi) {
+        const Target& T = targets[fills[fi]];
+        M.insert(T.a, T.b, Blk{fill_base + T.fill, M.size[T.a], M.size[T.b]});
+      }
       // factor record (before the node's actives are cleared)
       Factor f;
       f.type = SGF_FACTOR_ELIMINATION;
@@ -414,20 +541,6 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       S.nodes[e.x].phi = nullptr;
     }
   }
-  GemmBatch gs;
-  for (auto& T : targets) {
-    Blk* blk = M.find(T.a, T.b);  // T.a <= T.b: rows in a
-    std::vector<GemmSeg> sg;
-    for (auto& c : T.contrib) {
-      const EI& e = info[c.first];
-      sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.ld, e.ld, 1,
-                       e.E + (long long)e.off[c.second.second] * e.ld, e.ld, 1, e.m));
-    }
-    // diagonal blocks are kept valid in their lower triangle only: every
-    // consumer (Cholesky of the node, densify + Cholesky) reads only that
-    gs.add(blk->p, blk->cols, 1, blk->rows, blk->cols, -1.0, 1.0, sg, -1, T.a == T.b);
-  }
-  gs.launch(S.scratch, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -811,6 +924,7 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
 // merge into the next level (factorization.py:356-407)
 // ---------------------------------------------------------------------------
 void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kinds, const int8_t* interior) {
+  HostTimer ht("merge");
   cudaStream_t st = S.st;
   BlockTable& M = S.M;
   const int nc = (int)S.nodes.size();
@@ -854,21 +968,22 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
   // father blocks in the reference's creation order (sorted old keys)
   std::vector<uint64_t> keys;
   keys.reserve(M.map.size());
-  for (auto& kv : M.map) keys.push_back(kv.first);
+  M.map.for_each([&](uint64_t k, Blk&) { keys.push_back(k); });
   std::sort(keys.begin(), keys.end());
   BlockTable N;
   N.init(nsize);
   std::vector<std::pair<uint64_t, long long>> order;
-  std::unordered_map<uint64_t, long long> newoff;
+  FlatMap<long long> newoff(keys.size());
   long long tot = 0;
   for (uint64_t k : keys) {
-    const Blk& b = M.map[k];
+    const Blk& b = *M.map.find(k);
     if ((long long)b.rows * b.cols == 0) continue;
     const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
     const uint64_t fk = bkey(fof[a0], fof[b0]);
-    if (!newoff.count(fk)) {
+    auto ins = newoff.emplace(fk);
+    if (ins.second) {
       const int fa = (int)(fk >> 32), fb = (int)(fk & 0xffffffffu);
-      newoff[fk] = tot;
+      *ins.first = tot;
       order.push_back({fk, tot});
       tot += (long long)nsize[fa] * nsize[fb];
     }
@@ -880,7 +995,7 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
     N.insert(fa, fb, Blk{base + o.second, nsize[fa], nsize[fb]});
   }
   for (uint64_t k : keys) {
-    const Blk& b = M.map[k];
+    const Blk& b = *M.map.find(k);
     if ((long long)b.rows * b.cols == 0) continue;
     const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
     const int fa = fof[a0], fb = fof[b0], oa = oof[a0], ob = oof[b0];
@@ -934,14 +1049,13 @@ void final_dense(State& S) {
   SGF_CUDA(cudaMemsetAsync(D, 0, tt * sizeof(double), st));
   SGF_CUDA(cudaMemsetAsync(X, 0, tt * sizeof(double), st));
   CopyBatch cp;
-  for (auto& kv : M.map) {
-    const int a0 = (int)(kv.first >> 32), b0 = (int)(kv.first & 0xffffffffu);
+  M.map.for_each([&](uint64_t k, Blk& b) {
+    const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
     auto ia = off.find(a0), ib = off.find(b0);
-    if (ia == off.end() || ib == off.end()) continue;
-    const Blk& b = kv.second;
+    if (ia == off.end() || ib == off.end()) return;
     cp.add(b.p, b.cols, 1, D + (long long)ia->second * ldt + ib->second, ldt, 1, b.rows, b.cols);
     if (a0 != b0) cp.add(b.p, 1, b.cols, D + (long long)ib->second * ldt + ia->second, ldt, 1, b.cols, b.rows);
-  }
+  });
   cp.launch(S.scratch, st);
   std::vector<CholJob> jobs{CholJob{D, X, tot, -1, ldt}};
   chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
@@ -979,6 +1093,71 @@ std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<Le
   return o.str();
 }
 
+// Builds the apply plan on a worker thread, one level's factors at a time, in
+// submission order.  Factors live in a deque, so the pointers handed over stay
+// valid while the driver keeps appending; the worker reads only fields that are
+// final when a level's function returns.  Allocation and staging go through the
+// mutex-guarded chunk cache and pinned ring.
+class PlanWorker {
+ public:
+  explicit PlanWorker(Precond* P) : P_(P) {
+    SGF_CUDA(cudaGetDevice(&dev_));
+    plan_init(P);
+    th_ = std::thread([this] { run(); });
+  }
+  ~PlanWorker() { stop(); }
+  void push(size_t begin, size_t end) {
+    std::vector<const Factor*> fs;
+    for (size_t i = begin; i < end; ++i) fs.push_back(&P_->factors[i]);
+    if (fs.empty()) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    q_.push_back({begin, std::move(fs)});
+    cv_.notify_one();
+  }
+  // wait for every queued level; rethrows a failure of the worker
+  void finish() {
+    stop();
+    if (err_) std::rethrow_exception(err_);
+  }
+
+ private:
+  void stop() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ = true;
+    }
+    cv_.notify_one();
+    if (th_.joinable()) th_.join();
+  }
+  void run() {
+    cudaSetDevice(dev_);
+    for (;;) {
+      std::pair<size_t, std::vector<const Factor*>> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return done_ || !q_.empty(); });
+        if (q_.empty()) return;
+        job = std::move(q_.front());
+        q_.pop_front();
+      }
+      if (err_) continue;  // drain after a failure
+      try {
+        plan_extend_ptrs(P_, job.first, job.second);
+      } catch (...) {
+        err_ = std::current_exception();
+      }
+    }
+  }
+  Precond* P_;
+  int dev_ = 0;
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::pair<size_t, std::vector<const Factor*>>> q_;
+  bool done_ = false;
+  std::exception_ptr err_;
+};
+
 }  // namespace
 
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
@@ -1003,7 +1182,9 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.pi = a.pi_cols;
   S.P = P.get();
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
+  PlanWorker planner(P.get());  // destroyed (joined) before P and S
 
+  timeline_begin(S.st);
   { Phase ph("setup", 0, S.st); setup_level1(S); }
   S.peak = 0;
   std::vector<LevelStats> per_level;
@@ -1031,7 +1212,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       Phase ph("eliminate", t + 1, S.st);
       const size_t f0 = P->factors.size();
       eliminate_level(S, elim, t + 1);
-      plan_extend(P.get(), f0, P->factors.size());  // host work overlapping the level's kernels
+      planner.push(f0, P->factors.size());  // plan built on the worker while the level runs
     }
     ls.eliminated = (int)elim.size();
     S.scratch.release();  // chunks are reused in stream order: no sync needed
@@ -1043,7 +1224,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
         Phase ph("compress", t + 1, S.st);
         const size_t f0 = P->factors.size();
         compress_level(S, comp, t + 1, ls);
-        plan_extend(P.get(), f0, P->factors.size());
+        planner.push(f0, P->factors.size());
       }
     }
     for (auto& nd : S.nodes) max_after = std::max(max_after, (int)nd.active.size());
@@ -1066,7 +1247,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     Phase ph("dense", 0, S.st);
     const size_t f0 = P->factors.size();
     final_dense(S);
-    plan_extend(P.get(), f0, P->factors.size());
+    planner.push(f0, P->factors.size());
   }
   int final_size = 0;
   if (P->factors.size() > before) {
@@ -1096,8 +1277,9 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   }
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
                         (int)P->factors.size(), 0, nullptr);
-  if (!P->plan) plan_extend(P.get(), 0, 0);
+  planner.finish();
   plan_finish(P.get());
+  timeline_end(S.st);
   SGF_CUDA(cudaStreamSynchronize(S.st));
   return P.release();
 }

@@ -1,6 +1,7 @@
 // Device-resident preconditioner: the ordered elementary factors of the
 // reference (factorization.py:112-213) plus the level-batched apply plan.
 #pragma once
+#include <deque>
 #include <memory>
 
 #include "runtime.h"
@@ -30,13 +31,17 @@ struct ApplyPlan;
 void destroy_plan(ApplyPlan* p);
 ApplyPlan* build_plan(class Precond* P);
 void plan_extend(class Precond* P, size_t begin, size_t end);  // add groups of factors [begin, end)
+// same, reading the factors only through the given (stable) pointers: safe to
+// run on a worker thread while the driver keeps appending factors
+void plan_extend_ptrs(class Precond* P, size_t begin, const std::vector<const Factor*>& fs);
 void plan_finish(class Precond* P);
+void plan_init(class Precond* P);
 
 class Precond {
  public:
   Ctx* ctx = nullptr;
   int64_t n = 0;
-  std::vector<Factor> factors;
+  std::deque<Factor> factors;  // deque: stable element addresses while appending
   std::string stats;
   std::vector<int32_t> trace;  // (level, node, rank) triples
   Arena store;

@@ -129,6 +129,7 @@ void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   Stager& s = g_stage[st];
   const size_t need = (bytes + 255) & ~(size_t)255;
   if (s.off + need > s.cap) {
+    if (getenv("SGF_TRACE")) fprintf(stderr, "[stage] ring full (%zu + %zu > %zu): synchronising\n", s.off, need, s.cap);
     SGF_CUDA(cudaStreamSynchronize(st));  // every staged copy has landed
     s.off = 0;
     if (need > s.cap) {
@@ -223,7 +224,7 @@ static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const
                         const std::vector<GemmSeg>& segs, int big, cudaStream_t st) {
   const int bm = big ? 128 : 64;
   ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(h, segs, bm) : 0.0);
-  if (trace_level() < 2) {
+  if (trace_level() != 2) {
     SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
     return;
   }

@@ -3,7 +3,10 @@
 // apply plan (apply.cpp) and the C ABI (capi.cpp) build on this.
 #pragma once
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -69,6 +72,22 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// SGF_TRACE=4: host-side (no synchronisation) timing of a scope
+struct HostTimer {
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit HostTimer(const char* n) : name(n) {}
+  static bool on() {
+    static bool v = getenv("SGF_TRACE") && atoi(getenv("SGF_TRACE")) == 4;
+    return v;
+  }
+  ~HostTimer() {
+    if (on())
+      fprintf(stderr, "[host] %-24s %8.2f ms\n", name,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 // process-wide device chunk cache (runtime.cpp), per device
 void* chunk_get(size_t bytes, size_t* cap);
 void chunk_put(void* p, size_t cap);
@@ -122,7 +141,10 @@ struct Ctx {
   size_t pin_cap = 0;
   void* pinned(size_t bytes) {
     if (bytes > pin_cap) {
-      if (pin) cudaFreeHost(pin);
+      if (pin) {
+        cudaStreamSynchronize(stream);  // copies may still read the old buffer
+        cudaFreeHost(pin);
+      }
       pin = nullptr;
       pin_cap = 0;
       SGF_CUDA(cudaMallocHost(&pin, bytes));
@@ -153,8 +175,111 @@ inline uint64_t bkey(int a, int b) {
   return ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
 }
 
+// Open-addressing hash map for 64-bit block keys (linear probing, backward-
+// shift deletion): the symbolic phases do millions of lookups per level, where
+// a node-based map's allocation and pointer chasing dominate.  Key ~0 is the
+// empty marker (never a valid block key).
+template <class V>
+class FlatMap {
+ public:
+  static constexpr uint64_t EMPTY = ~0ull;
+  explicit FlatMap(size_t expect = 16) { reserve(expect); }
+  size_t size() const { return n_; }
+  void clear() {
+    std::fill(keys_.begin(), keys_.end(), EMPTY);
+    n_ = 0;
+  }
+  void reserve(size_t expect) {
+    size_t cap = 16;
+    while (cap < expect * 2) cap <<= 1;
+    if (cap > keys_.size()) rehash(cap);
+  }
+  V* find(uint64_t k) {
+    size_t i = slot(k);
+    for (;;) {
+      if (keys_[i] == k) return &vals_[i];
+      if (keys_[i] == EMPTY) return nullptr;
+      i = (i + 1) & mask_;
+    }
+  }
+  const V* find(uint64_t k) const { return const_cast<FlatMap*>(this)->find(k); }
+  bool contains(uint64_t k) const { return find(k) != nullptr; }
+  // returns the value slot and whether the key was new (value default-built)
+  std::pair<V*, bool> emplace(uint64_t k) {
+    if ((n_ + 1) * 2 > keys_.size()) rehash(keys_.size() * 2);
+    size_t i = slot(k);
+    for (;;) {
+      if (keys_[i] == k) return {&vals_[i], false};
+      if (keys_[i] == EMPTY) {
+        keys_[i] = k;
+        vals_[i] = V();
+        ++n_;
+        return {&vals_[i], true};
+      }
+      i = (i + 1) & mask_;
+    }
+  }
+  V& operator[](uint64_t k) { return *emplace(k).first; }
+  bool erase(uint64_t k) {
+    size_t i = slot(k);
+    for (;;) {
+      if (keys_[i] == EMPTY) return false;
+      if (keys_[i] == k) break;
+      i = (i + 1) & mask_;
+    }
+    // backward shift: pull later members of the probe run into the hole
+    size_t j = i;
+    for (;;) {
+      j = (j + 1) & mask_;
+      if (keys_[j] == EMPTY) break;
+      const size_t h = slot(keys_[j]);
+      const bool movable = (i <= j) ? (h <= i || h > j) : (h <= i && h > j);
+      if (movable) {
+        keys_[i] = keys_[j];
+        vals_[i] = vals_[j];
+        i = j;
+      }
+    }
+    keys_[i] = EMPTY;
+    --n_;
+    return true;
+  }
+  template <class F>
+  void for_each(F&& f) {
+    for (size_t i = 0; i < keys_.size(); ++i)
+      if (keys_[i] != EMPTY) f(keys_[i], vals_[i]);
+  }
+
+ private:
+  size_t slot(uint64_t k) const { return (size_t)((k * 0x9E3779B97F4A7C15ull) >> shift_); }
+  void rehash(size_t cap) {
+    std::vector<uint64_t> ok;
+    std::vector<V> ov;
+    ok.swap(keys_);
+    ov.swap(vals_);
+    keys_.assign(cap, EMPTY);
+    vals_.resize(cap);
+    mask_ = cap - 1;
+    shift_ = 64;
+    for (size_t c = cap; c > 1; c >>= 1) --shift_;
+    n_ = 0;
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (ok[i] != EMPTY) {
+        size_t s = slot(ok[i]);
+        while (keys_[s] != EMPTY) s = (s + 1) & mask_;
+        keys_[s] = ok[i];
+        vals_[s] = ov[i];
+        ++n_;
+      }
+  }
+  std::vector<uint64_t> keys_;
+  std::vector<V> vals_;
+  size_t mask_ = 0, n_ = 0;
+  int shift_ = 64;
+};
+
 struct BlockTable {
-  std::unordered_map<uint64_t, Blk> map;
+  FlatMap<Blk> map;
   std::vector<std::vector<int>> adj;
   std::vector<int> size;
   long long live = 0, peak = 0;
@@ -167,15 +292,11 @@ struct BlockTable {
     live = peak = 0;
   }
   static long long nbytes(const Blk& b) { return 8LL * b.rows * b.cols; }
-  Blk* find(int a, int b) {
-    auto it = map.find(bkey(a, b));
-    return it == map.end() ? nullptr : &it->second;
-  }
+  Blk* find(int a, int b) { return map.find(bkey(a, b)); }
   void insert(int a, int b, Blk blk) {
-    uint64_t k = bkey(a, b);
-    auto it = map.find(k);
-    if (it != map.end()) live -= nbytes(it->second);
-    map[k] = blk;
+    auto r = map.emplace(bkey(a, b));
+    if (!r.second) live -= nbytes(*r.first);
+    *r.first = blk;
     live += nbytes(blk);
     peak = std::max(peak, live);
     if (a != b) {
@@ -187,22 +308,20 @@ struct BlockTable {
     auto& v = adj[a];
     if (std::find(v.begin(), v.end(), b) == v.end()) v.push_back(b);
   }
+  void drop_key(uint64_t k) {
+    if (Blk* p = map.find(k)) {
+      live -= nbytes(*p);
+      map.erase(k);
+    }
+  }
   void drop(int a) {
     for (int b : adj[a]) {
-      auto it = map.find(bkey(a, b));
-      if (it != map.end()) {
-        live -= nbytes(it->second);
-        map.erase(it);
-      }
+      drop_key(bkey(a, b));
       auto& v = adj[b];
       v.erase(std::remove(v.begin(), v.end(), a), v.end());
     }
     adj[a].clear();
-    auto it = map.find(bkey(a, a));
-    if (it != map.end()) {
-      live -= nbytes(it->second);
-      map.erase(it);
-    }
+    drop_key(bkey(a, a));
   }
   std::vector<int> nbrs(int a) const {
     std::vector<int> v = adj[a];
