@@ -428,9 +428,10 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
 
 // ---------------------------------------------------------------------------
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
-  // values + int32 columns + int64 row pointers + x + y (+ b)
-  ProfScope ps(A->ctx->stream, PROF_SPMV, 12.0 * A->nnz + 8.0 * (A->n + 1) + (d_b ? 24.0 : 16.0) * A->n);
-  SGF_CUDA(launch_spmv((int)A->n, A->rp, A->ci, A->v, d_x, d_y, d_b, A->tpr, A->ctx->stream));
+  // values + int32 columns + row pointers + x + y (+ b)
+  ProfScope ps(A->ctx->stream, PROF_SPMV,
+               12.0 * A->nnz + (A->rp32 ? 4.0 : 8.0) * (A->n + 1) + (d_b ? 24.0 : 16.0) * A->n);
+  SGF_CUDA(launch_spmv((int)A->n, A->rp, A->rp32, A->ci, A->v, d_x, d_y, d_b, A->ctx->stream));
 }
 
 // PCG with the reference recurrence (krylov.py:34-102): true-residual

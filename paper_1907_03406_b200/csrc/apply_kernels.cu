@@ -171,38 +171,80 @@ cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, cons
 // ---------------------------------------------------------------------------
 constexpr int RED_BLOCKS = 296;
 
-// CSR SpMV y = A x (mode 0) or y = b - A x (mode 1); `tpr` lanes per row.
-template <int TPR>
-__global__ void __launch_bounds__(256) spmv_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ ci,
+// CSR SpMV y = A x (b == nullptr) or y = b - A x.  One warp per 32
+// consecutive rows: the warp streams the rows' contiguous nonzero range in
+// chunks of 256 with fully coalesced, independent loads (8 per lane in flight),
+// stages the products v[e] * x[ci[e]] in shared memory, and every lane then
+// sums its own row in storage order -- the sequential order of the reference's
+// CSR product (scipy), so the result does not depend on the launch shape.
+constexpr int SPMV_CH = 256;
+constexpr int SPMV_WARPS = 8;
+template <class RP>
+__global__ void __launch_bounds__(256, 4) spmv_kernel(int n, const RP* __restrict__ rp, const int* __restrict__ ci,
                                                    const double* __restrict__ v, const double* __restrict__ x,
                                                    double* __restrict__ y, const double* __restrict__ b) {
-  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int sub = threadIdx.x % TPR;
-  const long long stride = (long long)gridDim.x * blockDim.x / TPR;
-  // warp-uniform trip count so the shuffles below always see full warps
-  const long long wbase = (gt - (threadIdx.x & 31)) / TPR;
-  for (long long rw = wbase, row = gt / TPR; rw < n; rw += stride, row += stride) {
+  __shared__ double prod[SPMV_WARPS][SPMV_CH];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* pw = prod[w];
+  const long long nwarps = (long long)gridDim.x * SPMV_WARPS;
+  for (long long r0 = ((long long)blockIdx.x * SPMV_WARPS + w) * 32; r0 < n; r0 += nwarps * 32) {
+    const long long row = r0 + lane;
+    const int last = (int)min(31LL, n - 1 - r0);  // last valid lane
+    long long rs = 0, re = 0;
+    if (row < n) {
+      rs = (long long)rp[row];
+      re = (long long)rp[row + 1];
+    }
+    const long long e0 = __shfl_sync(0xffffffffu, rs, 0);
+    const long long e1 = __shfl_sync(0xffffffffu, re, last);
     double s = 0.0;
-    if (row < n)
-      for (long long e = rp[row] + sub; e < rp[row + 1]; e += TPR) s = fma(v[e], __ldg(x + ci[e]), s);
+    for (long long cs = e0; cs < e1; cs += SPMV_CH) {
+      const int cnt = (int)min((long long)SPMV_CH, e1 - cs);
+      int cj[SPMV_CH / 32];
+      double vj[SPMV_CH / 32];
 #pragma unroll
-    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
-    if (sub == 0 && row < n) y[row] = b ? b[row] - s : s;
+      for (int j = 0; j < SPMV_CH / 32; ++j) {
+        const int k = lane + 32 * j;
+        if (k < cnt) {
+          cj[j] = __ldcs(ci + cs + k);
+          vj[j] = __ldcs(v + cs + k);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < SPMV_CH / 32; ++j) {
+        const int k = lane + 32 * j;
+        if (k < cnt) pw[k] = vj[j] * __ldg(x + cj[j]);
+      }
+      __syncwarp();
+      const long long a = max(rs, cs), z = min(re, cs + cnt);
+      for (long long e = a; e < z; ++e) s += pw[e - cs];
+      __syncwarp();
+    }
+    if (row < n) y[row] = b ? b[row] - s : s;
   }
 }
 
-cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double* v, const double* x, double* y,
-                        const double* b, int tpr, cudaStream_t s) {
+__global__ void rowptr32_kernel(const long long* __restrict__ rp, int* __restrict__ out, long long n1) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n1; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (int)rp[i];
+}
+
+cudaError_t launch_rowptr32(const long long* rp, int* out, long long n1, cudaStream_t s) {
+  if (n1 <= 0) return cudaSuccess;
+  long long blocks = std::min<long long>((n1 + 255) / 256, 148 * 16);
+  count_launch(); rowptr32_kernel<<<(unsigned)blocks, 256, 0, s>>>(rp, out, n1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(int n, const long long* rp, const int* rp32, const int* ci, const double* v, const double* x,
+                        double* y, const double* b, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  long long threads = (long long)n * tpr;
-  long long blocks = (threads + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  switch (tpr) {
-    case 4: count_launch(); spmv_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    case 8: count_launch(); spmv_kernel<8><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    case 16: count_launch(); spmv_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-    default: count_launch(); spmv_kernel<32><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b); break;
-  }
+  const long long warps = ((long long)n + 31) / 32;
+  long long blocks = (warps + SPMV_WARPS - 1) / SPMV_WARPS;
+  if (blocks > 148 * 4) blocks = 148 * 4;  // 4 resident CTAs per SM (64 regs), grid-stride beyond
+  count_launch();
+  if (rp32) spmv_kernel<int><<<(unsigned)blocks, 256, 0, s>>>(n, rp32, ci, v, x, y, b);
+  else spmv_kernel<long long><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, b);
   return cudaGetLastError();
 }
 

@@ -257,8 +257,10 @@ int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, 
     SGF_CUDA(cudaMemcpyAsync(A->a.rp, indptr, (n + 1) * 8, k, st));
     SGF_CUDA(cudaMemcpyAsync(A->a.ci, indices, nnz * 4, k, st));
     SGF_CUDA(cudaMemcpyAsync(A->a.v, values, nnz * 8, k, st));
-    const double avg = n ? (double)nnz / n : 0.0;
-    A->a.tpr = avg <= 6 ? 4 : avg <= 12 ? 8 : avg <= 24 ? 16 : 32;
+    if (nnz <= (int64_t)INT32_MAX) {
+      A->a.rp32 = A->a.mem.alloc_t<int>(n + 1);
+      SGF_CUDA(launch_rowptr32(A->a.rp, A->a.rp32, n + 1, st));
+    }
     SGF_CUDA(cudaStreamSynchronize(st));
     *out = A;
   });

@@ -58,9 +58,9 @@ struct Csr {
   Ctx* ctx = nullptr;
   int64_t n = 0, nnz = 0;
   long long* rp = nullptr;
+  int* rp32 = nullptr;  // int32 row pointers when nnz fits (the SpMV reads these)
   int* ci = nullptr;
   double* v = nullptr;
-  int tpr = 8;
   Arena mem;
 };
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b);

@@ -42,8 +42,9 @@ cudaError_t launch_gather(const double* x, const int* idx, double* out, long lon
 cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s);
 cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
                            long long nt, cudaStream_t s, int add = 0);
-cudaError_t launch_spmv(int n, const long long* rp, const int* ci, const double* v, const double* x, double* y,
-                        const double* b, int tpr, cudaStream_t s);
+cudaError_t launch_spmv(int n, const long long* rp, const int* rp32, const int* ci, const double* v, const double* x,
+                        double* y, const double* b, cudaStream_t s);
+cudaError_t launch_rowptr32(const long long* rp, int* out, long long n1, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s);
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,

@@ -196,3 +196,25 @@ def test_polynomial_preservation_and_spd(scheme, degree):
         x = rng.standard_normal(prob.n)
         assert x @ P.apply_operator(x) > 0
         assert x @ P.apply_inverse(x) > 0
+
+
+def test_spmv_irregular_rows():
+    """CSR SpMV against scipy on ragged rows: empty rows, rows spanning
+    several 256-entry chunks, a row count that is not a multiple of 32."""
+    rng = np.random.default_rng(11)
+    n = 3001
+    lens = rng.integers(0, 12, n)
+    lens[::97] = 0
+    lens[5] = 700
+    lens[1500] = 257
+    rows = np.repeat(np.arange(n), lens)
+    cols = rng.integers(0, n, rows.size)
+    A = sp.csr_matrix((rng.standard_normal(rows.size), (rows, cols)), shape=(n, n))
+    A.sum_duplicates()
+    A.sort_indices()
+    x = rng.standard_normal(n)
+    y = sgf.DeviceCSR(A) @ x
+    ref = A @ x
+    assert np.max(np.abs(y - ref)) <= 1e-13 * max(np.max(np.abs(ref)), 1.0)
+    # zero rows give exact zeros
+    assert np.all(y[np.diff(A.indptr) == 0] == 0.0)
