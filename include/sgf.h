@@ -103,6 +103,20 @@ typedef struct {
   int64_t n_vertices;
   int degree;
   int components;
+  /* sharding across ranks, one process per GPU; shard_count
+     <= 1 disables it.  Every rank runs the same symbolic factorization; a
+     rank computes only the eliminations of the level-1 cells it owns
+     (cell_rank[c] == shard_rank; -1 marks top-separator cells, whose blocks
+     belong to rank 0) for levels 1..shard_stop_level.  Then `exchange` is
+     called with the block regions of the trailing matrix (identical layout
+     on every rank); it must sum them onto rank 0, which continues with the
+     remaining levels while the other ranks stop. */
+  int shard_rank;
+  int shard_count;
+  const int32_t* cell_rank;
+  int shard_stop_level;
+  int (*exchange)(void* user, int nregions, double* const* ptrs, const int64_t* counts);
+  void* exchange_user;
 } sgf_factor_args;
 
 typedef struct {
@@ -136,6 +150,20 @@ int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_ou
    mutates x (factorization.py:235-239 copies). */
 int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device);
 
+/* Sharded preconditioners: factors [0, n_local) belong to the rank's local
+   phase, [n_local, n) to the top part (rank 0).  n_local_unknowns = unknowns
+   eliminated by the local factors; n_top = unknowns still active when the
+   local phase ended (identical on every rank).  A single-GPU preconditioner
+   has n_local = all factors and n_top = 0. */
+int sgf_precond_shard_info(const sgf_precond* p, int64_t* n_local_factors, int64_t* n_local_unknowns,
+                           int64_t* n_top);
+/* which: 0 local eliminated unknowns, 1 top unknowns (int64) */
+int sgf_precond_shard_set(const sgf_precond* p, int which, int64_t* out, int64_t cap);
+/* In-place partial sweeps on a device n-vector: part 0 forward over the
+   local factors, 1 forward then backward over the top factors, 2 backward
+   over the local factors.  Parts 0, 1, 2 in sequence = apply_inverse. */
+int sgf_apply_part(sgf_precond* p, int part, double* y);
+
 int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                    const double* values, int on_device, sgf_csr** out);
 int sgf_csr_free(sgf_csr* a);
@@ -145,6 +173,13 @@ int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device);
    history must hold maxit + 2 doubles. */
 int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x, double tol, int maxit,
             int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
+
+/* PCG whose preconditioner is a callback on device n-vectors (out = M^-1 in,
+   enqueued on the context stream; nonzero return = failure); used by the
+   sharded solve, where M^-1 includes collectives. */
+typedef int (*sgf_precond_fn)(void* user, const double* in, double* out);
+int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const double* b, double* x, double tol,
+               int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
 
 /* instrumentation (no reference counterpart): kernels launched so far, and
    per-kernel-class CUDA-event timing.  Classes: 0 GEMM (work = flops),

@@ -29,7 +29,8 @@ EXPORTS = (
     "sgf_create", "sgf_destroy", "sgf_last_error", "sgf_stream", "sgf_sync", "sgf_factorize",
     "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
     "sgf_precond_num_factors", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
-    "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg",
+    "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
+    "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read",
 )
 PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec")
@@ -53,7 +54,15 @@ class FactorArgs(C.Structure):
         ("n_trace", C.c_int), ("trace", C.c_void_p),
         ("n_replay", C.c_int), ("replay_ptr", C.c_void_p), ("replay_perm", C.c_void_p),
         ("coords", C.c_void_p), ("n_vertices", C.c_int64), ("degree", C.c_int), ("components", C.c_int),
+        ("shard_rank", C.c_int), ("shard_count", C.c_int), ("cell_rank", C.c_void_p),
+        ("shard_stop_level", C.c_int), ("exchange", C.c_void_p), ("exchange_user", C.c_void_p),
     ]
+
+
+# int exchange(void* user, int nregions, double* const* ptrs, const int64_t* counts)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64))
+# int precond(void* user, const double* in, double* out)
+PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 
 
 class PcgReport(C.Structure):
@@ -96,6 +105,10 @@ def load_library(path=LIB_PATH):
             "sgf_csr_free": (i32, [vp]),
             "sgf_spmv": (i32, [vp, vp, vp, i32]),
             "sgf_pcg": (i32, [vp, vp, vp, vp, vp, d, i32, i32, i32, C.POINTER(PcgReport), vp]),
+            "sgf_pcg_cb": (i32, [vp, vp, PRECOND_FN, vp, vp, vp, d, i32, i32, i32, C.POINTER(PcgReport), vp]),
+            "sgf_precond_shard_info": (i32, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+            "sgf_precond_shard_set": (i32, [vp, i32, vp, i64]),
+            "sgf_apply_part": (i32, [vp, i32, vp]),
             "sgf_kernel_launches": (C.c_uint64, []),
             "sgf_profile_enable": (i32, [i32]),
             "sgf_profile_read": (i32, [vp, i32]),

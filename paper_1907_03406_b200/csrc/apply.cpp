@@ -396,6 +396,7 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   cudaStream_t st = P->ctx->stream;
   ApplyPlan* pl = P->plan;
   if (op < 0 || op > 3) fail(SGF_INVALID_ARG, "unknown apply operation");
+  if (P->sharded) fail(SGF_INVALID_ARG, "sharded preconditioner: apply through the collective sharded apply");
   if (op == SGF_APPLY_OPERATOR) {
     prepare_operator(P);
     if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -426,6 +427,27 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   SGF_CUDA(cudaMemcpyAsync(d_y, pl->work, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
 }
 
+// Partial sweeps in place (the sharded apply, sharded.py): groups never
+// straddle the local/top boundary because the plan is extended per level.
+void apply_part(Precond* P, int part, double* y) {
+  if (part < 0 || part > 2) fail(SGF_INVALID_ARG, "unknown apply part");
+  cudaStream_t st = P->ctx->stream;
+  ApplyPlan* pl = P->plan;
+  const size_t nl = P->local_count();
+  if (part == 0) {
+    for (auto& g : pl->groups)
+      if (g.f1 <= nl) forward_group(pl, g, y, st);
+  } else if (part == 1) {
+    for (auto& g : pl->groups)
+      if (g.f0 >= nl) forward_group(pl, g, y, st);
+    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it)
+      if (it->f0 >= nl) backward_group(pl, *it, y, st);
+  } else {
+    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it)
+      if (it->f1 <= nl) backward_group(pl, *it, y, st);
+  }
+}
+
 // ---------------------------------------------------------------------------
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
   // values + int32 columns + row pointers + x + y (+ b)
@@ -437,7 +459,7 @@ void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
 // PCG with the reference recurrence (krylov.py:34-102): true-residual
 // replacement every `true_every` iterations, confirmation of a tentative
 // convergence with the true residual, history semantics identical.
-void pcg(Ctx& ctx, Csr* A, Precond* P, const double* d_b, double* d_x, double tol, int maxit, int true_every,
+void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit, int true_every,
          sgf_pcg_report* rep, double* history) {
   cudaStream_t st = ctx.stream;
   const long long n = A->n;
@@ -460,7 +482,7 @@ void pcg(Ctx& ctx, Csr* A, Precond* P, const double* d_b, double* d_x, double to
     SGF_CUDA(cudaStreamSynchronize(st));
   };
   auto precond = [&](const double* in, double* out) {
-    if (P) apply_op(P, SGF_APPLY_INVERSE, in, out);
+    if (M) M(in, out);
     else SGF_CUDA(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   };
   int hl = 0;

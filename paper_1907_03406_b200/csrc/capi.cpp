@@ -291,23 +291,80 @@ int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device) {
   });
 }
 
+static void run_pcg(sgf_ctx* ctx, sgf_csr* a, const PrecFn& M, const double* b, double* x, double tol, int maxit,
+                    int true_every, int on_device, sgf_pcg_report* rep, double* history) {
+  cudaStream_t st = ctx->c.stream;
+  const long long n = a->a.n;
+  if (on_device) {
+    pcg(ctx->c, &a->a, M, b, x, tol, maxit, true_every, rep, history);
+  } else {
+    DevVec db(n, st), dx(n, st);
+    SGF_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, st));
+    pcg(ctx->c, &a->a, M, db.p, dx.p, tol, maxit, true_every, rep, history);
+    SGF_CUDA(cudaMemcpyAsync(x, dx.p, n * 8, cudaMemcpyDeviceToHost, st));
+  }
+  SGF_CUDA(cudaStreamSynchronize(st));
+}
+
 int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x, double tol, int maxit,
             int true_residual_every, int on_device, sgf_pcg_report* rep, double* history) {
   if (!ctx || !a || !b || !x || !rep || !history) return SGF_INVALID_ARG;
   return guarded(ctx, [&] {
     if (p && p->p->n != a->a.n) fail(SGF_SHAPE, "preconditioner and matrix sizes differ");
-    cudaStream_t st = ctx->c.stream;
-    const long long n = a->a.n;
-    if (on_device) {
-      pcg(ctx->c, &a->a, p ? p->p : nullptr, b, x, tol, maxit, true_residual_every, rep, history);
-    } else {
-      DevVec db(n, st), dx(n, st);
-      SGF_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, st));
-      pcg(ctx->c, &a->a, p ? p->p : nullptr, db.p, dx.p, tol, maxit, true_residual_every, rep, history);
-      SGF_CUDA(cudaMemcpyAsync(x, dx.p, n * 8, cudaMemcpyDeviceToHost, st));
+    PrecFn M;
+    if (p) {
+      Precond* P = p->p;
+      M = [P](const double* in, double* out) { apply_op(P, SGF_APPLY_INVERSE, in, out); };
     }
-    SGF_CUDA(cudaStreamSynchronize(st));
+    run_pcg(ctx, a, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
   });
+}
+
+int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const double* b, double* x, double tol,
+               int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history) {
+  if (!ctx || !a || !fn || !b || !x || !rep || !history) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    PrecFn M = [fn, user](const double* in, double* out) {
+      const int rc = fn(user, in, out);
+      if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "preconditioner callback failed");
+    };
+    run_pcg(ctx, a, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+  });
+}
+
+int sgf_precond_shard_info(const sgf_precond* p, int64_t* n_local_factors, int64_t* n_local_unknowns,
+                           int64_t* n_top) {
+  if (!p) return SGF_INVALID_ARG;
+  const Precond* P = p->p;
+  const size_t nl = P->local_count();
+  int64_t nu = 0;
+  for (size_t i = 0; i < nl; ++i) nu += (int64_t)P->factors[i].idx.size();
+  if (n_local_factors) *n_local_factors = (int64_t)nl;
+  if (n_local_unknowns) *n_local_unknowns = nu;
+  if (n_top) *n_top = (int64_t)P->top_idx.size();
+  return SGF_OK;
+}
+
+int sgf_precond_shard_set(const sgf_precond* p, int which, int64_t* out, int64_t cap) {
+  if (!p || !out || which < 0 || which > 1) return SGF_INVALID_ARG;
+  const Precond* P = p->p;
+  int64_t k = 0;
+  if (which == 0) {
+    for (size_t i = 0; i < P->local_count(); ++i)
+      for (int64_t u : P->factors[i].idx) {
+        if (k >= cap) return SGF_INVALID_ARG;
+        out[k++] = u;
+      }
+  } else {
+    if ((int64_t)P->top_idx.size() > cap) return SGF_INVALID_ARG;
+    std::copy(P->top_idx.begin(), P->top_idx.end(), out);
+  }
+  return SGF_OK;
+}
+
+int sgf_apply_part(sgf_precond* p, int part, double* y) {
+  if (!p || !y) return SGF_INVALID_ARG;
+  return guarded(p->ctx, [&] { apply_part(p->p, part, y); });
 }
 
 }  // extern "C"

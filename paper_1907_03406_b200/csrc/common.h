@@ -120,6 +120,8 @@ struct CsrScatter {
   const long long* up_off;
   double* base;
   long long n;
+  const int* cell_rank;      // sharded: owning rank per cell (-1 shared), nullptr = all entries
+  int my_rank;
 };
 
 // out[k] = base[k] + sign * sum_{q<nrb} part[q*stride + k], k < n

@@ -195,9 +195,15 @@ __global__ void __launch_bounds__(256) csr_scatter_kernel(const CsrScatter P) {
     const int ca = P.owner[r];
     const long long lr = P.local[r];
     const int u0 = P.up_ptr[ca], u1 = P.up_ptr[ca + 1];
+    const int ra = P.cell_rank ? P.cell_rank[ca] : 0;
     for (long long e = P.indptr[r]; e < P.indptr[r + 1]; ++e) {
       const int col = P.indices[e];
       const int cb = P.owner[col];
+      if (P.cell_rank) {  // a block belongs to the rank of its owned cell, shared-shared to rank 0
+        const int rb = P.cell_rank[cb];
+        const int ob = ra >= 0 ? ra : (rb >= 0 ? rb : 0);
+        if (ob != P.my_rank) continue;
+      }
       if (cb == ca) {
         P.base[P.diag_off[ca] + lr * P.size[ca] + P.local[col]] = P.values[e];
       } else if (cb > ca) {

@@ -59,6 +59,13 @@ struct State {
   long long peak = 0;
   int comp_counter = 0;  // compressions so far (reference execution order)
   Precond* P;
+  // sharding
+  bool sharded = false;
+  int my_rank = 0;
+  std::vector<int> node_rank;  // per node of the current level: owning rank, -1 = top separator
+  std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
+  long long fa_extra = 0;      // apply flops of other ranks' factors
+  int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
 };
 
@@ -232,6 +239,7 @@ void setup_level1(State& S) {
   S.lvl.reset(new Arena(S.st));
   double* base = S.lvl->alloc(std::max<long long>(total, 1));
   SGF_CUDA(cudaMemsetAsync(base, 0, std::max<long long>(total, 1) * sizeof(double), S.st));
+  S.regions.assign(1, {base, total});
   // blocks in lexicographic (a, b) order: the reference's insertion order
   std::vector<long long> diag_off(nc, -1);
   std::vector<std::vector<long long>> up_off(nc);
@@ -286,6 +294,9 @@ void setup_level1(State& S) {
     P.up_off = up_o.empty() ? d_ip : S.scratch.upload(up_o);
     P.base = base;
     P.n = n;
+    P.cell_rank = nullptr;
+    P.my_rank = S.my_rank;
+    if (S.sharded) P.cell_rank = S.scratch.upload(S.node_rank);
     SGF_CUDA(launch_csr_scatter(&P, S.st));
   }
 
@@ -379,6 +390,9 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     double *W, *X, *E;
   };
   std::vector<EI> info(elim.size());
+  // sharded: this rank computes only its own interiors; the symbolic part
+  // (fill, block table, flop and byte tallies) still covers every interior
+  std::vector<char> own(elim.size(), 1);
   CopyBatch cp;
   std::vector<CholJob> jobs;
   HostTimer ht0("elim setup+chol");
@@ -394,6 +408,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       e.c += M.size[j];
     }
     e.ld = pad_ld(e.m);
+    if (S.sharded) own[q] = S.node_rank[e.x] == S.my_rank;
+    if (!own[q]) continue;
     tot_w += (size_t)e.m * e.ld;
     tot_e += (size_t)e.c * e.ld;
   }
@@ -406,6 +422,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   size_t ow = 0, oe = 0;
   for (size_t q = 0; q < elim.size(); ++q) {
     EI& e = info[q];
+    if (!own[q]) continue;
     const size_t mm = (size_t)e.m * e.ld;
     e.W = Wall + ow;
     e.X = Xall + ow;
@@ -424,13 +441,17 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   }
   HostTimer hte("elim E gemm");
   GemmBatch ge;
-  for (auto& e : info) {
+  for (size_t qi = 0; qi < info.size(); ++qi) {
+    const EI& e = info[qi];
     long long f = (long long)e.m * e.m * e.m / 3;
     for (size_t q = 0; q < e.nb.size(); ++q) {
-      View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
-      ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
-             {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
-      f += (long long)e.m * e.m * v.rows;
+      const int rows = M.size[e.nb[q]];
+      if (own[qi]) {
+        View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
+        ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
+               {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
+      }
+      f += (long long)e.m * e.m * rows;
     }
     for (size_t p = 0; p < e.nb.size(); ++p)
       for (size_t q = p; q < e.nb.size(); ++q) f += 2LL * M.size[e.nb[p]] * e.m * M.size[e.nb[q]];
@@ -470,7 +491,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
               fill_elems += (long long)M.size[A] * M.size[B];
             }
           }
-          targets[*ins.first].contrib.push_back({(int)q, {(int)p, (int)r}});
+          if (own[q]) targets[*ins.first].contrib.push_back({(int)q, {(int)p, (int)r}});
         }
     }
   }
@@ -478,6 +499,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   if (fill_elems > 0) {
     fill_base = S.lvl->alloc(fill_elems);
     SGF_CUDA(cudaMemsetAsync(fill_base, 0, fill_elems * sizeof(double), st));
+    S.regions.push_back({fill_base, fill_elems});
   }
   // Schur GEMMs first (the level's largest device work), table bookkeeping after
   {
@@ -497,6 +519,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         br = M.size[T.a];
         bc = M.size[T.b];
       }
+      if (T.contrib.empty()) continue;  // sharded: no contributor on this rank
       sg.clear();
       for (auto& c : T.contrib) {
         const EI& e = info[c.first];
@@ -522,19 +545,24 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         M.insert(T.a, T.b, Blk{fill_base + T.fill, M.size[T.a], M.size[T.b]});
       }
       // factor record (before the node's actives are cleared)
-      Factor f;
-      f.type = SGF_FACTOR_ELIMINATION;
-      f.node = e.x;
-      f.level = level;
-      f.m = e.m;
-      f.ld = e.ld;
-      f.c = e.c;
-      f.idx = S.nodes[e.x].active;
-      for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
-      f.L = e.W;
-      f.inv = e.X;
-      f.E = e.E;
-      P->factors.push_back(std::move(f));
+      if (own[q]) {
+        Factor f;
+        f.type = SGF_FACTOR_ELIMINATION;
+        f.node = e.x;
+        f.level = level;
+        f.m = e.m;
+        f.ld = e.ld;
+        f.c = e.c;
+        f.idx = S.nodes[e.x].active;
+        for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
+        f.L = e.W;
+        f.inv = e.X;
+        f.E = e.E;
+        P->factors.push_back(std::move(f));
+      } else {  // another rank's factor: kept only in the tallies
+        S.fa_extra += 4LL * e.m * e.m + 4LL * e.m * e.c;
+        ++S.nf_extra;
+      }
       M.drop(e.x);
       M.size[e.x] = 0;
       S.nodes[e.x].active.clear();
@@ -990,6 +1018,13 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
   }
   double* base = nl->alloc(std::max<long long>(tot, 1));
   if (tot) SGF_CUDA(cudaMemsetAsync(base, 0, tot * sizeof(double), st));
+  S.regions.assign(1, {base, tot});
+  if (S.sharded) {
+    std::vector<int> nr(next_nc, -1);
+    for (int f = 0; f < next_nc; ++f)
+      if (!kids[f].empty()) nr[f] = S.node_rank[kids[f].front()];
+    S.node_rank.swap(nr);
+  }
   for (auto& o : order) {
     const int fa = (int)(o.first >> 32), fb = (int)(o.first & 0xffffffffu);
     N.insert(fa, fb, Blk{base + o.second, nsize[fa], nsize[fb]});
@@ -1183,6 +1218,36 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.P = P.get();
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
   PlanWorker planner(P.get());  // destroyed (joined) before P and S
+  if (a.shard_count > 1) {
+    if (!a.cell_rank || !a.exchange || a.shard_rank < 0 || a.shard_rank >= a.shard_count || a.shard_stop_level < 1)
+      fail(SGF_INVALID_ARG, "incomplete sharding arguments");
+    S.sharded = true;
+    S.my_rank = a.shard_rank;
+    S.node_rank.assign(a.cell_rank, a.cell_rank + a.level_ncells[0]);
+    for (int r : S.node_rank)
+      if (r < -1 || r >= a.shard_count) fail(SGF_INVALID_ARG, "cell rank out of range");
+  }
+  bool exchanged = false, stopped = false;
+  // end of the local phase: record the split, sum the trailing matrix onto
+  // rank 0 through the caller's collective; the other ranks stop here
+  auto end_local_phase = [&]() {
+    exchanged = true;
+    P->sharded = true;
+    P->n_local = P->factors.size();
+    for (auto& nd : S.nodes) P->top_idx.insert(P->top_idx.end(), nd.active.begin(), nd.active.end());
+    std::vector<double*> ptrs;
+    std::vector<int64_t> counts;
+    for (auto& r : S.regions)
+      if (r.second > 0) {
+        ptrs.push_back(r.first);
+        counts.push_back(r.second);
+      }
+    SGF_CUDA(cudaStreamSynchronize(S.st));
+    const int rc = a.exchange(a.exchange_user, (int)ptrs.size(), ptrs.data(), counts.data());
+    if (rc != 0) fail(SGF_CUDA, "shard exchange callback failed");
+    if (S.my_rank != 0) stopped = true;
+    else S.sharded = false;  // rank 0 now holds the whole trailing matrix and eliminates everything
+  };
 
   timeline_begin(S.st);
   { Phase ph("setup", 0, S.st); setup_level1(S); }
@@ -1216,6 +1281,10 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     }
     ls.eliminated = (int)elim.size();
     S.scratch.release();  // chunks are reused in stream order: no sync needed
+    if (S.sharded && t + 1 == a.shard_stop_level) {
+      end_local_phase();
+      if (stopped) break;
+    }
     if (compression && (t + 1) > a.skip_levels) {
       std::vector<int> comp;
       for (int c = 0; c < (int)S.nodes.size(); ++c)
@@ -1242,8 +1311,9 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       break;
     }
   }
+  if (S.sharded && !exchanged) end_local_phase();  // the hierarchy ended before the stop level
   size_t before = P->factors.size();
-  {
+  if (!stopped) {
     Phase ph("dense", 0, S.st);
     const size_t f0 = P->factors.size();
     final_dense(S);
@@ -1254,7 +1324,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     final_size = P->factors.back().m;
     S.peak = std::max(S.peak, S.M.peak);
   }
-  if (a.mode == SGF_MODE_LOWRANK && S.comp_counter < a.n_trace) {
+  if (!stopped && a.mode == SGF_MODE_LOWRANK && S.comp_counter < a.n_trace) {
     char buf[160];
     snprintf(buf, sizeof buf, "rank trace has %d unreplayed entries; first: [%d, %d, %d]", a.n_trace - S.comp_counter,
              a.trace[3 * S.comp_counter], a.trace[3 * S.comp_counter + 1], a.trace[3 * S.comp_counter + 2]);
@@ -1270,13 +1340,15 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     }
   S.scratch.release();
   S.lvl.reset();
-  long long fa = 0;
+  long long fa = S.fa_extra;
   for (auto& f : P->factors) {
     const long long m = f.m;
     fa += (f.type == SGF_FACTOR_ELIMINATION) ? 4 * m * m + 4 * m * f.c : 4 * m * m;
   }
+  // on a sharded rank 0 the tallies include the other ranks' factors, so the
+  // stats equal the single-GPU ones; the other ranks' stats cover their local phase
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
-                        (int)P->factors.size(), 0, nullptr);
+                        (int)P->factors.size() + S.nf_extra, 0, nullptr);
   planner.finish();
   plan_finish(P.get());
   timeline_end(S.st);

@@ -2,6 +2,7 @@
 // reference (factorization.py:112-213) plus the level-batched apply plan.
 #pragma once
 #include <deque>
+#include <functional>
 #include <memory>
 
 #include "runtime.h"
@@ -46,6 +47,12 @@ class Precond {
   std::vector<int32_t> trace;  // (level, node, rank) triples
   Arena store;
   ApplyPlan* plan = nullptr;
+  // sharding: factors [0, n_local) are the rank's local phase; top_idx are
+  // the unknowns active when it ended (empty on a single GPU)
+  bool sharded = false;
+  size_t n_local = 0;
+  std::vector<int64_t> top_idx;
+  size_t local_count() const { return sharded ? n_local : factors.size(); }
   ~Precond() {
     if (plan) destroy_plan(plan);
   }
@@ -53,6 +60,7 @@ class Precond {
 
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a);
 void apply_op(Precond* P, int op, const double* d_x, double* d_y);
+void apply_part(Precond* P, int part, double* d_y);
 
 struct Csr {
   Ctx* ctx = nullptr;
@@ -64,7 +72,9 @@ struct Csr {
   Arena mem;
 };
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b);
-void pcg(Ctx& ctx, Csr* A, Precond* P, const double* d_b, double* d_x, double tol, int maxit, int true_every,
+// preconditioner: out = M^-1 in on device vectors (empty = identity)
+using PrecFn = std::function<void(const double*, double*)>;
+void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit, int true_every,
          sgf_pcg_report* rep, double* history);
 
 }  // namespace sgf

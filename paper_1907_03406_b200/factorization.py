@@ -242,14 +242,16 @@ def _kind_mask(names):
 
 def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
               compression=True, mode="polynomial", rank_tol=DEFAULT_RANK_TOL,
-              rank_trace=None, *, replay_perms=None, device=0, device_values=None):
+              rank_trace=None, *, replay_perms=None, device=0, device_values=None, _shard=None):
     """Build the hierarchical preconditioner on the GPU (reference
     factorization.py:410-573).  `replay_perms` (parity mode) is a list of QR
     column permutations, one per compression in the reference's execution
     order, that the device QR follows instead of its own argmax.
     `device_values` optionally supplies the CSR values (in the order of
     problem.matrix.tocsr() with sorted indices) as a float64 CUDA tensor
-    already resident in HBM; the host matrix then only provides the pattern."""
+    already resident in HBM; the host matrix then only provides the pattern.
+    `_shard` (internal, sharded.py) maps (hierarchy, skip_levels,
+    compression) to the rank's sharding arguments."""
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}; expected one of {SCHEMES}")
     if mode not in MODES:
@@ -326,6 +328,13 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
         perm_all = np.ascontiguousarray(perm_all, dtype=np.int32)
         keep += [rp, perm_all]
         args.n_replay, args.replay_ptr, args.replay_perm = len(replay_perms), rp.ctypes.data, perm_all.ctypes.data
+    if _shard is not None:
+        sh = _shard(hier, int(skip_levels), bool(compression))
+        keep.append(sh)
+        args.shard_rank, args.shard_count = int(sh["rank"]), int(sh["count"])
+        args.cell_rank = sh["cell_rank"].ctypes.data
+        args.shard_stop_level = int(sh["stop_level"])
+        args.exchange = C.cast(sh["exchange"], C.c_void_p)
 
     L = N.lib()
     ctx = N.context(device)
