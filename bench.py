@@ -14,9 +14,10 @@ exact BASELINE shape (no dataset involved).
          (host CSR + RHS in, solution x back on the host), copies included.
 
 Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sgf|reference]
-N > 1 (torchrun): every rank factorizes and solves its own replica of the
-workload ("replicas only": the reference path has no exchange step to shard,
-see DESIGN.md); the step time is the max over ranks.
+N > 1 (torchrun, NCCL): the one 128^3 problem is sharded across the ranks
+(sharded.py: subtree ownership of the nested-dissection tree, rank-local
+elimination phase, trailing-matrix reduction onto rank 0, collective apply
+inside PCG); strong scaling, the step time is the max over ranks.
 """
 
 import argparse
@@ -89,16 +90,16 @@ class ClockSampler(object):
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(backend="nccl", same_gpu=False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if same_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     return ws, rank, local
 
 
@@ -108,7 +109,7 @@ def allmax(v, ws):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -179,7 +180,7 @@ def run_reference(args, ws, rank):
     line = {
         "impl": "reference", "metric": "factor+solve wall time (cfg4: 128^3 anisotropic Laplace)",
         "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": {"workload": "cfg4-aniso-128", "grid": [128, 128, 128],
                                                          "n": 2097152, "b": 9, "rank_tol": 1e-3, "pcg_rtol": 1e-12},
         "t_factor_s": ef, "t_solve_s": es,
@@ -196,6 +197,7 @@ def run_sgf(args, ws, rank, local):
 
     import paper_1907_03406_b200 as sgf
     from paper_1907_03406_b200 import _native as N
+    from paper_1907_03406_b200 import sharded as S
     from paper_1907_03406_b200.problems import CONFIGS, config_rhs
 
     torch.cuda.set_device(local)
@@ -222,9 +224,14 @@ def run_sgf(args, ws, rank, local):
 
     def step_device(rec=None):
         e0 = ev()
-        P = sgf.factorize(prob, device_values=vals, **opts)
-        e1 = ev()
-        x, rep = sgf.pcg(Ad, b_dev, precond=P, tol=1e-12)
+        if ws > 1:
+            P = S.factorize_sharded(prob, device_values=vals, **opts)
+            e1 = ev()
+            x, rep = S.pcg_sharded(Ad, b_dev, P, tol=1e-12)
+        else:
+            P = sgf.factorize(prob, device_values=vals, **opts)
+            e1 = ev()
+            x, rep = sgf.pcg(Ad, b_dev, precond=P, tol=1e-12)
         e2 = ev()
         if rec is not None:
             rec.append((e0, e1, e2, P.stats, rep))
@@ -233,8 +240,12 @@ def run_sgf(args, ws, rank, local):
 
     def step_e2e(rec=None):
         e0 = ev()
-        P = sgf.factorize(prob, **opts)
-        x, rep = sgf.pcg(A, rhs, precond=P, tol=1e-12)
+        if ws > 1:
+            P = S.factorize_sharded(prob, **opts)
+            x, rep = S.pcg_sharded(A, rhs, P, tol=1e-12)
+        else:
+            P = sgf.factorize(prob, **opts)
+            x, rep = sgf.pcg(A, rhs, precond=P, tol=1e-12)
         e1 = ev()
         if rec is not None:
             rec.append((e0, e1, rep))
@@ -298,7 +309,7 @@ def run_sgf(args, ws, rank, local):
                  "classes_ms": {k: round(v[0], 3) for k, v in prof.items()}})
     gemv = prof["gemv"]
     spmv = prof["spmv"]
-    extra = {
+    extra = {} if rank != 0 else {
         "fp64_tflops_factorize": stats["flops_factorize"] / tF / 1e12,
         "t_factor_s": tF, "t_solve_s": tS, "pcg_iterations": rep.iterations,
         "reference_pcg_iterations": 49, "final_rel_residual": rep.final_rel_residual, "check_residual": resid,
@@ -321,11 +332,12 @@ def run_sgf(args, ws, rank, local):
         line = {
             "metric": "factor+solve wall time (cfg4: 128^3 anisotropic Laplace)", "value": ms / 1e3, "unit": "s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "cfg4-aniso-128", "grid": [128, 128, 128], "n": prob.n, "nnz": int(A.nnz),
+            "config": {"workload": "cfg4-aniso-128" if CFG == 4 else f"cfg{CFG}-code-path-check-not-a-bench-value",
+                       "grid": list(prob.grid.dims), "n": prob.n, "nnz": int(A.nnz),
                        "b": c["b"], "rank_tol": c["rank_tol"], "scheme": "nest-2-2", "degree": 1,
-                       "pcg_rtol": 1e-12, "parallelism": f"replicas{ws}",
+                       "pcg_rtol": 1e-12, "parallelism": f"shard{ws}" if ws > 1 else "single",
                        "l2": "inputs and factors (>60 GB) exceed the 126 MB L2"},
             "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
@@ -355,8 +367,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sgf", choices=["sgf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # code-path checks only (numbers from these are not bench values): another
+    # config, gloo collectives, every rank on GPU 0
+    ap.add_argument("--cfg", type=int, default=4)
+    ap.add_argument("--dist-backend", default="nccl")
+    ap.add_argument("--same-gpu", action="store_true")
     args = ap.parse_args()
-    ws, rank, local = dist_setup() if args.impl == "sgf" else (int(os.environ.get("WORLD_SIZE", "1")),
+    global CFG
+    CFG = args.cfg
+    ws, rank, local = dist_setup(args.dist_backend, args.same_gpu) if args.impl == "sgf" else (int(os.environ.get("WORLD_SIZE", "1")),
                                                              int(os.environ.get("RANK", "0")), 0)
     if args.impl == "reference":
         run_reference(args, ws, rank)
