@@ -45,6 +45,12 @@ struct Group {
   double bytes_f1 = 0, bytes_f2 = 0, bytes_b1 = 0, bytes_b2 = 0;  // matrix bytes streamed
   double *xb = nullptr, *zb = nullptr, *acc = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr;  // workspaces
   size_t f0 = 0, f1 = 0;  // factor range
+  // level-1 eliminations in apply_inverse: G = A_BB^{-1} with the sparse couplings
+  bool sym = false;
+  SymvTask* sym_f = nullptr;  // zb = G xb
+  SymvTask* sym_b = nullptr;  // zb = xb - G acc
+  int nsym = 0, sym_maxm = 0;
+  double bytes_sym = 0;
   // apply_operator task lists (built on first use)
   GemvTask *oT = nullptr, *oE = nullptr, *oL = nullptr;
   int noT = 0, noE = 0, noL = 0;
@@ -202,13 +208,32 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
         r1.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb, f.m, 1.0});
         op += (long long)nrb * f.m;
       }
-      g.maxn1 = std::max(g.maxn1, f.m);
+        g.maxn1 = std::max(g.maxn1, f.m);
       g.maxn2 = std::max(g.maxn2, f.m);
       om += f.m;
       oc += f.c;
     }
     g.nm = om;
     g.nc = oc;
+    // level-1 eliminations with G and the coupling lists of the whole level
+    bool sym = g.type == SGF_FACTOR_ELIMINATION && P->l1.ready && om == P->l1.nb;
+    for (size_t i = rg.first; sym && i < rg.second; ++i) sym = fs[i]->G != nullptr && fs[i]->level == 1;
+    if (sym) {
+      std::vector<SymvTask> tf, tb;
+      long long o = 0;
+      for (size_t i = rg.first; i < rg.second; ++i) {
+        const Factor& f = *fs[i];
+        tf.push_back(SymvTask{f.G, f.ld, g.xb + o, nullptr, g.zb + o, f.m, 1.0});
+        tb.push_back(SymvTask{f.G, f.ld, g.acc + o, g.xb + o, g.zb + o, f.m, -1.0});
+        g.sym_maxm = std::max(g.sym_maxm, f.m);
+        g.bytes_sym += 4.0 * f.m * (f.m + 1.0);
+        o += f.m;
+      }
+      g.sym = true;
+      g.nsym = (int)tf.size();
+      g.sym_f = plan->mem.upload(tf);
+      g.sym_b = plan->mem.upload(tb);
+    }
     g.idx = plan->mem.upload(idx);
     g.nidx = plan->mem.upload(nidx);
     g.bytes_f1 = gemv_bytes(f1, 0);
@@ -274,6 +299,28 @@ static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t
   SGF_CUDA(launch_gemv(t, nt, mode, st));
 }
 
+// level-1 group of apply_inverse: v = G x_B, x_N -= A_NB v (forward, v kept
+// in x_B); y_B = v - G A_NB^T x_N (backward).  Equal to the reference's
+// L^{-1} / E = A_NB L^{-T} sweeps since E^T = L^{-1} A_NB^T and G = L^{-T} L^{-1}.
+static void symv(const SymvTask* t, int nt, int maxm, double bytes, cudaStream_t st) {
+  ProfScope ps(st, PROF_GEMV, bytes);
+  SGF_CUDA(launch_symv(t, nt, maxm, st));
+}
+
+static void forward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
+  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+  symv(g.sym_f, g.nsym, g.sym_maxm, g.bytes_sym, st);
+  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  SGF_CUDA(launch_sub_spmv(c.nf, c.f_rid, c.f_rp, c.f_ci, c.f_v, y, nullptr, 0, st));
+}
+
+static void backward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
+  SGF_CUDA(launch_sub_spmv(c.nb, nullptr, c.b_rp, c.b_ci, c.b_v, y, g.acc, 1, st));
+  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+  symv(g.sym_b, g.nsym, g.sym_maxm, g.bytes_sym, st);
+  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+}
+
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
   (void)pl;
   SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
@@ -300,11 +347,23 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
 }
 
 // y and x are device n-vectors; y may alias x
-static void sweeps(ApplyPlan* pl, int op, double* y, cudaStream_t st) {
+static void fwd(ApplyPlan* pl, const L1Couplings& c, const Group& g, bool full, double* y, cudaStream_t st) {
+  if (full && g.sym) forward_group_sym(c, g, y, st);
+  else forward_group(pl, g, y, st);
+}
+static void bwd(ApplyPlan* pl, const L1Couplings& c, const Group& g, bool full, double* y, cudaStream_t st) {
+  if (full && g.sym) backward_group_sym(c, g, y, st);
+  else backward_group(pl, g, y, st);
+}
+
+// `full`: both sweeps of apply_inverse run, so level-1 groups may use the
+// G form (its intermediate x_B differs from the L^{-1} half sweep's)
+static void sweeps(ApplyPlan* pl, const L1Couplings& c, int op, double* y, cudaStream_t st) {
+  const bool full = op == SGF_APPLY_INVERSE;
   if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE)
-    for (auto& g : pl->groups) forward_group(pl, g, y, st);
+    for (auto& g : pl->groups) fwd(pl, c, g, full, y, st);
   if (op == SGF_APPLY_INVERSE || op == SGF_APPLY_HALF_INVERSE_T)
-    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) backward_group(pl, *it, y, st);
+    for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it) bwd(pl, c, *it, full, y, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -406,7 +465,7 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   static const bool no_graph = getenv("SGF_NO_GRAPH") != nullptr;
   if (g_prof.on || no_graph) {  // per-kernel timing needs eager launches
     if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    sweeps(pl, op, d_y, st);
+    sweeps(pl, P->l1, op, d_y, st);
     return;
   }
   // the whole sweep sequence (~100 launches) replays as one CUDA graph on
@@ -415,7 +474,7 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
     cudaGraph_t g;
     SGF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     const unsigned long long before = g_kernel_launches;
-    sweeps(pl, op, pl->work, st);
+    sweeps(pl, P->l1, op, pl->work, st);
     SGF_CUDA(cudaStreamEndCapture(st, &g));
     pl->graph_launches[op] = g_kernel_launches - before;
     SGF_CUDA(cudaGraphInstantiate(&pl->graph[op], g, 0));
@@ -434,17 +493,18 @@ void apply_part(Precond* P, int part, double* y) {
   cudaStream_t st = P->ctx->stream;
   ApplyPlan* pl = P->plan;
   const size_t nl = P->local_count();
+  const L1Couplings& c = P->l1;
   if (part == 0) {
     for (auto& g : pl->groups)
-      if (g.f1 <= nl) forward_group(pl, g, y, st);
+      if (g.f1 <= nl) fwd(pl, c, g, true, y, st);
   } else if (part == 1) {
     for (auto& g : pl->groups)
-      if (g.f0 >= nl) forward_group(pl, g, y, st);
+      if (g.f0 >= nl) fwd(pl, c, g, true, y, st);
     for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it)
-      if (it->f0 >= nl) backward_group(pl, *it, y, st);
+      if (it->f0 >= nl) bwd(pl, c, *it, true, y, st);
   } else {
     for (auto it = pl->groups.rbegin(); it != pl->groups.rend(); ++it)
-      if (it->f1 <= nl) backward_group(pl, *it, y, st);
+      if (it->f1 <= nl) bwd(pl, c, *it, true, y, st);
   }
 }
 

@@ -93,6 +93,107 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
 }
 
 // ---------------------------------------------------------------------------
+// Symmetric GEMV from the lower triangle, one CTA per matrix (m <= 64*Q):
+// warp w takes rows i = w (mod 8); lane l owns the column pairs
+// 64q + 2l + {0,1}, so every stored entry is read once (16-byte loads) and
+// used twice: G_ij x_j into the row sum of i, G_ij x_i into lane-resident
+// column sums of j (strictly lower part).  Row sums are warp-reduced, column
+// sums of the 8 warps are added in fixed order through shared memory.
+// ---------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(256) symv_kernel(const SymvTask* __restrict__ tasks) {
+  extern __shared__ double sm[];
+  constexpr int MP = 64 * Q;
+  const SymvTask T = tasks[blockIdx.x];
+  const int m = T.m;
+  double* xs = sm;
+  double* yr = sm + MP;
+  double* cp = sm + 2 * MP;
+  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double c0[Q], c1[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) c0[q] = c1[q] = 0.0;
+  for (int i = warp; i < m; i += 8) {
+    const double2* row = reinterpret_cast<const double2*>(T.G + (long long)i * T.ld);
+    const double xi = xs[i];
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = 64 * q + 2 * lane;
+      if (j <= i) {
+        const double2 g = __ldcs(row + 32 * q + lane);
+        const double g1 = (j + 1 <= i) ? g.y : 0.0;  // G[i][i+1] is not stored
+        s = fma(g.x, xs[j], fma(g1, xs[j + 1], s));
+        if (j < i) c0[q] = fma(g.x, xi, c0[q]);
+        c1[q] = fma(g1, (j + 1 < i) ? xi : 0.0, c1[q]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) yr[i] = s;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    cp[warp * MP + 64 * q + 2 * lane] = c0[q];
+    cp[warp * MP + 64 * q + 2 * lane + 1] = c1[q];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += 256) {
+    double c = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += cp[w * MP + j];
+    const double v = yr[j] + c;
+    T.y[j] = T.base ? fma(T.sign, v, T.base[j]) : T.sign * v;
+  }
+}
+
+template <int Q>
+static cudaError_t symv_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
+  const size_t smem = (size_t)10 * 64 * Q * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(symv_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  count_launch(); symv_kernel<Q><<<ntasks, 256, smem, s>>>(d_tasks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  if (max_m <= 128) return symv_q<2>(d_tasks, ntasks, s);
+  if (max_m <= 256) return symv_q<4>(d_tasks, ntasks, s);
+  if (max_m <= 512) return symv_q<8>(d_tasks, ntasks, s);
+  if (max_m <= 768) return symv_q<12>(d_tasks, ntasks, s);
+  if (max_m <= 1024) return symv_q<16>(d_tasks, ntasks, s);
+  return cudaErrorInvalidValue;
+}
+
+// short sparse rows (level-1 couplings: 1-3 entries per row), thread per row
+__global__ void sub_spmv_kernel(int nrows, const int* __restrict__ rid, const int* __restrict__ rp,
+                                const int* __restrict__ ci, const double* __restrict__ v, double* __restrict__ x,
+                                double* __restrict__ out, int mode) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int e = rp[r]; e < rp[r + 1]; ++e) s = fma(v[e], x[ci[e]], s);
+    if (mode == 0) x[rid[r]] -= s;
+    else out[r] = s;
+  }
+}
+
+cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,
+                            double* out, int mode, cudaStream_t s) {
+  if (nrows <= 0) return cudaSuccess;
+  int blocks = (nrows + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  count_launch(); sub_spmv_kernel<<<blocks, 256, 0, s>>>(nrows, rid, rp, ci, v, x, out, mode);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // out[o] = sign_base*base[o] - sum_{q<nrb} part[poff + q*stride + k]  for the
 // flat segment layout described by RedSeg (one CTA-chunk per 256 entries).
 // ---------------------------------------------------------------------------

@@ -94,6 +94,18 @@ struct GemvTask {
 
 struct TriTask { double* p; int m; int ld; };
 
+// y = base + sign * G x for a symmetric m x m G whose lower triangle is
+// stored (row-major, ld); base may be null (then y = sign * G x)
+struct SymvTask {
+  const double* G;
+  long long ld;
+  const double* x;
+  const double* base;
+  double* y;
+  int m;
+  double sign;
+};
+
 struct QrFinishTask {
   const double* Nm;   // m x c panel holding the reflectors below the diagonal
   const double* tau;
@@ -149,6 +161,10 @@ cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int 
 cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,
                                   cudaStream_t s);
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s);
+cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
+// sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
+cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,
+                            double* out, int mode, cudaStream_t s);
 cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, const int* d_ld, int n,
                             double* d_out, cudaStream_t s);
 }  // namespace sgf

@@ -64,6 +64,7 @@ struct State {
   int my_rank = 0;
   std::vector<int> node_rank;  // per node of the current level: owning rank, -1 = top separator
   std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
+  bool l1_sym = true;          // level-1 apply through G = A_BB^{-1} and the sparse couplings
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
@@ -151,6 +152,100 @@ void timeline_end(cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
+// Level-1 couplings (precond.h L1Couplings): the CSR entries between the
+// unknowns of the level-1 interiors this rank eliminates (rows in factor
+// order) and their neighbours, in both orientations, values gathered on the
+// device from the CSR values.
+// ---------------------------------------------------------------------------
+void build_l1_couplings(State& S, const std::vector<int32_t>& owner, const double* d_vals) {
+  HostTimer ht("setup l1 couplings");
+  const sgf_factor_args& a = *S.a;
+  const int nc = a.level_ncells[0];
+  const int64_t n = a.n;
+  std::vector<char> el(nc, 0);
+  int maxm = 0;
+  for (int c = 0; c < nc; ++c) {
+    const int m = (int)(a.l1_ptr[c + 1] - a.l1_ptr[c]);
+    if (a.cell_interior[c] && m > 0 && (!S.sharded || S.node_rank[c] == S.my_rank)) {
+      el[c] = 1;
+      maxm = std::max(maxm, m);
+    }
+  }
+  if (maxm == 0 || maxm > 1024) {  // the symmetric kernel holds a row pair set per lane
+    S.l1_sym = false;
+    return;
+  }
+  // interior rows in cell order
+  std::vector<int64_t> rows;
+  for (int c = 0; c < nc; ++c)
+    if (el[c]) rows.insert(rows.end(), a.l1_unknowns + a.l1_ptr[c], a.l1_unknowns + a.l1_ptr[c + 1]);
+  const int64_t nb = (int64_t)rows.size();
+  std::vector<int> brp(nb + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < nb; ++r) {
+    const int64_t u = rows[r];
+    int k = 0;
+    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e) k += owner[a.indices[e]] != owner[u];
+    brp[r + 1] = k;
+  }
+  for (int64_t r = 0; r < nb; ++r) brp[r + 1] += brp[r];
+  std::vector<int> bci(std::max(brp[nb], 1)), bpos(std::max(brp[nb], 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < nb; ++r) {
+    const int64_t u = rows[r];
+    int k = brp[r];
+    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e)
+      if (owner[a.indices[e]] != owner[u]) {
+        bci[k] = a.indices[e];
+        bpos[k++] = (int)e;
+      }
+  }
+  // neighbour rows: unknowns outside the eliminated interiors coupled to them
+  std::vector<int> fcnt(n, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < n; ++u) {
+    if (el[owner[u]]) continue;
+    int k = 0;
+    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e) k += el[owner[a.indices[e]]];
+    fcnt[u] = k;
+  }
+  std::vector<int> frid, frp(1, 0);
+  for (int64_t u = 0; u < n; ++u)
+    if (fcnt[u]) {
+      frid.push_back((int)u);
+      frp.push_back(frp.back() + fcnt[u]);
+    }
+  const int64_t nf = (int64_t)frid.size();
+  std::vector<int> fci(std::max(frp[nf], 1)), fpos(std::max(frp[nf], 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < nf; ++r) {
+    const int64_t u = frid[r];
+    int k = frp[r];
+    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e)
+      if (el[owner[a.indices[e]]]) {
+        fci[k] = a.indices[e];
+        fpos[k++] = (int)e;
+      }
+  }
+  L1Couplings& L = S.P->l1;
+  Arena& st = S.P->store;
+  L.nb = (int)nb;
+  L.b_rp = st.upload(brp);
+  L.b_ci = st.upload(bci);
+  L.b_v = st.alloc(bci.size());
+  L.nf = (int)nf;
+  L.f_rid = nf ? st.upload(frid) : nullptr;
+  L.f_rp = st.upload(frp);
+  L.f_ci = st.upload(fci);
+  L.f_v = st.alloc(fci.size());
+  int* d_bpos = S.scratch.upload(bpos);
+  int* d_fpos = S.scratch.upload(fpos);
+  if (brp[nb]) SGF_CUDA(launch_gather(d_vals, d_bpos, L.b_v, brp[nb], S.st));
+  if (nf && frp[nf]) SGF_CUDA(launch_gather(d_vals, d_fpos, L.f_v, frp[nf], S.st));
+  L.ready = true;
+}
+
+// ---------------------------------------------------------------------------
 // level 1: nodes, basis rows, and the CSR -> block scatter (blockmatrix.py:97-144)
 // ---------------------------------------------------------------------------
 void setup_level1(State& S) {
@@ -215,6 +310,7 @@ void setup_level1(State& S) {
 
   // block discovery, per cell (rows of a cell are its unknowns): coupled
   // cells b > a; the symmetric pattern makes the (b, a) side redundant
+  HostTimer htd("setup discovery");
   std::vector<std::vector<int>> up(nc);
   std::vector<char> has_diag(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
@@ -256,6 +352,7 @@ void setup_level1(State& S) {
       off += (long long)sizes[c] * sizes[b];
     }
   }
+  HostTimer hts("setup scatter");
   // scatter the CSR entries into the blocks on the device (entries stored
   // once, in the (min,max) orientation)
   Phase ph_dst(" s-scatter", -1, S.st);
@@ -298,6 +395,7 @@ void setup_level1(State& S) {
     P.my_rank = S.my_rank;
     if (S.sharded) P.cell_rank = S.scratch.upload(S.node_rank);
     SGF_CUDA(launch_csr_scatter(&P, S.st));
+    if (S.l1_sym) build_l1_couplings(S, owner, d_vals);
   }
 
   // basis rows of every node: Pi[active] in cell order
@@ -439,6 +537,23 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     HostTimer htc("elim chol_inv_batch");
     chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
   }
+  // level 1: G = A_BB^{-1} = X^T X (X = L^{-1}), lower triangle, for the
+  // apply (precond.h L1Couplings); K range of tile (i0, j0) starts at max(i0, j0)
+  double* Gall = nullptr;
+  const bool want_g = level == 1 && S.l1_sym && P->l1.ready;
+  if (want_g && tot_w) {
+    Gall = P->store.alloc(tot_w);
+    GemmBatch gg;
+    size_t og = 0;
+    for (size_t q = 0; q < info.size(); ++q) {
+      if (!own[q]) continue;
+      const EI& e = info[q];
+      gg.add(Gall + og, e.ld, 1, e.m, e.m, 1.0, 0.0,
+             {seg(e.X, 1, e.ld, e.X, 1, e.ld, e.m, SEG_KSTART_M | SEG_KSTART_N)}, -1, true);
+      og += (size_t)e.m * e.ld;
+    }
+    gg.launch(S.scratch, st);
+  }
   HostTimer hte("elim E gemm");
   GemmBatch ge;
   for (size_t qi = 0; qi < info.size(); ++qi) {
@@ -558,6 +673,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         f.L = e.W;
         f.inv = e.X;
         f.E = e.E;
+        if (Gall) f.G = Gall + (e.X - Xall);
         P->factors.push_back(std::move(f));
       } else {  // another rank's factor: kept only in the tallies
         S.fa_extra += 4LL * e.m * e.m + 4LL * e.m * e.c;
@@ -993,6 +1109,7 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
       off += nsize[f];
     }
   }
+  HostTimer htk("merge keys+blocks");
   // father blocks in the reference's creation order (sorted old keys)
   std::vector<uint64_t> keys;
   keys.reserve(M.map.size());
@@ -1029,6 +1146,7 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
     const int fa = (int)(o.first >> 32), fb = (int)(o.first & 0xffffffffu);
     N.insert(fa, fb, Blk{base + o.second, nsize[fa], nsize[fb]});
   }
+  HostTimer htc("merge copy tasks");
   for (uint64_t k : keys) {
     const Blk& b = *M.map.find(k);
     if ((long long)b.rows * b.cols == 0) continue;
@@ -1217,6 +1335,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.pi = a.pi_cols;
   S.P = P.get();
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
+  S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
   PlanWorker planner(P.get());  // destroyed (joined) before P and S
   if (a.shard_count > 1) {
     if (!a.cell_rank || !a.exchange || a.shard_rank < 0 || a.shard_rank >= a.shard_count || a.shard_stop_level < 1)

@@ -23,9 +23,26 @@ struct Factor {
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator
+  double* G = nullptr;        // level-1 elimination: A_BB^{-1} = L^{-T} L^{-1} (lower triangle, ld)
   std::vector<int32_t> perm;  // compression: QR column permutation (first `steps` meaningful)
   int* perm_dev = nullptr;    // device copy until the end-of-factorization readback
   int ncols = 0;              // compression: columns of the rank basis N
+};
+
+// Level-1 couplings A_NB of the level-1 eliminations, which are still the
+// original sparse matrix entries: apply_inverse uses them with G = A_BB^{-1}
+// instead of streaming the dense E = A_NB L^{-T} twice (see apply.cpp).
+struct L1Couplings {
+  bool ready = false;
+  int nb = 0;                  // rows: level-1 interior unknowns, in factor order
+  int* b_rp = nullptr;         // [nb+1]
+  int* b_ci = nullptr;         // neighbour unknown ids
+  double* b_v = nullptr;
+  int nf = 0;                  // rows: neighbour unknowns coupled to those interiors
+  int* f_rid = nullptr;        // [nf] their ids
+  int* f_rp = nullptr;         // [nf+1]
+  int* f_ci = nullptr;         // interior unknown ids
+  double* f_v = nullptr;
 };
 
 struct ApplyPlan;
@@ -49,6 +66,7 @@ class Precond {
   ApplyPlan* plan = nullptr;
   // sharding: factors [0, n_local) are the rank's local phase; top_idx are
   // the unknowns active when it ended (empty on a single GPU)
+  L1Couplings l1;
   bool sharded = false;
   size_t n_local = 0;
   std::vector<int64_t> top_idx;
