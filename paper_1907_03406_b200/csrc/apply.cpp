@@ -45,6 +45,7 @@ struct Group {
   double bytes_f1 = 0, bytes_f2 = 0, bytes_b1 = 0, bytes_b2 = 0;  // matrix bytes streamed
   double *xb = nullptr, *zb = nullptr, *acc = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr;  // workspaces
   size_t f0 = 0, f1 = 0;  // factor range
+  int gn_rows = GN_ROWS, gt_rows = GT_ROWS;  // finer row blocks for groups of few large matrices
   // level-1 eliminations in apply_inverse: G = A_BB^{-1} with the sparse couplings
   bool sym = false;
   SymvTask* sym_f = nullptr;  // zb = G xb
@@ -94,15 +95,15 @@ struct ApplyPlan {
 void destroy_plan(ApplyPlan* p) { delete p; }
 
 static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y, int rows,
-                       int cols, int tri) {
-  for (int r0 = 0; r0 < rows; r0 += GN_ROWS) {
+                       int cols, int tri, int rows_per = GN_ROWS) {
+  for (int r0 = 0; r0 < rows; r0 += rows_per) {
     GemvTask t;
     t.A = A;
     t.lda = lda;
     t.x = x;
     t.y = y;
     t.r0 = r0;
-    t.r1 = std::min(rows, r0 + GN_ROWS);
+    t.r1 = std::min(rows, r0 + rows_per);
     t.c0 = 0;
     t.c1 = cols;
     t.tri = tri;
@@ -112,9 +113,9 @@ static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda,
 
 // partials part[rb*cols + k] = sum_{i in rb} A[i,k] x[i]; returns #row blocks
 static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* part,
-                      int rows, int cols, int tri) {
+                      int rows, int cols, int tri, int rows_per = GT_ROWS) {
   int nrb = 0;
-  for (int r0 = 0; r0 < rows; r0 += GT_ROWS, ++nrb)
+  for (int r0 = 0; r0 < rows; r0 += rows_per, ++nrb)
     for (int c0 = 0; c0 < cols; c0 += GT_COLS) {
       GemvTask t;
       t.A = A;
@@ -122,7 +123,7 @@ static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, 
       t.x = x;
       t.y = part + (long long)nrb * cols;
       t.r0 = r0;
-      t.r1 = std::min(rows, r0 + GT_ROWS);
+      t.r1 = std::min(rows, r0 + rows_per);
       t.c0 = c0;
       t.c1 = std::min(cols, c0 + GT_COLS);
       t.tri = tri;
@@ -169,12 +170,22 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.type = fs[rg.first]->type;
     g.f0 = begin + rg.first;
     g.f1 = begin + rg.second;
-    long long sm = 0, sc = 0, sp = 0;
+    long long sm = 0, sc = 0, sp = 0, ntn = 0, ntt = 0;
+    for (size_t i = rg.first; i < rg.second; ++i) {
+      const Factor& f = *fs[i];
+      const long long cb = (f.m + GT_COLS - 1) / GT_COLS;
+      ntn += (f.m + GN_ROWS - 1) / GN_ROWS + (f.c + GN_ROWS - 1) / GN_ROWS;
+      ntt += ((f.m + GT_ROWS - 1) / GT_ROWS + (f.c + GT_ROWS - 1) / GT_ROWS) * cb;
+    }
+    // a group of a few large matrices (top levels, final dense) would leave
+    // most SMs idle: one row per warp for gemv_n, 32-row partials for gemv_t
+    if (ntn < 4 * 148) g.gn_rows = 8;
+    if (ntt < 4 * 148) g.gt_rows = 32;
     for (size_t i = rg.first; i < rg.second; ++i) {
       const Factor& f = *fs[i];
       sm += f.m;
       sc += f.c;
-      const long long rbE = (f.c + GT_ROWS - 1) / GT_ROWS, rbL = (f.m + GT_ROWS - 1) / GT_ROWS;
+      const long long rbE = (f.c + g.gt_rows - 1) / g.gt_rows, rbL = (f.m + g.gt_rows - 1) / g.gt_rows;
       sp += (rbE + rbL) * f.m;  // apply_operator stacks both partial sets
     }
     g.xb = plan->mem.alloc(std::max(sm, 1LL));
@@ -192,19 +203,19 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       const Factor& f = *fs[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
-      add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri);
+      add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
-        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows);
         for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
-        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0) : 0;
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0, g.gt_rows) : 0;
         r1.push_back(RedSeg{g.part + op, g.xb + om, g.acc + om, f.m, nrb, f.m, -1.0});
         // second stage reuses the partial buffer after red1 consumed it
-        int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1);
+        int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1, g.gt_rows);
         r2.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb2, f.m, 1.0});
         op += std::max<long long>(nrb, nrb2) * f.m;
       } else {
-        int nrb = add_gemv_t(b1, f.inv, f.ld, g.xb + om, g.part + op, f.m, f.m, tri);
+        int nrb = add_gemv_t(b1, f.inv, f.ld, g.xb + om, g.part + op, f.m, f.m, tri, g.gt_rows);
         r1.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb, f.m, 1.0});
         op += (long long)nrb * f.m;
       }
@@ -404,14 +415,15 @@ static void prepare_operator(Precond* P) {
       const double* M = (f.type == SGF_FACTOR_COMPRESSION) ? f.LQ : f.L;
       const int tri = (f.type != SGF_FACTOR_COMPRESSION);
       // transpose pass: [L^T | (LQ)^T] x_B (+ E^T x_N), partial row blocks stacked
-      int nrb = add_gemv_t(t1, M, f.ld, g.xb + om, g.part + op, f.m, f.m, tri);
+      int nrb = add_gemv_t(t1, M, f.ld, g.xb + om, g.part + op, f.m, f.m, tri, g.gt_rows);
       if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0)
-        nrb += add_gemv_t(t1, f.E, f.ld, g.xn + oc, g.part + op + (long long)nrb * f.m, f.c, f.m, 0);
+        nrb += add_gemv_t(t1, f.E, f.ld, g.xn + oc, g.part + op + (long long)nrb * f.m, f.c, f.m, 0, g.gt_rows);
       rr.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb, f.m, 1.0});
       op += (long long)nrb * f.m;
       // forward pass: x_N += E x_B, x_B = [L | LQ] x_B
-      if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0) add_gemv_n(te, f.E, f.ld, g.xb + om, g.t + oc, f.c, f.m, 0);
-      add_gemv_n(tl, M, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri);
+      if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0)
+        add_gemv_n(te, f.E, f.ld, g.xb + om, g.t + oc, f.c, f.m, 0, g.gn_rows);
+      add_gemv_n(tl, M, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
       om += f.m;
       oc += f.c;
     }
