@@ -157,91 +157,70 @@ void timeline_end(cudaStream_t st) {
 // order) and their neighbours, in both orientations, values gathered on the
 // device from the CSR values.
 // ---------------------------------------------------------------------------
-void build_l1_couplings(State& S, const std::vector<int32_t>& owner, const double* d_vals) {
+void build_l1_couplings(State& S, const long long* d_ip, const int* d_ix, const int* d_own, const int* d_loc,
+                        const double* d_vals) {
   HostTimer ht("setup l1 couplings");
   const sgf_factor_args& a = *S.a;
   const int nc = a.level_ncells[0];
   const int64_t n = a.n;
   std::vector<char> el(nc, 0);
+  std::vector<int> bstart(nc, 0);
   int maxm = 0;
+  long long nb = 0;
   for (int c = 0; c < nc; ++c) {
     const int m = (int)(a.l1_ptr[c + 1] - a.l1_ptr[c]);
+    bstart[c] = (int)nb;
     if (a.cell_interior[c] && m > 0 && (!S.sharded || S.node_rank[c] == S.my_rank)) {
       el[c] = 1;
       maxm = std::max(maxm, m);
+      nb += m;
     }
   }
   if (maxm == 0 || maxm > 1024) {  // the symmetric kernel holds a row pair set per lane
     S.l1_sym = false;
     return;
   }
-  // interior rows in cell order
-  std::vector<int64_t> rows;
-  for (int c = 0; c < nc; ++c)
-    if (el[c]) rows.insert(rows.end(), a.l1_unknowns + a.l1_ptr[c], a.l1_unknowns + a.l1_ptr[c + 1]);
-  const int64_t nb = (int64_t)rows.size();
-  std::vector<int> brp(nb + 1, 0);
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < nb; ++r) {
-    const int64_t u = rows[r];
-    int k = 0;
-    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e) k += owner[a.indices[e]] != owner[u];
-    brp[r + 1] = k;
-  }
-  for (int64_t r = 0; r < nb; ++r) brp[r + 1] += brp[r];
-  std::vector<int> bci(std::max(brp[nb], 1)), bpos(std::max(brp[nb], 1));
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < nb; ++r) {
-    const int64_t u = rows[r];
-    int k = brp[r];
-    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e)
-      if (owner[a.indices[e]] != owner[u]) {
-        bci[k] = a.indices[e];
-        bpos[k++] = (int)e;
-      }
-  }
-  // neighbour rows: unknowns outside the eliminated interiors coupled to them
-  std::vector<int> fcnt(n, 0);
-#pragma omp parallel for schedule(static)
-  for (int64_t u = 0; u < n; ++u) {
-    if (el[owner[u]]) continue;
-    int k = 0;
-    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e) k += el[owner[a.indices[e]]];
-    fcnt[u] = k;
-  }
-  std::vector<int> frid, frp(1, 0);
-  for (int64_t u = 0; u < n; ++u)
-    if (fcnt[u]) {
-      frid.push_back((int)u);
-      frp.push_back(frp.back() + fcnt[u]);
-    }
-  const int64_t nf = (int64_t)frid.size();
-  std::vector<int> fci(std::max(frp[nf], 1)), fpos(std::max(frp[nf], 1));
-#pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < nf; ++r) {
-    const int64_t u = frid[r];
-    int k = frp[r];
-    for (int64_t e = a.indptr[u]; e < a.indptr[u + 1]; ++e)
-      if (el[owner[a.indices[e]]]) {
-        fci[k] = a.indices[e];
-        fpos[k++] = (int)e;
-      }
-  }
+  cudaStream_t st = S.st;
+  Arena& sc = S.scratch;
+  const char* d_el = sc.upload(el);
+  const int* d_bs = sc.upload(bstart);
+  int* rows = sc.alloc_t<int>(nb + 1);
+  int* bcnt = sc.alloc_t<int>(nb + 1);
+  int* fcnt = sc.alloc_t<int>(n + 1);
+  int* fflag = sc.alloc_t<int>(n + 1);
+  SGF_CUDA(cudaMemsetAsync(bcnt + nb, 0, sizeof(int), st));
+  SGF_CUDA(cudaMemsetAsync(fcnt + n, 0, sizeof(int), st));
+  SGF_CUDA(cudaMemsetAsync(fflag + n, 0, sizeof(int), st));
+  SGF_CUDA(l1_couplings_count(n, (int)nb, d_ip, d_ix, d_own, d_loc, d_el, d_bs, rows, bcnt, fcnt, fflag, st));
   L1Couplings& L = S.P->l1;
-  Arena& st = S.P->store;
+  Arena& store = S.P->store;
   L.nb = (int)nb;
-  L.b_rp = st.upload(brp);
-  L.b_ci = st.upload(bci);
-  L.b_v = st.alloc(bci.size());
-  L.nf = (int)nf;
-  L.f_rid = nf ? st.upload(frid) : nullptr;
-  L.f_rp = st.upload(frp);
-  L.f_ci = st.upload(fci);
-  L.f_v = st.alloc(fci.size());
-  int* d_bpos = S.scratch.upload(bpos);
-  int* d_fpos = S.scratch.upload(fpos);
-  if (brp[nb]) SGF_CUDA(launch_gather(d_vals, d_bpos, L.b_v, brp[nb], S.st));
-  if (nf && frp[nf]) SGF_CUDA(launch_gather(d_vals, d_fpos, L.f_v, frp[nf], S.st));
+  L.b_rp = store.alloc_t<int>(nb + 1);
+  int* fscan = sc.alloc_t<int>(n + 1);
+  int* fidx = sc.alloc_t<int>(n + 1);
+  size_t tb = 0, t1 = 0;
+  SGF_CUDA(scan_ints(bcnt, L.b_rp, nb, nullptr, &tb, st));
+  SGF_CUDA(scan_ints(fcnt, fscan, n, nullptr, &t1, st));
+  tb = std::max(tb, t1);
+  void* temp = sc.alloc_bytes(std::max<size_t>(tb, 256));
+  SGF_CUDA(scan_ints(bcnt, L.b_rp, nb, temp, &tb, st));
+  SGF_CUDA(scan_ints(fcnt, fscan, n, temp, &tb, st));
+  SGF_CUDA(scan_ints(fflag, fidx, n, temp, &tb, st));
+  // sizes for the allocations (the device is otherwise idle here)
+  int tot[3];
+  SGF_CUDA(cudaMemcpyAsync(&tot[0], L.b_rp + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaMemcpyAsync(&tot[1], fscan + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaMemcpyAsync(&tot[2], fidx + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SGF_CUDA(cudaStreamSynchronize(st));
+  L.b_ci = store.alloc_t<int>(std::max(tot[0], 1));
+  L.b_v = store.alloc(std::max(tot[0], 1));
+  L.nf = tot[2];
+  L.f_rid = store.alloc_t<int>(std::max(tot[2], 1));
+  L.f_rp = store.alloc_t<int>(tot[2] + 1);
+  L.f_ci = store.alloc_t<int>(std::max(tot[1], 1));
+  L.f_v = store.alloc(std::max(tot[1], 1));
+  SGF_CUDA(l1_couplings_fill(n, d_ip, d_ix, d_vals, d_own, d_loc, d_el, d_bs, L.b_rp, L.b_ci, L.b_v, fscan, fidx,
+                             L.f_rid, L.f_rp, L.f_ci, L.f_v, L.nf, st));
   L.ready = true;
 }
 
@@ -395,7 +374,7 @@ void setup_level1(State& S) {
     P.my_rank = S.my_rank;
     if (S.sharded) P.cell_rank = S.scratch.upload(S.node_rank);
     SGF_CUDA(launch_csr_scatter(&P, S.st));
-    if (S.l1_sym) build_l1_couplings(S, owner, d_vals);
+    if (S.l1_sym) build_l1_couplings(S, d_ip, d_ix, d_own, d_loc, d_vals);
   }
 
   // basis rows of every node: Pi[active] in cell order
@@ -650,6 +629,27 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   }
   {
     HostTimer ht("elim bookkeeping");
+    // factor records in parallel (they read the actives, cleared only below)
+    std::vector<Factor> recs(info.size());
+#pragma omp parallel for schedule(dynamic, 8)
+    for (size_t q = 0; q < info.size(); ++q) {
+      if (!own[q]) continue;
+      const EI& e = info[q];
+      Factor& f = recs[q];
+      f.type = SGF_FACTOR_ELIMINATION;
+      f.node = e.x;
+      f.level = level;
+      f.m = e.m;
+      f.ld = e.ld;
+      f.c = e.c;
+      f.idx = S.nodes[e.x].active;
+      f.nidx.reserve(e.c);
+      for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
+      f.L = e.W;
+      f.inv = e.X;
+      f.E = e.E;
+      if (Gall) f.G = Gall + (e.X - Xall);
+    }
     // replay the reference sequence for the table and its byte accounting:
     // interior q creates the fills it touches first, then is dropped
     size_t fi = 0;
@@ -661,20 +661,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
       // factor record (before the node's actives are cleared)
       if (own[q]) {
-        Factor f;
-        f.type = SGF_FACTOR_ELIMINATION;
-        f.node = e.x;
-        f.level = level;
-        f.m = e.m;
-        f.ld = e.ld;
-        f.c = e.c;
-        f.idx = S.nodes[e.x].active;
-        for (int j : e.nb) f.nidx.insert(f.nidx.end(), S.nodes[j].active.begin(), S.nodes[j].active.end());
-        f.L = e.W;
-        f.inv = e.X;
-        f.E = e.E;
-        if (Gall) f.G = Gall + (e.X - Xall);
-        P->factors.push_back(std::move(f));
+        P->factors.push_back(std::move(recs[q]));
       } else {  // another rank's factor: kept only in the tallies
         S.fa_extra += 4LL * e.m * e.m + 4LL * e.m * e.c;
         ++S.nf_extra;

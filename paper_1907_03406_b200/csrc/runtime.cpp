@@ -115,9 +115,17 @@ namespace {
 std::mutex g_cache_mu;
 std::map<int, std::multimap<size_t, void*>> g_cache;  // device -> (cap -> chunk)
 
+// The ring is split into NSEG segments used in order; leaving a segment
+// records an event, and re-entering it waits only for that event (work
+// enqueued a whole ring ago), never for the whole stream.
+constexpr int STAGE_NSEG = 8;
 struct Stager {
   char* buf = nullptr;
-  size_t cap = 0, off = 0;
+  size_t cap = 0, seg = 0;  // total, per segment
+  int cur = 0;
+  size_t off = 0;           // offset inside the current segment
+  cudaEvent_t ev[STAGE_NSEG] = {};
+  bool used[STAGE_NSEG] = {};
 };
 std::mutex g_stage_mu;
 std::map<cudaStream_t, Stager> g_stage;
@@ -128,17 +136,34 @@ void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_stage_mu);
   Stager& s = g_stage[st];
   const size_t need = (bytes + 255) & ~(size_t)255;
-  if (s.off + need > s.cap) {
-    if (getenv("SGF_TRACE")) fprintf(stderr, "[stage] ring full (%zu + %zu > %zu): synchronising\n", s.off, need, s.cap);
-    SGF_CUDA(cudaStreamSynchronize(st));  // every staged copy has landed
-    s.off = 0;
-    if (need > s.cap) {
-      if (s.buf) cudaFreeHost(s.buf);
-      s.cap = std::max(need, (size_t)256 << 20);
-      SGF_CUDA(cudaMallocHost((void**)&s.buf, s.cap));
+  if (need > s.seg) {  // (re)allocate a ring whose segments hold this upload
+    if (s.buf) {
+      SGF_CUDA(cudaStreamSynchronize(st));
+      cudaFreeHost(s.buf);
     }
+    s.seg = std::max(need, ((size_t)512 << 20) / STAGE_NSEG);
+    s.cap = s.seg * STAGE_NSEG;
+    SGF_CUDA(cudaMallocHost((void**)&s.buf, s.cap));
+    for (int k = 0; k < STAGE_NSEG; ++k) {
+      if (!s.ev[k]) SGF_CUDA(cudaEventCreateWithFlags(&s.ev[k], cudaEventDisableTiming));
+      s.used[k] = false;
+    }
+    s.cur = 0;
+    s.off = 0;
   }
-  char* p = s.buf + s.off;
+  if (s.off + need > s.seg) {
+    SGF_CUDA(cudaEventRecord(s.ev[s.cur], st));  // end of this segment's uses
+    s.used[s.cur] = true;
+    s.cur = (s.cur + 1) % STAGE_NSEG;
+    if (s.used[s.cur]) {
+      static const bool trace = getenv("SGF_TRACE") != nullptr;
+      if (trace && cudaEventQuery(s.ev[s.cur]) == cudaErrorNotReady)
+        fprintf(stderr, "[stage] waiting for staging segment %d\n", s.cur);
+      SGF_CUDA(cudaEventSynchronize(s.ev[s.cur]));
+    }
+    s.off = 0;
+  }
+  char* p = s.buf + (size_t)s.cur * s.seg + s.off;
   s.off += need;
   std::memcpy(p, src, bytes);
   SGF_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));

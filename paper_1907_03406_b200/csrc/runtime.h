@@ -45,6 +45,14 @@ cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, cons
 cudaError_t launch_spmv(int n, const long long* rp, const int* rp32, const int* ci, const double* v, const double* x,
                         double* y, const double* b, cudaStream_t s);
 cudaError_t launch_rowptr32(const long long* rp, int* out, long long n1, cudaStream_t s);
+cudaError_t l1_couplings_count(long long n, int nb, const long long* ip, const int* ix, const int* owner,
+                               const int* local, const char* el, const int* bstart, int* rows, int* bcnt, int* fcnt,
+                               int* fflag, cudaStream_t s);
+cudaError_t scan_ints(const int* in, int* out, long long count, void* temp, size_t* temp_bytes, cudaStream_t s);
+cudaError_t l1_couplings_fill(long long n, const long long* ip, const int* ix, const double* vals, const int* owner,
+                              const int* local, const char* el, const int* bstart, const int* brp, int* bci,
+                              double* bv, const int* fscan, const int* fidx, int* frid, int* frp, int* fci,
+                              double* fv, int nf, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s);
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
@@ -357,9 +365,18 @@ struct GemmBatch {
   // triangle only; tiles strictly above the diagonal are skipped
   void add(double* C, long long c_rs, long long c_cs, int M, int N, double alpha, double beta,
            const std::vector<GemmSeg>& sg, int force = -1, bool lower_only = false) {
+    add(C, c_rs, c_cs, M, N, alpha, beta, sg.data(), (int)sg.size(), force, lower_only);
+  }
+  // one segment (no temporary vector: a level adds ~1e5 of these)
+  void add(double* C, long long c_rs, long long c_cs, int M, int N, double alpha, double beta, const GemmSeg& s1,
+           int force = -1, bool lower_only = false) {
+    add(C, c_rs, c_cs, M, N, alpha, beta, &s1, 1, force, lower_only);
+  }
+  void add(double* C, long long c_rs, long long c_cs, int M, int N, double alpha, double beta, const GemmSeg* sg,
+           int nsg, int force, bool lower_only) {
     if (M <= 0 || N <= 0) return;
     int seg0 = (int)segs.size();
-    for (auto& s : sg) segs.push_back(s);
+    segs.insert(segs.end(), sg, sg + nsg);
     // the 64x64 configuration is the fastest on B200 for every shape measured
     // (tools/gemm_bench.cu); the 128x128 path stays available via force = 1
     bool use_big = force == 1;
@@ -377,12 +394,12 @@ struct GemmBatch {
         t.m0 = m0;
         t.n0 = n0;
         t.seg0 = seg0;
-        t.nseg = (int)sg.size();
+        t.nseg = nsg;
         t.alpha = alpha;
         t.beta = beta;
         dst.push_back(t);
       }
-    for (auto& s : sg) flops += 2LL * M * N * s.K;
+    for (int i = 0; i < nsg; ++i) flops += 2LL * M * N * sg[i].K;
   }
   bool empty() const { return big.empty() && small.empty(); }
   void launch(Arena& scratch, cudaStream_t st);
