@@ -1097,19 +1097,25 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
     }
   }
   HostTimer htk("merge keys+blocks");
-  // father blocks in the reference's creation order (sorted old keys)
-  std::vector<uint64_t> keys;
-  keys.reserve(M.map.size());
-  M.map.for_each([&](uint64_t k, Blk&) { keys.push_back(k); });
-  std::sort(keys.begin(), keys.end());
+  // every live child block lands in its father block at the children's
+  // offsets.  Father blocks are laid out in first-appearance order of a walk
+  // over the table (identical on every rank of a sharded run); their order
+  // does not matter otherwise: the copies hit disjoint regions, neighbour
+  // lists are sorted where used, and the live/peak tally only grows here.
+  struct MB {
+    Blk b;
+    int a0, b0;
+    long long off;  // father block offset in the new level region
+  };
+  std::vector<MB> mbs;
+  mbs.reserve(M.map.size());
   BlockTable N;
   N.init(nsize);
   std::vector<std::pair<uint64_t, long long>> order;
-  FlatMap<long long> newoff(keys.size());
+  FlatMap<long long> newoff(M.map.size());
   long long tot = 0;
-  for (uint64_t k : keys) {
-    const Blk& b = *M.map.find(k);
-    if ((long long)b.rows * b.cols == 0) continue;
+  M.map.for_each([&](uint64_t k, Blk& b) {
+    if ((long long)b.rows * b.cols == 0) return;
     const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
     const uint64_t fk = bkey(fof[a0], fof[b0]);
     auto ins = newoff.emplace(fk);
@@ -1119,7 +1125,8 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
       order.push_back({fk, tot});
       tot += (long long)nsize[fa] * nsize[fb];
     }
-  }
+    mbs.push_back(MB{b, a0, b0, *ins.first});
+  });
   double* base = nl->alloc(std::max<long long>(tot, 1));
   if (tot) SGF_CUDA(cudaMemsetAsync(base, 0, tot * sizeof(double), st));
   S.regions.assign(1, {base, tot});
@@ -1134,21 +1141,31 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
     N.insert(fa, fb, Blk{base + o.second, nsize[fa], nsize[fb]});
   }
   HostTimer htc("merge copy tasks");
-  for (uint64_t k : keys) {
-    const Blk& b = *M.map.find(k);
-    if ((long long)b.rows * b.cols == 0) continue;
-    const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
-    const int fa = fof[a0], fb = fof[b0], oa = oof[a0], ob = oof[b0];
-    if (fa == fb) {
-      Blk* t = N.find(fa, fa);
-      cp.add(b.p, b.cols, 1, t->p + (long long)oa * t->cols + ob, t->cols, 1, b.rows, b.cols);
-      if (a0 != b0) cp.add(b.p, 1, b.cols, t->p + (long long)ob * t->cols + oa, t->cols, 1, b.cols, b.rows);
-    } else if (fa < fb) {
-      Blk* t = N.find(fa, fb);
-      cp.add(b.p, b.cols, 1, t->p + (long long)oa * t->cols + ob, t->cols, 1, b.rows, b.cols);
-    } else {
-      Blk* t = N.find(fb, fa);
-      cp.add(b.p, 1, b.cols, t->p + (long long)ob * t->cols + oa, t->cols, 1, b.cols, b.rows);
+  {
+    const size_t nm = mbs.size();
+    std::vector<size_t> pos(nm + 1, 0);
+    for (size_t i = 0; i < nm; ++i)
+      pos[i + 1] = pos[i] + ((fof[mbs[i].a0] == fof[mbs[i].b0] && mbs[i].a0 != mbs[i].b0) ? 2 : 1);
+    const size_t base_task = cp.tasks.size();
+    cp.tasks.resize(base_task + pos[nm]);
+#pragma omp parallel for schedule(static)
+    for (size_t i = 0; i < nm; ++i) {
+      const MB& e = mbs[i];
+      const Blk& b = e.b;
+      const int fa = fof[e.a0], fb = fof[e.b0], oa = oof[e.a0], ob = oof[e.b0];
+      CopyTask* t = &cp.tasks[base_task + pos[i]];
+      double* fp = base + e.off;
+      if (fa == fb) {
+        const long long cols = nsize[fa];
+        t[0] = CopyTask{b.p, fp + (long long)oa * cols + ob, b.cols, 1, cols, 1, b.rows, b.cols};
+        if (e.a0 != e.b0) t[1] = CopyTask{b.p, fp + (long long)ob * cols + oa, 1, b.cols, cols, 1, b.cols, b.rows};
+      } else if (fa < fb) {
+        const long long cols = nsize[fb];
+        t[0] = CopyTask{b.p, fp + (long long)oa * cols + ob, b.cols, 1, cols, 1, b.rows, b.cols};
+      } else {
+        const long long cols = nsize[fa];
+        t[0] = CopyTask{b.p, fp + (long long)ob * cols + oa, 1, b.cols, cols, 1, b.cols, b.rows};
+      }
     }
   }
   {
