@@ -46,6 +46,7 @@ struct Group {
   double *xb = nullptr, *zb = nullptr, *acc = nullptr, *xn = nullptr, *t = nullptr, *part = nullptr;  // workspaces
   size_t f0 = 0, f1 = 0;  // factor range
   int gn_rows = GN_ROWS, gt_rows = GT_ROWS;  // finer row blocks for groups of few large matrices
+  int lpr1 = 32, lpr2 = 32;                   // mode-N lanes per row (inverse, couplings)
   // level-1 eliminations in apply_inverse: G = A_BB^{-1} with the sparse couplings
   bool sym = false;
   SymvTask* sym_f = nullptr;  // zb = G xb
@@ -59,6 +60,9 @@ struct Group {
   int noRed = 0;
   double bytes_oT = 0, bytes_oE = 0, bytes_oL = 0;
 };
+
+// lanes per row for mode-N rows of `len2` 16-byte words on average
+static int lanes_for(double len2) { return len2 <= 48 ? 8 : (len2 <= 96 ? 16 : 32); }
 
 // algorithmic bytes of the matrix entries a GEMV task list reads
 static double gemv_bytes(const std::vector<GemvTask>& v, int mode) {
@@ -249,6 +253,15 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.nidx = plan->mem.upload(nidx);
     g.bytes_f1 = gemv_bytes(f1, 0);
     g.bytes_f2 = gemv_bytes(f2, 0);
+    {
+      long long r1n = 0, r2n = 0;
+      for (size_t i = rg.first; i < rg.second; ++i) {
+        r1n += fs[i]->m;
+        r2n += fs[i]->c;
+      }
+      if (r1n) g.lpr1 = lanes_for(g.bytes_f1 / 16.0 / r1n);
+      if (r2n) g.lpr2 = lanes_for(g.bytes_f2 / 16.0 / r2n);
+    }
     g.bytes_b1 = gemv_bytes(b1, 1);
     g.bytes_b2 = gemv_bytes(b2, 1);
     g.fwd1 = plan->mem.upload(f1);
@@ -305,9 +318,9 @@ void plan_finish(Precond* P) {
   if (P->plan) std::vector<int>().swap(P->plan->tix);
 }
 
-static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t st) {
+static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t st, int lpr = 32) {
   ProfScope ps(st, PROF_GEMV, bytes);
-  SGF_CUDA(launch_gemv(t, nt, mode, st));
+  SGF_CUDA(launch_gemv(t, nt, mode, st, lpr));
 }
 
 // level-1 group of apply_inverse: v = G x_B, x_N -= A_NB v (forward, v kept
@@ -335,8 +348,8 @@ static void backward_group_sym(const L1Couplings& c, const Group& g, double* y, 
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
   (void)pl;
   SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
-  gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st);
-  if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, 0, g.bytes_f2, st);
+  gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st, g.lpr1);
+  if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, 0, g.bytes_f2, st, g.lpr2);
   SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, g.t, g.ntgt, st));
 }
@@ -536,22 +549,35 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
   cudaStream_t st = ctx.stream;
   const long long n = A->n;
   auto t0 = std::chrono::steady_clock::now();
-  Arena w(st, (size_t)8 * n * sizeof(double) + (1 << 20));
-  double* r = w.alloc(n);
-  double* z = w.alloc(n);
-  double* p = w.alloc(n);
-  double* q = w.alloc(n);
-  double* part = w.alloc(512);
-  double* sc = w.alloc(8);  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
-  double* hsc = nullptr;
-  SGF_CUDA(cudaMallocHost(&hsc, 8 * sizeof(double)));
-  struct HostFree {
-    double* p;
-    ~HostFree() { cudaFreeHost(p); }
-  } hf{hsc};
+  // workspace held by the matrix (allocated on its first solve): a solve
+  // allocates nothing, so it never waits in cudaMalloc / cudaFreeHost
+  const long long np = (n + 31) & ~31LL;  // 256-byte aligned vectors
+  if (!A->ws) {
+    A->ws = A->mem.alloc(4 * np + 512 + 8);
+    SGF_CUDA(cudaMallocHost((void**)&A->hsc, 8 * sizeof(double)));
+  }
+  double* r = A->ws;
+  double* z = r + np;
+  double* p = z + np;
+  double* q = p + np;
+  double* part = q + np;
+  double* sc = part + 512;  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  double* hsc = A->hsc;
+  // SGF_TRACE=5: host time spent waiting in each readback vs. issuing work
+  static const bool trace5 = getenv("SGF_TRACE") && atoi(getenv("SGF_TRACE")) == 5;
+  double t_wait = 0.0, t_issue = 0.0;
+  auto tlast = std::chrono::steady_clock::now();
   auto readback = [&](int lo, int cnt) {
     SGF_CUDA(cudaMemcpyAsync(hsc + lo, sc + lo, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
-    SGF_CUDA(cudaStreamSynchronize(st));
+    if (trace5) {
+      auto t1 = std::chrono::steady_clock::now();
+      t_issue += std::chrono::duration<double, std::milli>(t1 - tlast).count();
+      SGF_CUDA(cudaStreamSynchronize(st));
+      tlast = std::chrono::steady_clock::now();
+      t_wait += std::chrono::duration<double, std::milli>(tlast - t1).count();
+    } else {
+      SGF_CUDA(cudaStreamSynchronize(st));
+    }
   };
   auto precond = [&](const double* in, double* out) {
     if (M) M(in, out);
@@ -629,6 +655,7 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
   SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
   readback(3, 1);
   const double fin = std::sqrt(hsc[3]) / bnorm;
+  if (trace5) fprintf(stderr, "[pcg] %d iterations: host issue %.2f ms, waiting %.2f ms\n", it, t_issue, t_wait);
   rep->iterations = it;
   rep->converged = (converged && fin <= tol) ? 1 : 0;
   rep->final_rel_residual = fin;

@@ -20,34 +20,50 @@ namespace sgf {
 // (pad_ld), so rows are streamed with 128-bit loads: 4 x 16 B in flight per
 // lane, evict-first (each entry is read once per sweep); x stays cached.
 // (256, 8): at most 32 registers so 8 CTAs = 64 warps fit per SM (the
-// register limit capped residency at 4 CTAs and left HBM latency exposed)
+// register limit capped residency at 4 CTAs and left HBM latency exposed).
+// LPR lanes per row (8/16/32): short rows (small nodes, triangles) share a
+// warp so each lane still has 4 loads in flight and the reduction is shorter.
+template <int LPR>
 __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
+  constexpr int RPW = 32 / LPR;  // rows per warp pass
   const GemvTask T = tasks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = T.r0 + warp; i < T.r1; i += 8) {
-    const double* arow = T.A + (long long)i * T.lda;
-    const double2* a = reinterpret_cast<const double2*>(arow);
-    const int ke = T.tri ? min(T.c1, i + 1) : T.c1;  // c0 == 0 for every task
-    const int k2 = ke >> 1;
-    const double* x = T.x;
+  const int sub = lane % LPR, grp = lane / LPR;
+  for (int i0 = T.r0 + warp * RPW; i0 < T.r1; i0 += 8 * RPW) {  // warp-uniform
+    const int i = i0 + grp;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int k = lane;
-    for (; k + 96 < k2; k += 128) {
-      const double2 a0 = __ldcs(a + k), a1 = __ldcs(a + k + 32), a2 = __ldcs(a + k + 64), a3 = __ldcs(a + k + 96);
-      s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
-      s1 = fma(a1.x, x[2 * k + 64], fma(a1.y, x[2 * k + 65], s1));
-      s2 = fma(a2.x, x[2 * k + 128], fma(a2.y, x[2 * k + 129], s2));
-      s3 = fma(a3.x, x[2 * k + 192], fma(a3.y, x[2 * k + 193], s3));
+    if (i < T.r1) {
+      const double* arow = T.A + (long long)i * T.lda;
+      const double2* a = reinterpret_cast<const double2*>(arow);
+      const int ke = T.tri ? min(T.c1, i + 1) : T.c1;  // c0 == 0 for every task
+      const int k2 = ke >> 1;
+      const double* x = T.x;
+      int k = sub;
+      for (; k + 3 * LPR < k2; k += 4 * LPR) {
+        const double2 a0 = __ldcs(a + k), a1 = __ldcs(a + k + LPR), a2 = __ldcs(a + k + 2 * LPR),
+                      a3 = __ldcs(a + k + 3 * LPR);
+        s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
+        s1 = fma(a1.x, x[2 * (k + LPR)], fma(a1.y, x[2 * (k + LPR) + 1], s1));
+        s2 = fma(a2.x, x[2 * (k + 2 * LPR)], fma(a2.y, x[2 * (k + 2 * LPR) + 1], s2));
+        s3 = fma(a3.x, x[2 * (k + 3 * LPR)], fma(a3.y, x[2 * (k + 3 * LPR) + 1], s3));
+      }
+      if (k < k2) {  // tail: up to 4 predicated loads issued together
+        const double2 z = make_double2(0.0, 0.0);
+        const double2 a0 = __ldcs(a + k);
+        const double2 a1 = k + LPR < k2 ? __ldcs(a + k + LPR) : z;
+        const double2 a2 = k + 2 * LPR < k2 ? __ldcs(a + k + 2 * LPR) : z;
+        const double2 a3 = k + 3 * LPR < k2 ? __ldcs(a + k + 3 * LPR) : z;
+        s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
+        if (k + LPR < k2) s1 = fma(a1.x, x[2 * (k + LPR)], fma(a1.y, x[2 * (k + LPR) + 1], s1));
+        if (k + 2 * LPR < k2) s2 = fma(a2.x, x[2 * (k + 2 * LPR)], fma(a2.y, x[2 * (k + 2 * LPR) + 1], s2));
+        if (k + 3 * LPR < k2) s3 = fma(a3.x, x[2 * (k + 3 * LPR)], fma(a3.y, x[2 * (k + 3 * LPR) + 1], s3));
+      }
+      if ((ke & 1) && sub == 0) s0 = fma(arow[ke - 1], x[ke - 1], s0);
     }
-    for (; k < k2; k += 32) {
-      const double2 a0 = __ldcs(a + k);
-      s0 = fma(a0.x, x[2 * k], fma(a0.y, x[2 * k + 1], s0));
-    }
-    if ((ke & 1) && lane == 0) s0 = fma(arow[ke - 1], x[ke - 1], s0);
     double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) T.y[i] = s;
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (i < T.r1 && sub == 0) T.y[i] = s;
   }
 }
 
@@ -84,66 +100,89 @@ __global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restri
   if (k + 1 < T.c1) T.y[k + 1] = t0 + t1;
 }
 
-cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s) {
+cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s, int lpr) {
   if (ntasks <= 0) return cudaSuccess;
   count_launch();
-  if (mode == 0) gemv_n_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
-  else gemv_t_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
+  if (mode == 0) {
+    if (lpr == 8) gemv_n_kernel<8><<<ntasks, 256, 0, s>>>(d_tasks);
+    else if (lpr == 16) gemv_n_kernel<16><<<ntasks, 256, 0, s>>>(d_tasks);
+    else gemv_n_kernel<32><<<ntasks, 256, 0, s>>>(d_tasks);
+  } else {
+    gemv_t_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
+  }
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// Symmetric GEMV from the lower triangle, one CTA per matrix (m <= 64*Q):
-// warp w takes rows i = w (mod 8); lane l owns the column pairs
-// 64q + 2l + {0,1}, so every stored entry is read once (16-byte loads) and
-// used twice: G_ij x_j into the row sum of i, G_ij x_i into lane-resident
-// column sums of j (strictly lower part).  Row sums are warp-reduced, column
-// sums of the 8 warps are added in fixed order through shared memory.
+// Symmetric GEMV from the lower triangle, one CTA per matrix (m <= 64*Q).
+// Warp w takes the row pairs (p, m-1-p), p = w (mod 8): the two rows hold
+// m+1 entries together, so every pair issues the same ~Q+1 16-byte loads per
+// lane at once (lane l reads the column pairs 64q + 2l + {0,1}).  Each stored
+// entry is read once and used twice: G_ij x_j into the row sum of i (warp
+// reduction), G_ij x_i into the warp's column partials of j in shared memory
+// (strictly lower part).  Column partials of the 8 warps are added in fixed
+// order at the end.
 // ---------------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(256) symv_kernel(const SymvTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(256, Q <= 8 ? 4 : 2) symv_kernel(const SymvTask* __restrict__ tasks) {
   extern __shared__ double sm[];
   constexpr int MP = 64 * Q;
   const SymvTask T = tasks[blockIdx.x];
   const int m = T.m;
   double* xs = sm;
   double* yr = sm + MP;
-  double* cp = sm + 2 * MP;
-  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double c0[Q], c1[Q];
+  double* cp = sm + 2 * MP + warp * MP;
+  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
+  for (int i = lane; i < MP; i += 32) cp[i] = 0.0;
+  __syncthreads();
+  const int npairs = (m + 1) / 2;
+  for (int p = warp; p < npairs; p += 8) {
+    const int ra = p, rb = m - 1 - p;  // rb == ra for the middle row of an odd m
+    const int qa = (ra >> 6) + 1, qb = (rb == ra) ? 0 : (rb >> 6) + 1;
+    double2 g[Q + 1];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) c0[q] = c1[q] = 0.0;
-  for (int i = warp; i < m; i += 8) {
-    const double2* row = reinterpret_cast<const double2*>(T.G + (long long)i * T.ld);
-    const double xi = xs[i];
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
+    for (int v = 0; v <= Q; ++v) {
+      const bool isa = v < qa;
+      const int q = isa ? v : v - qa;
+      const int row = isa ? ra : rb;
       const int j = 64 * q + 2 * lane;
-      if (j <= i) {
-        const double2 g = __ldcs(row + 32 * q + lane);
-        const double g1 = (j + 1 <= i) ? g.y : 0.0;  // G[i][i+1] is not stored
-        s = fma(g.x, xs[j], fma(g1, xs[j + 1], s));
-        if (j < i) c0[q] = fma(g.x, xi, c0[q]);
-        c1[q] = fma(g1, (j + 1 < i) ? xi : 0.0, c1[q]);
-      }
+      const bool ok = (isa || q < qb) && j <= row;
+      g[v] = ok ? __ldcs(reinterpret_cast<const double2*>(T.G + (long long)row * T.ld + j)) : make_double2(0.0, 0.0);
+    }
+    const double xa = xs[ra], xb = xs[rb];
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int v = 0; v <= Q; ++v) {
+      const bool isa = v < qa;
+      const int q = isa ? v : v - qa;
+      const int row = isa ? ra : rb;
+      const int j = 64 * q + 2 * lane;
+      if (!(isa || q < qb) || j > row) continue;
+      const double g0 = g[v].x, g1 = (j + 1 <= row) ? g[v].y : 0.0;  // G[i][i+1] is not stored
+      const double t = fma(g0, xs[j], g1 * xs[j + 1]);
+      const double xi = isa ? xa : xb;
+      if (isa) sa += t;
+      else sb += t;
+      if (j < row) cp[j] = fma(g0, xi, cp[j]);
+      if (j + 1 < row) cp[j + 1] = fma(g1, xi, cp[j + 1]);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) yr[i] = s;
-  }
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    cp[warp * MP + 64 * q + 2 * lane] = c0[q];
-    cp[warp * MP + 64 * q + 2 * lane + 1] = c1[q];
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+      yr[ra] = sa;
+      if (rb != ra) yr[rb] = sb;
+    }
   }
   __syncthreads();
+  const double* cpa = sm + 2 * MP;
   for (int j = threadIdx.x; j < m; j += 256) {
     double c = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) c += cp[w * MP + j];
+    for (int w = 0; w < 8; ++w) c += cpa[w * MP + j];
     const double v = yr[j] + c;
     T.y[j] = T.base ? fma(T.sign, v, T.base[j]) : T.sign * v;
   }

@@ -160,7 +160,8 @@ cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_se
 cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s);
 cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,
                                   cudaStream_t s);
-cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s);
+// lpr: lanes per row of the mode-N kernel (8, 16 or 32)
+cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s, int lpr = 32);
 cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
 // sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
 cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,

@@ -88,6 +88,11 @@ struct Csr {
   int* ci = nullptr;
   double* v = nullptr;
   Arena mem;
+  double* ws = nullptr;   // PCG workspace (4n + 520), one solve at a time per matrix
+  double* hsc = nullptr;  // pinned scalars read back by the PCG
+  ~Csr() {
+    if (hsc) cudaFreeHost(hsc);
+  }
 };
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b);
 // preconditioner: out = M^-1 in on device vectors (empty = identity)
