@@ -231,6 +231,24 @@ void setup_level1(State& S) {
   const sgf_factor_args& a = *S.a;
   const int nc = a.level_ncells[0];
   const int64_t n = a.n;
+  const int pi = S.pi;
+  // One pinned staging region for every level-1 upload:
+  //   [indptr | indices | values | owner | local | Pi double buffer]
+  // staged with parallel copies, DMA enqueued without synchronisation (a
+  // helper thread staging during the block discovery was slower: it competes
+  // with the OpenMP loops for cores and memory bandwidth).
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const int64_t chunk_rows = std::max<int64_t>(1, ((int64_t)64 << 20) / (pi * (int64_t)sizeof(double)));
+  const size_t half = (size_t)std::min<int64_t>(chunk_rows, std::max<int64_t>(n, 1)) * pi;
+  const size_t o_ip = 0, o_ix = o_ip + al((n + 1) * 8), o_v = o_ix + al(std::max<int64_t>(a.nnz, 1) * 4);
+  const size_t o_own = o_v + (a.values_on_device ? 0 : al(std::max<int64_t>(a.nnz, 1) * 8));
+  const size_t o_loc = o_own + al(n * 4), o_phi = o_loc + al(n * 4);
+  char* pin = (char*)S.ctx->pinned(o_phi + 2 * half * sizeof(double));
+  long long* d_ip = S.scratch.alloc_t<long long>(n + 1);
+  int* d_ix = S.scratch.alloc_t<int>(std::max<int64_t>(a.nnz, 1));
+  double* d_vhost = a.values_on_device ? nullptr : S.scratch.alloc(std::max<int64_t>(a.nnz, 1));
+  int* d_own = S.scratch.alloc_t<int>(n);
+  int* d_loc = S.scratch.alloc_t<int>(n);
   std::vector<int32_t> owner(n, -1), local(n, 0);
   std::vector<int> sizes(nc);
   S.nodes.assign(nc, Node());
@@ -305,6 +323,7 @@ void setup_level1(State& S) {
     }
     std::sort(v.begin(), v.end());
   }
+  HostTimer htd2("setup blocks");
   S.M.init(sizes);
   long long total = 0;
   for (int c = 0; c < nc; ++c) {
@@ -322,12 +341,12 @@ void setup_level1(State& S) {
   for (int c = 0; c < nc; ++c) {
     if (has_diag[c]) {
       diag_off[c] = off;
-      S.M.insert(c, c, Blk{base + off, sizes[c], sizes[c]});
+      S.M.insert_new(c, c, Blk{base + off, sizes[c], sizes[c]});
       off += (long long)sizes[c] * sizes[c];
     }
     for (int b : up[c]) {
       up_off[c].push_back(off);
-      S.M.insert(c, b, Blk{base + off, sizes[c], sizes[b]});
+      S.M.insert_new(c, b, Blk{base + off, sizes[c], sizes[b]});
       off += (long long)sizes[c] * sizes[b];
     }
   }
@@ -344,20 +363,30 @@ void setup_level1(State& S) {
       up_o.insert(up_o.end(), up_off[c].begin(), up_off[c].end());
     }
     CsrScatter P;
-    long long* d_ip = S.scratch.alloc_t<long long>(n + 1);
-    int* d_ix = S.scratch.alloc_t<int>(std::max<int64_t>(a.nnz, 1));
-    int* d_own = S.scratch.alloc_t<int>(n);
-    int* d_loc = S.scratch.alloc_t<int>(n);
-    upload_pinned(*S.ctx, d_ip, a.indptr, (n + 1) * sizeof(long long));
-    upload_pinned(*S.ctx, d_ix, a.indices, a.nnz * sizeof(int));
-    upload_pinned(*S.ctx, d_own, owner.data(), n * sizeof(int));
-    upload_pinned(*S.ctx, d_loc, local.data(), n * sizeof(int));
-    const double* d_vals = a.values;
-    if (!a.values_on_device) {
-      double* dv = S.scratch.alloc(std::max<int64_t>(a.nnz, 1));
-      upload_pinned(*S.ctx, dv, a.values, a.nnz * sizeof(double));
-      d_vals = dv;
+    {
+      struct Piece {
+        size_t off;
+        void* dst;
+        const void* src;
+        size_t bytes;
+      };
+      std::vector<Piece> pieces = {{o_ip, d_ip, a.indptr, (size_t)(n + 1) * 8},
+                                   {o_ix, d_ix, a.indices, (size_t)a.nnz * 4},
+                                   {o_own, d_own, owner.data(), (size_t)n * 4},
+                                   {o_loc, d_loc, local.data(), (size_t)n * 4}};
+      if (d_vhost) pieces.push_back({o_v, d_vhost, a.values, (size_t)a.nnz * 8});
+      constexpr size_t BLK = (size_t)1 << 20;
+      for (auto& pc : pieces) {
+        const long long nb = (long long)((pc.bytes + BLK - 1) / BLK);
+#pragma omp parallel for schedule(static)
+        for (long long b = 0; b < nb; ++b) {
+          const size_t o = (size_t)b * BLK;
+          std::memcpy(pin + pc.off + o, (const char*)pc.src + o, std::min(BLK, pc.bytes - o));
+        }
+        if (pc.bytes) SGF_CUDA(cudaMemcpyAsync(pc.dst, pin + pc.off, pc.bytes, cudaMemcpyHostToDevice, S.st));
+      }
     }
+    const double* d_vals = a.values_on_device ? a.values : d_vhost;
     P.indptr = d_ip;
     P.indices = d_ix;
     P.values = d_vals;
@@ -379,18 +408,10 @@ void setup_level1(State& S) {
 
   // basis rows of every node: Pi[active] in cell order
   Phase ph_phi(" s-phi", -1, S.st);
-  const int pi = S.pi;
   // rows are generated straight into the context's pinned buffer, in chunks,
   // each chunk's DMA overlapping the generation of the next
   double* d_phi = S.lvl->alloc(std::max<size_t>((size_t)n * pi, 1));
-  const int64_t chunk_rows = std::max<int64_t>(1, ((int64_t)64 << 20) / (pi * (int64_t)sizeof(double)));
-  double* hp_buf[2] = {nullptr, nullptr};
-  {
-    const size_t half = (size_t)std::min<int64_t>(chunk_rows, std::max<int64_t>(n, 1)) * pi;
-    double* hp = (double*)S.ctx->pinned(2 * half * sizeof(double));
-    hp_buf[0] = hp;
-    hp_buf[1] = hp + half;
-  }
+  double* hp_buf[2] = {(double*)(pin + o_phi), (double*)(pin + o_phi) + half};
   cudaEvent_t done[2] = {nullptr, nullptr};
   SGF_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
   SGF_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));

@@ -313,6 +313,16 @@ struct BlockTable {
       add_adj(b, a);
     }
   }
+  // insert a block known to be new (setup: each pair appears once)
+  void insert_new(int a, int b, Blk blk) {
+    *map.emplace(bkey(a, b)).first = blk;
+    live += nbytes(blk);
+    peak = std::max(peak, live);
+    if (a != b) {
+      adj[a].push_back(b);
+      adj[b].push_back(a);
+    }
+  }
   void add_adj(int a, int b) {
     auto& v = adj[a];
     if (std::find(v.begin(), v.end(), b) == v.end()) v.push_back(b);
