@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
 // pivot candidates through distributed shared memory and three cluster
 // barriers.  Same arithmetic rules as qrcp_kernel above.
 // ---------------------------------------------------------------------------
-constexpr int QC = 8;             // CTAs per cluster
+constexpr int QC = 16;            // CTAs per cluster (non-portable size, allowed at launch)
 constexpr int QCT = 256;          // threads per CTA
 constexpr int QCW = QCT / 32;
 
@@ -403,6 +403,12 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = (size_t)max_m * sizeof(double);
   static size_t configured = 48 * 1024;
+  static bool nonportable = false;
+  if (!nonportable) {
+    cudaError_t e = cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    nonportable = true;
+  }
   if (smem > configured) {
     cudaError_t e =
         cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
