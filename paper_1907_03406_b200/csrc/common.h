@@ -77,6 +77,7 @@ struct QrTask {
   double tol;
   int* out_rank;       // -> rank
   int* out_steps;      // -> reflectors computed
+  double* tmp;         // m x c scratch panel (cluster variant: final column reorder)
 };
 
 // ---- apply / GEMV -----------------------------------------------------------------

@@ -790,7 +790,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   // pivoted QR (truncated at the rank), ranks read back
   std::vector<QrTask> qt(nw);
   int* d_out = S.scratch.alloc_t<int>(2 * nw);
-  int max_m = 1;
+  int max_m = 1, max_c = 1;
   for (int w = 0; w < nw; ++w) {
     CI& c = ci[w];
     QrTask& t = qt[w];
@@ -813,12 +813,14 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     t.tol = a.rank_tol;
     t.out_rank = d_out + w;
     t.out_steps = d_out + nw + w;
+    t.tmp = S.scratch.alloc((size_t)std::max(c.m, 1) * std::max(c.cN, 1));
     max_m = std::max(max_m, c.m);
+    max_c = std::max(max_c, c.cN);
   }
   {
     QrTask* d_qt = S.scratch.upload(qt);
     ProfScope ps(st, PROF_QR, 0.0);
-    SGF_CUDA(launch_qrcp(d_qt, nw, max_m, st));
+    SGF_CUDA(launch_qrcp(d_qt, nw, max_m, st, max_c));
   }
   std::vector<int> rs(2 * nw);
   SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -207,11 +207,16 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
 
 // ---------------------------------------------------------------------------
 // Cluster variant: one thread-block cluster of QC CTAs per node.  CTA q owns
-// the panel columns at positions j == q (mod QC) (norms, updates); every CTA
-// recomputes the reflector from the pivot column redundantly (identical
-// arithmetic => identical results), so per step the only exchange is the
-// pivot candidates through distributed shared memory and three cluster
-// barriers.  Same arithmetic rules as qrcp_kernel above.
+// the panel positions j == q (mod QC) (norms, updates); every CTA recomputes
+// the reflector from the pivot column redundantly (identical arithmetic =>
+// identical results).  Columns are never moved during the factorization:
+// every CTA keeps the same position -> column map in shared memory and applies
+// the pivot swap to it locally, and norms are kept per column.  A CTA's
+// candidate for step k+1 depends only on its own updates of step k, so one
+// cluster barrier per step suffices (candidates of k+1 and the updates of k
+// become visible together); the pivot column of step k is written back by its
+// owner after that barrier.  At the end the columns are put in position order
+// through a scratch panel.  Same arithmetic rules as qrcp_kernel above.
 // ---------------------------------------------------------------------------
 constexpr int QC = 16;            // CTAs per cluster (non-portable size, allowed at launch)
 constexpr int QCT = 256;          // threads per CTA
@@ -232,18 +237,24 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     qrcp_cluster_kernel(const QrTask* __restrict__ tasks) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ double v[];  // m
+  extern __shared__ double v[];  // m reflector entries, then c column ids
   __shared__ double red[QCW];
-  __shared__ double cand_v;
-  __shared__ int cand_i;
+  // candidates double-buffered by step parity: a fast CTA publishes step k+1
+  // while a slow one may still read step k
+  __shared__ double cand_v[2];
+  __shared__ int cand_i[2];
   __shared__ double s_amax;
+  __shared__ double wv[QCW];
+  __shared__ int wi[QCW];
   const int q = (int)cluster.block_rank();
   const QrTask T = tasks[blockIdx.x / QC];
   const int m = T.m, c = T.c, kmax = min(m, c);
+  int* col_of = reinterpret_cast<int*>(v + m);  // position -> column
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* N = T.Nm;
   const double eps = DBL_EPSILON;
 
+  for (int j = tid; j < c; j += QCT) col_of[j] = j;
   // initial norms of owned columns, local max |A|
   double amax = 0.0;
   for (int j = q + QC * warp; j < c; j += QC * QCW) {
@@ -257,7 +268,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     amax = fmax(amax, mx);
-    if (lane == 0) { T.nrm2[j] = s; T.ref2[j] = s; T.perm[j] = j; }
+    if (lane == 0) { T.nrm2[j] = s; T.ref2[j] = s; }
   }
   if (lane == 0) red[warp] = amax;
   __syncthreads();
@@ -275,28 +286,18 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
   const double floor_ = eps * fmax(amax, 1.0);
   const double floor2 = floor_ * floor_;
 
-  const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
-  int steps = 0;
-  double r00 = 0.0;
-  int pend_k = -1;       // column whose final values (R_kk, v) this CTA still has to store
-  double pend_r = 0.0;
-  for (int k = 0; k < limit; ++k) {
-    // store the previous step's pivot column (everyone has read it)
-    if (pend_k >= 0) {
-      double* col = N + (long long)pend_k * m;
-      for (int i = pend_k + 1 + tid; i < m; i += QCT) col[i] = v[i - pend_k];
-      if (tid == 0) col[pend_k] = pend_r;
-      pend_k = -1;
-    }
-    // local candidate (first max; or the replayed column)
+  // this CTA's pivot candidate for step k over its positions >= k (first max
+  // by position, or the replayed column)
+  auto local_candidate = [&](int k) {
     const bool rep = T.replay && k < T.nreplay;
     double bv = rep ? 0.0 : -1.0;
     int bi = c;
     for (int j = k + ((q - k) % QC + QC) % QC + QC * tid; j < c; j += QC * QCT) {
+      const int cj = col_of[j];
       if (rep) {
-        if (T.perm[j] == T.replay[k]) { bi = j; bv = 1.0; }
+        if (cj == T.replay[k]) { bv = 1.0; bi = j; }
       } else {
-        const double x = T.nrm2[j];
+        const double x = T.nrm2[cj];
         if (x > bv) { bv = x; bi = j; }
       }
     }
@@ -306,8 +307,6 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    __shared__ double wv[QCW];
-    __shared__ int wi[QCW];
     if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
     __syncthreads();
     if (tid == 0) {
@@ -315,34 +314,48 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
       int i0 = wi[0];
       for (int w = 1; w < QCW; ++w)
         if (wv[w] > b || (wv[w] == b && wi[w] < i0)) { b = wv[w]; i0 = wi[w]; }
-      cand_v = b;
-      cand_i = i0;
+      cand_v[k & 1] = b;
+      cand_i[k & 1] = i0;
     }
-    cluster.sync();  // B1: candidates visible
+  };
+
+  const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
+  int steps = 0;
+  double r00 = 0.0;
+  int pend_col = -1, pend_k = -1;  // pivot column whose final values this CTA still has to store
+  double pend_r = 0.0;
+  __syncthreads();
+  if (limit > 0) local_candidate(0);
+  for (int k = 0; k < limit; ++k) {
+    cluster.sync();  // candidates of k and every update of step k-1 visible
+    // store the previous step's pivot column (everyone has read it)
+    if (pend_col >= 0) {
+      double* col = N + (long long)pend_col * m;
+      for (int i = pend_k + 1 + tid; i < m; i += QCT) col[i] = v[i - pend_k];
+      if (tid == 0) col[pend_k] = pend_r;
+      pend_col = -1;
+    }
     int piv = c;
     {
       double b = -2.0;
       for (int r = 0; r < QC; ++r) {
-        const double ov = *cluster.map_shared_rank(&cand_v, r);
-        const int oi = *cluster.map_shared_rank(&cand_i, r);
+        const double ov = *cluster.map_shared_rank(&cand_v[k & 1], r);
+        const int oi = *cluster.map_shared_rank(&cand_i[k & 1], r);
         if (oi >= c) continue;
         if (ov > b || (ov == b && oi < piv)) { b = ov; piv = oi; }
       }
     }
     if (piv >= c) break;  // malformed replay
-    if (T.nrm2[piv] <= floor2) break;
-    if (piv != k && q == 0) {
-      double* a = N + (long long)k * m;
-      double* b = N + (long long)piv * m;
-      for (int i = tid; i < m; i += QCT) { const double t2 = a[i]; a[i] = b[i]; b[i] = t2; }
-      if (tid == 0) {
-        double t2 = T.nrm2[k]; T.nrm2[k] = T.nrm2[piv]; T.nrm2[piv] = t2;
-        t2 = T.ref2[k]; T.ref2[k] = T.ref2[piv]; T.ref2[piv] = t2;
-        int ti = T.perm[k]; T.perm[k] = T.perm[piv]; T.perm[piv] = ti;
-      }
+    if (T.nrm2[col_of[piv]] <= floor2) break;
+    __syncthreads();  // everyone has read col_of / v of the previous step
+    if (tid == 0 && piv != k) {
+      const int t2 = col_of[k];
+      col_of[k] = col_of[piv];
+      col_of[piv] = t2;
     }
-    cluster.sync();  // B2: pivot column in place
-    const double* xk = N + (long long)k * m;
+    __syncthreads();
+    const int ck = col_of[k];
+    const double* xk = N + (long long)ck * m;
     double ss = 0.0;
     for (int i = k + tid; i < m; i += QCT) ss = fma(xk[i], xk[i], ss);
     const double xn = sqrt(cblock_sum(ss, red));
@@ -357,7 +370,8 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     __syncthreads();
     const int len = m - k;
     for (int j = k + 1 + ((q - k - 1) % QC + QC) % QC + QC * warp; j < c; j += QC * QCW) {
-      double* col = N + (long long)j * m + k;
+      const int cj = col_of[j];
+      double* col = N + (long long)cj * m + k;
       double s = 0.0;
       for (int i = lane; i < len; i += 32) s = fma(v[i], col[i], s);
       s = warp_sum(s);
@@ -371,26 +385,44 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
       fresh = warp_sum(fresh);
       if (lane == 0) {
         const double rkj = col[0];
-        double nn = fmax(T.nrm2[j] - rkj * rkj, 0.0);
-        if (nn <= eps * T.ref2[j]) {
+        double nn = fmax(T.nrm2[cj] - rkj * rkj, 0.0);
+        if (nn <= eps * T.ref2[cj]) {
           nn = fresh;
-          T.ref2[j] = fmax(fresh, floor2);
+          T.ref2[cj] = fmax(fresh, floor2);
         }
-        T.nrm2[j] = nn;
+        T.nrm2[cj] = nn;
       }
     }
     if (k % QC == q) {
+      pend_col = ck;
       pend_k = k;
       pend_r = sgn * xn;
       if (tid == 0) T.tau[k] = tau;
     }
     steps = k + 1;
-    cluster.sync();  // B3: updates and norms visible; column k read by all
+    __syncthreads();  // this CTA's norms of step k written
+    if (k + 1 < limit) local_candidate(k + 1);
   }
-  if (pend_k >= 0) {
-    double* col = N + (long long)pend_k * m;
+  cluster.sync();  // every CTA is done reading the last pivot column
+  if (pend_col >= 0) {
+    double* col = N + (long long)pend_col * m;
     for (int i = pend_k + 1 + tid; i < m; i += QCT) col[i] = v[i - pend_k];
     if (tid == 0) col[pend_k] = pend_r;
+  }
+  cluster.sync();
+  // columns into position order through the scratch panel, permutation out
+  for (int j = q; j < c; j += QC) {
+    const double* src = N + (long long)col_of[j] * m;
+    double* dst = T.tmp + (long long)j * m;
+    for (int i = tid; i < m; i += QCT) dst[i] = src[i];
+  }
+  if (q == 0)
+    for (int j = tid; j < c; j += QCT) T.perm[j] = col_of[j];
+  cluster.sync();
+  for (int j = q; j < c; j += QC) {
+    const double* src = T.tmp + (long long)j * m;
+    double* dst = N + (long long)j * m;
+    for (int i = tid; i < m; i += QCT) dst[i] = src[i];
   }
   if (q == 0 && tid == 0) {
     *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : steps;
@@ -399,9 +431,9 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
   cluster.sync();  // keep every CTA's shared memory alive for remote reads
 }
 
-cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
+cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c) {
   if (ntasks <= 0) return cudaSuccess;
-  size_t smem = (size_t)max_m * sizeof(double);
+  size_t smem = (size_t)max_m * sizeof(double) + (size_t)max_c * sizeof(int);
   static size_t configured = 48 * 1024;
   static bool nonportable = false;
   if (!nonportable) {
