@@ -297,7 +297,8 @@ def run_sgf(args, ws, rank, local):
     mss, work, nl = prof[dom]
     if dom == "gemm":
         achieved = work / (mss * 1e-3) / 1e12
-        roof = {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        roof = {"bound": "tensor", "pipe": "DMMA (FP64 mma.sync; tcgen05 has no f64 kind)", "achieved": achieved,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS,
                 "peak_source": "measured DMMA f64 issue rate (tools/fp64_peak.cu, profiles/fp64_peak_r01.jsonl); "
                                "MEASURED_PEAKS.json has no FP64 figure"}
