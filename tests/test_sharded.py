@@ -84,3 +84,13 @@ def test_sharded_two_ranks_one_gpu():
 def test_sharded_single_rank_matches():
     res = _launch(1, "--mode", "solve", "--backend", "gloo", "--cases", "p3d30_b3")
     _check_solve(res, ["p3d30_b3"])
+
+
+@pytest.mark.gpu
+def test_sharded_three_ranks_uneven():
+    # 8 octants over 3 ranks (3/3/2): uneven ownership, shared blocks summed from three ranks
+    cases = ["p3d30_b3", "aniso26_b3"]
+    res = _launch(3, "--mode", "solve", "--backend", "gloo", "--cases", ",".join(cases))
+    assert res["world"] == 3
+    _check_solve(res, cases)
+    assert all(rk["p3d30_b3"]["local_factors"] > 0 for rk in res["ranks"])
