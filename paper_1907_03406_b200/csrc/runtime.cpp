@@ -263,11 +263,19 @@ static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
   const double f = useful_flops(h, segs, bm);
+  // executed: full bm x bm tiles over the same K ranges (padding included)
+  std::vector<GemmTask> hp(h);
+  for (auto& t : hp) {
+    t.M = t.m0 + bm;
+    t.N = t.n0 + bm;
+  }
+  const double fx = useful_flops(hp, segs, bm);
   long long ksum = 0;
   for (auto& t : h)
     for (int s = 0; s < t.nseg; ++s) ksum += segs[t.seg0 + s].K;
-  fprintf(stderr, "[gemm] %s tiles=%7zu avgK=%7.0f gflop=%9.3f ms=%8.3f tflops=%6.2f\n", big ? "128" : " 64",
-          h.size(), h.empty() ? 0.0 : (double)ksum / h.size(), f / 1e9, ms, f / (ms * 1e-3) / 1e12);
+  fprintf(stderr, "[gemm] %s tiles=%7zu avgK=%7.0f gflop=%9.3f ms=%8.3f tflops=%6.2f executed/useful=%5.2f\n",
+          big ? "128" : " 64", h.size(), h.empty() ? 0.0 : (double)ksum / h.size(), f / 1e9, ms,
+          f / (ms * 1e-3) / 1e12, fx / std::max(f, 1.0));
   cudaEventDestroy(a);
   cudaEventDestroy(b);
 }

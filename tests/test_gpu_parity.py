@@ -218,3 +218,30 @@ def test_spmv_irregular_rows():
     assert np.max(np.abs(y - ref)) <= 1e-13 * max(np.max(np.abs(ref)), 1.0)
     # zero rows give exact zeros
     assert np.all(y[np.diff(A.indptr) == 0] == 0.0)
+
+
+# The reference itself at full BASELINE size (BASELINE.md reference-run table,
+# OPENBLAS_NUM_THREADS=1): PCG iterations and the integer flop tallies, which
+# depend on every rank decision of the run (bit-exact structural gate).
+FULL_REFERENCE = {
+    3: dict(iters=64, flops_factorize=11_678_465_772_587, flops_apply=14_053_267_568, factors=4115),
+    4: dict(iters=49, flops_factorize=11_816_662_185_330, flops_apply=14_116_631_728, factors=4115),
+    5: dict(iters=36, flops_factorize=9_706_710_558_830, flops_apply=7_987_904_404, factors=1647),
+}
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_full_size_config_matches_reference_run(cfg):
+    from paper_1907_03406_b200.problems import CONFIGS, config_rhs
+    c = CONFIGS[cfg]
+    ref = FULL_REFERENCE[cfg]
+    prob = c["make"]()
+    P = sgf.factorize(prob, scheme="nest-2-2", degree=1, b=c["b"], rank_tol=c["rank_tol"])
+    assert P.stats["flops_factorize"] == ref["flops_factorize"]
+    assert P.stats["flops_apply"] == ref["flops_apply"]
+    assert P.stats["factors"] == ref["factors"]
+    rhs = config_rhs(prob.n, c["seed"])
+    x, rep = sgf.pcg(prob.matrix, rhs, precond=P, tol=1e-12)
+    assert rep.converged and abs(rep.iterations - ref["iters"]) <= 1
+    # the returned solution satisfies the tolerance against the host matrix
+    assert np.linalg.norm(rhs - prob.matrix @ x) <= 1.5e-12 * np.linalg.norm(rhs)
