@@ -17,7 +17,8 @@ import numpy as np
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgf.so")
+# SGF_LIB: alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("SGF_LIB") or os.path.join(_HERE, "libsgf.so")
 
 SGF_OK, SGF_NOT_SPD, SGF_SHAPE, SGF_INDEFINITE, SGF_INVALID_ARG, SGF_TRACE, SGF_CUDA, SGF_OOM, SGF_NON_SYMMETRIC = range(9)
 MODE = {"polynomial": 0, "lowrank": 1, "exact": 2}

@@ -116,15 +116,20 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
 // ---------------------------------------------------------------------------
 // Symmetric GEMV from the lower triangle, one CTA per matrix (m <= 64*Q).
 // Warp w takes the row pairs (p, m-1-p), p = w (mod 8): the two rows hold
-// m+1 entries together, so every pair issues the same ~Q+1 16-byte loads per
-// lane at once (lane l reads the column pairs 64q + 2l + {0,1}).  Each stored
-// entry is read once and used twice: G_ij x_j into the row sum of i (warp
-// reduction), G_ij x_i into the warp's column partials of j in shared memory
-// (strictly lower part).  Column partials of the 8 warps are added in fixed
-// order at the end.
+// m+1 entries together, so every pair issues the same Q+1 16-byte loads per
+// lane at once.  Lane l owns the column pairs 64q + 2l + {0,1}; slot s of a
+// pair reads column block q = s of row p, or q = Q-s of row m-1-p (the two
+// ranges never collide), so the column accumulators are indexed at compile
+// time and stay in registers.  Each stored entry is read once and used
+// twice: G_ij x_j into the row sum of i (warp reduction), G_ij x_i into the
+// lane's column sums of j (strictly lower part).  The 8 warps' column sums
+// are added in fixed order through shared memory at the end.
 // ---------------------------------------------------------------------------
+#ifndef SYMV_MINB
+#define SYMV_MINB 2
+#endif
 template <int Q>
-__global__ void __launch_bounds__(256, Q <= 8 ? 4 : 2) symv_kernel(const SymvTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(256, SYMV_MINB) symv_kernel(const SymvTask* __restrict__ tasks) {
   extern __shared__ double sm[];
   constexpr int MP = 64 * Q;
   const SymvTask T = tasks[blockIdx.x];
@@ -132,40 +137,52 @@ __global__ void __launch_bounds__(256, Q <= 8 ? 4 : 2) symv_kernel(const SymvTas
   double* xs = sm;
   double* yr = sm + MP;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* cp = sm + 2 * MP + warp * MP;
   for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
-  for (int i = lane; i < MP; i += 32) cp[i] = 0.0;
   __syncthreads();
+  double c0[Q], c1[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) c0[q] = c1[q] = 0.0;
   const int npairs = (m + 1) / 2;
   for (int p = warp; p < npairs; p += 8) {
     const int ra = p, rb = m - 1 - p;  // rb == ra for the middle row of an odd m
     const int qa = (ra >> 6) + 1, qb = (rb == ra) ? 0 : (rb >> 6) + 1;
+    const double* rowa = T.G + (long long)ra * T.ld;
+    const double* rowb = T.G + (long long)rb * T.ld;
     double2 g[Q + 1];
 #pragma unroll
-    for (int v = 0; v <= Q; ++v) {
-      const bool isa = v < qa;
-      const int q = isa ? v : v - qa;
-      const int row = isa ? ra : rb;
+    for (int s = 0; s <= Q; ++s) {
+      const bool isa = s < qa;
+      const int q = isa ? s : Q - s;
       const int j = 64 * q + 2 * lane;
-      const bool ok = (isa || q < qb) && j <= row;
-      g[v] = ok ? __ldcs(reinterpret_cast<const double2*>(T.G + (long long)row * T.ld + j)) : make_double2(0.0, 0.0);
+      const bool ok = isa ? (j <= ra) : (q < qb && j <= rb);
+      g[s] = ok ? __ldcs(reinterpret_cast<const double2*>((isa ? rowa : rowb) + j)) : make_double2(0.0, 0.0);
     }
     const double xa = xs[ra], xb = xs[rb];
     double sa = 0.0, sb = 0.0;
 #pragma unroll
-    for (int v = 0; v <= Q; ++v) {
-      const bool isa = v < qa;
-      const int q = isa ? v : v - qa;
-      const int row = isa ? ra : rb;
-      const int j = 64 * q + 2 * lane;
-      if (!(isa || q < qb) || j > row) continue;
-      const double g0 = g[v].x, g1 = (j + 1 <= row) ? g[v].y : 0.0;  // G[i][i+1] is not stored
-      const double t = fma(g0, xs[j], g1 * xs[j + 1]);
-      const double xi = isa ? xa : xb;
-      if (isa) sa += t;
-      else sb += t;
-      if (j < row) cp[j] = fma(g0, xi, cp[j]);
-      if (j + 1 < row) cp[j + 1] = fma(g1, xi, cp[j + 1]);
+    for (int s = 0; s <= Q; ++s) {
+      if (s < qa) {
+        if (s < Q) {
+          const int j = 64 * s + 2 * lane;
+          if (j <= ra) {
+            const double g0 = g[s].x, g1 = (j + 1 <= ra) ? g[s].y : 0.0;  // G[i][i+1] is not stored
+            sa = fma(g0, xs[j], fma(g1, xs[j + 1], sa));
+            if (j < ra) c0[s] = fma(g0, xa, c0[s]);
+            if (j + 1 < ra) c1[s] = fma(g1, xa, c1[s]);
+          }
+        }
+      } else if (s >= 1 && Q - s < qb) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int q = Q - s;
+        const int j = 64 * q + 2 * lane;
+        if (j <= rb) {
+          const double g0 = g[s].x, g1 = (j + 1 <= rb) ? g[s].y : 0.0;
+          sb = fma(g0, xs[j], fma(g1, xs[j + 1], sb));
+          if (j < rb) c0[Q - s] = fma(g0, xb, c0[Q - s]);
+          if (j + 1 < rb) c1[Q - s] = fma(g1, xb, c1[Q - s]);
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -176,6 +193,12 @@ __global__ void __launch_bounds__(256, Q <= 8 ? 4 : 2) symv_kernel(const SymvTas
       yr[ra] = sa;
       if (rb != ra) yr[rb] = sb;
     }
+  }
+  double* cp = sm + 2 * MP + warp * MP;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    cp[64 * q + 2 * lane] = c0[q];
+    cp[64 * q + 2 * lane + 1] = c1[q];
   }
   __syncthreads();
   const double* cpa = sm + 2 * MP;
