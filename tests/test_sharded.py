@@ -94,3 +94,11 @@ def test_sharded_three_ranks_uneven():
     assert res["world"] == 3
     _check_solve(res, cases)
     assert all(rk["p3d30_b3"]["local_factors"] > 0 for rk in res["ranks"])
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_backend_single_rank():
+    # the NCCL code path of the collectives (device buffers, library stream
+    # wrapped as the torch stream) with the one GPU this run has
+    res = _launch(1, "--mode", "solve", "--backend", "nccl", "--cases", "p3d30_b3")
+    _check_solve(res, ["p3d30_b3"])
