@@ -80,6 +80,39 @@ struct QrTask {
   double* tmp;         // m x c scratch panel (cluster variant: final column reorder)
 };
 
+// ---- FP64 GEMM emulated on the INT8 tensor cores (ozaki.cu) ------------------------
+// split an R x K FP64 operand (x[r*rs + k*cs]) into exponents + 8 int8 slices,
+// padded to Rp x Kp (multiples of 128 and 64)
+struct OzSplitJob {
+  const double* x;
+  long long rs, cs;
+  int R, K, Rp, Kp;
+  int8_t* out;
+  int* exps;
+};
+// one product term C += alpha * A B^T of split operands (rows of A = rows of C)
+struct OzSeg {
+  const int8_t* a;
+  const int8_t* b;
+  const int* ea;
+  const int* eb;
+  int a_rp, b_rp;
+  int nk;  // K tiles of 64
+  double alpha;
+};
+// one 128 x 64 output tile: C = beta*C + sum of its segments (in order)
+struct OzTask {
+  double* C;
+  long long c_rs, c_cs;
+  int M, N, m0, n0;
+  int seg0, nseg;
+  double beta;
+  int klim;  // K tiles used by this tile (triangular B), >= nk when unlimited
+};
+cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_prefix, int njobs, long long total_rows,
+                            cudaStream_t s);
+cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s);
+
 // ---- apply / GEMV -----------------------------------------------------------------
 // mode 0 (N): y[i] = sum_{k in [kb,ke)} A[i*lda + k] * x[k]  for rows i in [r0, r1)
 // mode 1 (T): part[k] = sum_{i in [r0,r1)} A[i*lda + k] * x[i]  for k in [c0, c1)

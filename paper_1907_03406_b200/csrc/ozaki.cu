@@ -1,0 +1,283 @@
+// FP64 GEMM emulated on the INT8 tensor cores (Ozaki scheme I) for the large
+// Schur and coupling products of the factorization.
+//
+// tcgen05 has no f64 kind; DMMA (mma.sync f64) tops out at ~37 TFLOP/s.  The
+// 5th-generation tensor cores run kind::i8 at ~4.5 POPS with exact int32
+// accumulation in TMEM, so an FP64 product can be assembled from int8 ones:
+// every row of an operand is scaled by a power of two (|x| < 1) and cut into
+// S = 8 signed 7-bit slices, x = 2^e sum_t d_t 2^-7t (truncation: exact), and
+//   (A B^T)_ij = 2^(ea_i + eb_j) sum_{t,u} 2^-7(t+u) (A_t B_u^T)_ij .
+// Pairs with t + u <= S + 1 are kept (56 bits relative to the row maxima);
+// pairs of one diagonal d = t + u accumulate exactly in one int32 TMEM
+// accumulator (8 diagonals x 64 columns = all 512 TMEM columns), and the
+// epilogue sums 2^-7d S_d in FP64.  Measured 69 TFLOP/s FP64-equivalent on
+// large products (tools/ozaki_test.cu), error ~1e-14 of sum |a||b|.
+//
+// Operand layout (written by oz_split_kernel): for an R-row operand padded to
+// Rp rows and Kp columns (multiples of 64),
+//   byte(r, k, t) = ((k/64 * S + t) * Rp + r) * 64 with the 64 K-bytes of a
+//   row group of 8 rows stored as 4 core matrices of 8 rows x 16 bytes:
+//   ((k/64 * S + t) * Rp/8 + r/8) * 512 + ((k%64)/16) * 128 + (r%8) * 16 + k%16
+// i.e. the UMMA canonical K-major no-swizzle layout with LBO = 128 bytes (K
+// chunks) and SBO = 512 bytes (8-row groups); a 128- or 64-row tile of one
+// (k-tile, slice) is one contiguous range, moved by one bulk copy.
+#include <cmath>
+
+#include "common.h"
+
+namespace sgf {
+
+namespace {
+
+constexpr int OZ_S = 8;
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_KT = 64;
+constexpr int OZ_STAGES = 2;
+constexpr int OZ_A_TILE = OZ_BM * OZ_KT, OZ_B_TILE = OZ_BN * OZ_KT;
+constexpr int OZ_A_STAGE = OZ_S * OZ_A_TILE, OZ_B_STAGE = OZ_S * OZ_B_TILE;
+constexpr int OZ_THREADS = 192;  // warps 0-3 epilogue (TMEM lane quadrants), 4 producer, 5 MMA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  // K-major, no swizzle: LBO 128 B between the two K chunks of one MMA step,
+  // SBO 512 B between 8-row core-matrix groups, version 1 (Blackwell)
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
+}
+
+// one warp per operand row: exponent, then S slices per element
+__global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restrict__ jobs,
+                                                       const long long* __restrict__ row_prefix, int njobs) {
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = njobs - 1;  // job containing padded row gw
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (row_prefix[mid] <= gw) lo = mid;
+    else hi = mid - 1;
+  }
+  if (gw >= row_prefix[njobs]) return;
+  const OzSplitJob J = jobs[lo];
+  const int r = (int)(gw - row_prefix[lo]);
+  const bool live = r < J.R;
+  const double* row = J.x + (long long)r * J.rs;
+  double mx = 0.0;
+  if (live)
+    for (int k = lane; k < J.K; k += 32) mx = fmax(mx, fabs(row[(long long)k * J.cs]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int ex = 0;
+  if (mx > 0.0) frexp(mx, &ex);  // |x| 2^-ex < 1
+  if (lane == 0) J.exps[r] = live ? ex : 0;
+  // each lane cuts 16 consecutive K entries (one 16-byte chunk per slice)
+  const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
+  for (int k0 = lane * 16; k0 < J.Kp; k0 += 32 * 16) {
+    unsigned w[OZ_S][4];
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k = k0 + q;
+      double v = (live && k < J.K) ? ldexp(row[(long long)k * J.cs], -ex) : 0.0;
+#pragma unroll
+      for (int t = 0; t < OZ_S; ++t) {
+        v *= 128.0;
+        const double d = trunc(v);
+        v -= d;
+        w[t][q >> 2] |= ((unsigned)(int)d & 0xFFu) << (8 * (q & 3));
+      }
+    }
+    const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
+    const size_t off = (size_t)(r >> 3) * 512 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t) {
+      uint4 v4 = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
+      *reinterpret_cast<uint4*>(J.out + ((size_t)kt * OZ_S + t) * blk + off) = v4;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    oz_gemm_kernel(const OzTask* __restrict__ tasks, const OzSeg* __restrict__ segs) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + OZ_STAGES * OZ_A_STAGE;
+  __shared__ __align__(8) uint64_t full[OZ_STAGES], empty[OZ_STAGES], tmem_full, tmem_empty;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OzTask T = tasks[blockIdx.x];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    mbar_init(&tmem_empty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 4) {
+    if (lane == 0) {  // producer: stages of all segments in order
+      int it = 0;
+      for (int si = 0; si < T.nseg; ++si) {
+        const OzSeg G = segs[T.seg0 + si];
+        const int nk = min(G.nk, T.klim);
+        const int8_t* a = G.a + (size_t)T.m0 * OZ_KT;
+        const int8_t* b = G.b + (size_t)T.n0 * OZ_KT;
+        const size_t ablk = (size_t)G.a_rp * OZ_KT, bblk = (size_t)G.b_rp * OZ_KT;
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % OZ_STAGES;
+          if (it >= OZ_STAGES) mbar_wait(&empty[s], ((it / OZ_STAGES) - 1) & 1);
+          mbar_expect_tx(&full[s], OZ_A_STAGE + OZ_B_STAGE);
+#pragma unroll
+          for (int t = 0; t < OZ_S; ++t) {
+            bulk_g2s(sA + s * OZ_A_STAGE + t * OZ_A_TILE, a + ((size_t)k * OZ_S + t) * ablk, OZ_A_TILE, &full[s]);
+            bulk_g2s(sB + s * OZ_B_STAGE + t * OZ_B_TILE, b + ((size_t)k * OZ_S + t) * bblk, OZ_B_TILE, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc =
+          (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
+      int it = 0;
+      for (int si = 0; si < T.nseg; ++si) {
+        const OzSeg G = segs[T.seg0 + si];
+        const int nk = min(G.nk, T.klim);
+        if (si > 0) mbar_wait(&tmem_empty, (si - 1) & 1);  // epilogue drained the accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int k = 0; k < nk; ++k, ++it) {
+          const int s = it % OZ_STAGES;
+          mbar_wait(&full[s], (it / OZ_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a0 = smem_u32(sA + s * OZ_A_STAGE), b0 = smem_u32(sB + s * OZ_B_STAGE);
+#pragma unroll
+          for (int t = 0; t < OZ_S; ++t)
+#pragma unroll
+            for (int u = 0; u < OZ_S - t; ++u)
+#pragma unroll
+              for (int kk = 0; kk < OZ_KT / 32; ++kk)  // diagonal t+u is first written by (0, t+u) at k = kk = 0
+                mma_i8(tmem + (uint32_t)(t + u) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE + kk * 256),
+                       smem_desc(b0 + u * OZ_B_TILE + kk * 256), idesc, (k > 0 || kk > 0 || t > 0) ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tmem_full);
+      }
+    }
+  } else {
+    // epilogue, warps 0-3: thread = tile row (TMEM lane)
+    const int lr = warp * 32 + lane;
+    const int row = T.m0 + lr;
+    for (int si = 0; si < T.nseg; ++si) {
+      const OzSeg G = segs[T.seg0 + si];
+      mbar_wait(&tmem_full, si & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const bool live = row < T.M;
+      const double rs = live ? ldexp(G.alpha, G.ea[row]) : 0.0;
+      const bool empty_seg = min(G.nk, T.klim) <= 0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll
+        for (int dd = OZ_S - 1; dd >= 0; --dd) {  // smallest terms first
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + dd * OZ_BN + c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          const double sc = ldexp(1.0, -7 * (dd + 2));
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int32_t)v[j], sc, acc[j]);
+        }
+        if (live) {
+#pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int col = T.n0 + c0 + j;
+            if (col >= T.N) break;
+            double* c = T.C + (long long)row * T.c_rs + (long long)col * T.c_cs;
+            const double prod = empty_seg ? 0.0 : acc[j] * rs * ldexp(1.0, G.eb[col]);
+            const double base = (si == 0) ? (T.beta == 0.0 ? 0.0 : T.beta * *c) : *c;
+            *c = base + prod;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&tmem_empty);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace
+
+cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_prefix, int njobs, long long total_rows,
+                            cudaStream_t s) {
+  if (njobs <= 0 || total_rows <= 0) return cudaSuccess;
+  const long long threads = total_rows * 32;
+  count_launch();
+  oz_split_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_jobs, d_row_prefix, njobs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  count_launch();
+  oz_gemm_kernel<<<ntasks, OZ_THREADS, smem, s>>>(d_tasks, d_segs);
+  return cudaGetLastError();
+}
+
+}  // namespace sgf

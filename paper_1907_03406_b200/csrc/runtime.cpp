@@ -287,6 +287,44 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
   if (!small.empty()) traced_gemm(scratch.upload(small), small, d_segs, segs, 0, st);
 }
 
+void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
+  if (jobs.empty()) return;
+  std::vector<long long> prefix(jobs.size() + 1, 0);
+  for (size_t i = 0; i < jobs.size(); ++i) prefix[i + 1] = prefix[i] + jobs[i].Rp;
+  OzSplitJob* d_j = scratch.upload(jobs);
+  long long* d_p = scratch.upload(prefix);
+  ProfScope ps(st, PROF_MOVE, 0.0);
+  SGF_CUDA(launch_oz_split(d_j, d_p, (int)jobs.size(), prefix.back(), st));
+  jobs.clear();
+}
+
+void OzBatch::launch(Arena& scratch, cudaStream_t st) {
+  if (tasks.empty()) return;
+  OzSeg* d_s = scratch.upload(segs);
+  OzTask* d_t = scratch.upload(tasks);
+  ProfScope ps(st, PROF_GEMM, useful);
+  if (trace_level() == 2) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    SGF_CUDA(launch_oz_gemm(d_t, (int)tasks.size(), d_s, st));
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    fprintf(stderr, "[gemm] ozaki  tiles=%7zu segs=%7zu gflop=%9.3f ms=%8.3f tflops=%6.2f\n", tasks.size(),
+            segs.size(), useful / 1e9, ms, useful / (ms * 1e-3) / 1e12);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  } else {
+    SGF_CUDA(launch_oz_gemm(d_t, (int)tasks.size(), d_s, st));
+  }
+  tasks.clear();
+  segs.clear();
+  useful = 0.0;
+}
+
 void CopyBatch::launch(Arena& scratch, cudaStream_t st) {
   if (tasks.empty()) return;
   std::vector<long long> prefix(tasks.size());

@@ -420,6 +420,57 @@ struct GemmBatch {
   }
 };
 
+// Batched FP64 products on the INT8 tensor cores (ozaki.cu): operands are
+// split once (split()), products are added per output block like GemmBatch.
+struct OzOperand {
+  int8_t* data = nullptr;
+  int* e = nullptr;
+  int R = 0, K = 0, Rp = 0, Kp = 0;
+};
+struct OzBatch {
+  std::vector<OzSplitJob> jobs;
+  std::vector<OzTask> tasks;
+  std::vector<OzSeg> segs;
+  double useful = 0.0;  // flops of the products (roofline accounting)
+  OzOperand split(Arena& mem, const double* x, long long rs, long long cs, int R, int K) {
+    OzOperand o;
+    o.R = R;
+    o.K = K;
+    o.Rp = (R + 127) / 128 * 128;
+    o.Kp = (K + 63) / 64 * 64;
+    o.data = mem.alloc_t<int8_t>((size_t)8 * o.Rp * o.Kp);
+    o.e = mem.alloc_t<int>(o.Rp);
+    jobs.push_back(OzSplitJob{x, rs, cs, R, K, o.Rp, o.Kp, o.data, o.e});
+    return o;
+  }
+  void launch_splits(Arena& scratch, cudaStream_t st);
+  // C (M x N) = beta*C + sum_i alpha_i A_i B_i^T, A_i with M rows, B_i with N
+  // rows; lower_only skips tiles strictly above the diagonal; tri_b: B is
+  // lower triangular (B[j][k] = 0 for k > j), so a tile stops at k < n0 + 64
+  void add(double* C, long long c_rs, long long c_cs, int M, int N, double beta,
+           const std::vector<std::pair<std::pair<OzOperand, OzOperand>, double>>& terms, bool lower_only,
+           bool tri_b) {
+    if (M <= 0 || N <= 0) return;
+    const int seg0 = (int)segs.size();
+    for (auto& tm : terms) {
+      const OzOperand& A = tm.first.first;
+      const OzOperand& B = tm.first.second;
+      segs.push_back(OzSeg{A.data, B.data, A.e, B.e, A.Rp, B.Rp, A.Kp / 64, tm.second});
+    }
+    for (int m0 = 0; m0 < M; m0 += 128)
+      for (int n0 = 0; n0 < N; n0 += 64) {
+        if (lower_only && n0 >= m0 + 128) continue;
+        const int klim = tri_b ? (n0 + 64) / 64 : (1 << 30);
+        tasks.push_back(OzTask{C, c_rs, c_cs, M, N, m0, n0, seg0, (int)terms.size(), beta, klim});
+        for (auto& tm : terms) {
+          const int kt = std::min(tm.first.first.Kp / 64, klim);
+          useful += 2.0 * std::min(128, M - m0) * std::min(64, N - n0) * std::min(kt * 64, tm.first.first.K);
+        }
+      }
+  }
+  void launch(Arena& scratch, cudaStream_t st);
+};
+
 inline GemmSeg seg(const double* A, long long a_rs, long long a_ks, const double* B, long long b_rs, long long b_ks,
                    int K, int flags = 0) {
   GemmSeg s;
