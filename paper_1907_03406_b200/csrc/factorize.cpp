@@ -65,6 +65,7 @@ struct State {
   std::vector<int> node_rank;  // per node of the current level: owning rank, -1 = top separator
   std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
   bool l1_sym = true;          // level-1 apply through G = A_BB^{-1} and the sparse couplings
+  int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
@@ -555,16 +556,33 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     gg.launch(S.scratch, st);
   }
   HostTimer hte("elim E gemm");
+  // Large nodes take the FP64 products on the INT8 tensor cores (ozaki.cu):
+  // E = A_NB X^T (X lower triangular) and the Schur updates E_a E_b^T, with
+  // every operand split once.  Small nodes keep the DMMA GEMM.
+  int maxm = 0;
+  for (size_t qi = 0; qi < info.size(); ++qi)
+    if (own[qi]) maxm = std::max(maxm, info[qi].m);
+  // (int32 accumulators hold 8 pairs x K x 127^2 exactly for K < 16.6k)
+  const bool use_oz = S.oz_min_m > 0 && maxm >= S.oz_min_m && maxm <= 16000;
+  OzBatch oz;
+  std::vector<std::vector<OzOperand>> eop(use_oz ? info.size() : 0);
   GemmBatch ge;
   for (size_t qi = 0; qi < info.size(); ++qi) {
     const EI& e = info[qi];
     long long f = (long long)e.m * e.m * e.m / 3;
+    OzOperand xop;
+    if (use_oz && own[qi]) xop = oz.split(S.scratch, e.X, e.ld, 1, e.m, e.m);
     for (size_t q = 0; q < e.nb.size(); ++q) {
       const int rows = M.size[e.nb[q]];
       if (own[qi]) {
         View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
-        ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
-               {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
+        if (use_oz) {
+          OzOperand aop = oz.split(S.scratch, v.p, v.rs, v.cs, v.rows, e.m);
+          oz.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 0.0, {{{aop, xop}, 1.0}}, false, true);
+        } else {
+          ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
+                 {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
+        }
       }
       f += (long long)e.m * e.m * rows;
     }
@@ -573,6 +591,18 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     S.flops += f;
   }
   ge.launch(S.scratch, st);
+  if (use_oz) {
+    oz.launch_splits(S.scratch, st);
+    oz.launch(S.scratch, st);
+    // the couplings as Schur operands, one split per neighbour block
+    for (size_t qi = 0; qi < info.size(); ++qi) {
+      if (!own[qi]) continue;
+      const EI& e = info[qi];
+      for (size_t q = 0; q < e.nb.size(); ++q)
+        eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m));
+    }
+    oz.launch_splits(S.scratch, st);
+  }
 
   // Schur targets in the reference's insertion order (ascending interior id,
   // neighbour pairs a <= b); a target first seen without a block is a fill,
@@ -643,10 +673,17 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
       // diagonal blocks are kept valid in their lower triangle only: every
       // consumer (Cholesky of the node, densify + Cholesky) reads only that
-      gs.add(bp, bc, 1, br, bc, -1.0, 1.0, sg, -1, T.a == T.b);
+      if (use_oz) {
+        std::vector<std::pair<std::pair<OzOperand, OzOperand>, double>> terms;
+        for (auto& c : T.contrib) terms.push_back({{eop[c.first][c.second.first], eop[c.first][c.second.second]}, -1.0});
+        oz.add(bp, bc, 1, br, bc, 1.0, terms, T.a == T.b, false);
+      } else {
+        gs.add(bp, bc, 1, br, bc, -1.0, 1.0, sg, -1, T.a == T.b);
+      }
     }
     HostTimer ht2("schur launch");
     gs.launch(S.scratch, st);
+    oz.launch(S.scratch, st);
   }
   {
     HostTimer ht("elim bookkeeping");
@@ -1363,6 +1400,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.P = P.get();
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
   S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
+  if (getenv("SGF_OZAKI_MIN_M")) S.oz_min_m = atoi(getenv("SGF_OZAKI_MIN_M"));
   PlanWorker planner(P.get());  // destroyed (joined) before P and S
   if (a.shard_count > 1) {
     if (!a.cell_rank || !a.exchange || a.shard_rank < 0 || a.shard_rank >= a.shard_count || a.shard_stop_level < 1)
