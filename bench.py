@@ -35,6 +35,8 @@ sys.path.insert(0, ROOT)
 
 CFG = 4
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA issue rate on this pool's B200 (profiles/fp64_peak_r01.jsonl)
+INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 tensor peak (nominal; MEASURED_PEAKS.json has no INT8 figure)
+INT8_PEAK_SOURCE = "nominal B200 dense INT8 (4.5 POPS); MEASURED_PEAKS.json has no INT8 figure"
 SURVEY_REF_FULL_S = 682.4 + 270.4  # reference at full cfg4 size, 1 BLAS thread
 CPU_SAMPLE_N = 40                  # bounded CPU sample: the same operator on a 40^3 grid
 
@@ -295,7 +297,14 @@ def run_sgf(args, ws, rank, local):
     pk, pk_kind = peaks()
     dom = max(prof, key=lambda k: prof[k][0])
     mss, work, nl = prof[dom]
-    if dom == "gemm":
+    if dom == "gemm_int8emu":
+        # FP64 products on the INT8 tensor cores: 36 int8 slice products per
+        # FP64 product (ozaki.cu); achieved/peak in INT8 tensor ops
+        achieved = 36.0 * work / (mss * 1e-3) / 1e12
+        roof = {"bound": "tensor", "pipe": "tcgen05 kind::i8 (FP64 emulated, 8 slices)", "achieved": achieved,
+                "peak": INT8_PEAK_TOPS, "unit": "TOPS", "frac": achieved / INT8_PEAK_TOPS,
+                "fp64_equivalent_tflops": work / (mss * 1e-3) / 1e12, "peak_source": INT8_PEAK_SOURCE}
+    elif dom == "gemm":
         achieved = work / (mss * 1e-3) / 1e12
         roof = {"bound": "tensor", "pipe": "DMMA (FP64 mma.sync; tcgen05 has no f64 kind)", "achieved": achieved,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -315,6 +324,8 @@ def run_sgf(args, ws, rank, local):
         "t_factor_s": tF, "t_solve_s": tS, "pcg_iterations": rep.iterations,
         "reference_pcg_iterations": 49, "final_rel_residual": rep.final_rel_residual, "check_residual": resid,
         "gemm_tflops": prof["gemm"][1] / max(prof["gemm"][0], 1e-9) / 1e9,
+        "int8emu_fp64_tflops": prof["gemm_int8emu"][1] / max(prof["gemm_int8emu"][0], 1e-9) / 1e9,
+        "int8emu_ms": prof["gemm_int8emu"][0], "int8emu_split_ms": prof["int8emu_split"][0],
         "apply_gemv_gbs": gemv[1] / max(gemv[0], 1e-9) / 1e6, "spmv_gbs": spmv[1] / max(spmv[0], 1e-9) / 1e6,
     }
 

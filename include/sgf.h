@@ -182,9 +182,11 @@ int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const do
                int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
 
 /* instrumentation (no reference counterpart): kernels launched so far, and
-   per-kernel-class CUDA-event timing.  Classes: 0 GEMM (work = flops),
+   per-kernel-class CUDA-event timing.  Classes: 0 GEMM on DMMA (work = flops),
    1 GEMV (bytes), 2 SpMV (bytes), 3 QR, 4 diagonal Cholesky, 5 copies (bytes),
-   6 vector ops.  out[3*cls + 0..2] = milliseconds, work, launches. */
+   6 vector ops, 7 FP64 products on the INT8 tensor cores (FP64 flops),
+   8 their operand splits (bytes).  out[3*cls + 0..2] = milliseconds, work,
+   launches. */
 uint64_t sgf_kernel_launches(void);
 int sgf_profile_enable(int on);
 int sgf_profile_read(double* out, int cap);

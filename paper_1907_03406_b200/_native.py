@@ -34,7 +34,7 @@ EXPORTS = (
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read",
 )
-PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec")
+PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec", "gemm_int8emu", "int8emu_split")
 
 
 class NativeUnavailable(RuntimeError):

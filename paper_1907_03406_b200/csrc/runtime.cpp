@@ -293,7 +293,10 @@ void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   for (size_t i = 0; i < jobs.size(); ++i) prefix[i + 1] = prefix[i] + jobs[i].Rp;
   OzSplitJob* d_j = scratch.upload(jobs);
   long long* d_p = scratch.upload(prefix);
-  ProfScope ps(st, PROF_MOVE, 0.0);
+  double bytes = 0.0;  // FP64 read + 8 slices written per element
+  if (g_prof.on)
+    for (auto& j : jobs) bytes += 16.0 * j.Rp * j.Kp;
+  ProfScope ps(st, PROF_OZSPLIT, bytes);
   SGF_CUDA(launch_oz_split(d_j, d_p, (int)jobs.size(), prefix.back(), st));
   jobs.clear();
 }
@@ -302,7 +305,7 @@ void OzBatch::launch(Arena& scratch, cudaStream_t st) {
   if (tasks.empty()) return;
   OzSeg* d_s = scratch.upload(segs);
   OzTask* d_t = scratch.upload(tasks);
-  ProfScope ps(st, PROF_GEMM, useful);
+  ProfScope ps(st, PROF_OZ, useful);
   if (trace_level() == 2) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);

@@ -65,7 +65,7 @@ cudaError_t launch_p_update(double* p, const double* z, long long n, const doubl
 // (bench.py's roofline numbers).  Classes: see PROF_* below.
 // ---------------------------------------------------------------------------
 enum { PROF_GEMM = 0, PROF_GEMV = 1, PROF_SPMV = 2, PROF_QR = 3, PROF_CHOL = 4, PROF_MOVE = 5, PROF_VEC = 6,
-       PROF_NCLS = 7 };
+       PROF_OZ = 7, PROF_OZSPLIT = 8, PROF_NCLS = 9 };
 struct Profiler {
   bool on = false;
   struct Rec { int cls; cudaEvent_t a, b; double work; long long launches; };
