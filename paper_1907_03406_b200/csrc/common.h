@@ -82,7 +82,7 @@ struct QrTask {
 
 // ---- FP64 GEMM emulated on the INT8 tensor cores (ozaki.cu) ------------------------
 // split an R x K FP64 operand (x[r*rs + k*cs]) into exponents + 8 int8 slices,
-// padded to Rp x Kp (multiples of 128 and 64)
+// padded to Rp x Kp (multiples of 128 and 32)
 struct OzSplitJob {
   const double* x;
   long long rs, cs;
@@ -97,10 +97,10 @@ struct OzSeg {
   const int* ea;
   const int* eb;
   int a_rp, b_rp;
-  int nk;  // K tiles of 64
+  int nk;  // K tiles of 32
   double alpha;
 };
-// one 128 x 64 output tile: C = beta*C + sum of its segments (in order)
+// one 128 x 128 output tile: C = beta*C + sum of its segments (in order)
 struct OzTask {
   double* C;
   long long c_rs, c_cs;

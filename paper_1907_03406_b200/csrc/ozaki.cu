@@ -9,18 +9,21 @@
 //   (A B^T)_ij = 2^(ea_i + eb_j) sum_{t,u} 2^-7(t+u) (A_t B_u^T)_ij .
 // Pairs with t + u <= S + 1 are kept (56 bits relative to the row maxima);
 // pairs of one diagonal d = t + u accumulate exactly in one int32 TMEM
-// accumulator (8 diagonals x 64 columns = all 512 TMEM columns), and the
-// epilogue sums 2^-7d S_d in FP64.  Measured 69 TFLOP/s FP64-equivalent on
-// large products (tools/ozaki_test.cu), error ~1e-14 of sum |a||b|.
+// accumulator.  The MMA shape is M=128, N=128 (tools/i8_peak.cu: N=64 issues
+// at only 61% of the 4.5 POPS reached from N=128 on), so the 8 diagonals
+// x 128 columns do not fit the 512 TMEM columns at once: a product runs in two
+// passes over K, diagonals d = 2..5 (slices 1..4 only) then d = 6..9, each
+// pass draining its 4 accumulators into the FP64 output.  The epilogue sums
+// 2^-7d S_d in FP64.  Error ~1e-14 of sum |a||b| (tools/ozaki_test.cu,
+// tools/oz_batch_test.cu).
 //
 // Operand layout (written by oz_split_kernel): for an R-row operand padded to
-// Rp rows and Kp columns (multiples of 64),
-//   byte(r, k, t) = ((k/64 * S + t) * Rp + r) * 64 with the 64 K-bytes of a
-//   row group of 8 rows stored as 4 core matrices of 8 rows x 16 bytes:
-//   ((k/64 * S + t) * Rp/8 + r/8) * 512 + ((k%64)/16) * 128 + (r%8) * 16 + k%16
-// i.e. the UMMA canonical K-major no-swizzle layout with LBO = 128 bytes (K
-// chunks) and SBO = 512 bytes (8-row groups); a 128- or 64-row tile of one
-// (k-tile, slice) is one contiguous range, moved by one bulk copy.
+// Rp rows (multiple of 128) and Kp columns (multiple of 32),
+//   byte(r, k, t) = ((k/32 * S + t) * Rp/8 + r/8) * 256 + ((k%32)/16) * 128 + (r%8) * 16 + k%16
+// i.e. the UMMA canonical K-major no-swizzle layout with LBO = 128 bytes (the
+// two K chunks of one K=32 MMA) and SBO = 256 bytes (8-row groups); the 128
+// rows of a tile of one (k-tile, slice) are one contiguous 4 KB range, moved
+// by one bulk copy.
 #include <cmath>
 
 #include "common.h"
@@ -30,11 +33,23 @@ namespace sgf {
 namespace {
 
 constexpr int OZ_S = 8;
-constexpr int OZ_BM = 128, OZ_BN = 64, OZ_KT = 64;
-constexpr int OZ_STAGES = 2;
+constexpr int OZ_BM = 128, OZ_BN = 128, OZ_KT = 32;
+constexpr int OZ_STAGES = 3;
 constexpr int OZ_A_TILE = OZ_BM * OZ_KT, OZ_B_TILE = OZ_BN * OZ_KT;
 constexpr int OZ_A_STAGE = OZ_S * OZ_A_TILE, OZ_B_STAGE = OZ_S * OZ_B_TILE;
+constexpr int OZ_H = OZ_S / 2;  // diagonals (and, in pass 0, slices) per pass
 constexpr int OZ_THREADS = 192;  // warps 0-3 epilogue (TMEM lane quadrants), 4 producer, 5 MMA
+
+#ifdef OZ_PROFILE
+// cycles: [0] MMA waiting for operands, [1] MMA waiting for the epilogue,
+// [2] MMA issuing, [3] epilogue draining, [4] epilogue waiting for the MMA
+__device__ unsigned long long oz_prof[8];
+#define OZ_T0() const long long _t0 = clock64()
+#define OZ_ACC(i) atomicAdd(&oz_prof[i], (unsigned long long)(clock64() - _t0))
+#else
+#define OZ_T0()
+#define OZ_ACC(i)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
@@ -62,8 +77,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   // K-major, no swizzle: LBO 128 B between the two K chunks of one MMA step,
-  // SBO 512 B between 8-row core-matrix groups, version 1 (Blackwell)
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+  // SBO 256 B between 8-row core-matrix groups, version 1 (Blackwell)
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
          ((uint64_t)1 << 46);
 }
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -120,7 +135,7 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
       }
     }
     const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
-    const size_t off = (size_t)(r >> 3) * 512 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
+    const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
 #pragma unroll
     for (int t = 0; t < OZ_S; ++t) {
       uint4 v4 = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
@@ -165,14 +180,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int8_t* a = G.a + (size_t)T.m0 * OZ_KT;
         const int8_t* b = G.b + (size_t)T.n0 * OZ_KT;
         const size_t ablk = (size_t)G.a_rp * OZ_KT, bblk = (size_t)G.b_rp * OZ_KT;
-        for (int k = 0; k < nk; ++k, ++it) {
-          const int s = it % OZ_STAGES;
-          if (it >= OZ_STAGES) mbar_wait(&empty[s], ((it / OZ_STAGES) - 1) & 1);
-          mbar_expect_tx(&full[s], OZ_A_STAGE + OZ_B_STAGE);
-#pragma unroll
-          for (int t = 0; t < OZ_S; ++t) {
-            bulk_g2s(sA + s * OZ_A_STAGE + t * OZ_A_TILE, a + ((size_t)k * OZ_S + t) * ablk, OZ_A_TILE, &full[s]);
-            bulk_g2s(sB + s * OZ_B_STAGE + t * OZ_B_TILE, b + ((size_t)k * OZ_S + t) * bblk, OZ_B_TILE, &full[s]);
+        for (int pass = 0; pass < 2; ++pass) {
+          const int ns = pass == 0 ? OZ_H : OZ_S;  // slices used by the pass
+          for (int k = 0; k < nk; ++k, ++it) {
+            const int s = it % OZ_STAGES;
+            if (it >= OZ_STAGES) mbar_wait(&empty[s], ((it / OZ_STAGES) - 1) & 1);
+            mbar_expect_tx(&full[s], (uint32_t)ns * (OZ_A_TILE + OZ_B_TILE));
+            for (int t = 0; t < ns; ++t) {
+              bulk_g2s(sA + s * OZ_A_STAGE + t * OZ_A_TILE, a + ((size_t)k * OZ_S + t) * ablk, OZ_A_TILE, &full[s]);
+              bulk_g2s(sB + s * OZ_B_STAGE + t * OZ_B_TILE, b + ((size_t)k * OZ_S + t) * bblk, OZ_B_TILE, &full[s]);
+            }
           }
         }
       }
@@ -181,73 +198,126 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
-      int it = 0;
+      int it = 0, drains = 0;
       for (int si = 0; si < T.nseg; ++si) {
         const OzSeg G = segs[T.seg0 + si];
         const int nk = min(G.nk, T.klim);
-        if (si > 0) mbar_wait(&tmem_empty, (si - 1) & 1);  // epilogue drained the accumulators
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        for (int k = 0; k < nk; ++k, ++it) {
-          const int s = it % OZ_STAGES;
-          mbar_wait(&full[s], (it / OZ_STAGES) & 1);
+        for (int pass = 0; pass < 2; ++pass, ++drains) {
+          if (drains > 0) {
+            OZ_T0();
+            mbar_wait(&tmem_empty, (drains - 1) & 1);  // epilogue drained the accumulators
+            OZ_ACC(1);
+          }
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a0 = smem_u32(sA + s * OZ_A_STAGE), b0 = smem_u32(sB + s * OZ_B_STAGE);
+          for (int k = 0; k < nk; ++k, ++it) {
+            const int s = it % OZ_STAGES;
+            {
+              OZ_T0();
+              mbar_wait(&full[s], (it / OZ_STAGES) & 1);
+              OZ_ACC(0);
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t a0 = smem_u32(sA + s * OZ_A_STAGE), b0 = smem_u32(sB + s * OZ_B_STAGE);
+            OZ_T0();
+            if (pass == 0) {
+              // diagonals 0..3 (slice pairs t + u <= 3); (0, d) writes diagonal d first
 #pragma unroll
-          for (int t = 0; t < OZ_S; ++t)
+              for (int t = 0; t < OZ_H; ++t)
 #pragma unroll
-            for (int u = 0; u < OZ_S - t; ++u)
+                for (int u = 0; u < OZ_H - t; ++u)
+                  mma_i8(tmem + (uint32_t)(t + u) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE),
+                         smem_desc(b0 + u * OZ_B_TILE), idesc, (k > 0 || t > 0) ? 1u : 0u);
+            } else {
+              // diagonals 4..7; (t, 7 - t... ) ordering: for t ascending the first
+              // pair of diagonal d is (max(0, d-7), ...) -> track the first write
 #pragma unroll
-              for (int kk = 0; kk < OZ_KT / 32; ++kk)  // diagonal t+u is first written by (0, t+u) at k = kk = 0
-                mma_i8(tmem + (uint32_t)(t + u) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE + kk * 256),
-                       smem_desc(b0 + u * OZ_B_TILE + kk * 256), idesc, (k > 0 || kk > 0 || t > 0) ? 1u : 0u);
-          mma_commit(&empty[s]);
+              for (int t = 0; t < OZ_S; ++t)
+#pragma unroll
+                for (int u = 0; u < OZ_S - t; ++u) {
+                  const int d = t + u;
+                  if (d < OZ_H) continue;
+                  const bool first = (k == 0) && (t == (d > OZ_S - 1 ? d - (OZ_S - 1) : 0));
+                  mma_i8(tmem + (uint32_t)(d - OZ_H) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE),
+                         smem_desc(b0 + u * OZ_B_TILE), idesc, first ? 0u : 1u);
+                }
+            }
+            mma_commit(&empty[s]);
+            OZ_ACC(2);
+          }
+          mma_commit(&tmem_full);
         }
-        mma_commit(&tmem_full);
       }
     }
   } else {
     // epilogue, warps 0-3: thread = tile row (TMEM lane)
     const int lr = warp * 32 + lane;
     const int row = T.m0 + lr;
+    // staging tile of this warp: 32 rows x 32 columns (+1 pad), so the C
+    // read-modify-write runs row by row with the 32 lanes on 32 consecutive
+    // columns (coalesced) instead of one row per thread
+    double* stg = reinterpret_cast<double*>(smem + OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE)) + warp * 32 * 33;
+    int drains = 0;
     for (int si = 0; si < T.nseg; ++si) {
       const OzSeg G = segs[T.seg0 + si];
-      mbar_wait(&tmem_full, si & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
       const bool live = row < T.M;
       const double rs = live ? ldexp(G.alpha, G.ea[row]) : 0.0;
       const bool empty_seg = min(G.nk, T.klim) <= 0;
+      for (int pass = 0; pass < 2; ++pass, ++drains) {
+        {
+          OZ_T0();
+          mbar_wait(&tmem_full, drains & 1);
+          if (threadIdx.x == 0) OZ_ACC(4);
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        OZ_T0();
+        const bool first = (si == 0 && pass == 0);
 #pragma unroll 1
-      for (int c0 = 0; c0 < OZ_BN; c0 += 16) {
-        double acc[16];
+        for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
+          double acc[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+          for (int j = 0; j < 32; ++j) acc[j] = 0.0;
 #pragma unroll
-        for (int dd = OZ_S - 1; dd >= 0; --dd) {  // smallest terms first
-          uint32_t v[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + dd * OZ_BN + c0));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-          const double sc = ldexp(1.0, -7 * (dd + 2));
+          for (int dd = OZ_H - 1; dd >= 0; --dd) {  // smallest terms first
+            const double sc = ldexp(1.0, -7 * (dd + pass * OZ_H + 2));
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int32_t)v[j], sc, acc[j]);
-        }
-        if (live) {
-#pragma unroll 4
-          for (int j = 0; j < 16; ++j) {
-            const int col = T.n0 + c0 + j;
-            if (col >= T.N) break;
-            double* c = T.C + (long long)row * T.c_rs + (long long)col * T.c_cs;
-            const double prod = empty_seg ? 0.0 : acc[j] * rs * ldexp(1.0, G.eb[col]);
-            const double base = (si == 0) ? (T.beta == 0.0 ? 0.0 : T.beta * *c) : *c;
-            *c = base + prod;
+            for (int h = 0; h < 2; ++h) {
+              uint32_t v[16];
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                  "[%16];"
+                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                    "=r"(v[15])
+                  : "r"(tmem + ((uint32_t)(warp * 32) << 16) + dd * OZ_BN + c0 + 16 * h));
+              asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[16 * h + j] = fma((double)(int32_t)v[j], sc, acc[16 * h + j]);
+            }
           }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = acc[j] * rs;
+          __syncwarp();
+          const int col = T.n0 + c0 + lane;
+          const bool cok = col < T.N && !empty_seg;
+          const double cs = cok ? ldexp(1.0, G.eb[col]) : 0.0;
+          // all loads of the 32 rows first (independent), then the stores
+          const int nrow = min(32, T.M - (T.m0 + warp * 32));
+          double* cbase = T.C + (long long)(T.m0 + warp * 32) * T.c_rs + (long long)col * T.c_cs;
+          const bool need_c = !(first && T.beta == 0.0);
+          double cv[32];
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr)
+            cv[rr] = (need_c && rr < nrow && col < T.N) ? __ldcg(cbase + (long long)rr * T.c_rs) : 0.0;
+          const double bscale = first ? T.beta : 1.0;
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr)
+            if (rr < nrow && col < T.N) cbase[(long long)rr * T.c_rs] = fma(bscale, cv[rr], stg[rr * 33 + lane] * cs);
+          __syncwarp();
         }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(&tmem_empty);
+        if (threadIdx.x == 0) OZ_ACC(3);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&tmem_empty);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -256,6 +326,17 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 }  // namespace
+
+#ifdef OZ_PROFILE
+extern "C" int sgf_oz_prof_read(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, oz_prof, sizeof(oz_prof));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(oz_prof, z, sizeof(z));
+  }
+  return e == cudaSuccess ? 0 : 1;
+}
+#endif
 
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_prefix, int njobs, long long total_rows,
                             cudaStream_t s) {
@@ -268,7 +349,7 @@ cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_pre
 
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE);
+  const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE) + 4 * 32 * 33 * sizeof(double);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -437,7 +437,7 @@ struct OzBatch {
     o.R = R;
     o.K = K;
     o.Rp = (R + 127) / 128 * 128;
-    o.Kp = (K + 63) / 64 * 64;
+    o.Kp = (K + 31) / 32 * 32;
     o.data = mem.alloc_t<int8_t>((size_t)8 * o.Rp * o.Kp);
     o.e = mem.alloc_t<int>(o.Rp);
     jobs.push_back(OzSplitJob{x, rs, cs, R, K, o.Rp, o.Kp, o.data, o.e});
@@ -455,16 +455,16 @@ struct OzBatch {
     for (auto& tm : terms) {
       const OzOperand& A = tm.first.first;
       const OzOperand& B = tm.first.second;
-      segs.push_back(OzSeg{A.data, B.data, A.e, B.e, A.Rp, B.Rp, A.Kp / 64, tm.second});
+      segs.push_back(OzSeg{A.data, B.data, A.e, B.e, A.Rp, B.Rp, A.Kp / 32, tm.second});
     }
     for (int m0 = 0; m0 < M; m0 += 128)
-      for (int n0 = 0; n0 < N; n0 += 64) {
+      for (int n0 = 0; n0 < N; n0 += 128) {
         if (lower_only && n0 >= m0 + 128) continue;
-        const int klim = tri_b ? (n0 + 64) / 64 : (1 << 30);
+        const int klim = tri_b ? (n0 + 128) / 32 : (1 << 30);
         tasks.push_back(OzTask{C, c_rs, c_cs, M, N, m0, n0, seg0, (int)terms.size(), beta, klim});
         for (auto& tm : terms) {
-          const int kt = std::min(tm.first.first.Kp / 64, klim);
-          useful += 2.0 * std::min(128, M - m0) * std::min(64, N - n0) * std::min(kt * 64, tm.first.first.K);
+          const int kt = std::min(tm.first.first.Kp / 32, klim);
+          useful += 2.0 * std::min(128, M - m0) * std::min(128, N - n0) * std::min(kt * 32, tm.first.first.K);
         }
       }
   }

@@ -12,6 +12,9 @@
 
 using namespace sgf;
 
+// present only in the OZ_PROFILE build of libsgf.so
+extern "C" int sgf_oz_prof_read(unsigned long long* out, int reset) __attribute__((weak));
+
 static std::mt19937_64 rng(7);
 
 static std::vector<double> rnd(size_t n, double spread) {
@@ -69,7 +72,7 @@ int main() {
     double worst = 0.0;
     for (int i = 0; i < M; ++i)
       for (int j = 0; j < N; ++j) {
-        if (c.lower && (j / 64) * 64 >= (i / 128) * 128 + 128) continue;  // tiles above the diagonal are skipped
+        if (c.lower && (j / 128) * 128 >= (i / 128) * 128 + 128) continue;  // tiles above the diagonal are skipped
         long double s = C0[(size_t)i * N + j], sa = std::fabs(C0[(size_t)i * N + j]);
         double ma = 0, mb = 0;  // the scheme's error scale: K * max|A_i| * max|B_j| * 2^-56
         for (int k = 0; k < K; ++k) {
@@ -94,6 +97,41 @@ int main() {
     fails += !ok;
     printf("{\"M\":%d,\"N\":%d,\"K\":%d,\"transA\":%d,\"lower\":%d,\"tri\":%d,\"two\":%d,\"max_err\":%.3e,\"ok\":%d}\n",
            M, N, K, c.transA, c.lower, c.tri, c.two, worst, ok);
+  }
+  // timing: a Schur-like batch (two products per tile, K = 1664)
+  {
+    const int M = 4096, N = 4096, K = 1664;
+    auto A1 = rnd((size_t)M * K, 1.0), B1 = rnd((size_t)N * K, 1.0);
+    double* dA = mem.alloc(A1.size());
+    double* dB = mem.alloc(B1.size());
+    double* dC = mem.alloc((size_t)M * N);
+    cudaMemcpy(dA, A1.data(), A1.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, B1.data(), B1.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemset(dC, 0, (size_t)M * N * 8);
+    OzBatch oz;
+    OzOperand a = oz.split(mem, dA, K, 1, M, K), b = oz.split(mem, dB, K, 1, N, K);
+    oz.launch_splits(mem, st);
+    for (int rep = 0; rep < 2; ++rep) {
+      oz.add(dC, N, 1, M, N, 1.0, {{{a, b}, -1.0}, {{a, b}, 1.0}}, false, false);
+      const double useful = oz.useful;
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+      oz.launch(mem, st);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (sgf_oz_prof_read) {
+        unsigned long long c[8];
+        sgf_oz_prof_read(c, 1);
+        printf("{\"cycles\": {\"mma_wait_operands\": %llu, \"mma_wait_epilogue\": %llu, \"mma_issue\": %llu, "
+               "\"epilogue_drain_thread0\": %llu, \"epilogue_wait_thread0\": %llu}}\n", c[0], c[1], c[2], c[3], c[4]);
+      }
+      printf("{\"timing\":\"2 products per 128x128 tile\",\"M\":%d,\"N\":%d,\"K\":%d,\"ms\":%.3f,\"fp64_tflops\":%.1f,"
+             "\"int8_tops\":%.0f}\n", M, N, K, ms, useful / (ms * 1e-3) / 1e12, 36 * useful / (ms * 1e-3) / 1e12);
+    }
   }
   cudaError_t e = cudaGetLastError();
   printf("cuda: %s, failures: %d\n", cudaGetErrorString(e), fails);
