@@ -109,8 +109,8 @@ struct OzTask {
   double beta;
   int klim;  // K tiles used by this tile (triangular B), >= nk when unlimited
 };
-cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_prefix, int njobs, long long total_rows,
-                            cudaStream_t s);
+cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
+                            long long total_groups, cudaStream_t s);
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s);
 
 // ---- apply / GEMV -----------------------------------------------------------------

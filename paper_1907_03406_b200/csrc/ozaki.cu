@@ -92,46 +92,63 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
 }
 
-// one warp per operand row: exponent, then S slices per element
+// One warp per group of 8 operand rows: lane l works on row (l & 7) and on
+// the 16-element K chunks c = (l >> 3) + 4 i, so for every slice the warp
+// stores two contiguous 256-byte runs (the core matrices of two K tiles).
+// Pass 1: row maxima (-> power-of-two exponents); pass 2: slices.
 __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restrict__ jobs,
-                                                       const long long* __restrict__ row_prefix, int njobs) {
+                                                       const long long* __restrict__ group_prefix, int njobs) {
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  int lo = 0, hi = njobs - 1;  // job containing padded row gw
+  if (gw >= group_prefix[njobs]) return;
+  int lo = 0, hi = njobs - 1;  // job containing row group gw
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (row_prefix[mid] <= gw) lo = mid;
+    if (group_prefix[mid] <= gw) lo = mid;
     else hi = mid - 1;
   }
-  if (gw >= row_prefix[njobs]) return;
   const OzSplitJob J = jobs[lo];
-  const int r = (int)(gw - row_prefix[lo]);
+  const int r = (int)(gw - group_prefix[lo]) * 8 + (lane & 7);
+  const int c0 = lane >> 3;
   const bool live = r < J.R;
   const double* row = J.x + (long long)r * J.rs;
   double mx = 0.0;
   if (live)
-    for (int k = lane; k < J.K; k += 32) mx = fmax(mx, fabs(row[(long long)k * J.cs]));
+    for (int k0 = c0 * 16; k0 < J.K; k0 += 64)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int q = 0; q < 16; ++q)
+        if (k0 + q < J.K) mx = fmax(mx, fabs(row[(long long)(k0 + q) * J.cs]));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   int ex = 0;
   if (mx > 0.0) frexp(mx, &ex);  // |x| 2^-ex < 1
-  if (lane == 0) J.exps[r] = live ? ex : 0;
-  // each lane cuts 16 consecutive K entries (one 16-byte chunk per slice)
+  if (lane < 8) J.exps[r] = live ? ex : 0;
   const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
-  for (int k0 = lane * 16; k0 < J.Kp; k0 += 32 * 16) {
+  for (int k0 = c0 * 16; k0 < J.Kp; k0 += 64) {
     unsigned w[OZ_S][4];
 #pragma unroll
     for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int k = k0 + q;
-      double v = (live && k < J.K) ? ldexp(row[(long long)k * J.cs], -ex) : 0.0;
+      const double x = (live && k < J.K) ? row[(long long)k * J.cs] : 0.0;
+      // integer slicing: |x| 2^-ex as a 56-bit fixed-point F (truncated, as the
+      // FP64 recurrence v *= 128, d = trunc(v), v -= d would give), its 7-bit
+      // groups are the digits, the sign applies to all of them
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+      const int bexp = (int)((bits >> 52) & 0x7FF);
+      unsigned long long F = 0;
+      if (bexp != 0) {  // zero (and subnormals, far below any row maximum) give 0
+        const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+        const int sh = bexp - 1075 + 56 - ex;  // F = |x| 2^(56-ex)
+        F = sh >= 0 ? (sh < 11 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
+      }
+      const bool neg = (long long)bits < 0;
 #pragma unroll
       for (int t = 0; t < OZ_S; ++t) {
-        v *= 128.0;
-        const double d = trunc(v);
-        v -= d;
-        w[t][q >> 2] |= ((unsigned)(int)d & 0xFFu) << (8 * (q & 3));
+        int d = (int)((F >> (7 * (OZ_S - 1 - t))) & 0x7F);
+        if (neg) d = -d;
+        w[t][q >> 2] |= ((unsigned)d & 0xFFu) << (8 * (q & 3));
       }
     }
     const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
@@ -338,12 +355,13 @@ extern "C" int sgf_oz_prof_read(unsigned long long* out, int reset) {
 }
 #endif
 
-cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_row_prefix, int njobs, long long total_rows,
-                            cudaStream_t s) {
-  if (njobs <= 0 || total_rows <= 0) return cudaSuccess;
-  const long long threads = total_rows * 32;
+// d_group_prefix: per job the first global 8-row group (njobs + 1 entries)
+cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
+                            long long total_groups, cudaStream_t s) {
+  if (njobs <= 0 || total_groups <= 0) return cudaSuccess;
+  const long long threads = total_groups * 32;
   count_launch();
-  oz_split_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_jobs, d_row_prefix, njobs);
+  oz_split_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_jobs, d_group_prefix, njobs);
   return cudaGetLastError();
 }
 

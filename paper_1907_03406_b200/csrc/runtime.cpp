@@ -289,8 +289,8 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
-  std::vector<long long> prefix(jobs.size() + 1, 0);
-  for (size_t i = 0; i < jobs.size(); ++i) prefix[i + 1] = prefix[i] + jobs[i].Rp;
+  std::vector<long long> prefix(jobs.size() + 1, 0);  // 8-row groups
+  for (size_t i = 0; i < jobs.size(); ++i) prefix[i + 1] = prefix[i] + jobs[i].Rp / 8;
   OzSplitJob* d_j = scratch.upload(jobs);
   long long* d_p = scratch.upload(prefix);
   double bytes = 0.0;  // FP64 read + 8 slices written per element
