@@ -70,6 +70,8 @@ static double gemv_bytes(const std::vector<GemvTask>& v, int mode) {
   for (const auto& t : v) {
     if (!t.tri) {
       b += 8.0 * (t.r1 - t.r0) * (t.c1 - t.c0);
+    } else if (t.tri == 2) {
+      for (int p = t.r0; p < t.r1; ++p) b += 8.0 * ((p + 1) + (t.c1 - 1 - p == p ? 0 : t.c1 - p));
     } else if (mode == 0) {
       for (int i = t.r0; i < t.r1; ++i) b += 8.0 * std::max(0, std::min(t.c1, i + 1) - t.c0);
     } else {
@@ -97,6 +99,25 @@ struct ApplyPlan {
 };
 
 void destroy_plan(ApplyPlan* p) { delete p; }
+
+// lower triangle in row pairs (p, rows-1-p): 32 pairs per task
+static void add_gemv_tri_pairs(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y,
+                               int rows) {
+  const int np = (rows + 1) / 2;
+  for (int p0 = 0; p0 < np; p0 += 32) {
+    GemvTask t;
+    t.A = A;
+    t.lda = lda;
+    t.x = x;
+    t.y = y;
+    t.r0 = p0;
+    t.r1 = std::min(np, p0 + 32);
+    t.c0 = 0;
+    t.c1 = rows;
+    t.tri = 2;
+    v.push_back(t);
+  }
+}
 
 static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y, int rows,
                        int cols, int tri, int rows_per = GN_ROWS) {
@@ -207,7 +228,8 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       const Factor& f = *fs[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
-      add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
+      if (tri && g.gn_rows == GN_ROWS) add_gemv_tri_pairs(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m);
+      else add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
         if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows);
@@ -260,6 +282,8 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
         r2n += fs[i]->c;
       }
       if (r1n) g.lpr1 = lanes_for(g.bytes_f1 / 16.0 / r1n);
+      for (auto& t : f1)
+        if (t.tri == 2) g.lpr1 = 32;  // row pairs run in the 32-lane kernel
       if (r2n) g.lpr2 = lanes_for(g.bytes_f2 / 16.0 / r2n);
     }
     g.bytes_b1 = gemv_bytes(b1, 1);

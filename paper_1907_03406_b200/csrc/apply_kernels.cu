@@ -23,10 +23,64 @@ namespace sgf {
 // register limit capped residency at 4 CTAs and left HBM latency exposed).
 // LPR lanes per row (8/16/32): short rows (small nodes, triangles) share a
 // warp so each lane still has 4 loads in flight and the reduction is shorter.
+// Triangular matrix in row pairs (task.tri == 2, rows of pair p: p and
+// c1-1-p, pairs [r0, r1)): the two rows hold c1+1 entries together, so each
+// warp iteration streams 4 full 16-byte loads per lane (row-per-warp leaves
+// the tail of every short row latency-bound; tools/gemv_tri_bench.cu:
+// +20-28% on 512..2400-row triangles).
+__device__ __forceinline__ void gemv_tri_pairs(const GemvTask& T) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = T.c1;
+  for (int p = T.r0 + warp; p < T.r1; p += 8) {
+    const int ra = p, rb = m - 1 - p;
+    const int na = (ra + 2) >> 1;  // 16-byte words covering k <= ra (A[ra][ra+1] is a stored zero)
+    const int nb = (rb == ra) ? 0 : (rb + 2) >> 1;
+    const double2* a = reinterpret_cast<const double2*>(T.A + (long long)ra * T.lda);
+    const double2* b = reinterpret_cast<const double2*>(T.A + (long long)rb * T.lda);
+    const int n = na + nb;
+    const double* x = T.x;
+    double sa = 0.0, sb = 0.0;
+    for (int w0 = 0; w0 < n; w0 += 128) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + lane + 32 * u;
+        v[u] = w < na ? __ldcs(a + w) : (w < n ? __ldcs(b + (w - na)) : make_double2(0.0, 0.0));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int w = w0 + lane + 32 * u;
+        if (w < na) {
+          const int k = 2 * w;
+          sa = fma(v[u].x, x[k], sa);
+          if (k + 1 <= ra) sa = fma(v[u].y, x[k + 1], sa);
+        } else if (w < n) {
+          const int k = 2 * (w - na);
+          sb = fma(v[u].x, x[k], sb);
+          if (k + 1 <= rb) sb = fma(v[u].y, x[k + 1], sb);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+      T.y[ra] = sa;
+      if (rb != ra) T.y[rb] = sb;
+    }
+  }
+}
+
 template <int LPR>
 __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
   constexpr int RPW = 32 / LPR;  // rows per warp pass
   const GemvTask T = tasks[blockIdx.x];
+  if (LPR == 32 && T.tri == 2) {
+    gemv_tri_pairs(T);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane % LPR, grp = lane / LPR;
   for (int i0 = T.r0 + warp * RPW; i0 < T.r1; i0 += 8 * RPW) {  // warp-uniform

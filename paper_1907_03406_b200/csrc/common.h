@@ -123,7 +123,8 @@ struct GemvTask {
   double* y;
   int r0, r1;
   int c0, c1;
-  int tri;             // 1: lower-triangular A (row i uses k <= i)
+  int tri;             // 1: lower-triangular A (row i uses k <= i); 2 (mode N): rows in pairs
+                       //    (p, c1-1-p) for pair indices p in [r0, r1)
 };
 
 struct TriTask { double* p; int m; int ld; };
