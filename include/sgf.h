@@ -181,6 +181,15 @@ typedef int (*sgf_precond_fn)(void* user, const double* in, double* out);
 int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const double* b, double* x, double tol,
                int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
 
+/* Host helper (partition.py:142-199, 232-242 for the level-1 cells): unknown
+   ids grouped by cell (cells in id order, vertices ascending, components
+   major within a cell) and the per-cell pointer, for a nested/general grid
+   level given per axis the index extent [lo, hi] of every label.  Cell id =
+   (rank_x * ty + rank_y) * tz + rank_z. */
+int sgf_cell_unknowns(int nx, int ny, int nz, int tx, int ty, int tz, const int64_t* lox, const int64_t* hix,
+                      const int64_t* loy, const int64_t* hiy, const int64_t* loz, const int64_t* hiz, int components,
+                      int64_t* out_ptr, int64_t* out_unknowns);
+
 /* instrumentation (no reference counterpart): kernels launched so far, and
    per-kernel-class CUDA-event timing.  Classes: 0 GEMM on DMMA (work = flops),
    1 GEMV (bytes), 2 SpMV (bytes), 3 QR, 4 diagonal Cholesky, 5 copies (bytes),

@@ -31,7 +31,7 @@ EXPORTS = (
     "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
     "sgf_precond_num_factors", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
-    "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part",
+    "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read",
 )
 PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec", "gemm_int8emu", "int8emu_split")
@@ -110,6 +110,7 @@ def load_library(path=LIB_PATH):
             "sgf_precond_shard_info": (i32, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
             "sgf_precond_shard_set": (i32, [vp, i32, vp, i64]),
             "sgf_apply_part": (i32, [vp, i32, vp]),
+            "sgf_cell_unknowns": (i32, [i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp]),
             "sgf_kernel_launches": (C.c_uint64, []),
             "sgf_profile_enable": (i32, [i32]),
             "sgf_profile_read": (i32, [vp, i32]),

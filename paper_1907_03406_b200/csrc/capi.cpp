@@ -223,6 +223,36 @@ int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device)
   });
 }
 
+int sgf_cell_unknowns(int nx, int ny, int nz, int tx, int ty, int tz, const int64_t* lox, const int64_t* hix,
+                      const int64_t* loy, const int64_t* hiy, const int64_t* loz, const int64_t* hiz, int components,
+                      int64_t* out_ptr, int64_t* out_unknowns) {
+  if (nx <= 0 || ny <= 0 || nz <= 0 || tx <= 0 || ty <= 0 || tz <= 0 || components <= 0 || !out_ptr || !out_unknowns)
+    return SGF_INVALID_ARG;
+  const long long nc = (long long)tx * ty * tz;
+  const long long nv = (long long)nx * ny * nz;
+  out_ptr[0] = 0;
+  for (long long c = 0; c < nc; ++c) {
+    const long long cx = c / ((long long)ty * tz), cy = (c / tz) % ty, cz = c % tz;
+    const long long size = (hix[cx] - lox[cx] + 1) * (hiy[cy] - loy[cy] + 1) * (hiz[cz] - loz[cz] + 1);
+    out_ptr[c + 1] = out_ptr[c] + size * components;
+  }
+  if (out_ptr[nc] != nv * components) return SGF_INVALID_ARG;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (long long c = 0; c < nc; ++c) {
+    const long long cx = c / ((long long)ty * tz), cy = (c / tz) % ty, cz = c % tz;
+    const long long size = (out_ptr[c + 1] - out_ptr[c]) / components;
+    int64_t* o = out_unknowns + out_ptr[c];
+    long long s = 0;
+    for (long long k = loz[cz]; k <= hiz[cz]; ++k)
+      for (long long j = loy[cy]; j <= hiy[cy]; ++j)
+        for (long long i = lox[cx]; i <= hix[cx]; ++i, ++s) {
+          const long long v = i + nx * (j + (long long)ny * k);
+          for (int q = 0; q < components; ++q) o[q * size + s] = v + q * nv;
+        }
+  }
+  return SGF_OK;
+}
+
 uint64_t sgf_kernel_launches(void) { return g_kernel_launches; }
 
 int sgf_profile_enable(int on) {

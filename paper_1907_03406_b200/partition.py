@@ -279,7 +279,26 @@ def expand_to_unknowns(cell, grid):
 
 def level1_unknowns(hier):
     """(unknown ids grouped by level-1 cell, CSR pointer): the expansion of
-    every level-1 cell, vectorised (input to the native factorization)."""
+    every level-1 cell (input to the native factorization), computed by the
+    native host helper sgf_cell_unknowns (OpenMP over cells)."""
+    from . import _native as N
+
+    hl = hier.hlevels[0]
+    nx, ny, nz = hier.grid.dims
+    tx, ty, tz = hl.shape
+    comps = hier.grid.components_per_vertex
+    ptr = np.empty(hl.ncells + 1, dtype=np.int64)
+    out = np.empty(hier.grid.n_vertices * comps, dtype=np.int64)
+    ax, ay, az = hl.axes
+    arrs = [np.ascontiguousarray(v, dtype=np.int64) for v in (ax.lo, ax.hi, ay.lo, ay.hi, az.lo, az.hi)]
+    st = N.lib().sgf_cell_unknowns(nx, ny, nz, tx, ty, tz, *[a.ctypes.data for a in arrs], comps, ptr.ctypes.data,
+                                   out.ctypes.data)
+    N.raise_for(st, None, "level-1 cell expansion")
+    return out, ptr
+
+
+def level1_unknowns_numpy(hier):
+    """Same as level1_unknowns, in numpy (cross-check in the CPU tests)."""
     hl = hier.hlevels[0]
     verts, vptr = hl.vertex_order()
     comps = hier.grid.components_per_vertex

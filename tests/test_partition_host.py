@@ -82,3 +82,16 @@ def test_basis_bitwise_matches_oracle(degree, comps):
     coords[:, 2] = 0.0 if degree == 1 else coords[:, 2]      # a zero column
     B = build_polynomial_basis(coords, degree, comps)
     assert np.array_equal(B.Pi, O.poly_basis(coords, degree, comps))
+
+
+def test_level1_unknowns_native_matches_numpy():
+    """The native cell expansion (sgf_cell_unknowns) equals the numpy one."""
+    from paper_1907_03406_b200.partition import (CartesianGrid, build_general_hierarchy, build_nested_hierarchy,
+                                                 level1_unknowns, level1_unknowns_numpy)
+    for dims, comps, b, gen in [((33, 17, 9), 1, 3, False), ((30, 17, 9), 3, 3, False), ((40, 40, 1), 1, 9, False),
+                                ((20, 20, 20), 1, 4, True), ((13, 11, 7), 3, 6, False)]:
+        g = CartesianGrid(dims=dims, components_per_vertex=comps)
+        h = (build_general_hierarchy if gen else build_nested_hierarchy)(g, b)
+        a, p = level1_unknowns(h)
+        a2, p2 = level1_unknowns_numpy(h)
+        assert np.array_equal(a, a2) and np.array_equal(p, p2)
