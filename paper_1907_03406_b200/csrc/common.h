@@ -107,7 +107,8 @@ struct OzTask {
   int M, N, m0, n0;
   int seg0, nseg;
   double beta;
-  int klim;  // K tiles used by this tile (triangular B), >= nk when unlimited
+  int klim;    // K tiles used by this tile end before klim (triangular operands), >= nk when unlimited
+  int kstart;  // ... and start at kstart
 };
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
                             long long total_groups, cudaStream_t s);

@@ -66,6 +66,7 @@ struct State {
   std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
   bool l1_sym = true;          // level-1 apply through G = A_BB^{-1} and the sparse couplings
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
+  int chol_oz_min_m = 1536;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
@@ -536,7 +537,9 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   cp.launch(S.scratch, st);
   {
     HostTimer htc("elim chol_inv_batch");
-    chol_inv_batch(*S.ctx, S.scratch, jobs, &S.chk);
+    // large nodes (level 3 at 128^3) factor recursively with their products
+    // on the INT8 tensor cores; the rest blocked on DMMA
+    chol_inv_rec(*S.ctx, S.scratch, jobs, &S.chk, S.chol_oz_min_m);
   }
   // level 1: G = A_BB^{-1} = X^T X (X = L^{-1}), lower triangle, for the
   // apply (precond.h L1Couplings); K range of tile (i0, j0) starts at max(i0, j0)
@@ -1401,6 +1404,8 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
   S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
   if (getenv("SGF_OZAKI_MIN_M")) S.oz_min_m = atoi(getenv("SGF_OZAKI_MIN_M"));
+  if (getenv("SGF_OZAKI_CHOL_MIN_M")) S.chol_oz_min_m = atoi(getenv("SGF_OZAKI_CHOL_MIN_M"));
+  if (S.oz_min_m <= 0) S.chol_oz_min_m = 0;
   PlanWorker planner(P.get());  // destroyed (joined) before P and S
   if (a.shard_count > 1) {
     if (!a.cell_rank || !a.exchange || a.shard_rank < 0 || a.shard_rank >= a.shard_count || a.shard_stop_level < 1)

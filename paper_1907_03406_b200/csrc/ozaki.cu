@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const size_t ablk = (size_t)G.a_rp * OZ_KT, bblk = (size_t)G.b_rp * OZ_KT;
         for (int pass = 0; pass < 2; ++pass) {
           const int ns = pass == 0 ? OZ_H : OZ_S;  // slices used by the pass
-          for (int k = 0; k < nk; ++k, ++it) {
+          for (int k = T.kstart; k < nk; ++k, ++it) {
             const int s = it % OZ_STAGES;
             if (it >= OZ_STAGES) mbar_wait(&empty[s], ((it / OZ_STAGES) - 1) & 1);
             mbar_expect_tx(&full[s], (uint32_t)ns * (OZ_A_TILE + OZ_B_TILE));
@@ -226,8 +226,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             OZ_ACC(1);
           }
           asm volatile("tcgen05.fence::after_thread_sync;");
-          for (int k = 0; k < nk; ++k, ++it) {
+          for (int k = T.kstart; k < nk; ++k, ++it) {
             const int s = it % OZ_STAGES;
+            const bool k0 = (k == T.kstart);
             {
               OZ_T0();
               mbar_wait(&full[s], (it / OZ_STAGES) & 1);
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
                 for (int u = 0; u < OZ_H - t; ++u)
                   mma_i8(tmem + (uint32_t)(t + u) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE),
-                         smem_desc(b0 + u * OZ_B_TILE), idesc, (k > 0 || t > 0) ? 1u : 0u);
+                         smem_desc(b0 + u * OZ_B_TILE), idesc, (!k0 || t > 0) ? 1u : 0u);
             } else {
               // diagonals 4..7; (t, 7 - t... ) ordering: for t ascending the first
               // pair of diagonal d is (max(0, d-7), ...) -> track the first write
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                 for (int u = 0; u < OZ_S - t; ++u) {
                   const int d = t + u;
                   if (d < OZ_H) continue;
-                  const bool first = (k == 0) && (t == (d > OZ_S - 1 ? d - (OZ_S - 1) : 0));
+                  const bool first = k0 && (t == (d > OZ_S - 1 ? d - (OZ_S - 1) : 0));
                   mma_i8(tmem + (uint32_t)(d - OZ_H) * OZ_BN, smem_desc(a0 + t * OZ_A_TILE),
                          smem_desc(b0 + u * OZ_B_TILE), idesc, first ? 0u : 1u);
                 }
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const OzSeg G = segs[T.seg0 + si];
       const bool live = row < T.M;
       const double rs = live ? ldexp(G.alpha, G.ea[row]) : 0.0;
-      const bool empty_seg = min(G.nk, T.klim) <= 0;
+      const bool empty_seg = min(G.nk, T.klim) <= T.kstart;
       for (int pass = 0; pass < 2; ++pass, ++drains) {
         {
           OZ_T0();

@@ -369,6 +369,111 @@ void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tas
 //      X[k, :k0]    = -D_k T_k                            (inverse, part 2)
 // The breakdown rule is the reference's (densela.py:105-110).
 // ---------------------------------------------------------------------------
+// Recursive split of the large nodes: with W = [A11 .; A21 A22] (lower part),
+//   (L11, X11) = chol_inv(A11);  L21 = A21 X11^T;  A22 -= L21 L21^T;
+//   (L22, X22) = chol_inv(A22);  X21 = -X22 (L21 X11)
+// The three products of each split run on the INT8 tensor cores (ozaki.cu);
+// halves below min_m, and small nodes, take the blocked kernel above.  The
+// pivot floor of every half is the enclosing node's (densela.py:105-110).
+void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check, int min_m) {
+  std::vector<CholJob> small, big;
+  for (auto& j : jobs) (j.m >= min_m && min_m > 0 ? big : small).push_back(j);
+  if (!small.empty()) chol_inv_batch(ctx, scratch, small, check);
+  if (big.empty()) return;
+  cudaStream_t st = ctx.stream;
+  const int nb = (int)big.size();
+  // pivot floors of the whole nodes, shared by their halves
+  for (int i = 0; i < nb; ++i)
+    if (!big[i].floor) {
+      double* f = scratch.alloc(1);
+      const double* wp = big[i].W;
+      std::vector<const double*> wv{wp};
+      std::vector<int> mv{big[i].m}, lv{big[i].ld};
+      SGF_CUDA(launch_max_diag(scratch.upload(wv), scratch.upload(mv), scratch.upload(lv), 1, f, st));
+      big[i].floor = f;
+    }
+  std::vector<int> m1(nb), m2(nb);
+  std::vector<CholJob> j11, j22;
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    m1[i] = ((j.m / 2) + 63) / 64 * 64;
+    m2[i] = j.m - m1[i];
+    CholJob h = j;
+    h.m = m1[i];
+    j11.push_back(h);
+  }
+  chol_inv_rec(ctx, scratch, j11, check, min_m);
+  // L21 = A21 X11^T  (X11 lower: tile k < n0 + 128)
+  OzBatch oz;
+  std::vector<OzOperand> a21(nb), x11(nb), x11t(nb), l21(nb);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    const long long ld = j.ld;
+    a21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i]);
+    x11[i] = oz.split(scratch, j.X, ld, 1, m1[i], m1[i]);
+  }
+  oz.launch_splits(scratch, st);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    const long long ld = j.ld;
+    oz.add(j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i], 0.0, {{{a21[i], x11[i]}, 1.0}}, false, true);
+  }
+  oz.launch(scratch, st);
+  // A22 -= L21 L21^T (lower part)
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    const long long ld = j.ld;
+    l21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i]);
+  }
+  oz.launch_splits(scratch, st);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    const long long ld = j.ld;
+    oz.add(j.W + (long long)m1[i] * ld + m1[i], ld, 1, m2[i], m2[i], 1.0, {{{l21[i], l21[i]}, -1.0}}, true, false);
+  }
+  oz.launch(scratch, st);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    CholJob h = j;
+    h.W = j.W + (long long)m1[i] * j.ld + m1[i];
+    h.X = j.X + (long long)m1[i] * j.ld + m1[i];
+    h.m = m2[i];
+    j22.push_back(h);
+  }
+  chol_inv_rec(ctx, scratch, j22, check, min_m);
+  // T = L21 X11 (as L21 . (X11^T)^T; X11^T upper: tile k >= n0), then
+  // X21 = -X22 T (X22 lower: tile k < m0 + 128)
+  std::vector<double*> T(nb);
+  std::vector<int> ldt(nb);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    ldt[i] = pad_ld(m1[i]);
+    T[i] = scratch.alloc((size_t)m2[i] * ldt[i]);
+    x11t[i] = oz.split(scratch, j.X, 1, j.ld, m1[i], m1[i]);
+  }
+  oz.launch_splits(scratch, st);
+  for (int i = 0; i < nb; ++i)
+    oz.add(T[i], ldt[i], 1, m2[i], m1[i], 0.0, {{{l21[i], x11t[i]}, 1.0}}, false, false, false, true);
+  oz.launch(scratch, st);
+  std::vector<OzOperand> x22(nb), tt(nb);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    const long long ld = j.ld;
+    x22[i] = oz.split(scratch, j.X + (long long)m1[i] * ld + m1[i], ld, 1, m2[i], m2[i]);
+    tt[i] = oz.split(scratch, T[i], 1, ldt[i], m1[i], m2[i]);
+  }
+  oz.launch_splits(scratch, st);
+  for (int i = 0; i < nb; ++i) {
+    const CholJob& j = big[i];
+    oz.add(j.X + (long long)m1[i] * j.ld, j.ld, 1, m2[i], m1[i], 0.0, {{{x22[i], tt[i]}, -1.0}}, false, false, true);
+  }
+  oz.launch(scratch, st);
+  // L has exact zeros above the diagonal: the A12 block of W
+  std::vector<TriTask> up;
+  for (int i = 0; i < nb; ++i) up.push_back(TriTask{big[i].W, big[i].m, big[i].ld});
+  zero_upper(scratch, st, up);
+}
+
 void CholCheck::verify(cudaStream_t st) {
   if (pend.empty()) return;
   SGF_CUDA(cudaStreamSynchronize(st));
@@ -447,7 +552,7 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
       d.ld = (int)ld;
       d.k0 = k0;
       d.nb = nb;
-      d.floor = d_floor + i;
+      d.floor = jobs[i].floor ? jobs[i].floor : d_floor + i;
       d.node = i;
       dt.push_back(d);
       xd.push_back(X);

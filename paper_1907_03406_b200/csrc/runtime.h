@@ -446,10 +446,12 @@ struct OzBatch {
   void launch_splits(Arena& scratch, cudaStream_t st);
   // C (M x N) = beta*C + sum_i alpha_i A_i B_i^T, A_i with M rows, B_i with N
   // rows; lower_only skips tiles strictly above the diagonal; tri_b: B is
-  // lower triangular (B[j][k] = 0 for k > j), so a tile stops at k < n0 + 64
+  // lower triangular (B[j][k] = 0 for k > j), so a tile stops at k < n0+128;
+  // tri_a: A lower triangular (stop at k < m0+128); upper_b: B upper
+  // triangular (B[j][k] = 0 for k < j), so a tile starts at k = n0
   void add(double* C, long long c_rs, long long c_cs, int M, int N, double beta,
            const std::vector<std::pair<std::pair<OzOperand, OzOperand>, double>>& terms, bool lower_only,
-           bool tri_b) {
+           bool tri_b, bool tri_a = false, bool upper_b = false) {
     if (M <= 0 || N <= 0) return;
     const int seg0 = (int)segs.size();
     for (auto& tm : terms) {
@@ -460,11 +462,15 @@ struct OzBatch {
     for (int m0 = 0; m0 < M; m0 += 128)
       for (int n0 = 0; n0 < N; n0 += 128) {
         if (lower_only && n0 >= m0 + 128) continue;
-        const int klim = tri_b ? (n0 + 128) / 32 : (1 << 30);
-        tasks.push_back(OzTask{C, c_rs, c_cs, M, N, m0, n0, seg0, (int)terms.size(), beta, klim});
+        int klim = 1 << 30;
+        if (tri_b) klim = std::min(klim, (n0 + 128) / 32);
+        if (tri_a) klim = std::min(klim, (m0 + 128) / 32);
+        const int kstart = upper_b ? n0 / 32 : 0;
+        tasks.push_back(OzTask{C, c_rs, c_cs, M, N, m0, n0, seg0, (int)terms.size(), beta, klim, kstart});
         for (auto& tm : terms) {
           const int kt = std::min(tm.first.first.Kp / 32, klim);
-          useful += 2.0 * std::min(128, M - m0) * std::min(128, N - n0) * std::min(kt * 32, tm.first.first.K);
+          const int ke = std::min(kt * 32, tm.first.first.K), kb = kstart * 32;
+          if (ke > kb) useful += 2.0 * std::min(128, M - m0) * std::min(128, N - n0) * (ke - kb);
         }
       }
   }
@@ -506,6 +512,7 @@ struct CholJob {
   int m;
   int node;  // for error messages
   int ld;    // leading dimension of W and X (>= m; even so rows are 16-byte aligned)
+  const double* floor = nullptr;  // pivot floor (device) of the enclosing matrix; null: from this W
 };
 
 // leading dimension of stored factor matrices: even, so every row starts
@@ -525,5 +532,9 @@ struct CholCheck {
   void verify(cudaStream_t st);
 };
 void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check = nullptr);
+// same, with nodes of at least min_m unknowns factored recursively: the
+// off-diagonal solve, the Schur update and the inverse's off-diagonal block
+// are FP64 products on the INT8 tensor cores (ozaki.cu), the halves recurse
+void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check, int min_m);
 
 }  // namespace sgf
