@@ -377,7 +377,8 @@ void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tas
 // pivot floor of every half is the enclosing node's (densela.py:105-110).
 void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check, int min_m) {
   std::vector<CholJob> small, big;
-  for (auto& j : jobs) (j.m >= min_m && min_m > 0 ? big : small).push_back(j);
+  // (the int32 accumulators of a product hold K < 16.6k exactly: halves <= 16000)
+  for (auto& j : jobs) (j.m >= min_m && min_m > 0 && j.m <= 32000 ? big : small).push_back(j);
   if (!small.empty()) chol_inv_batch(ctx, scratch, small, check);
   if (big.empty()) return;
   cudaStream_t st = ctx.stream;
