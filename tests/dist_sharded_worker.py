@@ -71,6 +71,9 @@ def solve_mode(args):
         "p3d30_exact": (lambda: PB.poisson7(30, spacing=1.0 / 31), dict(scheme="nest-2-2", degree=1, b=3,
                                                                            mode="exact")),
         "elast8_b3": (lambda: PB.elasticity_cube(8), dict(scheme="nest-2-2", degree=1, b=3, rank_tol=1e-2)),
+        # BASELINE config 2: level-3 nodes of 2654-3571 unknowns take the
+        # INT8-emulated products and the recursive Cholesky
+        "cfg2": (PB.CONFIGS[2]["make"], dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2)),
     }
     for name in args.cases.split(","):
         make, opts = cases[name]

@@ -102,3 +102,11 @@ def test_sharded_nccl_backend_single_rank():
     # wrapped as the torch stream) with the one GPU this run has
     res = _launch(1, "--mode", "solve", "--backend", "nccl", "--cases", "p3d30_b3")
     _check_solve(res, ["p3d30_b3"])
+
+
+@pytest.mark.gpu
+def test_sharded_cfg2_two_ranks():
+    # BASELINE config 2 at full size over two ranks: the large level-3 nodes
+    # run the INT8-emulated products inside the rank-local phase / on rank 0
+    res = _launch(2, "--mode", "solve", "--backend", "gloo", "--cases", "cfg2", timeout=1500)
+    _check_solve(res, ["cfg2"])
