@@ -1099,7 +1099,10 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
         }
         fr.push_back(r);
       }
-    compress_wave(S, nodes, seqno, fr, level, outs, pre);
+    {
+      Phase ph(" c-wave", w, S.st);
+      compress_wave(S, nodes, seqno, fr, level, outs, pre);
+    }
     S.scratch.release();
   }
   std::sort(outs.begin(), outs.end(), [](const CompOut& x, const CompOut& y) { return x.node < y.node; });
