@@ -7,9 +7,12 @@
 // order (partials are summed in row-block order, scatter-adds into shared
 // separator unknowns in ascending factor order), so results are bitwise
 // reproducible run to run.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.h"
+#include "ptx_util.cuh"
 
 namespace sgf {
 
@@ -265,6 +268,127 @@ __global__ void __launch_bounds__(256, SYMV_MINB) symv_kernel(const SymvTask* __
   }
 }
 
+// Same arithmetic (bitwise identical results), rows staged by the bulk copy
+// engine: every warp owns a ring of S pair slots in shared memory and its
+// lane 0 keeps S row pairs (two cp.async.bulk each, one mbarrier per slot)
+// in flight while the warp reduces the previous pair from shared memory.
+// With no operand registers the kernel fits 3 CTAs per SM at Q = 8, S = 2
+// (~200 KB of G in flight per SM, against ~70 KB issued by the register
+// version, whose loads also wait behind each pair's reduction).
+template <int Q, int S>
+__global__ void __launch_bounds__(256, 3) symv_bulk_kernel(const SymvTask* __restrict__ tasks) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar[8 * S];
+  constexpr int MP = 64 * Q;
+  constexpr int SLOT = MP + 2;  // doubles per pair: row a (even length) then row b
+  const SymvTask T = tasks[blockIdx.x];
+  const int m = T.m;
+  const long long ld = T.ld;
+  double* xs = sm;
+  double* yr = sm + MP;
+  double* ring = sm + 2 * MP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wring = ring + warp * S * SLOT;
+  uint64_t* wbar = bar + warp * S;
+  const int npairs = (m + 1) / 2;
+  auto issue = [&](int p, int s) {
+    const int ra = p, rb = m - 1 - p;
+    const uint32_t na = (uint32_t)((ra + 2) & ~1), nb = (rb == ra) ? 0u : (uint32_t)((rb + 2) & ~1);
+    ptx::mbar_expect_tx(&wbar[s], (na + nb) * 8u);
+    ptx::bulk_g2s(wring + s * SLOT, T.G + (long long)ra * ld, na * 8u, &wbar[s]);
+    if (nb) ptx::bulk_g2s(wring + s * SLOT + na, T.G + (long long)rb * ld, nb * 8u, &wbar[s]);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) ptx::mbar_init(&wbar[s], 1);
+    ptx::mbar_init_fence();
+    for (int s = 0; s < S; ++s)
+      if (warp + 8 * s < npairs) issue(warp + 8 * s, s);
+  }
+  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
+  __syncthreads();
+  double c0[Q], c1[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) c0[q] = c1[q] = 0.0;
+  int it = 0;
+  for (int p = warp; p < npairs; p += 8, ++it) {
+    const int s = it % S;
+    const int ra = p, rb = m - 1 - p;
+    const int qa = (ra >> 6) + 1, qb = (rb == ra) ? 0 : (rb >> 6) + 1;
+    const double* rowa = wring + s * SLOT;
+    const double* rowb = rowa + ((ra + 2) & ~1);
+    ptx::mbar_wait(&wbar[s], (it / S) & 1);
+    const double xa = xs[ra], xb = xs[rb];
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int t = 0; t <= Q; ++t) {
+      if (t < qa) {
+        if (t < Q) {
+          const int j = 64 * t + 2 * lane;
+          if (j <= ra) {
+            const double2 g = *reinterpret_cast<const double2*>(rowa + j);
+            const double g0 = g.x, g1 = (j + 1 <= ra) ? g.y : 0.0;
+            sa = fma(g0, xs[j], fma(g1, xs[j + 1], sa));
+            if (j < ra) c0[t] = fma(g0, xa, c0[t]);
+            if (j + 1 < ra) c1[t] = fma(g1, xa, c1[t]);
+          }
+        }
+      } else if (t >= 1 && Q - t < qb) {
+        const int q = Q - t;
+        const int j = 64 * q + 2 * lane;
+        if (j <= rb) {
+          const double2 g = *reinterpret_cast<const double2*>(rowb + j);
+          const double g0 = g.x, g1 = (j + 1 <= rb) ? g.y : 0.0;
+          sb = fma(g0, xs[j], fma(g1, xs[j + 1], sb));
+          if (j < rb) c0[q] = fma(g0, xb, c0[q]);
+          if (j + 1 < rb) c1[q] = fma(g1, xb, c1[q]);
+        }
+      }
+    }
+    __syncwarp();  // every lane has read the slot
+    if (lane == 0 && p + 8 * S < npairs) issue(p + 8 * S, s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+      yr[ra] = sa;
+      if (rb != ra) yr[rb] = sb;
+    }
+  }
+  __syncthreads();  // the column partials reuse the ring
+  double* cp = ring + warp * MP;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    cp[64 * q + 2 * lane] = c0[q];
+    cp[64 * q + 2 * lane + 1] = c1[q];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += 256) {
+    double c = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += ring[w * MP + j];
+    const double v = yr[j] + c;
+    T.y[j] = T.base ? fma(T.sign, v, T.base[j]) : T.sign * v;
+  }
+}
+
+template <int Q, int S>
+static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
+  // ring (8 warps x S slots) also holds the 8 x MP column partials at the end
+  const size_t ring = (size_t)8 * std::max(S * (64 * Q + 2), 64 * Q);
+  const size_t smem = (2 * (size_t)64 * Q + ring) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(symv_bulk_kernel<Q, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  count_launch(); symv_bulk_kernel<Q, S><<<ntasks, 256, smem, s>>>(d_tasks);
+  return cudaGetLastError();
+}
+
 template <int Q>
 static cudaError_t symv_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
   const size_t smem = (size_t)10 * 64 * Q * sizeof(double);
@@ -280,6 +404,13 @@ static cudaError_t symv_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
 
 cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
+  static const int variant = getenv("SGF_SYMV") ? atoi(getenv("SGF_SYMV")) : 1;
+  if (variant == 1) {
+    if (max_m <= 128) return symv_bulk_q<2, 4>(d_tasks, ntasks, s);
+    if (max_m <= 256) return symv_bulk_q<4, 3>(d_tasks, ntasks, s);
+    if (max_m <= 512) return symv_bulk_q<8, 2>(d_tasks, ntasks, s);
+    if (max_m <= 768) return symv_bulk_q<12, 2>(d_tasks, ntasks, s);
+  }
   if (max_m <= 128) return symv_q<2>(d_tasks, ntasks, s);
   if (max_m <= 256) return symv_q<4>(d_tasks, ntasks, s);
   if (max_m <= 512) return symv_q<8>(d_tasks, ntasks, s);

@@ -570,6 +570,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   OzBatch oz;
   std::vector<std::vector<OzOperand>> eop(use_oz ? info.size() : 0);
   GemmBatch ge;
+  long long fl_chol = 0, fl_e = 0, fl_s = 0;
   for (size_t qi = 0; qi < info.size(); ++qi) {
     const EI& e = info[qi];
     long long f = (long long)e.m * e.m * e.m / 3;
@@ -589,10 +590,19 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
       f += (long long)e.m * e.m * rows;
     }
+    long long fs = 0;
     for (size_t p = 0; p < e.nb.size(); ++p)
-      for (size_t q = p; q < e.nb.size(); ++q) f += 2LL * M.size[e.nb[p]] * e.m * M.size[e.nb[q]];
-    S.flops += f;
+      for (size_t q = p; q < e.nb.size(); ++q) fs += 2LL * M.size[e.nb[p]] * e.m * M.size[e.nb[q]];
+    S.flops += f + fs;
+    if (Phase::mode()) {
+      fl_chol += (long long)e.m * e.m * e.m / 3;
+      fl_e += f - (long long)e.m * e.m * e.m / 3;
+      fl_s += fs;
+    }
   }
+  if (Phase::mode())
+    fprintf(stderr, "[sgf] L%d eliminate: %zu nodes, max m %d, flops chol %.3e E %.3e schur %.3e (%s)\n", level,
+            info.size(), maxm, (double)fl_chol, (double)fl_e, (double)fl_s, use_oz ? "int8-emulated" : "dmma");
   ge.launch(S.scratch, st);
   if (use_oz) {
     oz.launch_splits(S.scratch, st);
@@ -866,6 +876,12 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));
   SGF_CUDA(cudaStreamSynchronize(st));
   S.chk.verify(st);  // a breakdown upstream must surface before ranks are used
+  if (Phase::mode() == 1) {
+    long long sm = 0, sc = 0, ss = 0;
+    for (int w = 0; w < nw; ++w) sm += ci[w].m, sc += ci[w].cN, ss += rs[nw + w];
+    fprintf(stderr, "[sgf] L%d wave: %d nodes, max m %d, max cols %d, mean m %.0f cols %.0f steps %.1f\n", level, nw,
+            max_m, max_c, (double)sm / nw, (double)sc / nw, (double)ss / nw);
+  }
 
   // reflectors V and the compact-WY T (Q = H_0...H_{s-1} = I - V T V^T)
   std::vector<QrFinishTask> ft(nw);
