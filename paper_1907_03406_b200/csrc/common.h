@@ -198,6 +198,40 @@ cudaError_t launch_scatter_values(const double* vals, const long long* dst, long
                                   cudaStream_t s);
 // lpr: lanes per row of the mode-N kernel (8, 16 or 32)
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s, int lpr = 32);
+// level-1 eliminations with sparse couplings (l1_sparse.cu)
+constexpr int L1_KMAX = 6;  // nonzeros per coupling row (CSR rows of <= 7 entries)
+struct L1RowTask {  // one coupling block, stored srows x scols row-major; A_NB = stored (trans = 0) or its transpose
+  const double* p;
+  int srows, scols, trans;
+  long long rl0;  // row-list index of A_NB row 0
+};
+struct L1ETask {  // the E rows of one interior: E (c x m, ld lde) from the row lists [rl0, rl0 + c) and X = L^{-1}
+  const double* X;
+  long long ldx;
+  double* E;
+  long long lde;
+  int m, c;
+  long long rl0;
+};
+struct L1Contrib {
+  long long rl_a, rl_b;  // row-list indices of the target's row 0 / column 0 in this interior's lists
+  const double* G;       // A_BB^{-1}, lower triangle
+  long long ldg;
+};
+struct L1SchurTask {  // rows [r0, r0+64) of target C (rows x cols), C -= sum of contributors [c0, c0+nc)
+  double* C;
+  long long ldc;
+  int r0, rows, cols, diag, c0, nc;
+};
+cudaError_t launch_l1_rows(const L1RowTask* d_tasks, int ntasks, int* rl_n, int* rl_k, double* rl_a, int* overflow,
+                           cudaStream_t s);
+cudaError_t launch_l1_e(const L1ETask* d_tasks, int ntasks, int max_m, int max_c, const int* rl_n, const int* rl_k,
+                        const double* rl_a, cudaStream_t s);
+inline bool l1_e_fits(int max_m, int max_c) {  // shared memory of launch_l1_e
+  return 16.0 * (max_m | 1) * 8 + (double)max_c * (L1_KMAX * 12 + 4) <= 220.0 * 1024;
+}
+cudaError_t launch_l1_schur(const L1SchurTask* d_tasks, int ntasks, const L1Contrib* d_contrib, const int* rl_n,
+                            const int* rl_k, const double* rl_a, cudaStream_t s);
 cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
 // sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
 cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,

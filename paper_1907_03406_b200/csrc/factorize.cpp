@@ -65,6 +65,8 @@ struct State {
   std::vector<int> node_rank;  // per node of the current level: owning rank, -1 = top separator
   std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
   bool l1_sym = true;          // level-1 apply through G = A_BB^{-1} and the sparse couplings
+  int64_t max_row_nnz = 0;     // longest CSR row (level-1 sparse elimination path when <= L1_KMAX + 1)
+  int* l1_overflow = nullptr;   // device flag: a coupling row exceeded L1_KMAX (internal error)
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
   int chol_oz_min_m = 1536;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
   long long fa_extra = 0;      // apply flops of other ranks' factors
@@ -284,8 +286,10 @@ void setup_level1(State& S) {
     }
     int pattern_bad = 0;
     double worst = 0.0;
-#pragma omp parallel for schedule(dynamic, 4096) reduction(| : pattern_bad) reduction(max : worst)
+    int64_t rowmax = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : pattern_bad) reduction(max : worst, rowmax)
     for (int64_t r = 0; r < n; ++r) {
+      rowmax = std::max<int64_t>(rowmax, a.indptr[r + 1] - a.indptr[r]);
       for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
         const int32_t c = a.indices[e];
         if (c <= r) continue;
@@ -299,6 +303,7 @@ void setup_level1(State& S) {
         if (!a.values_on_device) worst = std::max(worst, std::fabs(a.values[e] - a.values[a.indptr[c] + (f - b0)]));
       }
     }
+    S.max_row_nnz = rowmax;
     if (pattern_bad) fail(SGF_NON_SYMMETRIC, "matrix is not symmetric (pattern)");
     if (worst > 1e-12 * std::max(scale, 1e-300)) {
       char buf[128];
@@ -570,6 +575,24 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   OzBatch oz;
   std::vector<std::vector<OzOperand>> eop(use_oz ? info.size() : 0);
   GemmBatch ge;
+  // level 1 with short matrix rows: E and the Schur updates as gathers of
+  // L^{-1} and G (l1_sparse.cu); every coupling row has <= L1_KMAX nonzeros
+  static const bool no_l1_sparse = getenv("SGF_NO_L1SPARSE") != nullptr;
+  int maxc = 0;
+  for (size_t qi = 0; qi < info.size(); ++qi)
+    if (own[qi]) maxc = std::max(maxc, info[qi].c);
+  const bool sparse1 =
+      Gall && !use_oz && !no_l1_sparse && S.max_row_nnz <= L1_KMAX + 1 && l1_e_fits(maxm, maxc);
+  std::vector<long long> rl_base(info.size(), 0);
+  std::vector<L1RowTask> l1r;
+  std::vector<L1ETask> l1e;
+  long long rl_rows = 0;
+  if (sparse1)
+    for (size_t qi = 0; qi < info.size(); ++qi)
+      if (own[qi]) {
+        rl_base[qi] = rl_rows;
+        rl_rows += info[qi].c;
+      }
   long long fl_chol = 0, fl_e = 0, fl_s = 0;
   for (size_t qi = 0; qi < info.size(); ++qi) {
     const EI& e = info[qi];
@@ -580,7 +603,13 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       const int rows = M.size[e.nb[q]];
       if (own[qi]) {
         View v = view_of(M, e.nb[q], e.x);  // A_NB: |N| x m
-        if (use_oz) {
+        if (sparse1) {
+          // stored (N, B): v.cs == 1, |N| x m;  stored (B, N): v.rs == 1, m x |N|
+          const bool trans = v.rs == 1 && v.cs != 1;
+          l1r.push_back(L1RowTask{v.p, trans ? e.m : v.rows, trans ? v.rows : e.m, trans ? 1 : 0,
+                                  rl_base[qi] + e.off[q]});
+          if (q == 0) l1e.push_back(L1ETask{e.X, (long long)e.ld, e.E, (long long)e.ld, e.m, e.c, rl_base[qi]});
+        } else if (use_oz) {
           OzOperand aop = oz.split(S.scratch, v.p, v.rs, v.cs, v.rows, e.m);
           oz.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 0.0, {{{aop, xop}, 1.0}}, false, true);
         } else {
@@ -604,6 +633,21 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     fprintf(stderr, "[sgf] L%d eliminate: %zu nodes, max m %d, flops chol %.3e E %.3e schur %.3e (%s)\n", level,
             info.size(), maxm, (double)fl_chol, (double)fl_e, (double)fl_s, use_oz ? "int8-emulated" : "dmma");
   ge.launch(S.scratch, st);
+  int *rl_n = nullptr, *rl_k = nullptr;
+  double* rl_a = nullptr;
+  if (sparse1 && rl_rows > 0) {
+    rl_n = S.scratch.alloc_t<int>(rl_rows);
+    rl_k = S.scratch.alloc_t<int>(rl_rows * L1_KMAX);
+    rl_a = S.scratch.alloc(rl_rows * L1_KMAX);
+    if (!S.l1_overflow) {
+      S.l1_overflow = S.persist.alloc_t<int>(1);
+      SGF_CUDA(cudaMemsetAsync(S.l1_overflow, 0, sizeof(int), st));
+    }
+    SGF_CUDA(cudaMemsetAsync(rl_n, 0, rl_rows * sizeof(int), st));
+    ProfScope ps(st, PROF_MOVE, 0.0);
+    SGF_CUDA(launch_l1_rows(S.scratch.upload(l1r), (int)l1r.size(), rl_n, rl_k, rl_a, S.l1_overflow, st));
+    SGF_CUDA(launch_l1_e(S.scratch.upload(l1e), (int)l1e.size(), maxm, maxc, rl_n, rl_k, rl_a, st));
+  }
   if (use_oz) {
     oz.launch_splits(S.scratch, st);
     oz.launch(S.scratch, st);
@@ -664,6 +708,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     HostTimer ht("schur tasks");
     GemmBatch gs;
     std::vector<GemmSeg> sg;
+    std::vector<L1SchurTask> l1s;
+    std::vector<L1Contrib> l1c;
     for (auto& T : targets) {
       double* bp;
       int br, bc;
@@ -678,6 +724,17 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         bc = M.size[T.b];
       }
       if (T.contrib.empty()) continue;  // sharded: no contributor on this rank
+      if (sparse1) {
+        const int c0 = (int)l1c.size();
+        for (auto& c : T.contrib) {
+          const EI& e = info[c.first];
+          l1c.push_back(L1Contrib{rl_base[c.first] + e.off[c.second.first], rl_base[c.first] + e.off[c.second.second],
+                                  Gall + (e.X - Xall), (long long)e.ld});
+        }
+        for (int r0 = 0; r0 < br; r0 += 64)
+          l1s.push_back(L1SchurTask{bp, (long long)bc, r0, br, bc, T.a == T.b, c0, (int)T.contrib.size()});
+        continue;
+      }
       sg.clear();
       for (auto& c : T.contrib) {
         const EI& e = info[c.first];
@@ -695,6 +752,10 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
     }
     HostTimer ht2("schur launch");
+    if (!l1s.empty()) {
+      ProfScope ps(st, PROF_MOVE, 0.0);
+      SGF_CUDA(launch_l1_schur(S.scratch.upload(l1s), (int)l1s.size(), S.scratch.upload(l1c), rl_n, rl_k, rl_a, st));
+    }
     gs.launch(S.scratch, st);
     oz.launch(S.scratch, st);
   }
@@ -1540,6 +1601,11 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   }
   S.chk.verify(S.st);
   SGF_CUDA(cudaStreamSynchronize(S.st));
+  if (S.l1_overflow) {
+    int ov = 0;
+    SGF_CUDA(cudaMemcpy(&ov, S.l1_overflow, sizeof(int), cudaMemcpyDeviceToHost));
+    if (ov) fail(SGF_INVALID_ARG, "internal: level-1 coupling row with more nonzeros than its CSR row");
+  }
   for (auto& f : P->factors)
     if (f.perm_dev) {
       f.perm.resize(f.ncols);
