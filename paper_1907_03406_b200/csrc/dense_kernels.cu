@@ -3,6 +3,8 @@
 // triangle zeroing, per-node max diagonal.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "common.h"
 
 namespace sgf {
@@ -77,6 +79,74 @@ __global__ void __launch_bounds__(256) diag_chol_kernel(const DiagTask* __restri
   }
 }
 
+// Right-looking variant with the inverse fused into the same sweep: after
+// column j of L and row j of L^{-1} are final, one pass updates every later
+// row i at every position x <= i -- x > j: the trailing matrix,
+// S[i][x] -= L[i][j] L[x][j]; x <= j: the inverse rows, R[i][x] -= L[i][j] D[j][x]
+// (R = identity initially, D[j][:] = R[j][:] / L[j][j]).  Two barriers per
+// column and no serial dot products: the column latency is a few smem
+// round trips instead of a 16-deep dependent FMA chain (the left-looking
+// kernel above).  Same breakdown rule and outputs.
+__global__ void __launch_bounds__(256) diag_chol_rl_kernel(const DiagTask* __restrict__ tasks,
+                                                           int* __restrict__ status, double* __restrict__ pivval,
+                                                           double* const* __restrict__ xdiag,
+                                                           const int* __restrict__ ldx) {
+  extern __shared__ double dsm[];
+  double(*S)[65] = reinterpret_cast<double(*)[65]>(dsm);
+  double(*D)[65] = reinterpret_cast<double(*)[65]>(dsm + 64 * 65);
+  const DiagTask T = tasks[blockIdx.x];
+  const int nb = T.nb, tid = threadIdx.x;
+  const int x = tid & 63, rg = tid >> 6;
+  double* W = T.W + (long long)T.k0 * T.ld + T.k0;
+  for (int idx = tid; idx < nb * nb; idx += 256) {
+    const int r = idx / nb, c = idx % nb;
+    S[r][c] = W[(long long)r * T.ld + c];
+    D[r][c] = (r == c) ? 1.0 : 0.0;
+  }
+  const double floor_ = *T.floor;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double d = S[j][j];
+    if (!(d > floor_) || !isfinite(d)) {
+      if (tid == 0 && status[T.node] == 0) {
+        status[T.node] = T.k0 + j + 1;
+        pivval[T.node] = d;
+      }
+      return;  // uniform: every thread saw the same pivot
+    }
+    const double djj = sqrt(d);
+    // column j of L (rows below j), row j of L^{-1} (columns <= j)
+    if (rg == 0) {
+      if (x > j && x < nb) S[x][j] = S[x][j] / djj;
+    } else if (rg == 1) {
+      if (x <= j) D[j][x] = D[j][x] / djj;
+    }
+    __syncthreads();
+    if (rg == 0 && x == 0) S[j][j] = djj;
+    const double lxj = (x > j && x < nb) ? S[x][j] : 0.0;
+    const double dj = (x <= j) ? D[j][x] : 0.0;
+    for (int i = j + 1 + rg; i < nb; i += 4) {
+      if (x > i) continue;
+      const double lij = S[i][j];
+      if (x > j) S[i][x] = fma(-lij, lxj, S[i][x]);
+      else D[i][x] = fma(-lij, dj, D[i][x]);
+    }
+    __syncthreads();
+  }
+  double* X = xdiag ? xdiag[blockIdx.x] : nullptr;
+  const int lx = ldx ? ldx[blockIdx.x] : 0;
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int r = idx >> 6, c = idx & 63;
+    const bool in = (r < nb && c < nb && c <= r);
+    const double dv = in ? D[r][c] : 0.0;
+    T.Dinv[idx] = dv;
+    if (r < nb && c < nb) {
+      W[(long long)r * T.ld + c] = in ? S[r][c] : 0.0;
+      if (X) X[(long long)(T.k0 + r) * lx + T.k0 + c] = dv;
+    }
+  }
+}
+
 cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
                                 double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
@@ -86,6 +156,18 @@ cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_stat
     cudaError_t e = cudaFuncSetAttribute(diag_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
+  }
+  static const int variant = getenv("SGF_DIAG_CHOL") ? atoi(getenv("SGF_DIAG_CHOL")) : 1;
+  static bool configured_rl = false;
+  if (variant == 1) {
+    if (!configured_rl) {
+      cudaError_t e =
+          cudaFuncSetAttribute(diag_chol_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured_rl = true;
+    }
+    count_launch(); diag_chol_rl_kernel<<<ntasks, 256, smem, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
+    return cudaGetLastError();
   }
   count_launch(); diag_chol_kernel<<<ntasks, 256, smem, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
   return cudaGetLastError();
