@@ -62,7 +62,8 @@ struct Group {
 };
 
 // lanes per row for mode-N rows of `len2` 16-byte words on average
-static int lanes_for(double len2) { return len2 <= 48 ? 8 : (len2 <= 96 ? 16 : 32); }
+// (64: rows of >= 1536 entries, streamed through the bulk-copy kernel)
+static int lanes_for(double len2) { return len2 <= 48 ? 8 : (len2 <= 96 ? 16 : (len2 < 768 ? 32 : 64)); }
 
 // algorithmic bytes of the matrix entries a GEMV task list reads
 static double gemv_bytes(const std::vector<GemvTask>& v, int mode) {
@@ -282,8 +283,8 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
         r2n += fs[i]->c;
       }
       if (r1n) g.lpr1 = lanes_for(g.bytes_f1 / 16.0 / r1n);
-      for (auto& t : f1)
-        if (t.tri == 2) g.lpr1 = 32;  // row pairs run in the 32-lane kernel
+      for (auto& t : f1)  // row pairs: the 32-lane kernel, or the bulk one for long pairs (2x the mean row)
+        if (t.tri == 2) g.lpr1 = (r1n && lanes_for(2.0 * g.bytes_f1 / 16.0 / r1n) == 64) ? 64 : 32;
       if (r2n) g.lpr2 = lanes_for(g.bytes_f2 / 16.0 / r2n);
     }
     g.bytes_b1 = gemv_bytes(b1, 1);

@@ -157,9 +157,117 @@ __global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restri
   if (k + 1 < T.c1) T.y[k + 1] = t0 + t1;
 }
 
+// Mode N with the matrix rows staged by the bulk copy engine (long rows,
+// >= 1536 entries on average: lpr code 64; shorter rows lose more to the
+// per-CTA x staging and ring start-up than they gain).  Each warp walks its rows (or row pairs of a
+// triangle, tri == 2) in chunks of GB_CH entries; lane 0 keeps GB_S chunks in
+// flight in the warp's ring (one mbarrier per slot) while the warp reduces
+// the previous chunk against x staged in shared memory.  A row's chunks
+// accumulate into one per-lane sum; the warp reduction runs at the row's end.
+constexpr int GB_CH = 256, GB_S = 4, GB_XCAP = 4096;
+struct GbCursor {
+  int n = 0, sub = 0, off = 0;  // row (or pair) counter of the warp, row of the pair, offset in the row
+};
+// row index and its length for the cursor; false when the warp has no more rows
+__device__ __forceinline__ bool gb_row(const GemvTask& T, int warp, const GbCursor& c, int& row, int& len) {
+  const int q = T.r0 + warp + 8 * c.n;
+  if (q >= T.r1) return false;
+  if (T.tri == 2) {
+    row = c.sub ? T.c1 - 1 - q : q;
+    len = row + 1;
+  } else {
+    row = q;
+    len = T.tri ? min(T.c1, q + 1) : T.c1;
+  }
+  return true;
+}
+__device__ __forceinline__ void gb_advance(const GemvTask& T, int warp, GbCursor& c, int len) {
+  c.off += GB_CH;
+  if (c.off < len) return;
+  c.off = 0;
+  if (T.tri == 2 && c.sub == 0 && T.c1 - 1 - (T.r0 + warp + 8 * c.n) != T.r0 + warp + 8 * c.n) {
+    c.sub = 1;
+    return;
+  }
+  c.sub = 0;
+  ++c.n;
+}
+__global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __restrict__ tasks) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar[8 * GB_S];
+  const GemvTask T = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wring = sm + warp * GB_S * GB_CH;
+  double* xs = sm + 8 * GB_S * GB_CH;
+  uint64_t* wbar = bar + warp * GB_S;
+  GbCursor pc;  // producer cursor (lane 0)
+  auto issue = [&](int slot) -> bool {
+    int row, len;
+    if (!gb_row(T, warp, pc, row, len)) return false;
+    const int cl = min(GB_CH, len - pc.off);
+    const uint32_t bytes = (uint32_t)((cl + 1) & ~1) * 8u;  // even count: 16-byte multiple (ld even)
+    ptx::mbar_expect_tx(&wbar[slot], bytes);
+    ptx::bulk_g2s(wring + slot * GB_CH, T.A + (long long)row * T.lda + pc.off, bytes, &wbar[slot]);
+    gb_advance(T, warp, pc, len);
+    return true;
+  };
+  if (lane == 0) {
+    for (int s = 0; s < GB_S; ++s) ptx::mbar_init(&wbar[s], 1);
+    ptx::mbar_init_fence();
+    for (int s = 0; s < GB_S; ++s)
+      if (!issue(s)) break;
+  }
+  const bool sx = T.c1 <= GB_XCAP;
+  for (int i = threadIdx.x; i < T.c1 && sx; i += 256) xs[i] = T.x[i];
+  __syncthreads();
+  const double* xv = sx ? xs : T.x;
+  GbCursor cc;  // consumer cursor
+  double acc = 0.0;
+  for (int it = 0;; ++it) {
+    int row, len;
+    if (!gb_row(T, warp, cc, row, len)) break;
+    const int slot = it % GB_S;
+    const int off = cc.off, cl = min(GB_CH, len - off);
+    ptx::mbar_wait(&wbar[slot], (it / GB_S) & 1);
+    const double* ch = wring + slot * GB_CH;
+#pragma unroll
+    for (int t = 0; t < GB_CH / 64; ++t) {
+      const int j = 64 * t + 2 * lane;
+      if (j < cl) {
+        const double2 g = *reinterpret_cast<const double2*>(ch + j);
+        acc = fma(g.x, xv[off + j], acc);
+        if (j + 1 < cl) acc = fma(g.y, xv[off + j + 1], acc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) issue(slot);
+    if (off + GB_CH >= len) {  // row complete
+      double s = acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) T.y[row] = s;
+      acc = 0.0;
+    }
+    gb_advance(T, warp, cc, len);
+  }
+}
+
 cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStream_t s, int lpr) {
   if (ntasks <= 0) return cudaSuccess;
   count_launch();
+  static const int bulk = getenv("SGF_GEMV_BULK") ? atoi(getenv("SGF_GEMV_BULK")) : 1;
+  if (mode == 0 && lpr == 64 && bulk) {
+    const size_t smem = ((size_t)8 * GB_S * GB_CH + GB_XCAP) * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(gemv_n_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    gemv_n_bulk_kernel<<<ntasks, 256, smem, s>>>(d_tasks);
+    return cudaGetLastError();
+  }
+  if (lpr == 64) lpr = 32;
   if (mode == 0) {
     if (lpr == 8) gemv_n_kernel<8><<<ntasks, 256, 0, s>>>(d_tasks);
     else if (lpr == 16) gemv_n_kernel<16><<<ntasks, 256, 0, s>>>(d_tasks);
