@@ -68,7 +68,7 @@ struct State {
   int64_t max_row_nnz = 0;     // longest CSR row (level-1 sparse elimination path when <= L1_KMAX + 1)
   int* l1_overflow = nullptr;   // device flag: a coupling row exceeded L1_KMAX (internal error)
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
-  int chol_oz_min_m = 1536;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
+  int chol_oz_min_m = 1024;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
