@@ -341,21 +341,45 @@ void setup_level1(State& S) {
   double* base = S.lvl->alloc(std::max<long long>(total, 1));
   SGF_CUDA(cudaMemsetAsync(base, 0, std::max<long long>(total, 1) * sizeof(double), S.st));
   S.regions.assign(1, {base, total});
-  // blocks in lexicographic (a, b) order: the reference's insertion order
+  // blocks in lexicographic (a, b) order: the reference's insertion order.
+  // The table inserts are DRAM-latency bound (random slots): adjacency lists
+  // are sized first and every insert prefetches the slot of one 16 ahead.
   std::vector<long long> diag_off(nc, -1);
   std::vector<std::vector<long long>> up_off(nc);
+  {
+    std::vector<int> deg(nc, 0);
+    for (int c = 0; c < nc; ++c) {
+      deg[c] += (int)up[c].size();
+      for (int b : up[c]) ++deg[b];
+    }
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < nc; ++c) S.M.adj[c].reserve(deg[c]);
+  }
+  struct NewBlk {
+    int a, b;
+    long long off;
+  };
+  std::vector<NewBlk> nbk;
+  nbk.reserve(S.M.map.size() + nc * 8);
   long long off = 0;
   for (int c = 0; c < nc; ++c) {
     if (has_diag[c]) {
       diag_off[c] = off;
-      S.M.insert_new(c, c, Blk{base + off, sizes[c], sizes[c]});
+      nbk.push_back({c, c, off});
       off += (long long)sizes[c] * sizes[c];
     }
     for (int b : up[c]) {
       up_off[c].push_back(off);
-      S.M.insert_new(c, b, Blk{base + off, sizes[c], sizes[b]});
+      nbk.push_back({c, b, off});
       off += (long long)sizes[c] * sizes[b];
     }
+  }
+  S.M.map.reserve(nbk.size());
+  constexpr size_t PF = 16;
+  for (size_t i = 0; i < nbk.size(); ++i) {
+    if (i + PF < nbk.size()) S.M.map.prefetch(bkey(nbk[i + PF].a, nbk[i + PF].b));
+    const NewBlk& e = nbk[i];
+    S.M.insert_new(e.a, e.b, Blk{base + e.off, sizes[e.a], sizes[e.b]});
   }
   HostTimer hts("setup scatter");
   // scatter the CSR entries into the blocks on the device (entries stored
@@ -1518,6 +1542,11 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     else S.sharded = false;  // rank 0 now holds the whole trailing matrix and eliminates everything
   };
 
+  std::vector<std::pair<size_t, size_t>> plan_pend;
+  auto flush_plan = [&]() {
+    for (auto& r : plan_pend) planner.push(r.first, r.second);
+    plan_pend.clear();
+  };
   timeline_begin(S.st);
   { Phase ph("setup", 0, S.st); setup_level1(S); }
   S.peak = 0;
@@ -1546,7 +1575,11 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       Phase ph("eliminate", t + 1, S.st);
       const size_t f0 = P->factors.size();
       eliminate_level(S, elim, t + 1);
-      planner.push(f0, P->factors.size());  // plan built on the worker while the level runs
+      // the level's apply plan is built on the worker thread; handed over
+      // after the merge is enqueued, so the worker's task-list staging does not
+      // compete with the merge's host work (the device still has the
+      // level's kernels and the merge copies queued)
+      plan_pend.push_back({f0, P->factors.size()});
     }
     ls.eliminated = (int)elim.size();
     S.scratch.release();  // chunks are reused in stream order: no sync needed
@@ -1562,7 +1595,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
         Phase ph("compress", t + 1, S.st);
         const size_t f0 = P->factors.size();
         compress_level(S, comp, t + 1, ls);
-        planner.push(f0, P->factors.size());
+        plan_pend.push_back({f0, P->factors.size()});
       }
     }
     for (auto& nd : S.nodes) max_after = std::max(max_after, (int)nd.active.size());
@@ -1574,12 +1607,14 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
       Phase ph("merge", t + 1, S.st);
       merge_level(S, a.father + father_off, a.level_ncells[t + 1], a.cell_kind + cell_off,
                   a.cell_interior + cell_off);
+      flush_plan();
       father_off += ncell;
       S.peak = std::max(S.peak, old_live + S.M.live);
     } else {
       break;
     }
   }
+  flush_plan();
   if (S.sharded && !exchanged) end_local_phase();  // the hierarchy ended before the stop level
   size_t before = P->factors.size();
   if (!stopped) {

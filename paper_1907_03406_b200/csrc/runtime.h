@@ -8,6 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
 #include <string>
 #include <unordered_map>
 #include <utility>
@@ -184,24 +187,76 @@ inline uint64_t bkey(int a, int b) {
   return ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
 }
 
+// Process-wide pool of host buffers for the hash maps below: a map of a
+// level holds 10-20 MB, and fresh pages cost a fault each on first touch
+// (~10 ms per level-1 table); buffers of a finished factorization are reused.
+struct HostPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free;
+  size_t bytes = 0;
+  static constexpr size_t MAX = (size_t)2 << 30;
+  static HostPool& get() {
+    static HostPool* p = new HostPool;  // never destroyed: maps may outlive static destruction
+    return *p;
+  }
+};
+inline void* host_pool_get(size_t bytes) {
+  HostPool& hp = HostPool::get();
+  {
+    std::lock_guard<std::mutex> lk(hp.mu);
+    auto it = hp.free.find(bytes);
+    if (it != hp.free.end()) {
+      void* p = it->second;
+      hp.free.erase(it);
+      hp.bytes -= bytes;
+      return p;
+    }
+  }
+  void* p = std::malloc(bytes < 16 ? 16 : bytes);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+inline void host_pool_put(void* p, size_t bytes) {
+  if (!p) return;
+  HostPool& hp = HostPool::get();
+  std::lock_guard<std::mutex> lk(hp.mu);
+  if (hp.bytes + bytes > HostPool::MAX) {
+    std::free(p);
+    return;
+  }
+  hp.free.emplace(bytes, p);
+  hp.bytes += bytes;
+}
+
 // Open-addressing hash map for 64-bit block keys (linear probing, backward-
 // shift deletion): the symbolic phases do millions of lookups per level, where
 // a node-based map's allocation and pointer chasing dominate.  Key ~0 is the
-// empty marker (never a valid block key).
+// empty marker (never a valid block key).  V must be trivially copyable.
 template <class V>
 class FlatMap {
  public:
   static constexpr uint64_t EMPTY = ~0ull;
   explicit FlatMap(size_t expect = 16) { reserve(expect); }
+  FlatMap(const FlatMap&) = delete;
+  FlatMap& operator=(const FlatMap&) = delete;
+  FlatMap(FlatMap&& o) noexcept { steal(o); }
+  FlatMap& operator=(FlatMap&& o) noexcept {
+    if (this != &o) {
+      release();
+      steal(o);
+    }
+    return *this;
+  }
+  ~FlatMap() { release(); }
   size_t size() const { return n_; }
   void clear() {
-    std::fill(keys_.begin(), keys_.end(), EMPTY);
+    std::fill(keys_, keys_ + cap_, EMPTY);
     n_ = 0;
   }
   void reserve(size_t expect) {
     size_t cap = 16;
     while (cap < expect * 2) cap <<= 1;
-    if (cap > keys_.size()) rehash(cap);
+    if (cap > cap_) rehash(cap);
   }
   V* find(uint64_t k) {
     size_t i = slot(k);
@@ -213,9 +268,15 @@ class FlatMap {
   }
   const V* find(uint64_t k) const { return const_cast<FlatMap*>(this)->find(k); }
   bool contains(uint64_t k) const { return find(k) != nullptr; }
+  // the slot a key probes first (bulk inserts prefetch it ahead of use)
+  void prefetch(uint64_t k) const {
+    const size_t i = slot(k);
+    __builtin_prefetch(keys_ + i, 1);
+    __builtin_prefetch(vals_ + i, 1);
+  }
   // returns the value slot and whether the key was new (value default-built)
   std::pair<V*, bool> emplace(uint64_t k) {
-    if ((n_ + 1) * 2 > keys_.size()) rehash(keys_.size() * 2);
+    if ((n_ + 1) * 2 > cap_) rehash(cap_ * 2);
     size_t i = slot(k);
     for (;;) {
       if (keys_[i] == k) return {&vals_[i], false};
@@ -255,24 +316,43 @@ class FlatMap {
   }
   template <class F>
   void for_each(F&& f) {
-    for (size_t i = 0; i < keys_.size(); ++i)
+    for (size_t i = 0; i < cap_; ++i)
       if (keys_[i] != EMPTY) f(keys_[i], vals_[i]);
   }
 
  private:
   size_t slot(uint64_t k) const { return (size_t)((k * 0x9E3779B97F4A7C15ull) >> shift_); }
+  void release() {
+    if (keys_) host_pool_put(keys_, cap_ * sizeof(uint64_t));
+    if (vals_) host_pool_put(vals_, cap_ * sizeof(V));
+    keys_ = nullptr;
+    vals_ = nullptr;
+    cap_ = mask_ = n_ = 0;
+  }
+  void steal(FlatMap& o) {
+    keys_ = o.keys_;
+    vals_ = o.vals_;
+    cap_ = o.cap_;
+    mask_ = o.mask_;
+    n_ = o.n_;
+    shift_ = o.shift_;
+    o.keys_ = nullptr;
+    o.vals_ = nullptr;
+    o.cap_ = o.mask_ = o.n_ = 0;
+  }
   void rehash(size_t cap) {
-    std::vector<uint64_t> ok;
-    std::vector<V> ov;
-    ok.swap(keys_);
-    ov.swap(vals_);
-    keys_.assign(cap, EMPTY);
-    vals_.resize(cap);
+    uint64_t* ok = keys_;
+    V* ov = vals_;
+    const size_t ocap = cap_;
+    keys_ = (uint64_t*)host_pool_get(cap * sizeof(uint64_t));
+    vals_ = (V*)host_pool_get(cap * sizeof(V));
+    std::fill(keys_, keys_ + cap, EMPTY);
+    cap_ = cap;
     mask_ = cap - 1;
     shift_ = 64;
     for (size_t c = cap; c > 1; c >>= 1) --shift_;
     n_ = 0;
-    for (size_t i = 0; i < ok.size(); ++i)
+    for (size_t i = 0; i < ocap; ++i)
       if (ok[i] != EMPTY) {
         size_t s = slot(ok[i]);
         while (keys_[s] != EMPTY) s = (s + 1) & mask_;
@@ -280,10 +360,12 @@ class FlatMap {
         vals_[s] = ov[i];
         ++n_;
       }
+    if (ok) host_pool_put(ok, ocap * sizeof(uint64_t));
+    if (ov) host_pool_put(ov, ocap * sizeof(V));
   }
-  std::vector<uint64_t> keys_;
-  std::vector<V> vals_;
-  size_t mask_ = 0, n_ = 0;
+  uint64_t* keys_ = nullptr;
+  V* vals_ = nullptr;
+  size_t cap_ = 0, mask_ = 0, n_ = 0;
   int shift_ = 64;
 };
 
