@@ -431,6 +431,283 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
   cluster.sync();  // keep every CTA's shared memory alive for remote reads
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory resident variant (the panels of the compression levels fit a
+// 16-CTA cluster: m x c <= 1225 x 184 at 128^3 -> ~118 KB per CTA).  CTA q
+// holds the ORIGINAL columns cj == q (mod QC) in its shared memory for the
+// whole factorization, so a step touches no global memory:
+//   B1  cluster barrier: the updates and candidates of step k-1 are final;
+//       every CTA reads the 16 candidates (DSMEM) and picks the pivot (first
+//       maximum by position, or the replayed column) and applies the position
+//       swap to its copy of the position <-> column maps;
+//   the owner of the pivot column forms the reflector (norm, sign, tau) in its
+//   reflector buffer;
+//   B2  cluster barrier: every CTA copies the reflector (DSMEM) and updates its
+//       unpivoted columns (dot, axpy, norm downdate), then forms its candidate
+//       for step k+1; the owner stores R_kk and the reflector into the column.
+// Per-column arithmetic and reduction orders are those of the kernels above
+// (lane-strided FMA chains + warp_sum; block sums in fixed warp order).  At
+// the end every CTA writes its columns to their final positions in N.
+// ---------------------------------------------------------------------------
+struct QsCand {
+  double v;   // comparison value (downdated norm^2, or 1 for the replayed column)
+  double n2;  // the column's norm^2
+  int pos;    // position (c: none)
+};
+struct QsPiv {
+  double tau, rkk, xn;
+  int stop;
+};
+constexpr int QST = 384;          // threads of the shared-memory variant: one warp per owned column
+constexpr int QSW = QST / 32;
+constexpr int QS_VCH = 4;         // reflector copy: 16-byte loads in flight per thread
+__device__ double sblock_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < QSW; ++i) s += red[i];
+  return s;
+}
+__global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
+    qrcp_smem_kernel(const QrTask* __restrict__ tasks, int cpc) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double qs[];
+  __shared__ double red[QSW];
+  __shared__ QsCand cand[2];
+  __shared__ QsCand sel;
+  __shared__ QsPiv piv_s;
+  __shared__ double s_amax;
+  __shared__ double wv[QSW];
+  __shared__ int wi[QSW];
+  const int q = (int)cluster.block_rank();
+  const QrTask T = tasks[blockIdx.x / QC];
+  const int m = T.m, c = T.c, kmax = min(m, c);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double eps = DBL_EPSILON;
+  // layout: cpc owned columns (m each) | reflector buffer (m) | local reflector (m) | nrm2, ref2 (cpc each)
+  //         | col_of (c) | pos_of (c) | done (cpc)
+  const int mp = (m + 1) & ~1;  // column stride: every buffer 16-byte aligned
+  double* cols = qs;
+  double* vbuf = cols + (size_t)cpc * mp;
+  double* vloc = vbuf + mp;
+  double* nrm2 = vloc + mp;
+  double* ref2 = nrm2 + cpc;
+  int* col_of = reinterpret_cast<int*>(ref2 + cpc);
+  int* pos_of = col_of + c;
+  int* done = pos_of + c;
+  const int nown = (c > q) ? (c - q + QC - 1) / QC : 0;  // owned columns q, q+QC, ...
+  for (int j = tid; j < c; j += QST) {
+    col_of[j] = j;
+    pos_of[j] = j;
+  }
+  for (int l = tid; l < nown; l += QST) done[l] = 0;
+  for (int l = 0; l < nown; ++l) {
+    const double* src = T.Nm + (long long)(q + QC * l) * m;
+    double* dst = cols + (size_t)l * mp;
+    for (int i = tid; i < m; i += QST) dst[i] = src[i];
+  }
+  __syncthreads();
+  double amax = 0.0;
+  for (int l = warp; l < nown; l += QSW) {
+    const double* col = cols + (size_t)l * mp;
+    double s = 0.0, mx = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      s = fma(col[i], col[i], s);
+      mx = fmax(mx, fabs(col[i]));
+    }
+    s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    amax = fmax(amax, mx);
+    if (lane == 0) { nrm2[l] = s; ref2[l] = s; }
+  }
+  if (lane == 0) red[warp] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < QSW; ++i) mx = fmax(mx, red[i]);
+    s_amax = mx;
+  }
+  cluster.sync();
+  {
+    double mx = 0.0;
+    for (int r = 0; r < QC; ++r) mx = fmax(mx, *cluster.map_shared_rank(&s_amax, r));
+    amax = mx;
+  }
+  const double floor_ = eps * fmax(amax, 1.0);
+  const double floor2 = floor_ * floor_;
+
+  // this CTA's candidate for step k over its unpivoted columns: first maximum by position
+  auto local_candidate = [&](int k) {
+    const bool rep = T.replay && k < T.nreplay;
+    double bv = rep ? 0.0 : -1.0, bn = 0.0;
+    int bp = c;
+    for (int l = tid; l < nown; l += QST) {
+      if (done[l]) continue;
+      const int cj = q + QC * l, pj = pos_of[cj];
+      if (rep) {
+        if (cj == T.replay[k]) { bv = 1.0; bp = pj; bn = nrm2[l]; }
+      } else {
+        const double x = nrm2[l];
+        if (x > bv || (x == bv && pj < bp)) { bv = x; bp = pj; bn = x; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const double on = __shfl_xor_sync(0xffffffffu, bn, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bn = on; }
+    }
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bp; red[warp] = bn; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = wv[0], n = red[0];
+      int p0 = wi[0];
+      for (int w = 1; w < QSW; ++w)
+        if (wv[w] > b || (wv[w] == b && wi[w] < p0)) { b = wv[w]; p0 = wi[w]; n = red[w]; }
+      cand[k & 1] = QsCand{b, n, p0};
+    }
+  };
+
+  const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
+  int steps = 0;
+  double r00 = 0.0;
+  if (limit > 0) local_candidate(0);
+  for (int k = 0; k < limit; ++k) {
+    cluster.sync();  // B1: candidates of k, every update of k-1
+    if (warp == 0) {   // lane r < QC fetches CTA r's candidate; (value, position) order is total
+      QsCand o{-2.0, 0.0, c};
+      if (lane < QC) {
+        o = *cluster.map_shared_rank(&cand[k & 1], lane);
+        if (o.pos >= c) o.v = -2.0;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, o.v, d);
+        const double on = __shfl_xor_sync(0xffffffffu, o.n2, d);
+        const int op = __shfl_xor_sync(0xffffffffu, o.pos, d);
+        if (ov > o.v || (ov == o.v && op < o.pos)) { o.v = ov; o.n2 = on; o.pos = op; }
+      }
+      if (lane == 0) sel = o;
+    }
+    __syncthreads();
+    const int pp = sel.pos < c && sel.v > -2.0 ? sel.pos : c;
+    const double pn = sel.n2;
+    if (pp >= c) break;  // malformed replay
+    if (pn <= floor2) break;
+    const int pc = col_of[pp];  // pivot column (original index)
+    __syncthreads();            // every thread has read col_of[pp]
+    if (tid == 0 && pp != k) {  // position swap k <-> pp
+      const int ck = col_of[k];
+      col_of[k] = pc;
+      col_of[pp] = ck;
+      pos_of[pc] = k;
+      pos_of[ck] = pp;
+    }
+    const int owner = pc % QC;
+    if (owner == q) {
+      const int lp = pc / QC;
+      double* xk = cols + (size_t)lp * mp;
+      double ss = 0.0;
+      for (int i = k + tid; i < m; i += QST) ss = fma(xk[i], xk[i], ss);
+      const double xn = sqrt(sblock_sum(ss, red));
+      int stop = 0;
+      if (xn <= floor_) stop = 1;
+      const double r0 = (k == 0) ? xn : r00;
+      if (!stop && T.forced_rank < 0 && !(xn > T.tol * r0)) stop = 1;
+      const double x0 = xk[k];
+      const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
+      const double u1 = x0 - sgn * xn;
+      const double tau = -sgn * u1 / xn;
+      if (!stop)
+        for (int i = k + tid; i < m; i += QST) vbuf[i - k] = (i == k) ? 1.0 : xk[i] / u1;
+      if (tid == 0) piv_s = QsPiv{tau, sgn * xn, xn, stop};
+    }
+    cluster.sync();  // B2: the reflector is published
+    const QsPiv pv = *cluster.map_shared_rank(&piv_s, owner);
+    if (pv.stop) break;
+    if (k == 0) r00 = pv.xn;
+    const int len = m - k;
+    {  // remote reflector -> local, 16-byte loads all in flight before the stores
+      const double2* rv = reinterpret_cast<const double2*>(cluster.map_shared_rank(vbuf, owner));
+      double2* lv = reinterpret_cast<double2*>(vloc);
+      const int n2 = (len + 1) >> 1;
+      double2 t[QS_VCH];
+#pragma unroll
+      for (int u = 0; u < QS_VCH; ++u)
+        if (tid + QST * u < n2) t[u] = rv[tid + QST * u];
+#pragma unroll
+      for (int u = 0; u < QS_VCH; ++u)
+        if (tid + QST * u < n2) lv[tid + QST * u] = t[u];
+      for (int i = tid + QST * QS_VCH; i < n2; i += QST) lv[i] = rv[i];
+    }
+    __syncthreads();
+    if (owner == q) {  // the pivot column: R_kk and the reflector below it
+      const int lp = pc / QC;
+      double* xk = cols + (size_t)lp * mp;
+      for (int i = k + 1 + tid; i < m; i += QST) xk[i] = vloc[i - k];
+      if (tid == 0) {
+        xk[k] = pv.rkk;
+        done[lp] = 1;
+        T.tau[k] = pv.tau;
+      }
+    }
+    for (int l = warp; l < nown; l += QSW) {
+      const int cj = q + QC * l;
+      if (cj == pc || done[l]) continue;
+      double* col = cols + (size_t)l * mp + k;
+      double s = 0.0;
+      for (int i = lane; i < len; i += 32) s = fma(vloc[i], col[i], s);
+      s = warp_sum(s);
+      const double ts = pv.tau * s;
+      double fresh = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        const double nv = fma(-ts, vloc[i], col[i]);
+        col[i] = nv;
+        if (i > 0) fresh = fma(nv, nv, fresh);
+      }
+      fresh = warp_sum(fresh);
+      if (lane == 0) {
+        const double rkj = col[0];
+        double nn = fmax(nrm2[l] - rkj * rkj, 0.0);
+        if (nn <= eps * ref2[l]) {
+          nn = fresh;
+          ref2[l] = fmax(fresh, floor2);
+        }
+        nrm2[l] = nn;
+      }
+    }
+    steps = k + 1;
+    __syncthreads();  // norms and done flags of step k
+    if (k + 1 < limit) local_candidate(k + 1);
+  }
+  cluster.sync();  // every CTA has read its last remote data; all inputs were loaded long ago
+  // columns to their final positions, permutation out
+  for (int l = 0; l < nown; ++l) {
+    const int cj = q + QC * l;
+    const double* src = cols + (size_t)l * mp;
+    double* dst = T.Nm + (long long)pos_of[cj] * m;
+    for (int i = tid; i < m; i += QST) dst[i] = src[i];
+  }
+  if (q == 0)
+    for (int j = tid; j < c; j += QST) T.perm[j] = col_of[j];
+  if (q == 0 && tid == 0) {
+    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : steps;
+    *T.out_steps = steps;
+  }
+  cluster.sync();  // keep every CTA's shared memory alive for remote reads
+}
+
+static size_t qrcp_smem_bytes(int m, int c) {
+  const size_t cpc = (size_t)(c + QC - 1) / QC, mp = (size_t)((m + 1) & ~1);
+  return (cpc * mp + 2 * mp + 2 * cpc) * sizeof(double) + (2 * (size_t)c + cpc) * sizeof(int);
+}
+
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = (size_t)max_m * sizeof(double) + (size_t)max_c * sizeof(int);
@@ -450,6 +727,25 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
     configured = smem;
   }
   static int single = getenv("SGF_QR_SINGLE_CTA") ? 1 : 0;
+  static int smem_ok = getenv("SGF_QR_SMEM") ? atoi(getenv("SGF_QR_SMEM")) : 1;
+  const size_t sb = qrcp_smem_bytes(max_m, max_c);
+  if (!single && smem_ok && sb <= (size_t)220 << 10) {
+    static size_t conf_s = 0;
+    static bool np_s = false;
+    if (!np_s) {
+      cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      np_s = true;
+    }
+    if (sb > conf_s) {
+      cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      if (e != cudaSuccess) return e;
+      conf_s = sb;
+    }
+    count_launch();
+    qrcp_smem_kernel<<<ntasks * QC, QST, sb, s>>>(d_tasks, (max_c + QC - 1) / QC);
+    return cudaGetLastError();
+  }
   count_launch();
   if (single) qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
   else qrcp_cluster_kernel<<<ntasks * QC, QCT, smem, s>>>(d_tasks);
