@@ -995,7 +995,9 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     ProfScope ps(st, PROF_QR, 0.0);
     SGF_CUDA(launch_qr_finish(d_ft, nw, 0, st));
     gg.launch(S.scratch, st);
-    SGF_CUDA(launch_qr_finish(d_ft, nw, 1, st));
+    int max_s = 1;
+    for (int w = 0; w < nw; ++w) max_s = std::max(max_s, rs[nw + w]);
+    SGF_CUDA(launch_qr_finish(d_ft, nw, 1, st, max_s));
   }
   // inv = Q^T L^{-1} = L^{-1} - V T^T (V^T L^{-1}) and the basis update
   // Q1^T L^T Phi = first r rows of (L^T Phi - V T^T (V^T L^T Phi))

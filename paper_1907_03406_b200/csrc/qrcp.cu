@@ -772,15 +772,49 @@ __global__ void __launch_bounds__(QR_THREADS) qr_extract_v_kernel(const QrFinish
   }
 }
 
+// T recurrence (LAPACK larft, forward, columnwise) with T's upper triangle
+// (packed rows) and column k of G in shared memory: each step reads only
+// shared memory after one staged column (the global-memory form re-read T and
+// G every step).  Same summation order.
 __global__ void __launch_bounds__(QR_THREADS) qr_larft_kernel(const QrFinishTask* __restrict__ tasks) {
+  extern __shared__ double tsm[];
   const QrFinishTask F = tasks[blockIdx.x];
   const int s = *F.steps;
   const int tid = threadIdx.x;
   const double* G = F.G;  // s x s, G[a][b] = v_a . v_b
-  // T recurrence (LAPACK larft, forward, columnwise)
+  double* gk = tsm;       // column k of G
+  double* tp = tsm + s;   // packed upper T: row a holds T[a][a..s)
+  auto off = [s](int a) { return (long long)a * (2LL * s - a + 1) / 2; };
+  for (int k = 0; k < s; ++k) {
+    for (int b = tid; b < k; b += QR_THREADS) gk[b] = G[(long long)b * s + k];
+    const double tk = F.tau[k];
+    __syncthreads();
+    // T[a][k] = -tau_k sum_{a<=b<k} T[a][b] G[b][k], a < k   (T upper)
+    for (int a = tid; a < k; a += QR_THREADS) {
+      const double* ta = tp + off(a) - a;  // ta[b] = T[a][b]
+      double acc = 0.0;
+      for (int b = a; b < k; ++b) acc = fma(ta[b], gk[b], acc);
+      const double t = -tk * acc;
+      tp[off(a) + (k - a)] = t;
+      F.Tm[(long long)a * s + k] = t;
+    }
+    if (tid == 0) {
+      tp[off(k)] = tk;
+      F.Tm[(long long)k * s + k] = tk;
+    }
+    for (int a = k + 1 + tid; a < s; a += QR_THREADS) F.Tm[(long long)a * s + k] = 0.0;
+    __syncthreads();
+  }
+}
+
+// global-memory form for reflector counts whose T does not fit shared memory
+__global__ void __launch_bounds__(QR_THREADS) qr_larft_global_kernel(const QrFinishTask* __restrict__ tasks) {
+  const QrFinishTask F = tasks[blockIdx.x];
+  const int s = *F.steps;
+  const int tid = threadIdx.x;
+  const double* G = F.G;
   for (int k = 0; k < s; ++k) {
     const double tk = F.tau[k];
-    // w[a] = sum_{b<k} T[a][b] * G[b][k], a < k   (T upper)
     for (int a = tid; a < k; a += QR_THREADS) {
       double acc = 0.0;
       for (int b = a; b < k; ++b) acc = fma(F.Tm[(long long)a * s + b], G[b * s + k], acc);
@@ -792,11 +826,25 @@ __global__ void __launch_bounds__(QR_THREADS) qr_larft_kernel(const QrFinishTask
   }
 }
 
-cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s) {
+cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s, int max_s) {
   if (ntasks <= 0) return cudaSuccess;
   count_launch();
-  if (phase == 0) qr_extract_v_kernel<<<dim3(16, ntasks), QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
-  else qr_larft_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  if (phase == 0) {
+    qr_extract_v_kernel<<<dim3(16, ntasks), QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+  } else {
+    const size_t smem = ((size_t)max_s + (size_t)max_s * (max_s + 1) / 2) * sizeof(double);
+    if (smem > (size_t)220 << 10) {  // s > 232
+      qr_larft_global_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
+      return cudaGetLastError();
+    }
+    static size_t configured = 48 << 10;
+    if (smem > configured) {
+      cudaError_t e = cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = smem;
+    }
+    qr_larft_kernel<<<ntasks, QR_THREADS, smem, s>>>((const QrFinishTask*)d_tasks);
+  }
   return cudaGetLastError();
 }
 

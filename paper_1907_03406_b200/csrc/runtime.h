@@ -39,7 +39,7 @@ cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, in
                               cudaStream_t s);
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c = 0);
 cudaError_t launch_csr_scatter(const void* params, cudaStream_t s);
-cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s);
+cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s, int max_s = 0);
 cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s);
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
 cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s);
