@@ -68,6 +68,7 @@ struct State {
   int64_t max_row_nnz = 0;     // longest CSR row (level-1 sparse elimination path when <= L1_KMAX + 1)
   int* l1_overflow = nullptr;   // device flag: a coupling row exceeded L1_KMAX (internal error)
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
+  int oz_schur_min_m = 640;    // nodes this large (below oz_min_m) take only the Schur updates emulated
   int chol_oz_min_m = 1024;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
@@ -596,8 +597,12 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     if (own[qi]) maxm = std::max(maxm, info[qi].m);
   // (int32 accumulators hold 8 pairs x K x 127^2 exactly for K < 16.6k)
   const bool use_oz = S.oz_min_m > 0 && maxm >= S.oz_min_m && maxm <= 16000;
+  // mid-size nodes (level 2 at 128^3): E on DMMA (its K = m is too short for
+  // the emulated product's two-pass epilogue), the Schur updates emulated
+  const bool oz_schur = use_oz || (S.oz_schur_min_m > 0 && S.oz_min_m > 0 && maxm >= S.oz_schur_min_m &&
+                                   maxm <= 16000);
   OzBatch oz;
-  std::vector<std::vector<OzOperand>> eop(use_oz ? info.size() : 0);
+  std::vector<std::vector<OzOperand>> eop(oz_schur ? info.size() : 0);
   GemmBatch ge;
   // level 1 with short matrix rows: E and the Schur updates as gathers of
   // L^{-1} and G (l1_sparse.cu); every coupling row has <= L1_KMAX nonzeros
@@ -606,7 +611,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   for (size_t qi = 0; qi < info.size(); ++qi)
     if (own[qi]) maxc = std::max(maxc, info[qi].c);
   const bool sparse1 =
-      Gall && !use_oz && !no_l1_sparse && S.max_row_nnz <= L1_KMAX + 1 && l1_e_fits(maxm, maxc);
+      Gall && !oz_schur && !no_l1_sparse && S.max_row_nnz <= L1_KMAX + 1 && l1_e_fits(maxm, maxc);
   std::vector<long long> rl_base(info.size(), 0);
   std::vector<L1RowTask> l1r;
   std::vector<L1ETask> l1e;
@@ -655,7 +660,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   }
   if (Phase::mode())
     fprintf(stderr, "[sgf] L%d eliminate: %zu nodes, max m %d, flops chol %.3e E %.3e schur %.3e (%s)\n", level,
-            info.size(), maxm, (double)fl_chol, (double)fl_e, (double)fl_s, use_oz ? "int8-emulated" : "dmma");
+            info.size(), maxm, (double)fl_chol, (double)fl_e, (double)fl_s,
+            use_oz ? "int8-emulated" : (oz_schur ? "E dmma, schur int8-emulated" : "dmma"));
   ge.launch(S.scratch, st);
   int *rl_n = nullptr, *rl_k = nullptr;
   double* rl_a = nullptr;
@@ -675,6 +681,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   if (use_oz) {
     oz.launch_splits(S.scratch, st);
     oz.launch(S.scratch, st);
+  }
+  if (oz_schur) {
     // the couplings as Schur operands, one split per neighbour block
     for (size_t qi = 0; qi < info.size(); ++qi) {
       if (!own[qi]) continue;
@@ -767,7 +775,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
       // diagonal blocks are kept valid in their lower triangle only: every
       // consumer (Cholesky of the node, densify + Cholesky) reads only that
-      if (use_oz) {
+      if (oz_schur) {
         std::vector<std::pair<std::pair<OzOperand, OzOperand>, double>> terms;
         for (auto& c : T.contrib) terms.push_back({{eop[c.first][c.second.first], eop[c.first][c.second.second]}, -1.0});
         oz.add(bp, bc, 1, br, bc, 1.0, terms, T.a == T.b, false);
@@ -1511,6 +1519,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
   if (getenv("SGF_OZAKI_MIN_M")) S.oz_min_m = atoi(getenv("SGF_OZAKI_MIN_M"));
   if (getenv("SGF_OZAKI_CHOL_MIN_M")) S.chol_oz_min_m = atoi(getenv("SGF_OZAKI_CHOL_MIN_M"));
+  if (getenv("SGF_OZAKI_SCHUR_MIN_M")) S.oz_schur_min_m = atoi(getenv("SGF_OZAKI_SCHUR_MIN_M"));
   if (S.oz_min_m <= 0) S.chol_oz_min_m = 0;
   PlanWorker planner(P.get());  // destroyed (joined) before P and S
   if (a.shard_count > 1) {
