@@ -65,6 +65,7 @@ struct State {
   std::vector<int> node_rank;  // per node of the current level: owning rank, -1 = top separator
   std::vector<std::pair<double*, long long>> regions;  // device regions holding the level's blocks
   bool l1_sym = true;          // level-1 apply through G = A_BB^{-1} and the sparse couplings
+  std::vector<int> l1_bw;      // level-1 cells: lower bandwidth of the diagonal block (banded Cholesky)
   int64_t max_row_nnz = 0;     // longest CSR row (level-1 sparse elimination path when <= L1_KMAX + 1)
   int* l1_overflow = nullptr;   // device flag: a coupling row exceeded L1_KMAX (internal error)
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
@@ -318,17 +319,24 @@ void setup_level1(State& S) {
   HostTimer htd("setup discovery");
   std::vector<std::vector<int>> up(nc);
   std::vector<char> has_diag(nc, 0);
+  S.l1_bw.assign(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int c = 0; c < nc; ++c) {
     auto& v = up[c];
+    int bw = 0;  // lower bandwidth of the diagonal block in the cell's unknown order
     for (int64_t i = a.l1_ptr[c]; i < a.l1_ptr[c + 1]; ++i) {
       const int64_t r = a.l1_unknowns[i];
       for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
         const int cb = owner[a.indices[e]];
-        if (cb == c) has_diag[c] = 1;
-        else if (cb > c && std::find(v.begin(), v.end(), cb) == v.end()) v.push_back(cb);
+        if (cb == c) {
+          has_diag[c] = 1;
+          bw = std::max(bw, (int)(i - a.l1_ptr[c]) - local[a.indices[e]]);
+        } else if (cb > c && std::find(v.begin(), v.end(), cb) == v.end()) {
+          v.push_back(cb);
+        }
       }
     }
+    S.l1_bw[c] = bw;
     std::sort(v.begin(), v.end());
   }
   HostTimer htd2("setup blocks");
@@ -563,6 +571,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     if (!d) fail(SGF_NOT_SPD, "interior node without a diagonal block");
     cp.add(d->p, d->cols, 1, e.W, e.ld, 1, e.m, e.m);
     jobs.push_back(CholJob{e.W, e.X, e.m, e.x, e.ld});
+    if (level == 1 && !S.l1_bw.empty()) jobs.back().bw = std::max(1, S.l1_bw[e.x]);
   }
   cp.launch(S.scratch, st);
   {

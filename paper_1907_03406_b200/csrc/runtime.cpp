@@ -550,11 +550,18 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
       double* W = jobs[i].W;
       double* X = jobs[i].X;
       const int nb = std::min(64, m - k0), k1 = k0 + nb;
+      // banded W (level-1 interiors in lexicographic order): L[i][j] = 0 for
+      // i - j > bw, so the panel update and T_k only need K in [kb, k0) and
+      // rows below k1 + bw (the skipped products are exact zeros)
+      const bool band = jobs[i].bw > 0 && jobs[i].bw < m;
+      const int kb = band ? std::max(0, (k0 - jobs[i].bw) / 64 * 64) : 0;
+      const int rend = band ? std::min(m, k1 + jobs[i].bw) : m;
       if (k0 > 0) {
         // A: panel update and T_k (T_k is nb x k0 with leading dimension m)
-        ga.add(W + k0 * ld + k0, ld, 1, m - k0, nb, -1.0, 1.0,
-               {seg(W + k0 * ld, ld, 1, W + k0 * ld, ld, 1, k0)});
-        ga.add(tk[i], m, 1, nb, k0, 1.0, 0.0, {seg(W + k0 * ld, ld, 1, X, 1, ld, k0, SEG_KSTART_N)}, 0);
+        ga.add(W + k0 * ld + k0, ld, 1, rend - k0, nb, -1.0, 1.0,
+               {seg(W + k0 * ld + kb, ld, 1, W + k0 * ld + kb, ld, 1, k0 - kb)});
+        ga.add(tk[i], m, 1, nb, k0, 1.0, 0.0,
+               {seg(W + k0 * ld + kb, ld, 1, X + (long long)kb * ld, 1, ld, k0 - kb, kb ? 0 : SEG_KSTART_N)}, 0);
       }
       DiagTask d;
       d.W = W;
@@ -567,8 +574,8 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
       dt.push_back(d);
       xd.push_back(X);
       xl.push_back((int)ld);
-      if (m > k1)
-        gc.add(W + k1 * ld + k0, ld, 1, m - k1, nb, 1.0, 0.0,
+      if (rend > k1)
+        gc.add(W + k1 * ld + k0, ld, 1, rend - k1, nb, 1.0, 0.0,
                {seg(W + k1 * ld + k0, ld, 1, dinv[i], 64, 1, nb, SEG_KLIM_N)}, 0);
       if (k0 > 0)
         gc.add(X + k0 * ld, ld, 1, nb, k0, -1.0, 0.0, {seg(dinv[i], 64, 1, tk[i], 1, m, nb, SEG_KLIM_M)}, 0);

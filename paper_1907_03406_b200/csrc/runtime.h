@@ -595,6 +595,7 @@ struct CholJob {
   int node;  // for error messages
   int ld;    // leading dimension of W and X (>= m; even so rows are 16-byte aligned)
   const double* floor = nullptr;  // pivot floor (device) of the enclosing matrix; null: from this W
+  int bw = 0;  // lower bandwidth of W (W[i][j] == 0 for i - j > bw; L inherits it); 0: dense
 };
 
 // leading dimension of stored factor matrices: even, so every row starts
