@@ -297,6 +297,49 @@ __global__ void __launch_bounds__(256) csr_scatter_kernel(const CsrScatter P) {
   }
 }
 
+// Symmetry of the CSR matrix (blockmatrix.py:105-113): out[0] = max |A - A^T|
+// (a missing mirror counts as 0), out[1] = max |A|, both as the bit patterns
+// of non-negative doubles (ordered like the values, so atomicMax applies).
+// Column indices are sorted per row.
+__global__ void __launch_bounds__(256) sym_check_kernel(long long n, const long long* __restrict__ ip,
+                                                        const int* __restrict__ ix, const double* __restrict__ v,
+                                                        unsigned long long* __restrict__ out) {
+  double asym = 0.0, scale = 0.0;
+  for (long long r = blockIdx.x * 256LL + threadIdx.x; r < n; r += (long long)gridDim.x * 256) {
+    for (long long e = ip[r]; e < ip[r + 1]; ++e) {
+      const int c = ix[e];
+      const double a = v[e];
+      scale = fmax(scale, fabs(a));
+      long long lo = ip[c], hi = ip[c + 1];
+      while (lo < hi) {  // first index with ix >= r
+        const long long mid = (lo + hi) >> 1;
+        if (ix[mid] < r) lo = mid + 1;
+        else hi = mid;
+      }
+      const double b = (lo < ip[c + 1] && ix[lo] == r) ? v[lo] : 0.0;
+      asym = fmax(asym, fabs(a - b));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+    scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, (unsigned long long)__double_as_longlong(asym));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(scale));
+  }
+}
+
+cudaError_t launch_sym_check(long long n, const long long* ip, const int* ix, const double* v,
+                             unsigned long long* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  count_launch(); sym_check_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, ip, ix, v, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csr_scatter(const void* params, cudaStream_t s) {
   const CsrScatter& P = *(const CsrScatter*)params;
   if (P.n <= 0) return cudaSuccess;

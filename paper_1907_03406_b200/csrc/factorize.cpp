@@ -278,40 +278,16 @@ void setup_level1(State& S) {
   for (int64_t u = 0; u < n; ++u)
     if (owner[u] < 0) fail(SGF_INVALID_ARG, "node unknown lists do not cover all unknowns");
 
-  // symmetry of pattern and values (blockmatrix.py:107-113), indices sorted per row
+  // symmetry of pattern and values (blockmatrix.py:105-113) is checked on the
+  // device once the CSR is uploaded (sym_check_kernel), verified at the first
+  // synchronisation point before any other result; the host only needs the
+  // longest row here.  Column indices are sorted per row.
   {
     Phase ph(" s-sym", -1, S.st);
-    double scale = 0.0;
-    if (!a.values_on_device) {
-#pragma omp parallel for reduction(max : scale)
-      for (int64_t e = 0; e < a.nnz; ++e) scale = std::max(scale, std::fabs(a.values[e]));
-    }
-    int pattern_bad = 0;
-    double worst = 0.0;
     int64_t rowmax = 0;
-#pragma omp parallel for schedule(dynamic, 4096) reduction(| : pattern_bad) reduction(max : worst, rowmax)
-    for (int64_t r = 0; r < n; ++r) {
-      rowmax = std::max<int64_t>(rowmax, a.indptr[r + 1] - a.indptr[r]);
-      for (int64_t e = a.indptr[r]; e < a.indptr[r + 1]; ++e) {
-        const int32_t c = a.indices[e];
-        if (c <= r) continue;
-        const int32_t* b0 = a.indices + a.indptr[c];
-        const int32_t* b1 = a.indices + a.indptr[c + 1];
-        const int32_t* f = std::lower_bound(b0, b1, (int32_t)r);
-        if (f == b1 || *f != r) {
-          if (a.values_on_device || a.values[e] != 0.0) pattern_bad = 1;
-          continue;
-        }
-        if (!a.values_on_device) worst = std::max(worst, std::fabs(a.values[e] - a.values[a.indptr[c] + (f - b0)]));
-      }
-    }
+#pragma omp parallel for reduction(max : rowmax)
+    for (int64_t r = 0; r < n; ++r) rowmax = std::max<int64_t>(rowmax, a.indptr[r + 1] - a.indptr[r]);
     S.max_row_nnz = rowmax;
-    if (pattern_bad) fail(SGF_NON_SYMMETRIC, "matrix is not symmetric (pattern)");
-    if (worst > 1e-12 * std::max(scale, 1e-300)) {
-      char buf[128];
-      snprintf(buf, sizeof buf, "matrix is not symmetric (max asymmetry %.2e)", worst);
-      fail(SGF_NON_SYMMETRIC, buf);
-    }
   }
 
   // block discovery, per cell (rows of a cell are its unknowns): coupled
@@ -427,6 +403,12 @@ void setup_level1(State& S) {
       }
     }
     const double* d_vals = a.values_on_device ? a.values : d_vhost;
+    {
+      unsigned long long* sym = S.persist.alloc_t<unsigned long long>(2);
+      SGF_CUDA(cudaMemsetAsync(sym, 0, 2 * sizeof(unsigned long long), S.st));
+      SGF_CUDA(launch_sym_check(n, d_ip, d_ix, d_vals, sym, S.st));
+      S.chk.sym = sym;
+    }
     P.indptr = d_ip;
     P.indices = d_ix;
     P.values = d_vals;

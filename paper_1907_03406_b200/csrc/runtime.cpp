@@ -485,6 +485,21 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
 }
 
 void CholCheck::verify(cudaStream_t st) {
+  if (sym) {  // an asymmetric matrix is reported before anything computed from it
+    SGF_CUDA(cudaStreamSynchronize(st));
+    unsigned long long h[2];
+    SGF_CUDA(cudaMemcpy(h, sym, sizeof h, cudaMemcpyDeviceToHost));
+    sym = nullptr;
+    double asym, scale;
+    std::memcpy(&asym, &h[0], sizeof(double));
+    std::memcpy(&scale, &h[1], sizeof(double));
+    if (asym > sym_rtol * std::max(scale, 1e-300)) {
+      pend.clear();
+      char buf[128];
+      snprintf(buf, sizeof buf, "matrix is not symmetric (max asymmetry %.2e)", asym);
+      fail(SGF_NON_SYMMETRIC, buf);
+    }
+  }
   if (pend.empty()) return;
   SGF_CUDA(cudaStreamSynchronize(st));
   for (auto& p : pend) {

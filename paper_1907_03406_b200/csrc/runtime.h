@@ -39,6 +39,8 @@ cudaError_t launch_zero_upper(const void* d_tasks, const long long* d_prefix, in
                               cudaStream_t s);
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c = 0);
 cudaError_t launch_csr_scatter(const void* params, cudaStream_t s);
+cudaError_t launch_sym_check(long long n, const long long* ip, const int* ix, const double* v,
+                             unsigned long long* out, cudaStream_t s);
 cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s, int max_s = 0);
 cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s);
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
@@ -612,6 +614,9 @@ struct CholCheck {
     std::vector<int> nodes;
   };
   std::vector<Pending> pend;
+  // deferred matrix symmetry check (setup): [max |A - A^T|, max |A|] as double bits
+  unsigned long long* sym = nullptr;
+  double sym_rtol = 1e-12;
   void verify(cudaStream_t st);
 };
 void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check = nullptr);

@@ -145,6 +145,45 @@ def test_errors_map_to_reference_exceptions():
         sgf.pcg(-prob.matrix, np.ones(prob.n), precond=None, tol=1e-10)
 
 
+def test_asymmetric_matrix_rejected():
+    """blockmatrix.py:105-113: max |A - A^T| > 1e-12 max |A| raises, checked on
+    the device for host and device-resident values alike; a smaller asymmetry
+    passes."""
+    import torch
+
+    prob = sgf.poisson7(6)
+    A = prob.matrix.tocsr()
+    A.sort_indices()
+    r = 40
+    e = [k for k in range(A.indptr[r], A.indptr[r + 1]) if A.indices[k] != r][0]
+    scale = np.abs(A.data).max()
+
+    def with_entry(delta):
+        B = A.copy()
+        B.data[e] += delta
+        # check_symmetry=False: the constructor's own check is bypassed
+        return sgf.ProblemInstance(B, prob.coords, prob.grid, 1, prob.rhs, "p", check_symmetry=False), B
+
+    q, B = with_entry(1e-6 * scale)
+    with pytest.raises(sgf.NonSymmetricPatternError):
+        sgf.factorize(q)
+    with pytest.raises(sgf.NonSymmetricPatternError):
+        sgf.factorize(sgf.ProblemInstance(A, prob.coords, prob.grid, 1, prob.rhs, "p"),
+                      device_values=torch.tensor(B.data, device="cuda"))
+    q, _ = with_entry(1e-14 * scale)
+    P = sgf.factorize(q)
+    assert P.stats["flops_factorize"] > 0
+    # a structurally missing mirror entry is an asymmetry of its full value
+    C = A.tolil()
+    c = int(A.indices[e])
+    C[c, r] = 0.0
+    C = C.tocsr()
+    C.eliminate_zeros()
+    q = sgf.ProblemInstance(C, prob.coords, prob.grid, 1, prob.rhs, "p", check_symmetry=False)
+    with pytest.raises(sgf.NonSymmetricPatternError):
+        sgf.factorize(q)
+
+
 def test_pcg_edge_cases():
     prob = sgf.poisson7(7)
     P = sgf.factorize(prob, mode="exact")
