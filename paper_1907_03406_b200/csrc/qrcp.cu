@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <map>
 
 #include "common.h"
 
@@ -471,7 +472,8 @@ __device__ double sblock_sum(double v, double* red) {
   for (int i = 0; i < QSW; ++i) s += red[i];
   return s;
 }
-__global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
     qrcp_smem_kernel(const QrTask* __restrict__ tasks, int cpc) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -484,7 +486,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   __shared__ double wv[QSW];
   __shared__ int wi[QSW];
   const int q = (int)cluster.block_rank();
-  const QrTask T = tasks[blockIdx.x / QC];
+  const QrTask T = tasks[blockIdx.x / CS];
   const int m = T.m, c = T.c, kmax = min(m, c);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double eps = DBL_EPSILON;
@@ -499,14 +501,14 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   int* col_of = reinterpret_cast<int*>(ref2 + cpc);
   int* pos_of = col_of + c;
   int* done = pos_of + c;
-  const int nown = (c > q) ? (c - q + QC - 1) / QC : 0;  // owned columns q, q+QC, ...
+  const int nown = (c > q) ? (c - q + CS - 1) / CS : 0;  // owned columns q, q+CS, ...
   for (int j = tid; j < c; j += QST) {
     col_of[j] = j;
     pos_of[j] = j;
   }
   for (int l = tid; l < nown; l += QST) done[l] = 0;
   for (int l = 0; l < nown; ++l) {
-    const double* src = T.Nm + (long long)(q + QC * l) * m;
+    const double* src = T.Nm + (long long)(q + CS * l) * m;
     double* dst = cols + (size_t)l * mp;
     for (int i = tid; i < m; i += QST) dst[i] = src[i];
   }
@@ -535,7 +537,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   cluster.sync();
   {
     double mx = 0.0;
-    for (int r = 0; r < QC; ++r) mx = fmax(mx, *cluster.map_shared_rank(&s_amax, r));
+    for (int r = 0; r < CS; ++r) mx = fmax(mx, *cluster.map_shared_rank(&s_amax, r));
     amax = mx;
   }
   const double floor_ = eps * fmax(amax, 1.0);
@@ -548,7 +550,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
     int bp = c;
     for (int l = tid; l < nown; l += QST) {
       if (done[l]) continue;
-      const int cj = q + QC * l, pj = pos_of[cj];
+      const int cj = q + CS * l, pj = pos_of[cj];
       if (rep) {
         if (cj == T.replay[k]) { bv = 1.0; bp = pj; bn = nrm2[l]; }
       } else {
@@ -580,9 +582,9 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   if (limit > 0) local_candidate(0);
   for (int k = 0; k < limit; ++k) {
     cluster.sync();  // B1: candidates of k, every update of k-1
-    if (warp == 0) {   // lane r < QC fetches CTA r's candidate; (value, position) order is total
+    if (warp == 0) {   // lane r < CS fetches CTA r's candidate; (value, position) order is total
       QsCand o{-2.0, 0.0, c};
-      if (lane < QC) {
+      if (lane < CS) {
         o = *cluster.map_shared_rank(&cand[k & 1], lane);
         if (o.pos >= c) o.v = -2.0;
       }
@@ -609,9 +611,9 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
       pos_of[pc] = k;
       pos_of[ck] = pp;
     }
-    const int owner = pc % QC;
+    const int owner = pc % CS;
     if (owner == q) {
-      const int lp = pc / QC;
+      const int lp = pc / CS;
       double* xk = cols + (size_t)lp * mp;
       double ss = 0.0;
       for (int i = k + tid; i < m; i += QST) ss = fma(xk[i], xk[i], ss);
@@ -648,7 +650,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
     }
     __syncthreads();
     if (owner == q) {  // the pivot column: R_kk and the reflector below it
-      const int lp = pc / QC;
+      const int lp = pc / CS;
       double* xk = cols + (size_t)lp * mp;
       for (int i = k + 1 + tid; i < m; i += QST) xk[i] = vloc[i - k];
       if (tid == 0) {
@@ -658,7 +660,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
       }
     }
     for (int l = warp; l < nown; l += QSW) {
-      const int cj = q + QC * l;
+      const int cj = q + CS * l;
       if (cj == pc || done[l]) continue;
       double* col = cols + (size_t)l * mp + k;
       double s = 0.0;
@@ -689,7 +691,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   cluster.sync();  // every CTA has read its last remote data; all inputs were loaded long ago
   // columns to their final positions, permutation out
   for (int l = 0; l < nown; ++l) {
-    const int cj = q + QC * l;
+    const int cj = q + CS * l;
     const double* src = cols + (size_t)l * mp;
     double* dst = T.Nm + (long long)pos_of[cj] * m;
     for (int i = tid; i < m; i += QST) dst[i] = src[i];
@@ -703,9 +705,71 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QST)
   cluster.sync();  // keep every CTA's shared memory alive for remote reads
 }
 
+template <int CS>
 static size_t qrcp_smem_bytes(int m, int c) {
-  const size_t cpc = (size_t)(c + QC - 1) / QC, mp = (size_t)((m + 1) & ~1);
+  const size_t cpc = (size_t)(c + CS - 1) / CS, mp = (size_t)((m + 1) & ~1);
   return (cpc * mp + 2 * mp + 2 * cpc) * sizeof(double) + (2 * (size_t)c + cpc) * sizeof(int);
+}
+
+template <int CS>
+static cudaError_t qr_configure(size_t sb) {
+  static size_t conf = 0;
+  static bool np = false;
+  if (!np) {
+    cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    np = true;
+  }
+  if (sb > conf) {
+    cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    if (e != cudaSuccess) return e;
+    conf = sb;
+  }
+  return cudaSuccess;
+}
+
+template <int CS>
+static cudaError_t qr_launch_smem(const QrTask* d_tasks, int ntasks, size_t sb, int max_c, cudaStream_t s) {
+  cudaError_t e = qr_configure<CS>(sb);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  qrcp_smem_kernel<CS><<<ntasks * CS, QST, sb, s>>>(d_tasks, (max_c + CS - 1) / CS);
+  return cudaGetLastError();
+}
+
+// resident clusters of the shared-memory QR for a cluster size and shared
+// memory per CTA (cached: the occupancy query is a driver call)
+template <int CS>
+static int qr_active(size_t sb) {
+  if (qr_configure<CS>(sb) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS * 64);
+  cfg.blockDim = dim3(QST);
+  cfg.dynamicSmemBytes = sb;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = CS;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, qrcp_smem_kernel<CS>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+static int qr_active_clusters(int cs, size_t sb) {
+  static std::map<std::pair<int, size_t>, int> cache;
+  const size_t key_sb = (sb + 4095) / 4096 * 4096;
+  auto it = cache.find({cs, key_sb});
+  if (it != cache.end()) return it->second;
+  int n = cs == 16 ? qr_active<16>(key_sb) : cs == 12 ? qr_active<12>(key_sb) : cs == 10 ? qr_active<10>(key_sb)
+                                                                                           : qr_active<8>(key_sb);
+  cache[{cs, key_sb}] = n;
+  return n;
 }
 
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c) {
@@ -728,23 +792,35 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
   }
   static int single = getenv("SGF_QR_SINGLE_CTA") ? 1 : 0;
   static int smem_ok = getenv("SGF_QR_SMEM") ? atoi(getenv("SGF_QR_SMEM")) : 1;
-  const size_t sb = qrcp_smem_bytes(max_m, max_c);
-  if (!single && smem_ok && sb <= (size_t)220 << 10) {
-    static size_t conf_s = 0;
-    static bool np_s = false;
-    if (!np_s) {
-      cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      np_s = true;
+  // Cluster size: the panel must fit the cluster's shared memory, and the
+  // wave's nodes run in rounds of (resident clusters); pick the size with the
+  // fewest rounds (16-CTA clusters: at most 7 resident on the GPCs), ties to
+  // the larger cluster (fewer columns per warp).
+  constexpr size_t SMEM_CAP = (size_t)220 << 10;
+  if (!single && smem_ok) {
+    int best_cs = 0, best_rounds = 1 << 30;
+    size_t best_sb = 0;
+    const int cands[4] = {16, 12, 10, 8};
+    for (int cs : cands) {
+      if (smem_ok > 1 && cs != smem_ok) continue;  // SGF_QR_SMEM=<size> forces a cluster size
+      const size_t sb = cs == 16 ? qrcp_smem_bytes<16>(max_m, max_c)
+                        : cs == 12 ? qrcp_smem_bytes<12>(max_m, max_c)
+                        : cs == 10 ? qrcp_smem_bytes<10>(max_m, max_c)
+                                   : qrcp_smem_bytes<8>(max_m, max_c);
+      if (sb > SMEM_CAP) continue;
+      const int act = qr_active_clusters(cs, sb);
+      if (act <= 0) continue;
+      const int rounds = (ntasks + act - 1) / act;
+      if (rounds < best_rounds) {
+        best_rounds = rounds;
+        best_cs = cs;
+        best_sb = sb;
+      }
     }
-    if (sb > conf_s) {
-      cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-      if (e != cudaSuccess) return e;
-      conf_s = sb;
-    }
-    count_launch();
-    qrcp_smem_kernel<<<ntasks * QC, QST, sb, s>>>(d_tasks, (max_c + QC - 1) / QC);
-    return cudaGetLastError();
+    if (best_cs == 16) return qr_launch_smem<16>(d_tasks, ntasks, best_sb, max_c, s);
+    if (best_cs == 12) return qr_launch_smem<12>(d_tasks, ntasks, best_sb, max_c, s);
+    if (best_cs == 10) return qr_launch_smem<10>(d_tasks, ntasks, best_sb, max_c, s);
+    if (best_cs == 8) return qr_launch_smem<8>(d_tasks, ntasks, best_sb, max_c, s);
   }
   count_launch();
   if (single) qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
