@@ -283,10 +283,20 @@ int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, 
     A->a.rp = A->a.mem.alloc_t<long long>(n + 1);
     A->a.ci = A->a.mem.alloc_t<int>(std::max<int64_t>(nnz, 1));
     A->a.v = A->a.mem.alloc(std::max<int64_t>(nnz, 1));
-    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    SGF_CUDA(cudaMemcpyAsync(A->a.rp, indptr, (n + 1) * 8, k, st));
-    SGF_CUDA(cudaMemcpyAsync(A->a.ci, indices, nnz * 4, k, st));
-    SGF_CUDA(cudaMemcpyAsync(A->a.v, values, nnz * 8, k, st));
+    if (on_device) {
+      SGF_CUDA(cudaMemcpyAsync(A->a.rp, indptr, (n + 1) * 8, cudaMemcpyDeviceToDevice, st));
+      SGF_CUDA(cudaMemcpyAsync(A->a.ci, indices, nnz * 4, cudaMemcpyDeviceToDevice, st));
+      SGF_CUDA(cudaMemcpyAsync(A->a.v, values, nnz * 8, cudaMemcpyDeviceToDevice, st));
+    } else {  // host arrays: through the pinned staging ring (parallel copies, DMA overlapped)
+      auto up = [&](void* dst, const void* src, size_t bytes) {
+        constexpr size_t PIECE = (size_t)32 << 20;
+        for (size_t o = 0; o < bytes; o += PIECE)
+          stage_upload(st, (char*)dst + o, (const char*)src + o, std::min(PIECE, bytes - o));
+      };
+      up(A->a.rp, indptr, (size_t)(n + 1) * 8);
+      up(A->a.ci, indices, (size_t)nnz * 4);
+      up(A->a.v, values, (size_t)nnz * 8);
+    }
     if (nnz <= (int64_t)INT32_MAX) {
       A->a.rp32 = A->a.mem.alloc_t<int>(n + 1);
       SGF_CUDA(launch_rowptr32(A->a.rp, A->a.rp32, n + 1, st));
