@@ -111,7 +111,7 @@ struct OzTask {
   int kstart;  // ... and start at kstart
 };
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
-                            long long total_groups, cudaStream_t s);
+                            long long total_groups, cudaStream_t s, bool all_rowc = false);
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s);
 
 // ---- apply / GEMV -----------------------------------------------------------------

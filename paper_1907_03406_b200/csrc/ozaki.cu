@@ -25,6 +25,7 @@
 // rows of a tile of one (k-tile, slice) are one contiguous 4 KB range, moved
 // by one bulk copy.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.h"
 #include "ptx_util.cuh"
@@ -136,6 +137,95 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
       uint4 v4 = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
       *reinterpret_cast<uint4*>(J.out + ((size_t)kt * OZ_S + t) * blk + off) = v4;
     }
+  }
+}
+
+// Same split for row-contiguous operands (cs == 1), one CTA per 8-row group
+// with coalesced reads: warp w streams row w (lane = column), once for the
+// row maxima and once into a shared 8 x 512 tile from which the slices are
+// cut in the store-friendly lane mapping of oz_split_kernel.  (The warp-per-
+// group form reads 16-element runs per lane and fetched ~2x the operand bytes
+// from HBM.)  Identical output.
+constexpr int OZS_TK = 512, OZS_PITCH = OZS_TK + 4;
+__global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __restrict__ jobs,
+                                                           const long long* __restrict__ group_prefix, int njobs) {
+  __shared__ double tile[8 * OZS_PITCH];
+  __shared__ int sex[8];
+  const long long gw = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lo = 0, hi = njobs - 1;  // job containing row group gw
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (group_prefix[mid] <= gw) lo = mid;
+    else hi = mid - 1;
+  }
+  const OzSplitJob J = jobs[lo];
+  const int g0 = (int)(gw - group_prefix[lo]) * 8;
+  {  // pass 1: row maxima, warp w = row g0 + w
+    const int r = g0 + warp;
+    double mx = 0.0;
+    if (r < J.R) {
+      const double* row = J.x + (long long)r * J.rs;
+      for (int k = lane; k < J.K; k += 32) mx = fmax(mx, fabs(__ldg(row + k)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      int e = 0;
+      if (mx > 0.0) frexp(mx, &e);  // |x| 2^-ex < 1
+      sex[warp] = e;
+      if (r < J.R) J.exps[r] = e;
+    }
+  }
+  __syncthreads();
+  const int rl = lane & 7, r = g0 + rl;
+  const int ex = sex[rl];
+  const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
+  for (int kb = 0; kb < J.Kp; kb += OZS_TK) {
+    {  // stage rows g0..g0+7, columns [kb, kb + 512)
+      const int rr = g0 + warp;
+      const double* row = J.x + (long long)rr * J.rs;
+#pragma unroll 4
+      for (int i = lane; i < OZS_TK; i += 32) {
+        const int k = kb + i;
+        tile[warp * OZS_PITCH + i] = (rr < J.R && k < J.K) ? __ldg(row + k) : 0.0;
+      }
+    }
+    __syncthreads();
+    const int ci = warp * 4 + (lane >> 3);  // 16-element chunk of the tile
+    const int k0 = kb + ci * 16;
+    if (k0 < J.Kp) {
+      unsigned w[OZ_S][4];
+#pragma unroll
+      for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double x = tile[rl * OZS_PITCH + ci * 16 + q];
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+        const int bexp = (int)((bits >> 52) & 0x7FF);
+        unsigned long long F = 0;
+        if (bexp != 0) {
+          const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+          const int sh = bexp - 1075 + 56 - ex;  // F = |x| 2^(56-ex)
+          F = sh >= 0 ? (sh < 11 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
+        }
+        const bool neg = (long long)bits < 0;
+#pragma unroll
+        for (int t = 0; t < OZ_S; ++t) {
+          int d = (int)((F >> (7 * (OZ_S - 1 - t))) & 0x7F);
+          if (neg) d = -d;
+          w[t][q >> 2] |= ((unsigned)d & 0xFFu) << (8 * (q & 3));
+        }
+      }
+      const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
+      const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
+#pragma unroll
+      for (int t = 0; t < OZ_S; ++t) {
+        uint4 v4 = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
+        *reinterpret_cast<uint4*>(J.out + ((size_t)kt * OZ_S + t) * blk + off) = v4;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -336,10 +426,15 @@ extern "C" int sgf_oz_prof_read(unsigned long long* out, int reset) {
 
 // d_group_prefix: per job the first global 8-row group (njobs + 1 entries)
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
-                            long long total_groups, cudaStream_t s) {
+                            long long total_groups, cudaStream_t s, bool all_rowc) {
   if (njobs <= 0 || total_groups <= 0) return cudaSuccess;
-  const long long threads = total_groups * 32;
   count_launch();
+  static const int cta = getenv("SGF_OZ_SPLIT_WARP") ? 0 : 1;
+  if (cta && all_rowc && total_groups < (1LL << 31)) {
+    oz_split_cta_kernel<<<(unsigned)total_groups, 256, 0, s>>>(d_jobs, d_group_prefix, njobs);
+    return cudaGetLastError();
+  }
+  const long long threads = total_groups * 32;
   oz_split_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d_jobs, d_group_prefix, njobs);
   return cudaGetLastError();
 }

@@ -298,15 +298,22 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
-  std::vector<long long> prefix(jobs.size() + 1, 0);  // 8-row groups
-  for (size_t i = 0; i < jobs.size(); ++i) prefix[i + 1] = prefix[i] + jobs[i].Rp / 8;
-  OzSplitJob* d_j = scratch.upload(jobs);
-  long long* d_p = scratch.upload(prefix);
-  double bytes = 0.0;  // FP64 read + 8 slices written per element
-  if (g_prof.on)
-    for (auto& j : jobs) bytes += 16.0 * j.Rp * j.Kp;
-  ProfScope ps(st, PROF_OZSPLIT, bytes);
-  SGF_CUDA(launch_oz_split(d_j, d_p, (int)jobs.size(), prefix.back(), st));
+  // row-contiguous operands (coalesced CTA kernel) and the others, one launch each
+  std::vector<OzSplitJob> part[2];
+  for (auto& j : jobs) part[j.cs == 1 ? 0 : 1].push_back(j);
+  for (int w = 0; w < 2; ++w) {
+    auto& js = part[w];
+    if (js.empty()) continue;
+    std::vector<long long> prefix(js.size() + 1, 0);  // 8-row groups
+    for (size_t i = 0; i < js.size(); ++i) prefix[i + 1] = prefix[i] + js[i].Rp / 8;
+    OzSplitJob* d_j = scratch.upload(js);
+    long long* d_p = scratch.upload(prefix);
+    double bytes = 0.0;  // FP64 read + 8 slices written per element
+    if (g_prof.on)
+      for (auto& j : js) bytes += 16.0 * j.Rp * j.Kp;
+    ProfScope ps(st, PROF_OZSPLIT, bytes);
+    SGF_CUDA(launch_oz_split(d_j, d_p, (int)js.size(), prefix.back(), st, w == 0));
+  }
   jobs.clear();
 }
 
