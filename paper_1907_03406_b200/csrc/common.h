@@ -61,6 +61,7 @@ struct CopyTask {
   long long s_rs, s_cs;
   long long d_rs, d_cs;
   int rows, cols;
+  int lower = 0;  // 1: copy the lower triangle (col <= row), write zeros above it
 };
 
 // ---- column-pivoted QR (truncated at the rank) ------------------------------------

@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyTask* __restrict__ 
     for (int q = ty; q < 32; q += 8) {
       int r = src_rowc ? q : tx, c = src_rowc ? tx : q;
       int gr = r0 + r, gc = c0 + c;
-      if (gr < T.rows && gc < T.cols) buf[r][c] = T.src[(long long)gr * T.s_rs + (long long)gc * T.s_cs];
+      if (gr < T.rows && gc < T.cols)
+        buf[r][c] = (T.lower && gc > gr) ? 0.0 : T.src[(long long)gr * T.s_rs + (long long)gc * T.s_cs];
     }
     __syncthreads();
     const bool dst_rowc = (T.d_cs == 1);

@@ -551,8 +551,10 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     oe += (size_t)e.c * e.ld;
     Blk* d = M.find(e.x, e.x);
     if (!d) fail(SGF_NOT_SPD, "interior node without a diagonal block");
-    cp.add(d->p, d->cols, 1, e.W, e.ld, 1, e.m, e.m);
+    // diagonal blocks are valid in their lower triangle only: copy that, zero above
+    cp.add_lower(d->p, d->cols, 1, e.W, e.ld, 1, e.m);
     jobs.push_back(CholJob{e.W, e.X, e.m, e.x, e.ld});
+    jobs.back().upper_zero = true;
     if (level == 1 && !S.l1_bw.empty()) jobs.back().bw = std::max(1, S.l1_bw[e.x]);
   }
   cp.launch(S.scratch, st);
@@ -1174,8 +1176,9 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
       p.LP = S.lvl->alloc((size_t)m * pi);
       Blk* d = M.find(c, c);
       if (!d) fail(SGF_NOT_SPD, "compressed node without a diagonal block");
-      cp.add(d->p, d->cols, 1, p.L, p.ld, 1, m, m);
+      cp.add_lower(d->p, d->cols, 1, p.L, p.ld, 1, m);
       jobs.push_back(CholJob{p.L, p.X, m, c, p.ld});
+      jobs.back().upper_zero = true;
       pre[c] = p;
     }
     cp.launch(S.scratch, st);

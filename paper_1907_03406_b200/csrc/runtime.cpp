@@ -487,7 +487,8 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
   oz.launch(scratch, st);
   // L has exact zeros above the diagonal: the A12 block of W
   std::vector<TriTask> up;
-  for (int i = 0; i < nb; ++i) up.push_back(TriTask{big[i].W, big[i].m, big[i].ld});
+  for (int i = 0; i < nb; ++i)
+    if (!big[i].upper_zero) up.push_back(TriTask{big[i].W, big[i].m, big[i].ld});
   zero_upper(scratch, st, up);
 }
 
@@ -613,7 +614,8 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
     gc.launch(scratch, st);
   }
   std::vector<TriTask> tri;
-  for (auto& j : jobs) tri.push_back(TriTask{j.W, j.m, j.ld});
+  for (auto& j : jobs)
+    if (!j.upper_zero) tri.push_back(TriTask{j.W, j.m, j.ld});
   zero_upper(scratch, st, tri);
 
   CholCheck local;

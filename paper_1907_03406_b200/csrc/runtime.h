@@ -583,6 +583,13 @@ struct CopyBatch {
     CopyTask t{src, dst, s_rs, s_cs, d_rs, d_cs, rows, cols};
     tasks.push_back(t);
   }
+  // lower triangle of a square block, zeros above it (no separate zeroing pass)
+  void add_lower(const double* src, long long s_rs, long long s_cs, double* dst, long long d_rs, long long d_cs,
+                 int m) {
+    if (m <= 0) return;
+    CopyTask t{src, dst, s_rs, s_cs, d_rs, d_cs, m, m, 1};
+    tasks.push_back(t);
+  }
   void launch(Arena& scratch, cudaStream_t st);
 };
 
@@ -598,6 +605,7 @@ struct CholJob {
   int ld;    // leading dimension of W and X (>= m; even so rows are 16-byte aligned)
   const double* floor = nullptr;  // pivot floor (device) of the enclosing matrix; null: from this W
   int bw = 0;  // lower bandwidth of W (W[i][j] == 0 for i - j > bw; L inherits it); 0: dense
+  bool upper_zero = false;  // W's strict upper triangle is zero on entry (no zeroing pass at the end)
 };
 
 // leading dimension of stored factor matrices: even, so every row starts
