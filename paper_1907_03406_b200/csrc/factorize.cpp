@@ -255,7 +255,12 @@ void setup_level1(State& S) {
   double* d_vhost = a.values_on_device ? nullptr : S.scratch.alloc(std::max<int64_t>(a.nnz, 1));
   int* d_own = S.scratch.alloc_t<int>(n);
   int* d_loc = S.scratch.alloc_t<int>(n);
-  std::vector<int32_t> owner(n, -1), local(n, 0);
+  // owner / local live directly in their pinned upload slots (no host
+  // vectors to fault in, no staging copy)
+  int32_t* owner = (int32_t*)(pin + o_own);
+  int32_t* local = (int32_t*)(pin + o_loc);
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < n; ++u) owner[u] = -1;
   std::vector<int> sizes(nc);
   S.nodes.assign(nc, Node());
   int bad_cover = 0;
@@ -275,8 +280,10 @@ void setup_level1(State& S) {
     }
   }
   if (bad_cover || a.l1_ptr[nc] != n) fail(SGF_INVALID_ARG, "level-1 cells do not partition the unknowns");
-  for (int64_t u = 0; u < n; ++u)
-    if (owner[u] < 0) fail(SGF_INVALID_ARG, "node unknown lists do not cover all unknowns");
+  int hole = 0;
+#pragma omp parallel for schedule(static) reduction(| : hole)
+  for (int64_t u = 0; u < n; ++u) hole |= owner[u] < 0;
+  if (hole) fail(SGF_INVALID_ARG, "node unknown lists do not cover all unknowns");
 
   // symmetry of pattern and values (blockmatrix.py:105-113) is checked on the
   // device once the CSR is uploaded (sym_check_kernel), verified at the first
@@ -388,16 +395,18 @@ void setup_level1(State& S) {
       };
       std::vector<Piece> pieces = {{o_ip, d_ip, a.indptr, (size_t)(n + 1) * 8},
                                    {o_ix, d_ix, a.indices, (size_t)a.nnz * 4},
-                                   {o_own, d_own, owner.data(), (size_t)n * 4},
-                                   {o_loc, d_loc, local.data(), (size_t)n * 4}};
+                                   {o_own, d_own, nullptr, (size_t)n * 4},   // already in place
+                                   {o_loc, d_loc, nullptr, (size_t)n * 4}};
       if (d_vhost) pieces.push_back({o_v, d_vhost, a.values, (size_t)a.nnz * 8});
       constexpr size_t BLK = (size_t)1 << 20;
       for (auto& pc : pieces) {
         const long long nb = (long long)((pc.bytes + BLK - 1) / BLK);
+        if (pc.src) {
 #pragma omp parallel for schedule(static)
-        for (long long b = 0; b < nb; ++b) {
-          const size_t o = (size_t)b * BLK;
-          std::memcpy(pin + pc.off + o, (const char*)pc.src + o, std::min(BLK, pc.bytes - o));
+          for (long long b = 0; b < nb; ++b) {
+            const size_t o = (size_t)b * BLK;
+            std::memcpy(pin + pc.off + o, (const char*)pc.src + o, std::min(BLK, pc.bytes - o));
+          }
         }
         if (pc.bytes) SGF_CUDA(cudaMemcpyAsync(pc.dst, pin + pc.off, pc.bytes, cudaMemcpyHostToDevice, S.st));
       }
