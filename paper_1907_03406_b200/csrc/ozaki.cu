@@ -161,7 +161,10 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
   }
   const OzSplitJob J = jobs[lo];
   const int g0 = (int)(gw - group_prefix[lo]) * 8;
-  {  // pass 1: row maxima, warp w = row g0 + w
+  // trans: the 8 rows of a group are contiguous for every k (rs == 1): thread
+  // t reads row t & 7 at k = t >> 3 (+32 i), 64-byte runs per k
+  const bool trans = J.cs != 1;
+  if (!trans) {  // pass 1: row maxima, warp w = row g0 + w
     const int r = g0 + warp;
     double mx = 0.0;
     if (r < J.R) {
@@ -176,19 +179,44 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
       sex[warp] = e;
       if (r < J.R) J.exps[r] = e;
     }
+  } else {
+    const int r = g0 + (threadIdx.x & 7);
+    double mx = 0.0;
+    if (r < J.R)
+      for (int k = threadIdx.x >> 3; k < J.K; k += 32) mx = fmax(mx, fabs(__ldg(J.x + r + (long long)k * J.cs)));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    __shared__ double wm[8][8];
+    if (lane < 8) wm[warp][lane] = mx;
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      double m = 0.0;
+      for (int w = 0; w < 8; ++w) m = fmax(m, wm[w][threadIdx.x]);
+      int e = 0;
+      if (m > 0.0) frexp(m, &e);
+      sex[threadIdx.x] = e;
+      if (g0 + (int)threadIdx.x < J.R) J.exps[g0 + threadIdx.x] = e;
+    }
   }
   __syncthreads();
   const int rl = lane & 7, r = g0 + rl;
   const int ex = sex[rl];
   const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
   for (int kb = 0; kb < J.Kp; kb += OZS_TK) {
-    {  // stage rows g0..g0+7, columns [kb, kb + 512)
+    if (!trans) {  // stage rows g0..g0+7, columns [kb, kb + 512)
       const int rr = g0 + warp;
       const double* row = J.x + (long long)rr * J.rs;
 #pragma unroll 4
       for (int i = lane; i < OZS_TK; i += 32) {
         const int k = kb + i;
         tile[warp * OZS_PITCH + i] = (rr < J.R && k < J.K) ? __ldg(row + k) : 0.0;
+      }
+    } else {
+      const int rr = g0 + (threadIdx.x & 7);
+#pragma unroll 4
+      for (int i = threadIdx.x >> 3; i < OZS_TK; i += 32) {
+        const int k = kb + i;
+        tile[(threadIdx.x & 7) * OZS_PITCH + i] = (rr < J.R && k < J.K) ? __ldg(J.x + rr + (long long)k * J.cs) : 0.0;
       }
     }
     __syncthreads();

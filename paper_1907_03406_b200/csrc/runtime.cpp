@@ -300,7 +300,7 @@ void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
   // row-contiguous operands (coalesced CTA kernel) and the others, one launch each
   std::vector<OzSplitJob> part[2];
-  for (auto& j : jobs) part[j.cs == 1 ? 0 : 1].push_back(j);
+  for (auto& j : jobs) part[(j.cs == 1 || j.rs == 1) ? 0 : 1].push_back(j);  // the CTA kernel reads both
   for (int w = 0; w < 2; ++w) {
     auto& js = part[w];
     if (js.empty()) continue;
@@ -399,16 +399,23 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
   if (big.empty()) return;
   cudaStream_t st = ctx.stream;
   const int nb = (int)big.size();
-  // pivot floors of the whole nodes, shared by their halves
-  for (int i = 0; i < nb; ++i)
-    if (!big[i].floor) {
-      double* f = scratch.alloc(1);
-      const double* wp = big[i].W;
-      std::vector<const double*> wv{wp};
-      std::vector<int> mv{big[i].m}, lv{big[i].ld};
-      SGF_CUDA(launch_max_diag(scratch.upload(wv), scratch.upload(mv), scratch.upload(lv), 1, f, st));
-      big[i].floor = f;
+  // pivot floors of the whole nodes, shared by their halves (one launch)
+  {
+    std::vector<const double*> wv;
+    std::vector<int> mv, lv, who;
+    for (int i = 0; i < nb; ++i)
+      if (!big[i].floor) {
+        wv.push_back(big[i].W);
+        mv.push_back(big[i].m);
+        lv.push_back(big[i].ld);
+        who.push_back(i);
+      }
+    if (!wv.empty()) {
+      double* f = scratch.alloc(wv.size());
+      SGF_CUDA(launch_max_diag(scratch.upload(wv), scratch.upload(mv), scratch.upload(lv), (int)wv.size(), f, st));
+      for (size_t k = 0; k < who.size(); ++k) big[who[k]].floor = f + k;
     }
+  }
   std::vector<int> m1(nb), m2(nb);
   std::vector<CholJob> j11, j22;
   for (int i = 0; i < nb; ++i) {
