@@ -28,6 +28,12 @@ import sys
 import threading
 import time
 
+# torchrun sets OMP_NUM_THREADS=1 per rank; the native host pipeline (block
+# discovery, staging copies, task lists) is OpenMP-parallel, so give each
+# rank its share of the host cores instead (before any OpenMP runtime loads)
+if "LOCAL_WORLD_SIZE" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1":
+    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // max(1, int(os.environ["LOCAL_WORLD_SIZE"]))))
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
