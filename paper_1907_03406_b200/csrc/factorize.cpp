@@ -1294,19 +1294,33 @@ void merge_level(State& S, const int64_t* father, int next_nc, const int8_t* kin
   std::vector<std::pair<uint64_t, long long>> order;
   FlatMap<long long> newoff(M.map.size());
   long long tot = 0;
+  // live blocks in table-walk order, then the father-key inserts with the
+  // slot of the insert 16 ahead prefetched (DRAM-latency bound otherwise)
+  struct LiveBlk {
+    Blk b;
+    int a0, b0;
+    uint64_t fk;
+  };
+  std::vector<LiveBlk> live;
+  live.reserve(M.map.size());
   M.map.for_each([&](uint64_t k, Blk& b) {
     if ((long long)b.rows * b.cols == 0) return;
     const int a0 = (int)(k >> 32), b0 = (int)(k & 0xffffffffu);
-    const uint64_t fk = bkey(fof[a0], fof[b0]);
-    auto ins = newoff.emplace(fk);
+    live.push_back(LiveBlk{b, a0, b0, bkey(fof[a0], fof[b0])});
+  });
+  constexpr size_t PF = 16;
+  for (size_t i = 0; i < live.size(); ++i) {
+    if (i + PF < live.size()) newoff.prefetch(live[i + PF].fk);
+    const LiveBlk& L = live[i];
+    auto ins = newoff.emplace(L.fk);
     if (ins.second) {
-      const int fa = (int)(fk >> 32), fb = (int)(fk & 0xffffffffu);
+      const int fa = (int)(L.fk >> 32), fb = (int)(L.fk & 0xffffffffu);
       *ins.first = tot;
-      order.push_back({fk, tot});
+      order.push_back({L.fk, tot});
       tot += (long long)nsize[fa] * nsize[fb];
     }
-    mbs.push_back(MB{b, a0, b0, *ins.first});
-  });
+    mbs.push_back(MB{L.b, L.a0, L.b0, *ins.first});
+  }
   double* base = nl->alloc(std::max<long long>(tot, 1));
   if (tot) SGF_CUDA(cudaMemsetAsync(base, 0, tot * sizeof(double), st));
   S.regions.assign(1, {base, tot});

@@ -346,11 +346,35 @@ void OzBatch::launch(Arena& scratch, cudaStream_t st) {
 
 void CopyBatch::launch(Arena& scratch, cudaStream_t st) {
   if (tasks.empty()) return;
-  std::vector<long long> prefix(tasks.size());
+  const size_t nt = tasks.size();
+  std::vector<long long> prefix(nt);
   long long tot = 0;
-  for (size_t i = 0; i < tasks.size(); ++i) {
-    prefix[i] = tot;
-    tot += (long long)((tasks[i].rows + 31) / 32) * ((tasks[i].cols + 31) / 32);
+  auto tiles = [&](size_t i) { return (long long)((tasks[i].rows + 31) / 32) * ((tasks[i].cols + 31) / 32); };
+  if (nt < 65536) {
+    for (size_t i = 0; i < nt; ++i) {
+      prefix[i] = tot;
+      tot += tiles(i);
+    }
+  } else {  // large merges: blocked two-pass exclusive scan
+    constexpr size_t B = 4096;
+    const size_t nb = (nt + B - 1) / B;
+    std::vector<long long> bsum(nb + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (size_t b = 0; b < nb; ++b) {
+      long long s = 0;
+      for (size_t i = b * B; i < std::min(nt, (b + 1) * B); ++i) s += tiles(i);
+      bsum[b + 1] = s;
+    }
+    for (size_t b = 0; b < nb; ++b) bsum[b + 1] += bsum[b];
+#pragma omp parallel for schedule(static)
+    for (size_t b = 0; b < nb; ++b) {
+      long long s = bsum[b];
+      for (size_t i = b * B; i < std::min(nt, (b + 1) * B); ++i) {
+        prefix[i] = s;
+        s += tiles(i);
+      }
+    }
+    tot = bsum[nb];
   }
   CopyTask* d_t = scratch.upload(tasks);
   long long* d_p = scratch.upload(prefix);
