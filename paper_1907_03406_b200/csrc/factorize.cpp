@@ -698,20 +698,28 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   // Schur targets in the reference's insertion order (ascending interior id,
   // neighbour pairs a <= b); a target first seen without a block is a fill,
   // created zero (blockmatrix.py:65-72) when its first contributor runs
+  // contributions of a target: a list threaded through one flat array (in
+  // ascending interior order; no per-target heap allocation)
+  struct Contrib {
+    int q, p, r, next;
+  };
   struct Target {
     int a, b;
     int q0;                 // first contributing interior (creation point of a fill)
     long long fill = -1;    // offset in the fill region, -1: existing block
-    std::vector<std::pair<int, std::pair<int, int>>> contrib;
+    int head = -1, tail = -1, count = 0;
   };
   HostTimer ht1("elim targets");
   std::vector<Target> targets;
+  std::vector<Contrib> cbuf;
   std::vector<int> fills;  // target ids of fills, in creation order
   long long fill_elems = 0;
   {
     size_t pairs = 0;
     for (auto& e : info) pairs += e.nb.size() * (e.nb.size() + 1) / 2;
-    FlatMap<int> tix(pairs / 4 + 16);
+    FlatMap<int> tix(pairs / 2 + 16);
+    targets.reserve(pairs / 2 + 16);
+    cbuf.reserve(pairs);
     for (size_t q = 0; q < info.size(); ++q) {
       const EI& e = info[q];
       for (size_t p = 0; p < e.nb.size(); ++p)
@@ -720,14 +728,22 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
           auto ins = tix.emplace(bkey(A, B));
           if (ins.second) {
             *ins.first = (int)targets.size();
-            targets.push_back(Target{A, B, (int)q, -1, {}});
+            targets.push_back(Target{A, B, (int)q, -1});
             if (!M.find(A, B)) {
               targets.back().fill = fill_elems;
               fills.push_back(*ins.first);
               fill_elems += (long long)M.size[A] * M.size[B];
             }
           }
-          if (own[q]) targets[*ins.first].contrib.push_back({(int)q, {(int)p, (int)r}});
+          if (own[q]) {
+            Target& T = targets[*ins.first];
+            const int ci = (int)cbuf.size();
+            cbuf.push_back(Contrib{(int)q, (int)p, (int)r, -1});
+            if (T.tail >= 0) cbuf[T.tail].next = ci;
+            else T.head = ci;
+            T.tail = ci;
+            ++T.count;
+          }
         }
     }
   }
@@ -757,29 +773,31 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         br = M.size[T.a];
         bc = M.size[T.b];
       }
-      if (T.contrib.empty()) continue;  // sharded: no contributor on this rank
+      if (T.count == 0) continue;  // sharded: no contributor on this rank
       if (sparse1) {
         const int c0 = (int)l1c.size();
-        for (auto& c : T.contrib) {
-          const EI& e = info[c.first];
-          l1c.push_back(L1Contrib{rl_base[c.first] + e.off[c.second.first], rl_base[c.first] + e.off[c.second.second],
-                                  Gall + (e.X - Xall), (long long)e.ld});
+        for (int ci = T.head; ci >= 0; ci = cbuf[ci].next) {
+          const Contrib& c = cbuf[ci];
+          const EI& e = info[c.q];
+          l1c.push_back(L1Contrib{rl_base[c.q] + e.off[c.p], rl_base[c.q] + e.off[c.r], Gall + (e.X - Xall),
+                                  (long long)e.ld});
         }
         for (int r0 = 0; r0 < br; r0 += 64)
-          l1s.push_back(L1SchurTask{bp, (long long)bc, r0, br, bc, T.a == T.b, c0, (int)T.contrib.size()});
+          l1s.push_back(L1SchurTask{bp, (long long)bc, r0, br, bc, T.a == T.b, c0, T.count});
         continue;
       }
       sg.clear();
-      for (auto& c : T.contrib) {
-        const EI& e = info[c.first];
-        sg.push_back(seg(e.E + (long long)e.off[c.second.first] * e.ld, e.ld, 1,
-                         e.E + (long long)e.off[c.second.second] * e.ld, e.ld, 1, e.m));
+      for (int ci = T.head; ci >= 0; ci = cbuf[ci].next) {
+        const Contrib& c = cbuf[ci];
+        const EI& e = info[c.q];
+        sg.push_back(seg(e.E + (long long)e.off[c.p] * e.ld, e.ld, 1, e.E + (long long)e.off[c.r] * e.ld, e.ld, 1, e.m));
       }
       // diagonal blocks are kept valid in their lower triangle only: every
       // consumer (Cholesky of the node, densify + Cholesky) reads only that
       if (oz_schur) {
         std::vector<std::pair<std::pair<OzOperand, OzOperand>, double>> terms;
-        for (auto& c : T.contrib) terms.push_back({{eop[c.first][c.second.first], eop[c.first][c.second.second]}, -1.0});
+        for (int ci = T.head; ci >= 0; ci = cbuf[ci].next)
+          terms.push_back({{eop[cbuf[ci].q][cbuf[ci].p], eop[cbuf[ci].q][cbuf[ci].r]}, -1.0});
         oz.add(bp, bc, 1, br, bc, 1.0, terms, T.a == T.b, false);
       } else {
         gs.add(bp, bc, 1, br, bc, -1.0, 1.0, sg, -1, T.a == T.b);
