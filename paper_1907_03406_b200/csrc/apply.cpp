@@ -256,13 +256,16 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     // level-1 eliminations with G and the coupling lists of the whole level
     bool sym = g.type == SGF_FACTOR_ELIMINATION && P->l1.ready && om == P->l1.nb;
     for (size_t i = rg.first; sym && i < rg.second; ++i) sym = fs[i]->G != nullptr && fs[i]->level == 1;
+    g.idx = plan->mem.upload(idx);
     if (sym) {
       std::vector<SymvTask> tf, tb;
       long long o = 0;
       for (size_t i = rg.first; i < rg.second; ++i) {
         const Factor& f = *fs[i];
-        tf.push_back(SymvTask{f.G, f.ld, g.xb + o, nullptr, g.zb + o, f.m, 1.0});
-        tb.push_back(SymvTask{f.G, f.ld, g.acc + o, g.xb + o, g.zb + o, f.m, -1.0});
+        // unfused form: x/base/result in the group's gathered buffers; fused
+        // form (launch_symv_fused): through idx on the full vector
+        tf.push_back(SymvTask{f.G, f.ld, g.xb + o, nullptr, g.zb + o, f.m, 1.0, g.idx + o, 1});
+        tb.push_back(SymvTask{f.G, f.ld, g.acc + o, g.xb + o, g.zb + o, f.m, -1.0, g.idx + o, 0});
         g.sym_maxm = std::max(g.sym_maxm, f.m);
         g.bytes_sym += 4.0 * f.m * (f.m + 1.0);
         o += f.m;
@@ -272,7 +275,6 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       g.sym_f = plan->mem.upload(tf);
       g.sym_b = plan->mem.upload(tb);
     }
-    g.idx = plan->mem.upload(idx);
     g.nidx = plan->mem.upload(nidx);
     g.bytes_f1 = gemv_bytes(f1, 0);
     g.bytes_f2 = gemv_bytes(f2, 0);
@@ -356,18 +358,30 @@ static void symv(const SymvTask* t, int nt, int maxm, double bytes, cudaStream_t
   SGF_CUDA(launch_symv(t, nt, maxm, st));
 }
 
+// with the fused symv, the gather of x_B and the scatter of the result go
+// through the nodes' index arrays inside the kernel (two launches fewer per sweep)
 static void forward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
-  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
-  symv(g.sym_f, g.nsym, g.sym_maxm, g.bytes_sym, st);
-  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  if (symv_fused_ok(g.sym_maxm)) {
+    ProfScope ps(st, PROF_GEMV, g.bytes_sym);
+    SGF_CUDA(launch_symv_fused(g.sym_f, g.nsym, g.sym_maxm, y, st));
+  } else {
+    SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+    symv(g.sym_f, g.nsym, g.sym_maxm, g.bytes_sym, st);
+    SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  }
   SGF_CUDA(launch_sub_spmv(c.nf, c.f_rid, c.f_rp, c.f_ci, c.f_v, y, nullptr, 0, st));
 }
 
 static void backward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
   SGF_CUDA(launch_sub_spmv(c.nb, nullptr, c.b_rp, c.b_ci, c.b_v, y, g.acc, 1, st));
-  SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
-  symv(g.sym_b, g.nsym, g.sym_maxm, g.bytes_sym, st);
-  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  if (symv_fused_ok(g.sym_maxm)) {
+    ProfScope ps(st, PROF_GEMV, g.bytes_sym);
+    SGF_CUDA(launch_symv_fused(g.sym_b, g.nsym, g.sym_maxm, y, st));
+  } else {
+    SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
+    symv(g.sym_b, g.nsym, g.sym_maxm, g.bytes_sym, st);
+    SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
+  }
 }
 
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {

@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(256, SYMV_MINB) symv_kernel(const SymvTask* __
 // (~200 KB of G in flight per SM, against ~70 KB issued by the register
 // version, whose loads also wait behind each pair's reduction).
 template <int Q, int S>
-__global__ void __launch_bounds__(256, 3) symv_bulk_kernel(const SymvTask* __restrict__ tasks) {
+__global__ void __launch_bounds__(256, 3) symv_bulk_kernel(const SymvTask* __restrict__ tasks, double* __restrict__ v) {
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bar[8 * S];
   constexpr int MP = 64 * Q;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256, 3) symv_bulk_kernel(const SymvTask* __res
     for (int s = 0; s < S; ++s)
       if (warp + 8 * s < npairs) issue(warp + 8 * s, s);
   }
-  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? T.x[i] : 0.0;
+  for (int i = threadIdx.x; i < MP; i += 256) xs[i] = i < m ? ((v && T.gather_x) ? v[T.idx[i]] : T.x[i]) : 0.0;
   __syncthreads();
   double c0[Q], c1[Q];
 #pragma unroll
@@ -476,13 +476,18 @@ __global__ void __launch_bounds__(256, 3) symv_bulk_kernel(const SymvTask* __res
     double c = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) c += ring[w * MP + j];
-    const double v = yr[j] + c;
-    T.y[j] = T.base ? fma(T.sign, v, T.base[j]) : T.sign * v;
+    const double r = yr[j] + c;
+    if (v) {  // fused: base from and result to the full vector (this node's unknowns only)
+      const int u = T.idx[j];
+      v[u] = T.base ? fma(T.sign, r, v[u]) : T.sign * r;
+    } else {
+      T.y[j] = T.base ? fma(T.sign, r, T.base[j]) : T.sign * r;
+    }
   }
 }
 
 template <int Q, int S>
-static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
+static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s, double* v = nullptr) {
   // ring (8 warps x S slots) also holds the 8 x MP column partials at the end
   const size_t ring = (size_t)8 * std::max(S * (64 * Q + 2), 64 * Q);
   const size_t smem = (2 * (size_t)64 * Q + ring) * sizeof(double);
@@ -493,7 +498,7 @@ static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  count_launch(); symv_bulk_kernel<Q, S><<<ntasks, 256, smem, s>>>(d_tasks);
+  count_launch(); symv_bulk_kernel<Q, S><<<ntasks, 256, smem, s>>>(d_tasks, v);
   return cudaGetLastError();
 }
 
@@ -510,10 +515,25 @@ static cudaError_t symv_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static int symv_variant() {
+  static const int variant = getenv("SGF_SYMV") ? atoi(getenv("SGF_SYMV")) : 1;
+  return variant;
+}
+
+bool symv_fused_ok(int max_m) { return symv_variant() == 1 && max_m <= 768; }
+
+cudaError_t launch_symv_fused(const SymvTask* d_tasks, int ntasks, int max_m, double* v, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  if (max_m <= 128) return symv_bulk_q<2, 4>(d_tasks, ntasks, s, v);
+  if (max_m <= 256) return symv_bulk_q<4, 3>(d_tasks, ntasks, s, v);
+  if (max_m <= 512) return symv_bulk_q<8, 2>(d_tasks, ntasks, s, v);
+  if (max_m <= 768) return symv_bulk_q<12, 2>(d_tasks, ntasks, s, v);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  static const int variant = getenv("SGF_SYMV") ? atoi(getenv("SGF_SYMV")) : 1;
-  if (variant == 1) {
+  if (symv_variant() == 1) {
     if (max_m <= 128) return symv_bulk_q<2, 4>(d_tasks, ntasks, s);
     if (max_m <= 256) return symv_bulk_q<4, 3>(d_tasks, ntasks, s);
     if (max_m <= 512) return symv_bulk_q<8, 2>(d_tasks, ntasks, s);

@@ -141,6 +141,8 @@ struct SymvTask {
   double* y;
   int m;
   double sign;
+  const int* idx = nullptr;  // the node's unknowns in the full vector (fused gather/scatter, see launch_symv)
+  int gather_x = 0;          // fused: x = v[idx] (else x as given)
 };
 
 struct QrFinishTask {
@@ -234,6 +236,10 @@ inline bool l1_e_fits(int max_m, int max_c) {  // shared memory of launch_l1_e
 cudaError_t launch_l1_schur(const L1SchurTask* d_tasks, int ntasks, const L1Contrib* d_contrib, const int* rl_n,
                             const int* rl_k, const double* rl_a, cudaStream_t s);
 cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStream_t s);
+// fused form on a full vector v: x = v[idx] (gather_x) or the task's x, base = v[idx] when the
+// task has a base, result written to v[idx]; false when the selected kernel has no fused form
+bool symv_fused_ok(int max_m);
+cudaError_t launch_symv_fused(const SymvTask* d_tasks, int ntasks, int max_m, double* v, cudaStream_t s);
 // sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
 cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,
                             double* out, int mode, cudaStream_t s);
