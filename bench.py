@@ -31,8 +31,11 @@ import time
 # torchrun sets OMP_NUM_THREADS=1 per rank; the native host pipeline (block
 # discovery, staging copies, task lists) is OpenMP-parallel, so give each
 # rank its share of the host cores instead (before any OpenMP runtime loads)
+# (the reference arm runs on rank 0 alone and takes every host core)
 if "LOCAL_WORLD_SIZE" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1":
-    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // max(1, int(os.environ["LOCAL_WORLD_SIZE"]))))
+    _ref_arm = "reference" in sys.argv[1:] and "--impl" in sys.argv[1:]
+    _share = 1 if _ref_arm else max(1, int(os.environ["LOCAL_WORLD_SIZE"]))
+    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // _share))
 
 import numpy as np
 
