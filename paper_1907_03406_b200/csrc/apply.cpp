@@ -520,6 +520,7 @@ void apply_op(Precond* P, int op, const double* d_x, double* d_y) {
   ApplyPlan* pl = P->plan;
   if (op < 0 || op > 3) fail(SGF_INVALID_ARG, "unknown apply operation");
   if (P->sharded) fail(SGF_INVALID_ARG, "sharded preconditioner: apply through the collective sharded apply");
+  if (op != SGF_APPLY_INVERSE) materialize_l1_e(P);  // the L^{-1}/E form reads the level-1 couplings
   if (op == SGF_APPLY_OPERATOR) {
     prepare_operator(P);
     if (d_y != d_x) SGF_CUDA(cudaMemcpyAsync(d_y, d_x, P->n * sizeof(double), cudaMemcpyDeviceToDevice, st));

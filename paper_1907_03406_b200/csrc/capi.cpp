@@ -156,6 +156,7 @@ int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_ou
         break;
       case 2:
         need(8LL * f.c * f.m);
+        materialize_l1_e(p->p);
         if (f.c)
           SGF_CUDA(cudaMemcpy2DAsync(host_out, 8 * f.m, f.E, 8 * f.ld, 8 * f.m, f.c, cudaMemcpyDeviceToHost, st));
         break;

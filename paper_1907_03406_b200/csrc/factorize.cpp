@@ -668,9 +668,10 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   int *rl_n = nullptr, *rl_k = nullptr;
   double* rl_a = nullptr;
   if (sparse1 && rl_rows > 0) {
-    rl_n = S.scratch.alloc_t<int>(rl_rows);
-    rl_k = S.scratch.alloc_t<int>(rl_rows * L1_KMAX);
-    rl_a = S.scratch.alloc(rl_rows * L1_KMAX);
+    // the row lists outlive the level: E is formed from them on first use
+    rl_n = P->store.alloc_t<int>(rl_rows);
+    rl_k = P->store.alloc_t<int>(rl_rows * L1_KMAX);
+    rl_a = P->store.alloc(rl_rows * L1_KMAX);
     if (!S.l1_overflow) {
       S.l1_overflow = S.persist.alloc_t<int>(1);
       SGF_CUDA(cudaMemsetAsync(S.l1_overflow, 0, sizeof(int), st));
@@ -678,7 +679,19 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     SGF_CUDA(cudaMemsetAsync(rl_n, 0, rl_rows * sizeof(int), st));
     ProfScope ps(st, PROF_MOVE, 0.0);
     SGF_CUDA(launch_l1_rows(S.scratch.upload(l1r), (int)l1r.size(), rl_n, rl_k, rl_a, S.l1_overflow, st));
-    SGF_CUDA(launch_l1_e(S.scratch.upload(l1e), (int)l1e.size(), maxm, maxc, rl_n, rl_k, rl_a, st));
+    static const bool eager = getenv("SGF_L1E_EAGER") != nullptr;
+    if (eager) {
+      SGF_CUDA(launch_l1_e(S.scratch.upload(l1e), (int)l1e.size(), maxm, maxc, rl_n, rl_k, rl_a, st));
+    } else {
+      auto& pe = P->l1e;
+      pe.pending = true;
+      pe.tasks = l1e;
+      pe.max_m = maxm;
+      pe.max_c = maxc;
+      pe.rl_n = rl_n;
+      pe.rl_k = rl_k;
+      pe.rl_a = rl_a;
+    }
   }
   if (use_oz) {
     oz.launch_splits(S.scratch, st);
@@ -1709,6 +1722,20 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   timeline_end(S.st);
   SGF_CUDA(cudaStreamSynchronize(S.st));
   return P.release();
+}
+
+void materialize_l1_e(Precond* P) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& pe = P->l1e;
+  if (!pe.pending) return;
+  cudaStream_t st = P->ctx->stream;
+  L1ETask* d = P->store.alloc_t<L1ETask>(pe.tasks.size());
+  SGF_CUDA(cudaMemcpyAsync(d, pe.tasks.data(), pe.tasks.size() * sizeof(L1ETask), cudaMemcpyHostToDevice, st));
+  SGF_CUDA(launch_l1_e(d, (int)pe.tasks.size(), pe.max_m, pe.max_c, pe.rl_n, pe.rl_k, pe.rl_a, st));
+  SGF_CUDA(cudaStreamSynchronize(st));  // the host task list goes away below
+  pe.pending = false;
+  std::vector<L1ETask>().swap(pe.tasks);
 }
 
 }  // namespace sgf

@@ -67,6 +67,18 @@ class Precond {
   // sharding: factors [0, n_local) are the rank's local phase; top_idx are
   // the unknowns active when it ended (empty on a single GPU)
   L1Couplings l1;
+  // level-1 couplings E = A_NB L^{-T} of the sparse level-1 path are formed
+  // on first use (apply_inverse and the Schur updates never read them; the
+  // half sweeps, apply_operator and the host factor views do): the row lists
+  // and the task list are kept until then (materialize_l1_e)
+  struct L1EPending {
+    bool pending = false;
+    std::vector<L1ETask> tasks;
+    int max_m = 0, max_c = 0;
+    int* rl_n = nullptr;
+    int* rl_k = nullptr;
+    double* rl_a = nullptr;
+  } l1e;
   bool sharded = false;
   size_t n_local = 0;
   std::vector<int64_t> top_idx;
@@ -77,6 +89,7 @@ class Precond {
 };
 
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a);
+void materialize_l1_e(Precond* P);  // form the pending level-1 couplings E (stream ordered)
 void apply_op(Precond* P, int op, const double* d_x, double* d_y);
 void apply_part(Precond* P, int part, double* d_y);
 

@@ -26,6 +26,7 @@ VARIANTS = {
     "qr_l2_panel": {"SGF_QR_SMEM": "0"},               # cluster QR with the panel in L2
     "qr_cluster16": {"SGF_QR_SMEM": "16"},             # shared-memory QR forced to 16-CTA clusters
     "l1_dense": {"SGF_NO_L1SPARSE": "1"},              # level-1 E and Schur as dense DMMA GEMMs
+    "l1_e_eager": {"SGF_L1E_EAGER": "1"},              # level-1 couplings E formed during the factorization
     "diag_left_looking": {"SGF_DIAG_CHOL": "0"},       # left-looking 64x64 diagonal Cholesky
     "split_warp": {"SGF_OZ_SPLIT_WARP": "1"},          # warp-per-group operand split
     "l2_schur_dmma": {"SGF_OZAKI_SCHUR_MIN_M": "0"},   # level-2 Schur on DMMA
