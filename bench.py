@@ -59,36 +59,50 @@ def peaks():
 
 
 class ClockSampler(object):
-    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+    """Clocks and throttle reasons during the timed region: one background
+    `nvidia-smi --query-gpu=... -lms 200` process (B200_PROFILING.md clocks
+    line), started before and stopped after the region.  (Spawning a fresh
+    nvidia-smi per sample re-initialises NVML each time and perturbed the
+    host-driven PCG loop.)"""
 
     def __init__(self, gpu):
         self.gpu = gpu
         self.rows = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:
+            for line in self._p.stdout:
+                line = line.strip()
+                if line:
+                    self.rows.append([v.strip() for v in line.split(",")])
+        except Exception:
+            pass
+
+    def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
-
-    def __enter__(self):
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+            time.sleep(0.3)  # first sample before the region starts
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+        if self._t.is_alive():
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.rows:
