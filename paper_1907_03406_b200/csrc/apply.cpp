@@ -299,6 +299,9 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.nb1 = (int)b1.size();
     g.bwd2 = plan->mem.upload(b2);
     g.nb2 = (int)b2.size();
+    // the group's final reduction scatters straight into the full vector
+    // (backward_group): its segments carry the nodes' index arrays
+    for (auto& r : (g.type == SGF_FACTOR_ELIMINATION ? r2 : r1)) r.idx = g.idx + (r.out - g.zb);
     g.red1 = plan->mem.upload(r1);
     g.nred1 = (int)r1.size();
     g.red2 = plan->mem.upload(r2);
@@ -401,12 +404,11 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
     gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
     gemv(g.bwd2, g.nb2, 1, g.bytes_b2, st);
-    SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st));
+    SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st, y));  // + scatter into y
   } else {
     gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
-    SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
+    SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st, y));  // + scatter into y
   }
-  SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
 }
 
 // y and x are device n-vectors; y may alias x

@@ -572,20 +572,21 @@ cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int*
 // out[o] = sign_base*base[o] - sum_{q<nrb} part[poff + q*stride + k]  for the
 // flat segment layout described by RedSeg (one CTA-chunk per 256 entries).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) reduce_parts_kernel(const RedSeg* __restrict__ segs) {
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const RedSeg* __restrict__ segs, double* __restrict__ v) {
   const RedSeg R = segs[blockIdx.y];
   const int k = blockIdx.x * 256 + threadIdx.x;
   if (k >= R.n) return;
   double s = 0.0;
   for (int q = 0; q < R.nrb; ++q) s += R.part[(long long)q * R.stride + k];
   const double b = R.base ? R.base[k] : 0.0;
-  R.out[k] = b + R.sign * s;
+  if (v && R.idx) v[R.idx[k]] = b + R.sign * s;  // fused scatter into the full vector
+  else R.out[k] = b + R.sign * s;
 }
 
-cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s) {
+cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s, double* v) {
   if (nseg <= 0 || max_n <= 0) return cudaSuccess;
   dim3 grid((max_n + 255) / 256, nseg);
-  count_launch(); reduce_parts_kernel<<<grid, 256, 0, s>>>((const RedSeg*)d_segs);
+  count_launch(); reduce_parts_kernel<<<grid, 256, 0, s>>>((const RedSeg*)d_segs, v);
   return cudaGetLastError();
 }
 

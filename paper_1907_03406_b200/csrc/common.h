@@ -184,6 +184,7 @@ struct RedSeg {
   int nrb;
   int stride;
   double sign;
+  const int* idx = nullptr;  // fused scatter: with a full vector v, the result goes to v[idx[k]] instead of out[k]
 };
 
 }  // namespace sgf

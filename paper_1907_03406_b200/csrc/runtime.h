@@ -42,7 +42,7 @@ cudaError_t launch_csr_scatter(const void* params, cudaStream_t s);
 cudaError_t launch_sym_check(long long n, const long long* ip, const int* ix, const double* v,
                              unsigned long long* out, cudaStream_t s);
 cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStream_t s, int max_s = 0);
-cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s);
+cudaError_t launch_reduce_parts(const void* d_segs, int nseg, int max_n, cudaStream_t s, double* v = nullptr);
 cudaError_t launch_gather(const double* x, const int* idx, double* out, long long n, cudaStream_t s);
 cudaError_t launch_scatter(const double* v, const int* idx, double* x, long long n, cudaStream_t s);
 cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, const long long* pos, const double* t,
