@@ -13,6 +13,19 @@ exact BASELINE shape (no dataset involved).
   e2e    the same step through the public API with host numpy inputs
          (host CSR + RHS in, solution x back on the host), copies included.
 
+Beside the headline the line carries, per BASELINE config cfg1..cfg5
+(`configs`): t_F, t_S, PCG iterations against the reference's, ms per
+apply_inverse and its GB/s, FP64 TFLOP/s over the factorization; and the
+headline step with every FP64 product on IEEE DMMA (`ieee_fp64`: the INT8
+emulation switched off).
+
+CPU reference (never extrapolated): `--impl reference` runs the reference
+package itself (oracle/_ref, built from /root/reference by
+oracle/build_ref.sh) on the full cfg4 problem, one factorize + pcg with one
+BLAS thread, timed as the reference's own harness does (reference
+bench.py:157-166); the GPU arm's `cpu_baseline` runs the same with every
+host core as BLAS threads, after the GPU measurements.
+
 Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sgf|reference]
 N > 1 (torchrun, NCCL): the one 128^3 problem is sharded across the ranks
 (sharded.py: subtree ownership of the nested-dissection tree, rank-local
@@ -46,8 +59,12 @@ CFG = 4
 FP64_PEAK_TFLOPS = 37.1  # measured DMMA issue rate on this pool's B200 (profiles/fp64_peak_r01.jsonl)
 INT8_PEAK_TOPS = 4500.0  # B200 dense INT8 tensor peak (nominal; MEASURED_PEAKS.json has no INT8 figure)
 INT8_PEAK_SOURCE = "nominal B200 dense INT8 (4.5 POPS); MEASURED_PEAKS.json has no INT8 figure"
-SURVEY_REF_FULL_S = 682.4 + 270.4  # reference at full cfg4 size, 1 BLAS thread
-CPU_SAMPLE_N = 40                  # bounded CPU sample: the same operator on a 40^3 grid
+METRIC = "factor+solve wall time (cfg4: 128^3 anisotropic Laplace)"
+REF_ARM_TIMEOUT_S = 1700           # the driver's per-step limit is 1800 s
+BENCH_BUDGET_S = 1700              # the GPU arm's cpu_baseline gets what is left of this
+# PCG iterations of the reference itself per BASELINE config (reference runs:
+# tests/golden/cfg1.npz, cfg2.npz, cfg4_full.npz)
+REF_ITERS = {1: 12, 2: 16, 3: 64, 4: 49, 5: 36}
 
 
 def peaks():
@@ -146,72 +163,62 @@ def barrier(ws):
         dist.barrier()
 
 
-def cpu_reference_step(sample_n):
-    """One bounded CPU step of the reference algorithm (oracle port): factorize
-    + pcg on the cfg4 operator at sample_n^3.  Returns (t_F, t_S, stats, iters)."""
-    from oracle import sgf_oracle as O
-    from paper_1907_03406_b200 import problems as pr
-
-    c = pr.CONFIGS[CFG]
-    p = pr.anisotropic7(sample_n, 1e-3)
-    rhs = pr.config_rhs(p.n, c["seed"])
+def run_reference_subprocess(cfg, threads, timeout_s, n=None):
+    """The reference package (oracle/_ref) on one BASELINE config in a child
+    process with `threads` BLAS threads (fixed before numpy loads).  Returns
+    (result dict or None, error string or None, wall seconds)."""
+    env = dict(os.environ)
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        env[k] = str(threads)
+    cmd = [sys.executable, os.path.join(ROOT, "oracle", "ref_bench.py"), "--cfg", str(cfg)]
+    if n:
+        cmd += ["--n", str(n)]
     t = time.perf_counter()
-    P = O.factorize(p.matrix, p.coords, p.grid.dims, 1, scheme="nest-2-2", degree=1, b=c["b"],
-                    rank_tol=c["rank_tol"])
-    tf = time.perf_counter() - t
-    t = time.perf_counter()
-    x, rep = O.pcg(p.matrix, rhs, P.apply_inverse, tol=1e-12)
-    ts = time.perf_counter() - t
-    return tf, ts, P.stats, rep.iterations
-
-
-def extrapolate(tf, ts, st, it, full):
-    """Scale a sample's times to the full config: factorization by the
-    reference flop tally, solve by apply work x (iterations + 1)."""
-    ef = tf * full["flops_factorize"] / st["flops_factorize"]
-    es = ts * (full["flops_apply"] * (full["iters"] + 1)) / (st["flops_apply"] * (it + 1))
-    return ef, es
-
-
-def blas_threads():
     try:
-        from threadpoolctl import threadpool_info
-
-        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        return os.cpu_count() or 1
+        p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=max(timeout_s, 1))
+    except subprocess.TimeoutExpired:
+        return None, f"did not finish within {timeout_s:.0f} s", time.perf_counter() - t
+    wall = time.perf_counter() - t
+    if p.returncode != 0:
+        return None, (p.stderr.strip().splitlines() or ["failed"])[-1][:300], wall
+    try:
+        return json.loads(p.stdout.strip().splitlines()[-1]), None, wall
+    except Exception as e:  # noqa: BLE001
+        return None, f"unparsable output: {e}", wall
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args, ws, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port; the
-    Python reference itself is not present on the GPU box) on bounded samples
-    of the workload, reported in the same unit as the GPU arm."""
+    """--impl reference: the reference package itself (oracle/_ref) on the full
+    cfg4 problem, one factorize + pcg with one BLAS thread (reference
+    bench.py:157-166 protocol).  One full-size step takes ~15 minutes on one
+    core, so exactly one step is run whatever --steps/--warmup say, and the
+    line reports the steps actually run."""
     if rank != 0:
         return
-    full = {"flops_factorize": 11816662185330, "flops_apply": 14116631728, "iters": 49}  # cfg4 (SURVEY 6)
-    times = []
-    for s in range(args.warmup + args.steps):
-        tf, ts, st, it = cpu_reference_step(CPU_SAMPLE_N)
-        if s >= args.warmup:
-            times.append(extrapolate(tf, ts, st, it, full) + (tf, ts))
-    ef = float(np.mean([t[0] for t in times]))
-    es = float(np.mean([t[1] for t in times]))
-    v = ef + es
-    sample = (f"anisotropic 7-point diag(1,1,1e-3) on {CPU_SAMPLE_N}^3 (n={CPU_SAMPLE_N ** 3}), "
-              f"nest-2-2 b=9 rank_tol 1e-3: t_F {np.mean([t[2] for t in times]):.2f}s, "
-              f"t_S {np.mean([t[3] for t in times]):.2f}s, scaled to 128^3 by reference flops_factorize "
-              f"and flops_apply x (iterations+1)")
+    t0 = time.perf_counter()
+    res, err, wall = run_reference_subprocess(CFG, 1, REF_ARM_TIMEOUT_S)
+    base = {"impl": "reference", "metric": METRIC, "unit": "s", "n_gpus": ws, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
+    if res is None:
+        print(json.dumps({**base, "unavailable": f"reference run failed: {err}"}), flush=True)
+        return
+    v = res["t_factor_s"] + res["t_solve_s"]
     line = {
-        "impl": "reference", "metric": "factor+solve wall time (cfg4: 128^3 anisotropic Laplace)",
-        "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": "cfg4-aniso-128", "grid": [128, 128, 128],
-                                                         "n": 2097152, "b": 9, "rank_tol": 1e-3, "pcg_rtol": 1e-12},
-        "t_factor_s": ef, "t_solve_s": es,
-        "cpu_baseline": {"value": v, "unit": "s", "cores": blas_threads(), "kind": "port", "sample": sample},
+        **base, "value": v, "steps": 1, "warmup": 0, "requested_steps": args.steps,
+        "requested_warmup": args.warmup, "ms_per_step": v * 1e3,
+        "config": {"workload": f"cfg{CFG}-aniso-128" if CFG == 4 else f"cfg{CFG}", "grid": res["grid"],
+                   "n": res["n"], "b": res["b"], "rank_tol": res["rank_tol"], "scheme": "nest-2-2", "degree": 1,
+                   "pcg_rtol": 1e-12, "parallelism": "cpu, 1 BLAS thread"},
+        "t_factor_s": res["t_factor_s"], "t_solve_s": res["t_solve_s"], "pcg_iterations": res["iterations"],
+        "flops_factorize": res["flops_factorize"], "fp64_tflops_factorize": res["flops_factorize"] / res["t_factor_s"] / 1e12,
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference",
+                         "sample": f"the whole cfg{CFG} workload (n={res['n']}), one factorize + pcg of the reference "
+                                   f"package (oracle/_ref, polyprec {res['polyprec']}), OPENBLAS_NUM_THREADS=1, "
+                                   f"host {res['cpu_count']} cpus; problem generation {res['t_generate_s']:.1f} s "
+                                   f"not timed"},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "survey_reference_full_s": SURVEY_REF_FULL_S,
+        "reference_wall_s": wall, "arm_wall_s": time.perf_counter() - t0,
     }
     print(json.dumps(line), flush=True)
 
@@ -352,17 +359,54 @@ def run_sgf(args, ws, rank, local):
         "apply_gemv_gbs": gemv[1] / max(gemv[0], 1e-9) / 1e6, "spmv_gbs": spmv[1] / max(spmv[0], 1e-9) / 1e6,
     }
 
+    # the same headline step with every FP64 product on IEEE DMMA (no INT8
+    # emulation): what the factorization costs in native FP64
+    ieee = None
+    if ws == 1 and not args.no_extras:
+        os.environ["SGF_OZAKI_MIN_M"] = "0"
+        try:
+            step_device()
+            torch.cuda.synchronize()
+            rec3 = []
+            for _ in range(max(1, min(args.steps, 3))):
+                step_device(rec3)
+            torch.cuda.synchronize()
+        finally:
+            del os.environ["SGF_OZAKI_MIN_M"]
+        tFi = float(np.mean([r[0].elapsed_time(r[1]) for r in rec3])) / 1e3
+        tSi = float(np.mean([r[1].elapsed_time(r[2]) for r in rec3])) / 1e3
+        ieee = {"value": tFi + tSi, "unit": "s", "steps": len(rec3), "t_factor_s": tFi, "t_solve_s": tSi,
+                "pcg_iterations": rec3[-1][4].iterations,
+                "executed_fp64_tflops": rec3[-1][3]["flops_factorize"] / tFi / 1e12,
+                "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                "note": "SGF_OZAKI_MIN_M=0: every dense FP64 product on DMMA (IEEE FP64); the reference flop "
+                        "tally / t_F; level-1 sparse gathers count as their reference flops"}
+    del Ad
+
+    # every BASELINE config: factor / apply / solve (device-resident inputs)
+    configs = {}
+    if ws == 1 and not args.no_extras:
+        for k in (1, 2, 3, 4, 5):
+            configs[f"cfg{k}"] = measure_config(k, local)
+
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        full = {"flops_factorize": stats["flops_factorize"], "flops_apply": stats["flops_apply"],
-                "iters": rep.iterations}
-        tf, ts, st, it = cpu_reference_step(CPU_SAMPLE_N)
-        ef, es = extrapolate(tf, ts, st, it, full)
-        cpu = {"value": ef + es, "unit": "s", "cores": blas_threads(), "kind": "port",
-               "sample": f"oracle (numpy port of the reference) on the cfg4 operator at {CPU_SAMPLE_N}^3: "
-                         f"t_F {tf:.2f}s + t_S {ts:.2f}s ({it} iterations), scaled to 128^3 by flops_factorize "
-                         f"and flops_apply x (iterations+1); reference measured at full size in SURVEY: "
-                         f"{SURVEY_REF_FULL_S:.0f}s"}
+    if rank == 0 and ws == 1 and args.cpu_baseline != "none":
+        left = BENCH_BUDGET_S - (time.perf_counter() - T_START)
+        threads = os.cpu_count() or 1
+        n_sample = None if args.cpu_baseline == "full" else 48
+        res, err, wall = run_reference_subprocess(CFG, threads, left, n=n_sample)
+        if res is not None:
+            cpu = {"value": res["t_factor_s"] + res["t_solve_s"], "unit": "s", "cores": threads, "kind": "reference",
+                   "t_factor_s": res["t_factor_s"], "t_solve_s": res["t_solve_s"], "pcg_iterations": res["iterations"],
+                   "sample": (f"the whole cfg{CFG} workload (n={res['n']}): one factorize + pcg of the reference "
+                              f"package (oracle/_ref, polyprec {res['polyprec']}), OPENBLAS_NUM_THREADS={threads} "
+                              f"(all host cores), timed as reference bench.py:157-166"
+                              if n_sample is None else
+                              f"bounded sample: the cfg{CFG} operator on a {n_sample}^3 grid (n={res['n']}), "
+                              f"reference package, OPENBLAS_NUM_THREADS={threads}; not the bench config")}
+        else:
+            cpu = {"value": None, "unit": "s", "cores": threads, "kind": "reference",
+                   "sample": f"reference run on the whole cfg{CFG} workload with {threads} BLAS threads: {err}"}
     if rank == 0:
         line = {
             "metric": "factor+solve wall time (cfg4: 128^3 anisotropic Laplace)", "value": ms / 1e3, "unit": "s",
@@ -379,9 +423,79 @@ def run_sgf(args, ws, rank, local):
                                         "int32 accumulation) for larger nodes"},
             "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
+            "ieee_fp64": ieee, "configs": configs,
         }
         line.update(extra)
         print(json.dumps(line), flush=True)
+
+
+def measure_config(k, local, steps=2):
+    """t_F, t_S, iterations, apply time / bandwidth and FP64 rate for BASELINE
+    config k with device-resident CSR values and RHS (one warm-up step)."""
+    import torch
+
+    import paper_1907_03406_b200 as sgf
+    from paper_1907_03406_b200 import _native as N
+    from paper_1907_03406_b200.problems import CONFIGS, config_rhs
+
+    c = CONFIGS[k]
+    prob = c["make"]()
+    A = prob.matrix.tocsr()
+    A.sort_indices()
+    rhs = config_rhs(prob.n, c["seed"])
+    opts = dict(scheme="nest-2-2", degree=1, b=c["b"], rank_tol=c["rank_tol"], device=local)
+    vals = torch.tensor(A.data, dtype=torch.float64, device="cuda")
+    Ad = sgf.DeviceCSR(device=local, indptr=torch.tensor(A.indptr, dtype=torch.int64, device="cuda"),
+                       indices=torch.tensor(A.indices, dtype=torch.int32, device="cuda"), values=vals, n=prob.n)
+    b_dev = torch.tensor(rhs, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(N.lib().sgf_stream(N.context(local)))
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    out = []
+    for s in range(steps + 1):
+        e0 = ev()
+        P = sgf.factorize(prob, device_values=vals, **opts)
+        e1 = ev()
+        x, rep = sgf.pcg(Ad, b_dev, precond=P, tol=1e-12)
+        e2 = ev()
+        torch.cuda.synchronize()
+        if s:
+            out.append((e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3, rep))
+        if s < steps:
+            del P
+    # apply_inverse alone: time and the bytes its sweeps stream (native profile)
+    y = torch.empty_like(b_dev)
+    for _ in range(2):
+        y = P.apply_inverse(b_dev)
+    torch.cuda.synchronize()
+    N.profile_enable(True)
+    a0 = ev()
+    na = 5
+    for _ in range(na):
+        y = P.apply_inverse(b_dev)
+    a1 = ev()
+    torch.cuda.synchronize()
+    prof = N.profile_read()
+    N.profile_enable(False)
+    ms_apply = a0.elapsed_time(a1) / na
+    apply_bytes = sum(prof[c][1] for c in ("gemv", "copy", "vec")) / na
+    tF = float(np.mean([o[0] for o in out]))
+    tS = float(np.mean([o[1] for o in out]))
+    rep = out[-1][2]
+    st = P.stats
+    return {"grid": list(prob.grid.dims), "n": prob.n, "nnz": int(A.nnz), "b": c["b"], "rank_tol": c["rank_tol"],
+            "t_factor_s": tF, "t_solve_s": tS, "factor_plus_solve_s": tF + tS, "steps": steps,
+            "pcg_iterations": rep.iterations, "reference_pcg_iterations": REF_ITERS[k],
+            "final_rel_residual": rep.final_rel_residual,
+            "fp64_tflops_factorize": st["flops_factorize"] / tF / 1e12,
+            "fp64_frac_of_dmma_peak": st["flops_factorize"] / tF / 1e12 / FP64_PEAK_TFLOPS,
+            "ms_per_apply": ms_apply, "apply_gbs": apply_bytes / (ms_apply * 1e-3) / 1e9,
+            "apply_frac_of_hbm": apply_bytes / (ms_apply * 1e-3) / 1e9 / peaks()[0]["hbm_gbs"],
+            "flops_factorize": st["flops_factorize"], "flops_apply": st["flops_apply"]}
 
 
 def stats_pi(stats):
@@ -398,13 +512,19 @@ def traffic_from_profiles(kernel):
         return None
 
 
+T_START = time.perf_counter()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sgf", choices=["sgf", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline", default="full", choices=["full", "sample", "none"],
+                    help="GPU arm's CPU reference leg: the whole cfg4 run on all host cores (default, ~10-15 min), "
+                         "a 48^3 sample, or none")
+    ap.add_argument("--no-extras", action="store_true", help="skip the per-config and IEEE-FP64 lines")
     # code-path checks only (numbers from these are not bench values): another
     # config, gloo collectives, every rank on GPU 0
     ap.add_argument("--cfg", type=int, default=4)

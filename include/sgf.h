@@ -181,6 +181,24 @@ typedef int (*sgf_precond_fn)(void* user, const double* in, double* out);
 int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const double* b, double* x, double tol,
                int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
 
+/* PCG over general operators (krylov.py:28-31 _as_linop: matvec / precond
+   may be matrices, `@`-able objects or callables).  Exactly one of `a` (a
+   device CSR) and `mv` (out = A in on device n-vectors, enqueued on the
+   context stream; nonzero return = failure) is given; at most one of `p`
+   and `pf`.  The recurrence, dots and vector updates run on the device as
+   in sgf_pcg; only the callbacks run wherever the caller put them. */
+typedef int (*sgf_matvec_fn)(void* user, const double* in, double* out);
+int sgf_pcg_ops(sgf_ctx* ctx, int64_t n, sgf_csr* a, sgf_matvec_fn mv, void* mv_user, sgf_precond* p,
+                sgf_precond_fn pf, void* pf_user, const double* b, double* x, double tol, int maxit,
+                int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
+
+/* Stream-ordered copy on the context stream (host or device pointers,
+   cudaMemcpyDefault), synchronised before returning. */
+int sgf_memcpy(sgf_ctx* ctx, void* dst, const void* src, int64_t bytes);
+/* Make the context stream wait for all work enqueued so far on `stream`
+   (a cudaStream_t, e.g. torch's current stream) before its next launch. */
+int sgf_stream_wait(sgf_ctx* ctx, void* stream);
+
 /* Host helper (partition.py:142-199, 232-242 for the level-1 cells): unknown
    ids grouped by cell (cells in id order, vertices ascending, components
    major within a cell) and the per-cell pointer, for a nested/general grid

@@ -32,7 +32,8 @@ EXPORTS = (
     "sgf_precond_num_factors", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
-    "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read",
+    "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read", "sgf_pcg_ops", "sgf_memcpy",
+    "sgf_stream_wait",
 )
 PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec", "gemm_int8emu", "int8emu_split")
 
@@ -64,6 +65,8 @@ class FactorArgs(C.Structure):
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64))
 # int precond(void* user, const double* in, double* out)
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+# int matvec(void* user, const double* in, double* out)
+MATVEC_FN = PRECOND_FN
 
 
 class PcgReport(C.Structure):
@@ -74,6 +77,7 @@ class PcgReport(C.Structure):
 _lib = None
 _lock = threading.Lock()
 _ctx = {}
+_ctx_device = {}
 
 
 def load_library(path=LIB_PATH):
@@ -111,6 +115,10 @@ def load_library(path=LIB_PATH):
             "sgf_precond_shard_set": (i32, [vp, i32, vp, i64]),
             "sgf_apply_part": (i32, [vp, i32, vp]),
             "sgf_cell_unknowns": (i32, [i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp]),
+            "sgf_pcg_ops": (i32, [vp, i64, vp, MATVEC_FN, vp, vp, PRECOND_FN, vp, vp, vp, d, i32, i32, i32,
+                                  C.POINTER(PcgReport), vp]),
+            "sgf_memcpy": (i32, [vp, vp, vp, i64]),
+            "sgf_stream_wait": (i32, [vp, vp]),
             "sgf_kernel_launches": (C.c_uint64, []),
             "sgf_profile_enable": (i32, [i32]),
             "sgf_profile_read": (i32, [vp, i32]),
@@ -158,7 +166,42 @@ def context(device=0):
         raise NativeUnavailable(f"cannot create a CUDA context on device {device}: {msg}")
     with _lock:
         _ctx[device] = h
+        _ctx_device[h.value] = int(device)
     return h
+
+
+def context_device(ctx):
+    """The CUDA device index a native context was created on."""
+    return _ctx_device[ctx.value]
+
+
+def order_after_torch(ctx, device=None):
+    """Make the native context stream wait for everything enqueued so far on
+    torch's current stream of the context's device: a tensor a torch kernel
+    is still producing is not read early (the native stream is a separate,
+    non-blocking stream).  Native calls synchronise their own stream before
+    returning, so their outputs are ready for torch."""
+    import torch
+
+    dev = context_device(ctx) if device is None else device
+    s = torch.cuda.current_stream(dev).cuda_stream
+    raise_for(lib().sgf_stream_wait(ctx, C.c_void_p(s)), ctx)
+
+
+def check_device_tensor(t, dtype, device, what):
+    """Validate a CUDA tensor handed to the native code by pointer: dtype,
+    contiguity and device (a mismatch would read out of bounds or garbage)."""
+    import torch
+
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{what} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if t.device.index != device:
+        raise ValueError(f"{what} is on cuda:{t.device.index} but the context is on cuda:{device}")
+    return torch
 
 
 def kernel_launches():

@@ -586,8 +586,8 @@ void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
 // PCG with the reference recurrence (krylov.py:34-102): true-residual
 // replacement every `true_every` iterations, confirmation of a tentative
 // convergence with the true residual, history semantics identical.
-void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit, int true_every,
-         sgf_pcg_report* rep, double* history) {
+void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit,
+         int true_every, sgf_pcg_report* rep, double* history) {
   cudaStream_t st = ctx.stream;
   const long long n = A->n;
   auto t0 = std::chrono::steady_clock::now();
@@ -619,6 +619,15 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
       t_wait += std::chrono::duration<double, std::milli>(tlast - t1).count();
     } else {
       SGF_CUDA(cudaStreamSynchronize(st));
+    }
+  };
+  // out = A in, or out = b - A in when b is given
+  auto matvec = [&](const double* in, double* out, const double* b) {
+    if (Aop) {
+      Aop(in, out);
+      if (b) SGF_CUDA(launch_residual(b, out, n, st));
+    } else {
+      spmv(A, in, out, b);
     }
   };
   auto precond = [&](const double* in, double* out) {
@@ -655,11 +664,11 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
   int it = 0;
   while (it < maxit) {
     ++it;
-    spmv(A, p, q, nullptr);
+    matvec(p, q, nullptr);
     SGF_CUDA(launch_dot(p, q, n, part, sc, 1, st));
     SGF_CUDA(launch_xr_update(d_x, r, p, q, n, sc, part, sc, 3, st));
     if (true_every > 0 && it % true_every == 0) {
-      spmv(A, d_x, r, d_b);
+      matvec(d_x, r, d_b);
       SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
     }
     readback(1, 3);
@@ -670,7 +679,7 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
     }
     double rel = std::sqrt(hsc[3]) / bnorm;
     if (rel <= tol) {
-      spmv(A, d_x, r, d_b);
+      matvec(d_x, r, d_b);
       SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
       readback(3, 1);
       rel = std::sqrt(hsc[3]) / bnorm;
@@ -693,7 +702,7 @@ void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, doub
     SGF_CUDA(launch_p_update(p, z, n, sc, st));
     SGF_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
-  spmv(A, d_x, r, d_b);
+  matvec(d_x, r, d_b);
   SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
   readback(3, 1);
   const double fin = std::sqrt(hsc[3]) / bnorm;

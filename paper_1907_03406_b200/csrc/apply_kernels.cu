@@ -786,6 +786,17 @@ __global__ void __launch_bounds__(256) p_update_kernel(double* __restrict__ p, c
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) p[i] = z[i] + beta * p[i];
 }
 
+// out = b - out (the residual of a callback operator's product)
+__global__ void __launch_bounds__(256) residual_kernel(const double* __restrict__ b, double* __restrict__ out,
+                                                       long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) out[i] = b[i] - out[i];
+}
+
+cudaError_t launch_residual(const double* b, double* out, long long n, cudaStream_t s) {
+  count_launch(); residual_kernel<<<RED_BLOCKS, 256, 0, s>>>(b, out, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s) {
   count_launch(); dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part);

@@ -24,6 +24,9 @@ thread_local std::string g_orphan_error;
 template <class F>
 int guarded(sgf_ctx* ctx, F&& f) {
   try {
+    // every entry point runs on its context's device (a process may hold
+    // contexts on several GPUs)
+    if (ctx && ctx->c.stream) SGF_CUDA(cudaSetDevice(ctx->c.device));
     f();
     return SGF_OK;
   } catch (const Error& e) {
@@ -77,6 +80,7 @@ int sgf_destroy(sgf_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     cudaStreamDestroy(ctx->c.stream);
   }
+  if (ctx->c.order_ev) cudaEventDestroy(ctx->c.order_ev);
   delete ctx;
   return SGF_OK;
 }
@@ -332,16 +336,16 @@ int sgf_spmv(sgf_csr* a, const double* x, double* y, int on_device) {
   });
 }
 
-static void run_pcg(sgf_ctx* ctx, sgf_csr* a, const PrecFn& M, const double* b, double* x, double tol, int maxit,
-                    int true_every, int on_device, sgf_pcg_report* rep, double* history) {
+static void run_pcg(sgf_ctx* ctx, sgf_csr* a, const MatFn& Aop, const PrecFn& M, const double* b, double* x, double tol,
+                    int maxit, int true_every, int on_device, sgf_pcg_report* rep, double* history) {
   cudaStream_t st = ctx->c.stream;
   const long long n = a->a.n;
   if (on_device) {
-    pcg(ctx->c, &a->a, M, b, x, tol, maxit, true_every, rep, history);
+    pcg(ctx->c, &a->a, Aop, M, b, x, tol, maxit, true_every, rep, history);
   } else {
     DevVec db(n, st), dx(n, st);
     SGF_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, st));
-    pcg(ctx->c, &a->a, M, db.p, dx.p, tol, maxit, true_every, rep, history);
+    pcg(ctx->c, &a->a, Aop, M, db.p, dx.p, tol, maxit, true_every, rep, history);
     SGF_CUDA(cudaMemcpyAsync(x, dx.p, n * 8, cudaMemcpyDeviceToHost, st));
   }
   SGF_CUDA(cudaStreamSynchronize(st));
@@ -352,12 +356,13 @@ int sgf_pcg(sgf_ctx* ctx, sgf_csr* a, sgf_precond* p, const double* b, double* x
   if (!ctx || !a || !b || !x || !rep || !history) return SGF_INVALID_ARG;
   return guarded(ctx, [&] {
     if (p && p->p->n != a->a.n) fail(SGF_SHAPE, "preconditioner and matrix sizes differ");
+    if ((p && p->ctx != ctx) || a->ctx != ctx) fail(SGF_INVALID_ARG, "matrix, preconditioner and solve must share a context");
     PrecFn M;
     if (p) {
       Precond* P = p->p;
       M = [P](const double* in, double* out) { apply_op(P, SGF_APPLY_INVERSE, in, out); };
     }
-    run_pcg(ctx, a, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+    run_pcg(ctx, a, MatFn(), M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
   });
 }
 
@@ -365,11 +370,69 @@ int sgf_pcg_cb(sgf_ctx* ctx, sgf_csr* a, sgf_precond_fn fn, void* user, const do
                int maxit, int true_residual_every, int on_device, sgf_pcg_report* rep, double* history) {
   if (!ctx || !a || !fn || !b || !x || !rep || !history) return SGF_INVALID_ARG;
   return guarded(ctx, [&] {
+    if (a->ctx != ctx) fail(SGF_INVALID_ARG, "matrix and solve must share a context");
     PrecFn M = [fn, user](const double* in, double* out) {
       const int rc = fn(user, in, out);
       if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "preconditioner callback failed");
     };
-    run_pcg(ctx, a, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+    run_pcg(ctx, a, MatFn(), M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+  });
+}
+
+int sgf_pcg_ops(sgf_ctx* ctx, int64_t n, sgf_csr* a, sgf_matvec_fn mv, void* mv_user, sgf_precond* p,
+                sgf_precond_fn pf, void* pf_user, const double* b, double* x, double tol, int maxit,
+                int true_residual_every, int on_device, sgf_pcg_report* rep, double* history) {
+  if (!ctx || (!a && !mv) || (a && mv) || (p && pf) || !b || !x || !rep || !history || n < 0) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    if (a && a->a.n != n) fail(SGF_SHAPE, "matrix and right-hand side sizes differ");
+    if (p && p->p->n != n) fail(SGF_SHAPE, "preconditioner and right-hand side sizes differ");
+    if ((a && a->ctx != ctx) || (p && p->ctx != ctx))
+      fail(SGF_INVALID_ARG, "matrix, preconditioner and solve must share a context");
+    MatFn Aop;
+    if (mv)
+      Aop = [mv, mv_user](const double* in, double* out) {
+        const int rc = mv(mv_user, in, out);
+        if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "operator callback failed");
+      };
+    PrecFn M;
+    if (p) {
+      Precond* P = p->p;
+      M = [P](const double* in, double* out) { apply_op(P, SGF_APPLY_INVERSE, in, out); };
+    } else if (pf) {
+      M = [pf, pf_user](const double* in, double* out) {
+        const int rc = pf(pf_user, in, out);
+        if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "preconditioner callback failed");
+      };
+    }
+    if (a) {
+      run_pcg(ctx, a, Aop, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+    } else {
+      // an operator callback: a matrix-less workspace owner of size n
+      sgf_csr W;
+      W.ctx = ctx;
+      W.a.ctx = &ctx->c;
+      W.a.mem.set_stream(ctx->c.stream);
+      W.a.n = n;
+      run_pcg(ctx, &W, Aop, M, b, x, tol, maxit, true_residual_every, on_device, rep, history);
+    }
+  });
+}
+
+int sgf_memcpy(sgf_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  if (!ctx || bytes < 0 || (bytes && (!dst || !src))) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    if (bytes) SGF_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, ctx->c.stream));
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sgf_stream_wait(sgf_ctx* ctx, void* stream) {
+  if (!ctx) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    if (!stream || (cudaStream_t)stream == ctx->c.stream) return;
+    if (!ctx->c.order_ev) SGF_CUDA(cudaEventCreateWithFlags(&ctx->c.order_ev, cudaEventDisableTiming));
+    SGF_CUDA(cudaEventRecord(ctx->c.order_ev, (cudaStream_t)stream));
+    SGF_CUDA(cudaStreamWaitEvent(ctx->c.stream, ctx->c.order_ev, 0));
   });
 }
 

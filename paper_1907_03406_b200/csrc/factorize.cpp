@@ -71,6 +71,7 @@ struct State {
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
   int oz_schur_min_m = 640;    // nodes this large (below oz_min_m) take only the Schur updates emulated
   int chol_oz_min_m = 1024;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
+  std::vector<std::string> warnings;  // reference warnings.warn messages (stats "warnings", raised by Python)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
   explicit State(cudaStream_t s) : scratch(s), persist(s, (size_t)4 << 20) { chk.arena = &persist; }
@@ -1239,7 +1240,8 @@ void compress_level(State& S, const std::vector<int>& comp, int level, LevelStat
         seqno.push_back(S.comp_counter + i);
         int r = forced[i];
         if (r > M.size[comp[i]]) {
-          fprintf(stderr, "warning: forced rank %d exceeds node size %d; clipping\n", r, M.size[comp[i]]);
+          S.warnings.push_back("forced rank " + std::to_string(r) + " exceeds node size " +
+                               std::to_string(M.size[comp[i]]) + "; clipping");
           r = M.size[comp[i]];
         }
         fr.push_back(r);
@@ -1455,8 +1457,7 @@ void final_dense(State& S) {
 
 std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<LevelStats>& lv, int max_after,
                        int max_seen, int final_dense, long long flops, long long flops_apply, long long peak,
-                       int nfactors, int b_used, const char* scheme_unused) {
-  (void)scheme_unused;
+                       int nfactors, const std::vector<std::string>& warnings) {
   std::ostringstream o;
   o << "{\"n\": " << n << ", \"levels\": " << lv.size() << ", \"per_level\": [";
   for (size_t i = 0; i < lv.size(); ++i) {
@@ -1469,8 +1470,9 @@ std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<Le
   o << "], \"max_node_size\": " << max_after << ", \"max_node_seen\": " << max_seen
     << ", \"final_dense_size\": " << final_dense << ", \"flops_factorize\": " << flops
     << ", \"flops_apply\": " << flops_apply << ", \"peak_blocks_bytes\": " << peak << ", \"factors\": " << nfactors
-    << "}";
-  (void)b_used;
+    << ", \"warnings\": [";
+  for (size_t i = 0; i < warnings.size(); ++i) o << (i ? ", " : "") << "\"" << warnings[i] << "\"";
+  o << "]}";
   (void)a;
   return o.str();
 }
@@ -1716,7 +1718,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   // on a sharded rank 0 the tallies include the other ranks' factors, so the
   // stats equal the single-GPU ones; the other ranks' stats cover their local phase
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
-                        (int)P->factors.size() + S.nf_extra, 0, nullptr);
+                        (int)P->factors.size() + S.nf_extra, S.warnings);
   planner.finish();
   plan_finish(P.get());
   timeline_end(S.st);

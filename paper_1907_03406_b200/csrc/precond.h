@@ -110,7 +110,11 @@ struct Csr {
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b);
 // preconditioner: out = M^-1 in on device vectors (empty = identity)
 using PrecFn = std::function<void(const double*, double*)>;
-void pcg(Ctx& ctx, Csr* A, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit, int true_every,
-         sgf_pcg_report* rep, double* history);
+// operator: out = A in on device vectors (empty = A's own CSR SpMV)
+using MatFn = std::function<void(const double*, double*)>;
+// A owns the PCG workspace; with an operator callback its CSR arrays may be
+// absent (only A->n is used)
+void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit,
+         int true_every, sgf_pcg_report* rep, double* history);
 
 }  // namespace sgf

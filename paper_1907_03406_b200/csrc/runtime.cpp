@@ -486,6 +486,8 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
     h.W = j.W + (long long)m1[i] * j.ld + m1[i];
     h.X = j.X + (long long)m1[i] * j.ld + m1[i];
     h.m = m2[i];
+    // the A22 update writes whole diagonal tiles: its upper part is no longer zero
+    h.upper_zero = false;
     j22.push_back(h);
   }
   chol_inv_rec(ctx, scratch, j22, check, min_m);

@@ -63,6 +63,7 @@ cudaError_t launch_dot(const double* a, const double* b, long long n, double* pa
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
                              double* part, double* out, int slot, cudaStream_t s);
 cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s);
+cudaError_t launch_residual(const double* b, double* out, long long n, cudaStream_t s);
 
 
 // ---------------------------------------------------------------------------
@@ -148,6 +149,7 @@ class Arena {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaEvent_t order_ev = nullptr;  // sgf_stream_wait: orders the stream after a foreign one
   std::string last_error;
   // grow-only pinned staging buffer for large host->device uploads; callers
   // synchronise the stream before reusing it

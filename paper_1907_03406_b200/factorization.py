@@ -163,6 +163,7 @@ class Preconditioner(object):
         self.degree = degree
         self.mode = mode
         self._factors = None
+        self.device = N.context_device(ctx)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -187,14 +188,22 @@ class Preconditioner(object):
         return self._factors
 
     def _run(self, op, x):
+        from .krylov import _Captured, _Probe
+
+        if isinstance(x, _Probe):  # pcg looking inside `lambda v: P.apply_inverse(v)`
+            return _Captured(self, op)
         dev = not isinstance(x, np.ndarray) and hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
         if dev:
             import torch
 
             if x.dtype != torch.float64 or x.dim() != 1 or x.shape[0] != self.n:
                 raise ShapeMismatchError(f"expected a float64 vector of length {self.n}, got {tuple(x.shape)}")
+            if x.device.index != self.device:
+                raise ValueError(f"vector is on cuda:{x.device.index}, the preconditioner on cuda:{self.device}")
             xin = x.contiguous()
             y = torch.empty_like(xin)
+            # the native stream must not read x before torch has written it
+            N.order_after_torch(self._ctx, self.device)
             st = N.lib().sgf_apply(self._h, op, xin.data_ptr(), y.data_ptr(), 1)
             N.raise_for(st, self._ctx)
             return y
@@ -260,6 +269,11 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
         compression = False
     if mode == "lowrank" and compression and rank_trace is None:
         raise ValueError("mode='lowrank' requires the rank trace of a polynomial run")
+    if rank_trace is not None and not (mode == "lowrank" and compression) and len(rank_trace.entries):
+        # the reference iterates the trace only in low-rank mode and then
+        # rejects leftover entries (factorization.py:543-549)
+        raise RuntimeError(f"rank trace has {len(rank_trace.entries)} unreplayed entries; "
+                           f"first: {json.dumps(list(rank_trace.entries[0]))}")
     grid = problem.grid
     n = grid.n_unknowns
     if problem.matrix.shape != (n, n):
@@ -299,8 +313,11 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
     args.indptr, args.indices, args.values = indptr.ctypes.data, indices.ctypes.data, values.ctypes.data
     args.values_on_device = 0
     if device_values is not None:
-        if tuple(device_values.shape) != (A.nnz,) or not device_values.is_cuda:
+        import torch
+
+        if tuple(device_values.shape) != (A.nnz,) or not getattr(device_values, "is_cuda", False):
             raise ShapeMismatchError("device_values must be a CUDA vector with one entry per nonzero")
+        N.check_device_tensor(device_values, torch.float64, int(device), "device_values")
         args.values, args.values_on_device = device_values.data_ptr(), 1
     # Pi is built natively from the coordinates (same rule as basis.py)
     args.pi_cols, args.phi = pi_cols, None
@@ -338,10 +355,14 @@ def factorize(problem, scheme="nest-2-2", degree=1, b=None, skip_levels=None,
 
     L = N.lib()
     ctx = N.context(device)
+    if device_values is not None:
+        N.order_after_torch(ctx, int(device))
     h = C.c_void_p()
     st = L.sgf_factorize(ctx, C.byref(args), C.byref(h))
     N.raise_for(st, ctx)
     native = json.loads(L.sgf_precond_stats_json(h).decode())
+    for msg in native.get("warnings", []):
+        warnings.warn(msg)
     stats = {
         "n": n, "scheme": scheme, "degree": degree,
         "mode": mode if compression else "exact",

@@ -3,6 +3,8 @@
 Run once in the build container (where /root/reference exists):
 
     python tests/golden/make_golden.py [--with-cfg2]
+    python tests/golden/make_golden.py cfg4_full   # one slim full-size case
+                                                   # (cfg3_full cfg4_full cfg5_full tpfa40_b9; ~15 min, ~49 GB each)
 
 It imports `polyprec` read-only from /root/reference/pkg/src with the BLAS
 pinned as SURVEY.md 8c prescribes (OPENBLAS_NUM_THREADS=1,
@@ -203,6 +205,184 @@ def run_case(name, prob, opts, store_factors=False, pcg_tol=1e-12, rhs_seed=0, l
           "bytes=%d" % os.path.getsize(path), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Slim fixtures for the full-size BASELINE configs (cfg3/4/5) and the 40^3
+# TPFA case whose level-3 node has >= 1024 unknowns (INT8-emulated products
+# on the GPU).  Dense factors and n-vectors are far too large to commit, so a
+# fixture keeps: digests of the matrix and of the hierarchy (bitwise pins of
+# the product's generators and partition), the rank trace, every QR
+# permutation (for pivot replay), the stats, strided samples and seeded
+# Gaussian projections of apply_inverse / apply_operator / the PCG solution,
+# the whole PCG history, and for a selection of factors (the emulated
+# eliminations, the compressions after them, the final dense factor) their
+# index sets, two columns and seeded projections of L / E / Q1.  Seeds:
+# vector projections rng(7).standard_normal((4, n)); factor k uses
+# rng(1000 + k) for the m-side and rng(2000 + k) for the c-side.
+# ---------------------------------------------------------------------------
+
+import hashlib  # noqa: E402
+
+STRIDE = 32
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def matrix_digest(A):
+    A = A.tocsr()
+    A.sort_indices()
+    return digest(A.indptr.astype(np.int64), A.indices.astype(np.int64), A.data.astype(np.float64))
+
+
+def hierarchy_digest(prob, scheme, b):
+    arrs = hierarchy_arrays(prob, scheme, b)
+    L = int(arrs["h_levels"])
+    out = []
+    for t in range(L):
+        parts = [arrs[f"h{t}_cov"], arrs[f"h{t}_kind"], arrs[f"h{t}_interior"]]
+        if f"h{t}_father" in arrs:
+            parts.append(arrs[f"h{t}_father"].astype(np.int32))
+        out.append(digest(*parts))
+    return out
+
+
+def vec_sample(d, key, y, proj):
+    d[f"{key}_s"] = np.ascontiguousarray(y[::STRIDE])
+    d[f"{key}_p"] = proj @ y
+    d[f"{key}_norm"] = np.float64(np.linalg.norm(y))
+
+
+def select_factors(P):
+    kinds = [type(f).__name__ for f in P.factors]
+    ms = [len(f.idx) for f in P.factors]
+    pick = set()
+
+    def spread(lst, k=3):
+        if not lst:
+            return []
+        if len(lst) <= k:
+            return lst
+        return [lst[0], lst[len(lst) // 2], lst[-1]][:k]
+
+    big = [k for k, (t, m) in enumerate(zip(kinds, ms)) if t == "EliminationFactor" and m >= 1024]
+    mid = [k for k, (t, m) in enumerate(zip(kinds, ms)) if t == "EliminationFactor" and 640 <= m < 1024]
+    small = [k for k, (t, m) in enumerate(zip(kinds, ms)) if t == "EliminationFactor" and m < 640]
+    comp = [k for k, t in enumerate(kinds) if t == "CompressionFactor"]
+    pick.update(spread(big))
+    pick.update(spread(mid, 2))
+    pick.update(small[:1])
+    pick.update(spread(comp))
+    pick.update(comp[-3:])
+    pick.update(k for k, t in enumerate(kinds) if t == "DenseFactor")
+    return sorted(pick)
+
+
+def sample_factor(d, k, f):
+    typ = type(f).__name__
+    m = len(f.idx)
+    W = np.random.default_rng(1000 + k).standard_normal((2, m))
+    cols = np.random.default_rng(1000 + k).choice(m, size=min(2, m), replace=False) if m else np.zeros(0, int)
+    d[f"f{k}_type"] = np.array(typ)
+    d[f"f{k}_idx"] = f.idx.astype(np.int64)
+    d[f"f{k}_node"] = np.int64(-1 if f.node is None else f.node)
+    L = f.L
+    d[f"f{k}_LW"] = L @ W.T
+    d[f"f{k}_LtW"] = L.T @ W.T
+    d[f"f{k}_Lcols"] = np.asarray(cols, np.int64)
+    d[f"f{k}_Lcol"] = L[:, cols]
+    if typ == "EliminationFactor":
+        if f.couplings:
+            E = np.vstack([E for _, E in f.couplings])
+            Eidx = np.concatenate([i for i, _ in f.couplings]).astype(np.int64)
+        else:
+            E, Eidx = np.zeros((0, m)), np.zeros(0, np.int64)
+        V = np.random.default_rng(2000 + k).standard_normal((2, len(Eidx)))
+        d[f"f{k}_Eidx"] = Eidx
+        d[f"f{k}_EW"] = E @ W.T
+        d[f"f{k}_EtV"] = E.T @ V.T
+        d[f"f{k}_Ecol"] = E[:, cols]
+    if typ == "CompressionFactor":
+        r = int(f.retained)
+        Q1 = f.Q[:, :r]
+        d[f"f{k}_r"] = np.int64(r)
+        d[f"f{k}_Q1col"] = np.ascontiguousarray(Q1[:, :min(r, 4)])
+        Wr = np.random.default_rng(3000 + k).standard_normal((2, r))
+        d[f"f{k}_Q1W"] = Q1 @ Wr.T
+        d[f"f{k}_Q1tW"] = Q1.T @ W.T
+
+
+def run_full(name, prob, opts, rhs_seed, full_vectors=False):
+    import time
+    _perms.clear()
+    A = prob.matrix.tocsr()
+    n = prob.n
+    t0 = time.perf_counter()
+    P = pp.factorize(prob, **opts)
+    t_f = time.perf_counter() - t0
+    perms = list(_perms)
+    rhs = np.random.default_rng(rhs_seed).uniform(-1.0, 1.0, n)
+    proj = np.random.default_rng(7).standard_normal((4, n))
+    d = dict(
+        full=np.int8(1), n=np.int64(n), rhs_seed=np.int64(rhs_seed),
+        matrix_digest=np.array(matrix_digest(A)),
+        hier_digest=np.array(hierarchy_digest(prob, opts.get("scheme", "nest-2-2"), P.stats["b"])),
+        opts=json.dumps(opts), stats=json.dumps(P.stats),
+        rank_trace=np.array(P.rank_trace.entries, dtype=np.int64).reshape(-1, 3),
+        perm_ptr=np.cumsum([0] + [len(p) for p in perms]).astype(np.int64),
+        perm_all=np.concatenate(perms) if perms else np.zeros(0, np.int64),
+        blas=json.dumps({k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OPENBLAS_CORETYPE")}),
+        versions=json.dumps({"numpy": np.__version__, "scipy": __import__("scipy").__version__,
+                             "polyprec": pp.__version__}),
+    )
+    y = P.apply_inverse(rhs)
+    vec_sample(d, "apply_inverse", y, proj)
+    if full_vectors:
+        d["apply_inverse"] = y
+    w = P.apply_operator(rhs)
+    vec_sample(d, "apply_operator", w, proj)
+    del y, w
+    t0 = time.perf_counter()
+    x, rep = pp.pcg(lambda v: A @ v, rhs, precond=P.apply_inverse, tol=1e-12, maxit=5000)
+    t_s = time.perf_counter() - t0
+    d.update(pcg_hist=np.array(rep.residual_history), pcg_iters=np.int64(rep.iterations),
+             pcg_final=np.float64(rep.final_rel_residual), pcg_conv=np.int8(rep.converged))
+    vec_sample(d, "pcg_x", x, proj)
+    sel = select_factors(P)
+    d["sampled_factors"] = np.array(sel, np.int64)
+    d["nfactors"] = np.int64(len(P.factors))
+    d["factor_types"] = np.array([{"EliminationFactor": 0, "CompressionFactor": 1, "DenseFactor": 2}[
+        type(f).__name__] for f in P.factors], np.int8)
+    d["factor_sizes"] = np.array([len(f.idx) for f in P.factors], np.int64)
+    for k in sel:
+        sample_factor(d, k, P.factors[k])
+    d["ref_times"] = json.dumps({"t_factor_s": t_f, "t_solve_s": t_s, "host": os.uname().nodename,
+                                 "cpus": os.cpu_count()})
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **d)
+    print(name, "n=%d" % n, "factors=%d" % len(P.factors), "sampled=%d" % len(sel),
+          "t_F=%.1f t_S=%.1f iters=%d" % (t_f, t_s, rep.iterations),
+          "bytes=%d" % os.path.getsize(path), flush=True)
+
+
+FULL_CASES = {
+    "cfg3_full": lambda: run_full("cfg3_full", tpfa(128, 2), dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2),
+                                  rhs_seed=3),
+    "cfg4_full": lambda: run_full("cfg4_full", aniso(128, 1e-3),
+                                  dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-3), rhs_seed=4),
+    "cfg5_full": lambda: run_full("cfg5_full", elast(64, 5), dict(scheme="nest-2-2", degree=1, b=6, rank_tol=1e-2),
+                                  rhs_seed=6),
+    "tpfa40_b9": lambda: run_full("tpfa40_b9", tpfa(40, 2), dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2),
+                                  rhs_seed=3, full_vectors=True),
+}
+
+
 def main():
     T = "nest-2-2"
     run_case("p3d9_exact", pp.poisson7(9), dict(scheme=T, degree=1, mode="exact"), store_factors=True)
@@ -232,4 +412,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    full = [a for a in sys.argv[1:] if a in FULL_CASES]
+    if full:
+        for a in full:
+            FULL_CASES[a]()
+    else:
+        main()
