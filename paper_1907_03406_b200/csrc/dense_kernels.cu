@@ -306,10 +306,12 @@ __global__ void __launch_bounds__(256) sym_check_kernel(long long n, const long 
                                                         const int* __restrict__ ix, const double* __restrict__ v,
                                                         unsigned long long* __restrict__ out) {
   double asym = 0.0, scale = 0.0;
+  bool nonfinite = false;
   for (long long r = blockIdx.x * 256LL + threadIdx.x; r < n; r += (long long)gridDim.x * 256) {
     for (long long e = ip[r]; e < ip[r + 1]; ++e) {
       const int c = ix[e];
       const double a = v[e];
+      nonfinite |= !isfinite(a);
       scale = fmax(scale, fabs(a));
       long long lo = ip[c], hi = ip[c + 1];
       while (lo < hi) {  // first index with ix >= r
@@ -330,6 +332,8 @@ __global__ void __launch_bounds__(256) sym_check_kernel(long long n, const long 
     atomicMax(out, (unsigned long long)__double_as_longlong(asym));
     atomicMax(out + 1, (unsigned long long)__double_as_longlong(scale));
   }
+  // NaN / Inf anywhere (fmax above skips NaN): out[2] != 0
+  if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicMax(out + 2, 1ULL);
 }
 
 cudaError_t launch_sym_check(long long n, const long long* ip, const int* ix, const double* v,

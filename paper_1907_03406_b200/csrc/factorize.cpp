@@ -414,8 +414,8 @@ void setup_level1(State& S) {
     }
     const double* d_vals = a.values_on_device ? a.values : d_vhost;
     {
-      unsigned long long* sym = S.persist.alloc_t<unsigned long long>(2);
-      SGF_CUDA(cudaMemsetAsync(sym, 0, 2 * sizeof(unsigned long long), S.st));
+      unsigned long long* sym = S.persist.alloc_t<unsigned long long>(3);
+      SGF_CUDA(cudaMemsetAsync(sym, 0, 3 * sizeof(unsigned long long), S.st));
       SGF_CUDA(launch_sym_check(n, d_ip, d_ix, d_vals, sym, S.st));
       S.chk.sym = sym;
     }

@@ -528,9 +528,13 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
 void CholCheck::verify(cudaStream_t st) {
   if (sym) {  // an asymmetric matrix is reported before anything computed from it
     SGF_CUDA(cudaStreamSynchronize(st));
-    unsigned long long h[2];
+    unsigned long long h[3];
     SGF_CUDA(cudaMemcpy(h, sym, sizeof h, cudaMemcpyDeviceToHost));
     sym = nullptr;
+    if (h[2]) {  // densela.py:43-49 _as_matrix
+      pend.clear();
+      fail(SGF_INVALID_ARG, "matrix contains NaN or Inf entries");
+    }
     double asym, scale;
     std::memcpy(&asym, &h[0], sizeof(double));
     std::memcpy(&scale, &h[1], sizeof(double));

@@ -284,3 +284,22 @@ def test_full_size_config_matches_reference_run(cfg):
     assert rep.converged and abs(rep.iterations - ref["iters"]) <= 1
     # the returned solution satisfies the tolerance against the host matrix
     assert np.linalg.norm(rhs - prob.matrix @ x) <= 1.5e-12 * np.linalg.norm(rhs)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_matrix_raises_value_error(bad):
+    """reference densela.py:43-49 (_as_matrix): NaN/Inf entries -> ValueError,
+    for host and device-resident values."""
+    import torch
+
+    prob = sgf.poisson7(6)
+    A = prob.matrix.tocsr()
+    A.sort_indices()
+    B = A.copy()
+    B.data[17] = bad
+    q = sgf.ProblemInstance(B, prob.coords, prob.grid, 1, prob.rhs, "p", check_symmetry=False)
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        sgf.factorize(q)
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        sgf.factorize(sgf.ProblemInstance(A, prob.coords, prob.grid, 1, prob.rhs, "p"),
+                      device_values=torch.tensor(B.data, device="cuda"))
