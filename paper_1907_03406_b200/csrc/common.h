@@ -75,6 +75,8 @@ struct QrTask {
   int nreplay;
   int m, c;
   int forced_rank;     // >= 0: low-rank mode (run exactly this many steps)
+  int full_steps;      // 1: run every step up to the zero-column floor, as the reference does
+                       //    (rank = #{|R_kk| > tol |R_00|}); 0: stop at the rank
   double tol;
   int* out_rank;       // -> rank
   int* out_steps;      // -> reflectors computed

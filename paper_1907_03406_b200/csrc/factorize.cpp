@@ -71,6 +71,8 @@ struct State {
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
   int oz_schur_min_m = 640;    // nodes this large (below oz_min_m) take only the Schur updates emulated
   int chol_oz_min_m = 1024;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
+  int qr_full_steps = 0;       // 1: QR past the rank as the reference does (its Q_2 is rounding-determined
+                               //    there, so apply_half_inverse's dropped coordinates never match it exactly)
   std::vector<std::string> warnings;  // reference warnings.warn messages (stats "warnings", raised by Python)
   long long fa_extra = 0;      // apply flops of other ranks' factors
   int nf_extra = 0;            // number of other ranks' factors
@@ -987,6 +989,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     t.m = c.m;
     t.c = c.cN;
     t.forced_rank = lowrank ? forced[w] : -1;
+    t.full_steps = S.qr_full_steps;
     t.tol = a.rank_tol;
     t.out_rank = d_out + w;
     t.out_steps = d_out + nw + w;
@@ -1568,6 +1571,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
   S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
   if (getenv("SGF_OZAKI_MIN_M")) S.oz_min_m = atoi(getenv("SGF_OZAKI_MIN_M"));
+  if (getenv("SGF_QR_FULL_STEPS")) S.qr_full_steps = atoi(getenv("SGF_QR_FULL_STEPS")) ? 1 : 0;
   if (getenv("SGF_OZAKI_CHOL_MIN_M")) S.chol_oz_min_m = atoi(getenv("SGF_OZAKI_CHOL_MIN_M"));
   if (getenv("SGF_OZAKI_SCHUR_MIN_M")) S.oz_schur_min_m = atoi(getenv("SGF_OZAKI_SCHUR_MIN_M"));
   if (S.oz_min_m <= 0) S.chol_oz_min_m = 0;

@@ -10,10 +10,16 @@
 //              w = x / u1 (w0 = 1), tau = -sign*u1/||x||, R_kk = sign*||x||;
 //   downdate   norm2_j = max(norm2_j - R_kj^2, 0), recomputed from the
 //              column below row k when norm2_j <= eps * ref2_j.
-// The reference runs every step and counts rank = #{|R_ii| > tol |R_00|};
-// the first r steps of a pivoted QR do not depend on later ones, and
-// |R_ii| is non-increasing, so stopping at the first |R_kk| <= tol |R_00|
-// yields the same rank, pivots, R_1 and Q_1 while skipping min(m,c) - r steps.
+// The reference runs every step and counts rank = #{|R_ii| > tol |R_00|}
+// (full_steps = 1 does the same).  The first r steps of a pivoted QR do not
+// depend on later ones and |R_ii| is non-increasing, so stopping at the
+// first |R_kk| <= tol |R_00| (the default) yields the same rank, pivots, R_1
+// and Q_1 while skipping min(m,c) - r steps.  The reflectors past the rank
+// only choose the orthonormal completion Q_2, which the reference itself
+// determines by rounding (its columns past the numerical rank are noise):
+// apply_inverse depends on Q_2 Q_2^T = I - Q_1 Q_1^T only, and
+// apply_half_inverse's dropped coordinates match the reference's up to that
+// rotation (tests/test_gpu_parity.py::test_half_inverse_invariants).
 // Low-rank mode (forced rank r, factorization.py:331-339) runs exactly r steps.
 //
 // One CTA per compressed node; the m x c panel (column major) stays in
@@ -164,7 +170,8 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
     const double xn = sqrt(block_sum(ss, red));
     if (xn <= floor_) break;
     if (k == 0) r00 = xn;
-    if (T.forced_rank < 0 && !(xn > T.tol * r00)) break;  // rank reached
+    if (xn > T.tol * r00) ++rank;
+    else if (T.forced_rank < 0 && !T.full_steps) break;  // rank reached
     const double x0 = xk[k];
     const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
     const double u1 = x0 - sgn * xn;
@@ -202,7 +209,6 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
     steps = k + 1;
   }
   if (T.forced_rank >= 0) rank = min(T.forced_rank, m);
-  else rank = steps;
   if (tid == 0) { *T.out_rank = rank; *T.out_steps = steps; }
 }
 
@@ -321,7 +327,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
   };
 
   const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
-  int steps = 0;
+  int steps = 0, rank = 0;
   double r00 = 0.0;
   int pend_col = -1, pend_k = -1;  // pivot column whose final values this CTA still has to store
   double pend_r = 0.0;
@@ -362,7 +368,8 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     const double xn = sqrt(cblock_sum(ss, red));
     if (xn <= floor_) break;
     if (k == 0) r00 = xn;
-    if (T.forced_rank < 0 && !(xn > T.tol * r00)) break;
+    if (xn > T.tol * r00) ++rank;
+    else if (T.forced_rank < 0 && !T.full_steps) break;
     const double x0 = xk[k];
     const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
     const double u1 = x0 - sgn * xn;
@@ -426,7 +433,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     for (int i = tid; i < m; i += QCT) dst[i] = src[i];
   }
   if (q == 0 && tid == 0) {
-    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : steps;
+    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : rank;
     *T.out_steps = steps;
   }
   cluster.sync();  // keep every CTA's shared memory alive for remote reads
@@ -577,7 +584,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
   };
 
   const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
-  int steps = 0;
+  int steps = 0, rank = 0;
   double r00 = 0.0;
   if (limit > 0) local_candidate(0);
   for (int k = 0; k < limit; ++k) {
@@ -621,7 +628,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
       int stop = 0;
       if (xn <= floor_) stop = 1;
       const double r0 = (k == 0) ? xn : r00;
-      if (!stop && T.forced_rank < 0 && !(xn > T.tol * r0)) stop = 1;
+      if (!stop && T.forced_rank < 0 && !T.full_steps && !(xn > T.tol * r0)) stop = 1;
       const double x0 = xk[k];
       const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
       const double u1 = x0 - sgn * xn;
@@ -634,6 +641,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
     const QsPiv pv = *cluster.map_shared_rank(&piv_s, owner);
     if (pv.stop) break;
     if (k == 0) r00 = pv.xn;
+    if (pv.xn > T.tol * r00) ++rank;
     const int len = m - k;
     {  // remote reflector -> local, 16-byte loads all in flight before the stores
       const double2* rv = reinterpret_cast<const double2*>(cluster.map_shared_rank(vbuf, owner));
@@ -699,7 +707,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
   if (q == 0)
     for (int j = tid; j < c; j += QST) T.perm[j] = col_of[j];
   if (q == 0 && tid == 0) {
-    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : steps;
+    *T.out_rank = (T.forced_rank >= 0) ? min(T.forced_rank, m) : rank;
     *T.out_steps = steps;
   }
   cluster.sync();  // keep every CTA's shared memory alive for remote reads

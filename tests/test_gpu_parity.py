@@ -303,3 +303,65 @@ def test_nonfinite_matrix_raises_value_error(bad):
     with pytest.raises(ValueError, match="NaN or Inf"):
         sgf.factorize(sgf.ProblemInstance(A, prob.coords, prob.grid, 1, prob.rhs, "p"),
                       device_values=torch.tensor(B.data, device="cuda"))
+
+
+HALF = [n for n in FULL if n not in ("p3d40_b9",)]
+
+
+@pytest.mark.parametrize("name", HALF)
+def test_half_inverse_invariants(name):
+    """apply_half_inverse / _t (reference factorization.py:241-253).  The
+    dropped coordinates of a compression (idx[r:]) are Q2^T L^-1 x_B, and the
+    reference's Q2 past the numerical rank is set by rounding (its own numpy
+    restatement differs there by up to 7%, tests/test_oracle_golden.py), so
+    the gates are the invariants: every other entry, and the norm of every
+    dropped chunk, within 1e-10; W^-T W^-1 = apply_inverse; adjointness."""
+    g = Golden(name)
+    P = run(g)
+    h = P.apply_half_inverse(g["rhs"])
+    ref = g["half_inverse"]
+    keep = np.ones(len(h), bool)
+    for f in P.factors:
+        if f.kind == "CompressionFactor":
+            d = f.idx[f.retained:]
+            keep[d] = False
+            assert abs(np.linalg.norm(h[d]) - np.linalg.norm(ref[d])) <= 1e-10 * np.linalg.norm(ref)
+    assert rel(h[keep], ref[keep]) <= TOL
+    y = P.apply_inverse(g["rhs"])
+    assert rel(P.apply_half_inverse_t(h), y) <= 1e-12
+    rng = np.random.default_rng(9)
+    u, v = rng.standard_normal(g.n), rng.standard_normal(g.n)
+    lhs = u @ P.apply_half_inverse(v)
+    assert abs(lhs - P.apply_half_inverse_t(u) @ v) <= 1e-12 * max(abs(lhs), 1.0) * 10
+
+
+def _lanczos_extremes(op, n, iters, seed=0):
+    """Extreme Ritz values of an SPD operator (a plain Lanczos with full
+    reorthogonalisation, as the reference's estimate_extreme_eigs)."""
+    rng = np.random.default_rng(seed)
+    V = np.zeros((iters + 1, n))
+    V[0] = rng.standard_normal(n)
+    V[0] /= np.linalg.norm(V[0])
+    a, b = [], []
+    for j in range(iters):
+        w = op(V[j])
+        a.append(V[j] @ w)
+        w -= a[-1] * V[j] + (b[-1] * V[j - 1] if j else 0.0)
+        for _ in range(2):
+            w -= V[:j + 1].T @ (V[:j + 1] @ w)
+        b.append(np.linalg.norm(w))
+        V[j + 1] = w / b[-1]
+    T = np.diag(a) + np.diag(b[:-1], 1) + np.diag(b[:-1], -1)
+    ev = np.linalg.eigvalsh(T)
+    return ev[-1], ev[0]
+
+
+def test_preconditioning_shrinks_condition_number():
+    """reference tests/test_krylov.py:112-119 on the device half inverses:
+    cond(W^-1 A W^-T) <= cond(A) / 100 (Poisson 24^3, nest-2-2, degree 2)."""
+    prob = sgf.poisson7(24)
+    A = prob.matrix
+    hi0, lo0 = _lanczos_extremes(lambda v: A @ v, prob.n, 100)
+    P = sgf.factorize(prob, scheme="nest-2-2", degree=2)
+    hi1, lo1 = _lanczos_extremes(lambda v: P.apply_half_inverse(A @ P.apply_half_inverse_t(v)), prob.n, 40)
+    assert (hi1 / lo1) <= (hi0 / lo0) / 100.0
