@@ -27,6 +27,13 @@
  *   sgf_precond_rank_trace factorization.py:73-109   Preconditioner.rank_trace
  *   sgf_precond_factor_*   factorization.py:112-213  factor attributes (.idx .L .Q .retained
  *                                                    .node .couplings)
+ *   sgf_factor_apply       factorization.py:126-209  factor .solve_forward / .solve_transpose /
+ *                                                    .mult_transpose / .mult_forward
+ *   sgf_pcg_ops            krylov.py:28-102          pcg with callable / @-able operators
+ *   sgf_potrf_batched      densela.py:87-116         cholesky(A)
+ *   sgf_trsm_batched       densela.py:119-146        tri_solve(chol, B, mode)
+ *   sgf_qrcp_batched       densela.py:149-217        pivoted_qr(A, rank_tol, full_q)
+ *   sgf_gemm               densela.py:79-84          matmul(a, b)
  */
 #ifndef SGF_H
 #define SGF_H
@@ -198,6 +205,40 @@ int sgf_memcpy(sgf_ctx* ctx, void* dst, const void* src, int64_t bytes);
 /* Make the context stream wait for all work enqueued so far on `stream`
    (a cudaStream_t, e.g. torch's current stream) before its next launch. */
 int sgf_stream_wait(sgf_ctx* ctx, void* stream);
+
+/* One factor's operation, in place on an n-vector (device pointer when
+   on_device != 0, else host): op 0 solve_forward, 1 solve_transpose,
+   2 mult_transpose, 3 mult_forward (factorization.py:126-148, 173-183,
+   199-209: EliminationFactor / CompressionFactor / DenseFactor methods). */
+enum { SGF_SOLVE_FORWARD = 0, SGF_SOLVE_TRANSPOSE = 1, SGF_MULT_TRANSPOSE = 2, SGF_MULT_FORWARD = 3 };
+int sgf_factor_apply(sgf_precond* p, int k, int op, double* x, int on_device);
+
+/* Per-primitive entry points (densela.py:79-217).  Matrices are row-major
+   DEVICE buffers; the per-matrix size / leading-dimension / pointer arrays
+   and the outputs status / rank are HOST arrays of `batch` entries.
+   sgf_potrf_batched  cholesky (densela.py:87-116): L_b lower with zeros
+     above; status_b = SGF_INVALID_ARG (NaN/Inf, densela.py:43-49),
+     SGF_NON_SYMMETRIC (max|A-A^T| > 1e-12 max|A|, :97-104), SGF_NOT_SPD
+     (pivot <= 1e-14 max diag, :105-110; pivot_index / pivot_value report it)
+   sgf_trsm_batched   tri_solve (densela.py:119-146): mode 0 X = L^-1 B
+     (m x nrhs), 1 X = L^-T B, 2 X = B L^-T (nrhs x m)
+   sgf_qrcp_batched   pivoted_qr (densela.py:149-217): A (m x c) ->
+     perm (c, int32), R (min(m,c) x c upper trapezoid), Q (m x min(m,c), or
+     m x m when full_q), rank = #{|R_ii| > rank_tol |R_00|}; steps = the
+     Householder reflections performed
+   sgf_gemm           matmul (densela.py:79-84): C = alpha A B + beta C,
+     A m x k, B k x n */
+int sgf_potrf_batched(sgf_ctx* ctx, int batch, const int32_t* m, const double* const* A, const int32_t* lda,
+                      double* const* L, const int32_t* ldl, int32_t* status, int32_t* pivot_index,
+                      double* pivot_value);
+int sgf_trsm_batched(sgf_ctx* ctx, int batch, const int32_t* m, const int32_t* nrhs, const int32_t* mode,
+                     const double* const* L, const int32_t* ldl, const double* const* B, const int32_t* ldb,
+                     double* const* X, const int32_t* ldx);
+int sgf_qrcp_batched(sgf_ctx* ctx, int batch, const int32_t* m, const int32_t* c, const double* const* A,
+                     const int32_t* lda, double rank_tol, int full_q, double* const* Q, double* const* R,
+                     int32_t* const* perm, int32_t* rank, int32_t* steps);
+int sgf_gemm(sgf_ctx* ctx, int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+             double beta, double* C, int ldc);
 
 /* Host helper (partition.py:142-199, 232-242 for the level-1 cells): unknown
    ids grouped by cell (cells in id order, vertices ascending, components

@@ -24,6 +24,7 @@ SGF_OK, SGF_NOT_SPD, SGF_SHAPE, SGF_INDEFINITE, SGF_INVALID_ARG, SGF_TRACE, SGF_
 MODE = {"polynomial": 0, "lowrank": 1, "exact": 2}
 APPLY_INVERSE, APPLY_HALF_INVERSE, APPLY_HALF_INVERSE_T, APPLY_OPERATOR = range(4)
 FACTOR_TYPES = {0: "EliminationFactor", 1: "CompressionFactor", 2: "DenseFactor"}
+SOLVE_FORWARD, SOLVE_TRANSPOSE, MULT_TRANSPOSE, MULT_FORWARD = range(4)
 
 # functions the header declares (checked by tests/test_native_abi.py)
 EXPORTS = (
@@ -33,7 +34,7 @@ EXPORTS = (
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read", "sgf_pcg_ops", "sgf_memcpy",
-    "sgf_stream_wait",
+    "sgf_stream_wait", "sgf_factor_apply", "sgf_potrf_batched", "sgf_trsm_batched", "sgf_qrcp_batched", "sgf_gemm",
 )
 PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec", "gemm_int8emu", "int8emu_split")
 
@@ -119,6 +120,11 @@ def load_library(path=LIB_PATH):
                                   C.POINTER(PcgReport), vp]),
             "sgf_memcpy": (i32, [vp, vp, vp, i64]),
             "sgf_stream_wait": (i32, [vp, vp]),
+            "sgf_factor_apply": (i32, [vp, i32, i32, vp, i32]),
+            "sgf_potrf_batched": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "sgf_trsm_batched": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "sgf_qrcp_batched": (i32, [vp, i32, vp, vp, vp, vp, d, i32, vp, vp, vp, vp, vp]),
+            "sgf_gemm": (i32, [vp, i32, i32, i32, d, vp, i32, vp, i32, d, vp, i32]),
             "sgf_kernel_launches": (C.c_uint64, []),
             "sgf_profile_enable": (i32, [i32]),
             "sgf_profile_read": (i32, [vp, i32]),

@@ -3,6 +3,7 @@
 #include <cstdio>
 
 #include "precond.h"
+#include "primitives.h"
 
 using namespace sgf;
 
@@ -469,6 +470,62 @@ int sgf_precond_shard_set(const sgf_precond* p, int which, int64_t* out, int64_t
 int sgf_apply_part(sgf_precond* p, int part, double* y) {
   if (!p || !y) return SGF_INVALID_ARG;
   return guarded(p->ctx, [&] { apply_part(p->p, part, y); });
+}
+
+int sgf_factor_apply(sgf_precond* p, int k, int op, double* x, int on_device) {
+  if (!p || !x) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = p->ctx;
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->c.stream;
+    const long long n = p->p->n;
+    if (on_device) {
+      factor_apply(p->p, k, op, x);
+    } else {
+      DevVec d(n, st);
+      SGF_CUDA(cudaMemcpyAsync(d.p, x, n * 8, cudaMemcpyHostToDevice, st));
+      factor_apply(p->p, k, op, d.p);
+      SGF_CUDA(cudaMemcpyAsync(x, d.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    SGF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int sgf_potrf_batched(sgf_ctx* ctx, int batch, const int32_t* m, const double* const* A, const int32_t* lda,
+                      double* const* L, const int32_t* ldl, int32_t* status, int32_t* pivot_index,
+                      double* pivot_value) {
+  if (!ctx || batch < 0 || (batch && (!m || !A || !lda || !L || !ldl || !status))) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    for (int b = 0; b < batch; ++b)
+      if (m[b] < 0 || lda[b] < m[b] || ldl[b] < m[b]) fail(SGF_INVALID_ARG, "bad matrix size or leading dimension");
+    potrf_batched(ctx->c, batch, m, A, lda, L, ldl, status, pivot_index, pivot_value);
+  });
+}
+
+int sgf_trsm_batched(sgf_ctx* ctx, int batch, const int32_t* m, const int32_t* nrhs, const int32_t* mode,
+                     const double* const* L, const int32_t* ldl, const double* const* B, const int32_t* ldb,
+                     double* const* X, const int32_t* ldx) {
+  if (!ctx || batch < 0 || (batch && (!m || !nrhs || !mode || !L || !ldl || !B || !ldb || !X || !ldx)))
+    return SGF_INVALID_ARG;
+  return guarded(ctx, [&] { trsm_batched(ctx->c, batch, m, nrhs, mode, L, ldl, B, ldb, X, ldx); });
+}
+
+int sgf_qrcp_batched(sgf_ctx* ctx, int batch, const int32_t* m, const int32_t* c, const double* const* A,
+                     const int32_t* lda, double rank_tol, int full_q, double* const* Q, double* const* R,
+                     int32_t* const* perm, int32_t* rank, int32_t* steps) {
+  if (!ctx || batch < 0 || (batch && (!m || !c || !A || !lda || !Q || !R || !perm || !rank))) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    for (int b = 0; b < batch; ++b)
+      if (m[b] < 0 || c[b] < 0 || lda[b] < c[b]) fail(SGF_INVALID_ARG, "bad matrix size or leading dimension");
+    qrcp_batched(ctx->c, batch, m, c, A, lda, rank_tol, full_q, Q, R, perm, rank, steps);
+  });
+}
+
+int sgf_gemm(sgf_ctx* ctx, int m, int n, int k, double alpha, const double* A, int lda, const double* B, int ldb,
+             double beta, double* C, int ldc) {
+  if (!ctx || m < 0 || n < 0 || k < 0 || (m && n && !C)) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    if (m && n) gemm(ctx->c, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  });
 }
 
 }  // extern "C"

@@ -64,6 +64,15 @@ cudaError_t launch_xr_update(double* x, double* r, const double* p, const double
                              double* part, double* out, int slot, cudaStream_t s);
 cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s);
 cudaError_t launch_residual(const double* b, double* out, long long n, cudaStream_t s);
+// factor_ops.cu: small dense kernels of the per-factor methods and per-primitive entry points
+cudaError_t launch_dmv(const double* M, long long ld, int rows, int inner, int trans, const double* v, double* y,
+                       double alpha, double beta, cudaStream_t s);
+cudaError_t launch_dense_check(const double* const* A, const int* m, const int* ld, int n, double* out, int* bad,
+                               cudaStream_t s);
+cudaError_t launch_form_q(const double* V, const double* tau, int m, int s, int qcols, double* Q, double* work,
+                          cudaStream_t st);
+cudaError_t launch_trsv(const double* L, long long ldl, int m, int nvec, const double* B, long long bvs,
+                        long long bes, double* X, long long xvs, long long xes, int trans, cudaStream_t s);
 
 
 // ---------------------------------------------------------------------------

@@ -135,6 +135,43 @@ class _FactorView(object):
         nidx = self._get(3, (self.c,), np.int64)
         return [(nidx, E)] if self.c else []
 
+    def _op(self, op, x):
+        """One factor operation in place on a full n-vector x (a float64 numpy
+        array, or a CUDA tensor on the preconditioner's device), as the
+        reference's factor methods mutate their argument."""
+        pre = self._pre
+        if not isinstance(x, np.ndarray) and getattr(x, "is_cuda", False):
+            import torch
+
+            N.check_device_tensor(x, torch.float64, pre.device, "x")
+            if x.shape != (pre.n,):
+                raise ShapeMismatchError(f"expected a vector of length {pre.n}, got {tuple(x.shape)}")
+            N.order_after_torch(pre._ctx, pre.device)
+            N.raise_for(N.lib().sgf_factor_apply(pre._h, self._k, op, x.data_ptr(), 1), pre._ctx)
+            return
+        if not isinstance(x, np.ndarray) or x.dtype != np.float64 or x.shape != (pre.n,):
+            raise ShapeMismatchError(f"expected a float64 numpy vector of length {pre.n}")
+        buf = x if x.flags["C_CONTIGUOUS"] else np.ascontiguousarray(x)
+        N.raise_for(N.lib().sgf_factor_apply(pre._h, self._k, op, buf.ctypes.data, 0), pre._ctx)
+        if buf is not x:
+            x[:] = buf
+
+    def solve_forward(self, x):
+        """reference factorization.py:126-130 / 173-174 / 199-200."""
+        self._op(N.SOLVE_FORWARD, x)
+
+    def solve_transpose(self, x):
+        """reference factorization.py:132-136 / 176-177 / 202-203."""
+        self._op(N.SOLVE_TRANSPOSE, x)
+
+    def mult_transpose(self, x):
+        """reference factorization.py:138-142 / 179-180 / 205-206."""
+        self._op(N.MULT_TRANSPOSE, x)
+
+    def mult_forward(self, x):
+        """reference factorization.py:144-148 / 182-183 / 208-209."""
+        self._op(N.MULT_FORWARD, x)
+
     def apply_flops(self):
         m = self.m
         return 4 * m * m + (4 * m * self.c if self.kind == "EliminationFactor" else 0)
