@@ -28,7 +28,7 @@ void factor_apply(Precond* P, int k, int op, double* d_x) {
   if (op < 0 || op > 3) fail(SGF_INVALID_ARG, "unknown factor operation");
   cudaStream_t st = P->ctx->stream;
   Factor& f = P->factors[k];
-  if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0 && !f.E) materialize_l1_e(P);
+  if (f.type == SGF_FACTOR_ELIMINATION && f.c > 0) materialize_l1_e(P);  // pending level-1 couplings
   Arena scratch(st);
   const int m = f.m, c = f.c;
   const long long ld = f.ld;
