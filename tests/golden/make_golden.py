@@ -371,6 +371,48 @@ def run_full(name, prob, opts, rhs_seed, full_vectors=False):
           "bytes=%d" % os.path.getsize(path), flush=True)
 
 
+def augment_history_spread(name, prob, opts, rhs_seed):
+    """Add the reference's own rounding sensitivity to a full-size fixture:
+    the same factorization (pivots replayed from the fixture), then the PCG
+    history once with the fixture's matvec `A @ v` (must reproduce the stored
+    history bitwise) and once with `tril(A) @ v + triu(A, 1) @ v` (the same
+    operator summed in another order: a rounding-level perturbation).  Ill-conditioned
+    configs (cfg3, 10^6 contrast) amplify such perturbations through the CG
+    recurrence far beyond 1e-10; pcg_hist_alt bounds what agreement with the
+    reference can mean there."""
+    path = os.path.join(HERE, f"{name}.npz")
+    z = dict(np.load(path))
+    A = prob.matrix.tocsr()
+    n = prob.n
+    rhs = np.random.default_rng(rhs_seed).uniform(-1.0, 1.0, n)
+    P = pp.factorize(prob, **opts)
+    x, rep = pp.pcg(lambda v: A @ v, rhs, precond=P.apply_inverse, tol=1e-12, maxit=5000)
+    same = np.array_equal(np.array(rep.residual_history), z["pcg_hist"])
+    import scipy.sparse as sps
+    Al, Au = sps.tril(A).tocsr(), sps.triu(A, 1).tocsr()
+    x2, rep2 = pp.pcg(lambda v: Al @ v + Au @ v, rhs, precond=P.apply_inverse, tol=1e-12, maxit=5000)
+    z["pcg_hist_alt"] = np.array(rep2.residual_history)
+    z["pcg_iters_alt"] = np.int64(rep2.iterations)
+    z["pcg_hist_repro"] = np.int8(same)
+    np.savez_compressed(path, **z)
+    h, a = z["pcg_hist"], z["pcg_hist_alt"]
+    k = min(len(h), len(a)) - 1
+    print(name, "history reproduced bitwise:", same, "iters", rep.iterations, rep2.iterations,
+          "max rel spread %.2e" % np.max(np.abs(h[:k] - a[:k]) / h[:k]), flush=True)
+
+
+AUGMENT = {
+    "cfg3_full": lambda: augment_history_spread("cfg3_full", tpfa(128, 2),
+                                                dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2), 3),
+    "cfg4_full": lambda: augment_history_spread("cfg4_full", aniso(128, 1e-3),
+                                                dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-3), 4),
+    "cfg5_full": lambda: augment_history_spread("cfg5_full", elast(64, 5),
+                                                dict(scheme="nest-2-2", degree=1, b=6, rank_tol=1e-2), 6),
+    "tpfa40_b9": lambda: augment_history_spread("tpfa40_b9", tpfa(40, 2),
+                                                dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2), 3),
+}
+
+
 FULL_CASES = {
     "cfg3_full": lambda: run_full("cfg3_full", tpfa(128, 2), dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2),
                                   rhs_seed=3),
@@ -412,6 +454,11 @@ def main():
 
 
 if __name__ == "__main__":
+    if "--augment" in sys.argv:
+        for a in sys.argv[1:]:
+            if a in AUGMENT:
+                AUGMENT[a]()
+        sys.exit(0)
     full = [a for a in sys.argv[1:] if a in FULL_CASES]
     if full:
         for a in full:

@@ -49,6 +49,16 @@ def main(name, free=False):
     h = np.array(rep.residual_history)
     ref = g["pcg_hist"]
     k = min(len(h), len(ref)) - 1
+    if "pcg_hist_alt" in g:
+        alt = g["pcg_hist_alt"]
+        n = min(k, len(alt) - 1)
+        print("  reference's own history spread (A@v vs tril+triu order): max %.2e" %
+              np.max(np.abs(alt[:n] - ref[:n]) / ref[:n]))
+    from test_full_size_golden import stable_prefix
+    print("  1e-10 gate applies to history[0:%d] of %d" % (stable_prefix(g, k), k))
+    bad = np.nonzero(np.abs(h[:k] - ref[:k]) > 1e-10 * ref[:k])[0]
+    for i in bad[:12]:
+        print(f"    history[{i}] gpu {h[i]:.6e} ref {ref[i]:.6e} rel {abs(h[i] - ref[i]) / ref[i]:.2e}")
     print(f"  pcg iters {rep.iterations} (ref {int(g['pcg_iters'])}), max hist rel err "
           f"{np.max(np.abs(h[:k] - ref[:k]) / ref[:k]):.2e}, x errs",
           ["%.2e" % v for v in g.vec_errors("pcg_x", x, proj)])
