@@ -29,8 +29,9 @@ host core as BLAS threads, after the GPU measurements.
 Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sgf|reference]
 N > 1 (torchrun, NCCL): the one 128^3 problem is sharded across the ranks
 (sharded.py: subtree ownership of the nested-dissection tree, rank-local
-elimination phase, trailing-matrix reduction onto rank 0, collective apply
-inside PCG); strong scaling, the step time is the max over ranks.
+elimination phase, the ranks' nonzero trailing blocks summed onto rank 0,
+distributed-vector PCG with halo-exchange SpMV and the staged sharded
+apply); strong scaling, the step time is the max over ranks.
 """
 
 import argparse
@@ -259,7 +260,7 @@ def run_sgf(args, ws, rank, local):
         if ws > 1:
             P = S.factorize_sharded(prob, device_values=vals, **opts)
             e1 = ev()
-            x, rep = S.pcg_sharded(Ad, b_dev, P, tol=1e-12)
+            x, rep = S.pcg_sharded(A, b_dev, P, tol=1e-12)  # host pattern: halo plan (built once)
         else:
             P = sgf.factorize(prob, device_values=vals, **opts)
             e1 = ev()

@@ -69,6 +69,18 @@ typedef struct sgf_ctx sgf_ctx;
 typedef struct sgf_precond sgf_precond;
 typedef struct sgf_csr sgf_csr;
 
+/* What one rank contributes to the trailing matrix at the end of the
+   sharded local phase (see sgf_factor_args.exchange). */
+typedef struct {
+  int64_t nblocks;          /* live trailing-matrix blocks: the same sorted list on every rank */
+  int64_t nsend;            /* blocks holding nonzero data on this rank */
+  const int32_t* send_idx;  /* host [nsend]: their positions in the block list */
+  const int32_t* send_meta; /* host [4*nsend]: node a, node b, rank of a, rank of b (-1 = top separator) */
+  const double* send_buf;   /* device: the blocks' entries packed in send_idx order */
+  int64_t send_len;         /* doubles in send_buf */
+  void* accum;              /* rank 0: handle for sgf_exchange_accumulate */
+} sgf_exchange;
+
 typedef struct {
   /* matrix: CSR pattern on the host, values on host or device */
   int64_t n;
@@ -114,15 +126,18 @@ typedef struct {
      <= 1 disables it.  Every rank runs the same symbolic factorization; a
      rank computes only the eliminations of the level-1 cells it owns
      (cell_rank[c] == shard_rank; -1 marks top-separator cells, whose blocks
-     belong to rank 0) for levels 1..shard_stop_level.  Then `exchange` is
-     called with the block regions of the trailing matrix (identical layout
-     on every rank); it must sum them onto rank 0, which continues with the
-     remaining levels while the other ranks stop. */
+     belong to rank 0) for the eliminations of levels 1..shard_stop_level.
+     Then `exchange` is called once on every rank with the trailing-matrix
+     blocks this rank holds nonzero data for (its own cells' blocks and its
+     partial Schur sums of shared blocks, packed); the callback must deliver
+     every other rank's contribution to rank 0, which adds them in ascending
+     rank order with sgf_exchange_accumulate before returning, and continues
+     with the remaining levels while the other ranks stop. */
   int shard_rank;
   int shard_count;
   const int32_t* cell_rank;
   int shard_stop_level;
-  int (*exchange)(void* user, int nregions, double* const* ptrs, const int64_t* counts);
+  int (*exchange)(void* user, const sgf_exchange* x);
   void* exchange_user;
 } sgf_factor_args;
 
@@ -157,6 +172,11 @@ int sgf_precond_factor_copy(const sgf_precond* p, int k, int what, void* host_ou
    mutates x (factorization.py:235-239 copies). */
 int sgf_apply(sgf_precond* p, int op, const double* x, double* y, int on_device);
 
+/* Rank 0 inside its exchange callback: add another rank's packed blocks
+   (positions idx[0..n) of the block list, entries packed in that order;
+   `packed` is a device pointer) into the trailing matrix. */
+int sgf_exchange_accumulate(void* accum, const int32_t* idx, int64_t n, const double* packed);
+
 /* Sharded preconditioners: factors [0, n_local) belong to the rank's local
    phase, [n_local, n) to the top part (rank 0).  n_local_unknowns = unknowns
    eliminated by the local factors; n_top = unknowns still active when the
@@ -170,6 +190,21 @@ int sgf_precond_shard_set(const sgf_precond* p, int which, int64_t* out, int64_t
    local factors, 1 forward then backward over the top factors, 2 backward
    over the local factors.  Parts 0, 1, 2 in sequence = apply_inverse. */
 int sgf_apply_part(sgf_precond* p, int part, double* y);
+/* The sharded apply_inverse on distributed vectors (entries owned by this
+   rank: its local unknowns, plus the top unknowns on rank 0; others zero),
+   in three stages around the caller's collectives on top_buf (n_top):
+     stage 0: y = x; local forward sweeps; top_buf = y[top] - x[top]
+              -> caller sums top_buf onto rank 0
+     stage 1 (rank 0): y[top] = x[top] + top_buf; top sweeps; top_buf = y[top]
+              -> caller broadcasts top_buf
+     stage 2: y[top] = top_buf; local backward sweeps; non-owned entries of
+              y zeroed when mask != 0
+   Device pointers; x is not modified. */
+int sgf_apply_shard(sgf_precond* p, int stage, const double* x, double* y, double* top_buf, int mask);
+/* Device vector helpers on the context stream: out[i] = x[idx[i]] and
+   y[idx[i]] = v[i] (int32 device indices). */
+int sgf_vec_gather(sgf_ctx* ctx, const double* x, const int32_t* idx, double* out, int64_t n);
+int sgf_vec_scatter(sgf_ctx* ctx, const double* v, const int32_t* idx, double* y, int64_t n);
 
 int sgf_csr_create(sgf_ctx* ctx, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                    const double* values, int on_device, sgf_csr** out);
@@ -198,6 +233,17 @@ typedef int (*sgf_matvec_fn)(void* user, const double* in, double* out);
 int sgf_pcg_ops(sgf_ctx* ctx, int64_t n, sgf_csr* a, sgf_matvec_fn mv, void* mv_user, sgf_precond* p,
                 sgf_precond_fn pf, void* pf_user, const double* b, double* x, double tol, int maxit,
                 int true_residual_every, int on_device, sgf_pcg_report* rep, double* history);
+
+/* Distributed PCG (the sharded solve): every vector is a full-length device
+   vector holding this rank's owned entries (zero elsewhere); `mv` computes
+   the owned rows of A in (after its own halo exchange), `pf` the sharded
+   preconditioner, and `reduce` sums nvals host doubles in place across the
+   ranks (same order on every rank, so every rank takes the same branches).
+   Same recurrence and report as sgf_pcg. */
+typedef int (*sgf_reduce_fn)(void* user, double* vals, int nvals);
+int sgf_pcg_dist(sgf_ctx* ctx, int64_t n, sgf_matvec_fn mv, void* mv_user, sgf_precond_fn pf, void* pf_user,
+                 sgf_reduce_fn reduce, void* reduce_user, const double* b, double* x, double tol, int maxit,
+                 int true_residual_every, sgf_pcg_report* rep, double* history);
 
 /* Stream-ordered copy on the context stream (host or device pointers,
    cudaMemcpyDefault), synchronised before returning. */

@@ -35,6 +35,7 @@ EXPORTS = (
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read", "sgf_pcg_ops", "sgf_memcpy",
     "sgf_stream_wait", "sgf_factor_apply", "sgf_potrf_batched", "sgf_trsm_batched", "sgf_qrcp_batched", "sgf_gemm",
+    "sgf_exchange_accumulate", "sgf_apply_shard", "sgf_vec_gather", "sgf_vec_scatter", "sgf_pcg_dist",
 )
 PROF_CLASSES = ("gemm", "gemv", "spmv", "qr", "chol", "copy", "vec", "gemm_int8emu", "int8emu_split")
 
@@ -62,8 +63,17 @@ class FactorArgs(C.Structure):
     ]
 
 
-# int exchange(void* user, int nregions, double* const* ptrs, const int64_t* counts)
-EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64))
+class Exchange(C.Structure):
+    """sgf_exchange (include/sgf.h): one rank's trailing-matrix contribution."""
+    _fields_ = [("nblocks", C.c_int64), ("nsend", C.c_int64), ("send_idx", C.POINTER(C.c_int32)),
+                ("send_meta", C.POINTER(C.c_int32)), ("send_buf", C.c_void_p), ("send_len", C.c_int64),
+                ("accum", C.c_void_p)]
+
+
+# int exchange(void* user, const sgf_exchange* x)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(Exchange))
+# int reduce(void* user, double* vals, int n)
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
 # int precond(void* user, const double* in, double* out)
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 # int matvec(void* user, const double* in, double* out)
@@ -125,6 +135,12 @@ def load_library(path=LIB_PATH):
             "sgf_trsm_batched": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "sgf_qrcp_batched": (i32, [vp, i32, vp, vp, vp, vp, d, i32, vp, vp, vp, vp, vp]),
             "sgf_gemm": (i32, [vp, i32, i32, i32, d, vp, i32, vp, i32, d, vp, i32]),
+            "sgf_exchange_accumulate": (i32, [vp, vp, i64, vp]),
+            "sgf_apply_shard": (i32, [vp, i32, vp, vp, vp, i32]),
+            "sgf_vec_gather": (i32, [vp, vp, vp, vp, i64]),
+            "sgf_vec_scatter": (i32, [vp, vp, vp, vp, i64]),
+            "sgf_pcg_dist": (i32, [vp, i64, MATVEC_FN, vp, PRECOND_FN, vp, REDUCE_FN, vp, vp, vp, d, i32, i32,
+                                   C.POINTER(PcgReport), vp]),
             "sgf_kernel_launches": (C.c_uint64, []),
             "sgf_profile_enable": (i32, [i32]),
             "sgf_profile_read": (i32, [vp, i32]),

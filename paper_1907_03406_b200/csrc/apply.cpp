@@ -575,6 +575,42 @@ void apply_part(Precond* P, int part, double* y) {
   }
 }
 
+// The sharded apply_inverse on distributed vectors (sgf_apply_shard): the
+// local sweeps, the top unknowns' exchange buffer and the ownership mask as
+// native steps, so the caller only runs the collectives on top_buf.
+void apply_shard(Precond* P, int stage, const double* x, double* y, double* top_buf, int mask) {
+  cudaStream_t st = P->ctx->stream;
+  const long long n = P->n, nt = (long long)P->top_idx.size();
+  if (!P->d_top) {
+    std::vector<int> t(P->top_idx.begin(), P->top_idx.end());
+    std::vector<unsigned char> own(n, 0);
+    for (size_t i = 0; i < P->local_count(); ++i)
+      for (int64_t u : P->factors[i].idx) own[u] = 1;
+    if (P->shard_rank == 0)
+      for (int64_t u : P->top_idx) own[u] = 1;
+    P->d_top = P->store.alloc_t<int>(std::max<long long>(nt, 1));
+    P->d_owned = P->store.alloc_t<unsigned char>(std::max<long long>(n, 1));
+    if (nt) SGF_CUDA(cudaMemcpyAsync(P->d_top, t.data(), nt * sizeof(int), cudaMemcpyHostToDevice, st));
+    SGF_CUDA(cudaMemcpyAsync(P->d_owned, own.data(), n, cudaMemcpyHostToDevice, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+  }
+  if (stage == 0) {
+    if (y != x) SGF_CUDA(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    apply_part(P, 0, y);
+    SGF_CUDA(launch_gather_diff(y, x, P->d_top, top_buf, nt, st));
+  } else if (stage == 1) {
+    SGF_CUDA(launch_scatter_base(y, x, P->d_top, top_buf, nt, st));
+    apply_part(P, 1, y);
+    SGF_CUDA(launch_gather(y, P->d_top, top_buf, nt, st));
+  } else if (stage == 2) {
+    SGF_CUDA(launch_scatter_base(y, nullptr, P->d_top, top_buf, nt, st));
+    apply_part(P, 2, y);
+    if (mask) SGF_CUDA(launch_mask(y, P->d_owned, n, st));
+  } else {
+    fail(SGF_INVALID_ARG, "unknown apply stage");
+  }
+}
+
 // ---------------------------------------------------------------------------
 void spmv(Csr* A, const double* d_x, double* d_y, const double* d_b) {
   // values + int32 columns + row pointers + x + y (+ b)
@@ -711,6 +747,119 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
   rep->converged = (converged && fin <= tol) ? 1 : 0;
   rep->final_rel_residual = fin;
   rep->history_len = hl;
+  rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Distributed PCG (the sharded solve, sgf_pcg_dist): the reference recurrence
+// (krylov.py:34-102) on vectors holding this rank's owned entries.  Every
+// inner product is a local partial (non-owned entries are zero) summed across
+// the ranks by the caller's `reduce` before anything uses it, so the scalars
+// -- and every branch -- are identical on all ranks.  A's owned rows come
+// from the caller's operator (halo exchange + row-block SpMV), M^-1 from the
+// sharded apply.
+void pcg_dist(Ctx& ctx, int64_t n, const MatFn& Aop, const PrecFn& M, const ReduceFn& reduce, const double* d_b,
+              double* d_x, double tol, int maxit, int true_every, sgf_pcg_report* rep, double* history) {
+  cudaStream_t st = ctx.stream;
+  auto t0 = std::chrono::steady_clock::now();
+  Arena ws(st);
+  const long long np = (n + 31) & ~31LL;
+  double* r = ws.alloc(4 * np + 512 + 8);
+  double* z = r + np;
+  double* p = z + np;
+  double* q = p + np;
+  double* part = q + np;
+  double* sc = part + 512;  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  double* hsc = nullptr;
+  SGF_CUDA(cudaMallocHost((void**)&hsc, 8 * sizeof(double)));
+  struct Pin {
+    double* p;
+    ~Pin() { cudaFreeHost(p); }
+  } pin{hsc};
+  // device scalar -> host, summed over the ranks, written back for the kernels
+  auto global = [&](int slot) {
+    SGF_CUDA(cudaMemcpyAsync(hsc + slot, sc + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+    reduce(hsc + slot, 1);
+    SGF_CUDA(cudaMemcpyAsync(sc + slot, hsc + slot, sizeof(double), cudaMemcpyHostToDevice, st));
+    return hsc[slot];
+  };
+  auto residual = [&]() {  // r = b - A x
+    Aop(d_x, r);
+    SGF_CUDA(launch_residual(d_b, r, n, st));
+  };
+  int hl = 0;
+  SGF_CUDA(launch_dot(d_b, d_b, n, part, sc, 4, st));
+  const double bnorm = std::sqrt(global(4));
+  SGF_CUDA(cudaMemsetAsync(d_x, 0, n * sizeof(double), st));
+  if (bnorm == 0.0) {
+    history[hl++] = 0.0;
+    rep->iterations = 0;
+    rep->converged = 1;
+    rep->final_rel_residual = 0.0;
+    rep->history_len = hl;
+    SGF_CUDA(cudaStreamSynchronize(st));
+    rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return;
+  }
+  SGF_CUDA(cudaMemcpyAsync(r, d_b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  history[hl++] = 1.0;
+  M(r, z);
+  SGF_CUDA(launch_dot(r, z, n, part, sc, 0, st));
+  if (global(0) <= 0.0) {
+    char buf[96];
+    snprintf(buf, sizeof buf, "initial r'Mr = %.3e is not positive", hsc[0]);
+    fail(SGF_INDEFINITE, buf);
+  }
+  SGF_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  bool converged = false;
+  int it = 0;
+  while (it < maxit) {
+    ++it;
+    Aop(p, q);
+    SGF_CUDA(launch_dot(p, q, n, part, sc, 1, st));
+    const double pAp = global(1);
+    if (pAp <= 0.0) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "p'Ap = %.3e at iteration %d", pAp, it);
+      fail(SGF_INDEFINITE, buf);
+    }
+    SGF_CUDA(launch_xr_update(d_x, r, p, q, n, sc, part, sc, 3, st));
+    if (true_every > 0 && it % true_every == 0) {
+      residual();
+      SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+    }
+    double rel = std::sqrt(global(3)) / bnorm;
+    if (rel <= tol) {
+      residual();
+      SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+      rel = std::sqrt(global(3)) / bnorm;
+      history[hl++] = rel;
+      if (rel <= tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      history[hl++] = rel;
+    }
+    M(r, z);
+    SGF_CUDA(launch_dot(r, z, n, part, sc, 2, st));
+    const double rz_new = global(2);
+    if (rz_new <= 0.0) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "r'Mr = %.3e at iteration %d", rz_new, it);
+      fail(SGF_INDEFINITE, buf);
+    }
+    SGF_CUDA(launch_p_update(p, z, n, sc, st));
+    SGF_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  residual();
+  SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
+  const double fin = std::sqrt(global(3)) / bnorm;
+  rep->iterations = it;
+  rep->converged = (converged && fin <= tol) ? 1 : 0;
+  rep->final_rel_residual = fin;
+  rep->history_len = hl;
+  SGF_CUDA(cudaStreamSynchronize(st));
   rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

@@ -528,4 +528,60 @@ int sgf_gemm(sgf_ctx* ctx, int m, int n, int k, double alpha, const double* A, i
   });
 }
 
+int sgf_exchange_accumulate(void* accum, const int32_t* idx, int64_t n, const double* packed) {
+  if (!accum || n < 0 || (n && (!idx || !packed))) return SGF_INVALID_ARG;
+  return guarded(nullptr, [&] { exchange_accumulate((ShardExchange*)accum, idx, n, packed); });
+}
+
+int sgf_apply_shard(sgf_precond* p, int stage, const double* x, double* y, double* top_buf, int mask) {
+  if (!p || !x || !y || (!top_buf && !p->p->top_idx.empty())) return SGF_INVALID_ARG;
+  return guarded(p->ctx, [&] {
+    if (!p->p->sharded) fail(SGF_INVALID_ARG, "not a sharded preconditioner");
+    apply_shard(p->p, stage, x, y, top_buf, mask);
+    SGF_CUDA(cudaStreamSynchronize(p->ctx->c.stream));
+  });
+}
+
+int sgf_vec_gather(sgf_ctx* ctx, const double* x, const int32_t* idx, double* out, int64_t n) {
+  if (!ctx || n < 0 || (n && (!x || !idx || !out))) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    SGF_CUDA(launch_gather(x, idx, out, n, ctx->c.stream));
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sgf_vec_scatter(sgf_ctx* ctx, const double* v, const int32_t* idx, double* y, int64_t n) {
+  if (!ctx || n < 0 || (n && (!v || !idx || !y))) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    SGF_CUDA(launch_scatter(v, idx, y, n, ctx->c.stream));
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sgf_pcg_dist(sgf_ctx* ctx, int64_t n, sgf_matvec_fn mv, void* mv_user, sgf_precond_fn pf, void* pf_user,
+                 sgf_reduce_fn reduce, void* reduce_user, const double* b, double* x, double tol, int maxit,
+                 int true_residual_every, sgf_pcg_report* rep, double* history) {
+  if (!ctx || !mv || !reduce || !b || !x || !rep || !history || n < 0) return SGF_INVALID_ARG;
+  return guarded(ctx, [&] {
+    MatFn Aop = [mv, mv_user](const double* in, double* out) {
+      const int rc = mv(mv_user, in, out);
+      if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "operator callback failed");
+    };
+    PrecFn M;
+    if (pf)
+      M = [pf, pf_user](const double* in, double* out) {
+        const int rc = pf(pf_user, in, out);
+        if (rc != 0) fail(rc > 0 && rc <= SGF_NON_SYMMETRIC ? rc : SGF_CUDA, "preconditioner callback failed");
+      };
+    else
+      M = [ctx, n](const double* in, double* out) {
+        SGF_CUDA(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->c.stream));
+      };
+    ReduceFn R = [reduce, reduce_user](double* v, int k) {
+      if (reduce(reduce_user, v, k) != 0) fail(SGF_CUDA, "reduction callback failed");
+    };
+    pcg_dist(ctx->c, n, Aop, M, R, b, x, tol, maxit, true_residual_every, rep, history);
+  });
+}
+
 }  // extern "C"

@@ -184,4 +184,89 @@ cudaError_t launch_trsv(const double* L, long long ldl, int m, int nvec, const d
   return cudaGetLastError();
 }
 
+// ---- sharded factorization / apply / PCG helpers ------------------------------
+// flags[b] = 1 when block b (ptrs[b], counts[b] doubles) holds a nonzero
+__global__ void nonzero_flags_kernel(const double* const* __restrict__ ptrs, const long long* __restrict__ counts,
+                                     int* __restrict__ flags) {
+  const int b = blockIdx.x;
+  const double* p = ptrs[b];
+  int nz = 0;
+  for (long long i = threadIdx.x; i < counts[b] && !nz; i += blockDim.x) nz = p[i] != 0.0;
+  nz = __syncthreads_or(nz);
+  if (threadIdx.x == 0) flags[b] = nz;
+}
+
+cudaError_t launch_nonzero_flags(const double* const* ptrs, const long long* counts, int n, int* flags,
+                                 cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  nonzero_flags_kernel<<<n, 256, 0, s>>>(ptrs, counts, flags);
+  return cudaGetLastError();
+}
+
+// dst[b][i] += packed[offs[b] + i]  (one block per destination block)
+__global__ void add_packed_kernel(double* const* __restrict__ dst, const long long* __restrict__ counts,
+                                  const long long* __restrict__ offs, const double* __restrict__ packed) {
+  const int b = blockIdx.x;
+  double* d = dst[b];
+  const double* s = packed + offs[b];
+  for (long long i = threadIdx.x; i < counts[b]; i += blockDim.x) d[i] += s[i];
+}
+
+cudaError_t launch_add_packed(double* const* dst, const long long* counts, const long long* offs, int n,
+                              const double* packed, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  add_packed_kernel<<<n, 256, 0, s>>>(dst, counts, offs, packed);
+  return cudaGetLastError();
+}
+
+// out[i] = y[idx[i]] - x[idx[i]]   (changes of the top unknowns)
+__global__ void gather_diff_kernel(const double* __restrict__ y, const double* __restrict__ x,
+                                   const int* __restrict__ idx, double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const int k = idx[i];
+    out[i] = y[k] - x[k];
+  }
+}
+// y[idx[i]] = base[idx[i]] + d[i]  (base may be null: y[idx[i]] = d[i])
+__global__ void scatter_base_kernel(double* __restrict__ y, const double* __restrict__ base,
+                                    const int* __restrict__ idx, const double* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    const int k = idx[i];
+    y[k] = (base ? base[k] : 0.0) + d[i];
+  }
+}
+// y[i] = 0 where owned[i] == 0
+__global__ void mask_kernel(double* __restrict__ y, const unsigned char* __restrict__ owned, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+    if (!owned[i]) y[i] = 0.0;
+}
+
+static unsigned grid_n(long long n) {
+  long long g = (n + 255) / 256;
+  return (unsigned)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
+}
+
+cudaError_t launch_gather_diff(const double* y, const double* x, const int* idx, double* out, long long n,
+                               cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  gather_diff_kernel<<<grid_n(n), 256, 0, s>>>(y, x, idx, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_base(double* y, const double* base, const int* idx, const double* d, long long n,
+                                cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  scatter_base_kernel<<<grid_n(n), 256, 0, s>>>(y, base, idx, d, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_mask(double* y, const unsigned char* owned, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  mask_kernel<<<grid_n(n), 256, 0, s>>>(y, owned, n);
+  return cudaGetLastError();
+}
+
 }  // namespace sgf

@@ -1458,6 +1458,58 @@ void final_dense(State& S) {
   P->factors.push_back(std::move(f));
 }
 
+// End of the sharded local phase: the live trailing-matrix blocks in key
+// order (the same list on every rank: the symbolic loop is identical), the
+// ones holding nonzero data on this rank (own cells' blocks, partial Schur
+// sums of shared blocks; an all-zero block contributes nothing to the sum),
+// packed into one device buffer for the caller's collective.
+void build_exchange(State& S, ShardExchange& X) {
+  cudaStream_t st = S.st;
+  std::vector<std::pair<uint64_t, Blk>> blks;
+  S.M.map.for_each([&](uint64_t k, Blk& b) {
+    if ((long long)b.rows * b.cols > 0 && b.p) blks.push_back({k, b});
+  });
+  std::sort(blks.begin(), blks.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+  const int nb = (int)blks.size();
+  X.st = st;
+  X.ptrs.resize(nb);
+  X.counts.resize(nb);
+  X.total = 0;
+  for (int i = 0; i < nb; ++i) {
+    X.ptrs[i] = blks[i].second.p;
+    X.counts[i] = (long long)blks[i].second.rows * blks[i].second.cols;
+    X.total += 8 * X.counts[i];
+  }
+  std::vector<int> flags(std::max(nb, 1), 0);
+  if (nb) {
+    int* d_flags = S.scratch.alloc_t<int>(nb);
+    SGF_CUDA(launch_nonzero_flags(S.scratch.upload(X.ptrs), S.scratch.upload(X.counts), nb, d_flags, st));
+    SGF_CUDA(cudaMemcpyAsync(flags.data(), d_flags, nb * sizeof(int), cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+  }
+  long long off = 0;
+  CopyBatch cp;
+  std::vector<long long> offs;
+  for (int i = 0; i < nb; ++i) {
+    if (!flags[i]) continue;
+    X.send_idx.push_back(i);
+    const int a0 = (int)(blks[i].first >> 32), b0 = (int)(blks[i].first & 0xffffffffu);
+    X.send_meta.insert(X.send_meta.end(), {a0, b0, S.node_rank[a0], S.node_rank[b0]});
+    offs.push_back(off);
+    off += X.counts[i];
+  }
+  X.send_len = off;
+  X.send_buf = S.scratch.alloc(std::max<long long>(off, 1));
+  // pack: every block is a contiguous row-major rows x cols matrix
+  for (size_t j = 0; j < X.send_idx.size(); ++j) {
+    const Blk& b = blks[X.send_idx[j]].second;
+    cp.add(b.p, b.cols, 1, X.send_buf + offs[j], b.cols, 1, b.rows, b.cols);
+  }
+  cp.launch(S.scratch, st);
+  SGF_CUDA(cudaStreamSynchronize(st));
+  X.scratch = &S.scratch;
+}
+
 std::string stats_json(const sgf_factor_args& a, int64_t n, const std::vector<LevelStats>& lv, int max_after,
                        int max_seen, int final_dense, long long flops, long long flops_apply, long long peak,
                        int nfactors, const std::vector<std::string>& warnings) {
@@ -1547,6 +1599,25 @@ class PlanWorker {
 
 }  // namespace
 
+void exchange_accumulate(ShardExchange* X, const int32_t* idx, int64_t n, const double* packed) {
+  std::vector<double*> dst(n);
+  std::vector<long long> cnt(n), offs(n);
+  long long off = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (idx[j] < 0 || idx[j] >= (int64_t)X->ptrs.size()) fail(SGF_INVALID_ARG, "exchange block index out of range");
+    dst[j] = X->ptrs[idx[j]];
+    cnt[j] = X->counts[idx[j]];
+    offs[j] = off;
+    off += cnt[j];
+  }
+  if (n) {
+    Arena& sc = *X->scratch;
+    SGF_CUDA(launch_add_packed(sc.upload(dst), sc.upload(cnt), sc.upload(offs), (int)n, packed, X->st));
+  }
+  SGF_CUDA(cudaStreamSynchronize(X->st));
+}
+
+
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   if (a.n <= 0 || a.nlevels <= 0 || !a.indptr || !a.indices || !a.values || !a.l1_ptr || !a.l1_unknowns)
     fail(SGF_INVALID_ARG, "incomplete factorization arguments");
@@ -1591,18 +1662,23 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   auto end_local_phase = [&]() {
     exchanged = true;
     P->sharded = true;
+    P->shard_rank = S.my_rank;
     P->n_local = P->factors.size();
     for (auto& nd : S.nodes) P->top_idx.insert(P->top_idx.end(), nd.active.begin(), nd.active.end());
-    std::vector<double*> ptrs;
-    std::vector<int64_t> counts;
-    for (auto& r : S.regions)
-      if (r.second > 0) {
-        ptrs.push_back(r.first);
-        counts.push_back(r.second);
-      }
-    SGF_CUDA(cudaStreamSynchronize(S.st));
-    const int rc = a.exchange(a.exchange_user, (int)ptrs.size(), ptrs.data(), counts.data());
+    ShardExchange X;
+    build_exchange(S, X);
+    sgf_exchange e;
+    e.nblocks = (int64_t)X.ptrs.size();
+    e.nsend = (int64_t)X.send_idx.size();
+    e.send_idx = X.send_idx.data();
+    e.send_meta = X.send_meta.data();
+    e.send_buf = X.send_buf;
+    e.send_len = X.send_len;
+    e.accum = S.my_rank == 0 ? &X : nullptr;
+    const int rc = a.exchange(a.exchange_user, &e);
     if (rc != 0) fail(SGF_CUDA, "shard exchange callback failed");
+    SGF_CUDA(cudaStreamSynchronize(S.st));
+    P->exchange_log.push_back({(int64_t)X.send_idx.size(), 8 * X.send_len, (int64_t)X.ptrs.size(), X.total});
     if (S.my_rank != 0) stopped = true;
     else S.sharded = false;  // rank 0 now holds the whole trailing matrix and eliminates everything
   };

@@ -1,6 +1,7 @@
 // Device-resident preconditioner: the ordered elementary factors of the
 // reference (factorization.py:112-213) plus the level-batched apply plan.
 #pragma once
+#include <array>
 #include <deque>
 #include <functional>
 #include <memory>
@@ -82,11 +83,31 @@ class Precond {
   bool sharded = false;
   size_t n_local = 0;
   std::vector<int64_t> top_idx;
+  // sharded: per exchange {blocks sent, bytes sent, blocks in the list, bytes of the whole list}
+  std::vector<std::array<int64_t, 4>> exchange_log;
+  // sharded apply (sgf_apply_shard): device top indices and owned-entry flags, built on first use
+  int shard_rank = 0;
+  int* d_top = nullptr;
+  unsigned char* d_owned = nullptr;
   size_t local_count() const { return sharded ? n_local : factors.size(); }
   ~Precond() {
     if (plan) destroy_plan(plan);
   }
 };
+
+// the trailing-matrix contribution of one rank at the end of the sharded local phase
+struct ShardExchange {
+  cudaStream_t st = nullptr;
+  Arena* scratch = nullptr;
+  std::vector<double*> ptrs;     // every live block, key order
+  std::vector<long long> counts;
+  long long total = 0;           // bytes of all blocks
+  std::vector<int32_t> send_idx;
+  std::vector<int32_t> send_meta;
+  double* send_buf = nullptr;
+  long long send_len = 0;
+};
+void exchange_accumulate(ShardExchange* X, const int32_t* idx, int64_t n, const double* packed);
 
 Precond* factorize(Ctx& ctx, const sgf_factor_args& a);
 void materialize_l1_e(Precond* P);  // form the pending level-1 couplings E (stream ordered)
@@ -116,5 +137,10 @@ using MatFn = std::function<void(const double*, double*)>;
 // absent (only A->n is used)
 void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b, double* d_x, double tol, int maxit,
          int true_every, sgf_pcg_report* rep, double* history);
+// sums host doubles in place across the ranks of a sharded solve
+using ReduceFn = std::function<void(double*, int)>;
+void pcg_dist(Ctx& ctx, int64_t n, const MatFn& Aop, const PrecFn& M, const ReduceFn& reduce, const double* d_b,
+              double* d_x, double tol, int maxit, int true_every, sgf_pcg_report* rep, double* history);
+void apply_shard(Precond* P, int stage, const double* x, double* y, double* top_buf, int mask);
 
 }  // namespace sgf

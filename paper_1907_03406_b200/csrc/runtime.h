@@ -73,6 +73,15 @@ cudaError_t launch_form_q(const double* V, const double* tau, int m, int s, int 
                           cudaStream_t st);
 cudaError_t launch_trsv(const double* L, long long ldl, int m, int nvec, const double* B, long long bvs,
                         long long bes, double* X, long long xvs, long long xes, int trans, cudaStream_t s);
+cudaError_t launch_nonzero_flags(const double* const* ptrs, const long long* counts, int n, int* flags,
+                                 cudaStream_t s);
+cudaError_t launch_add_packed(double* const* dst, const long long* counts, const long long* offs, int n,
+                              const double* packed, cudaStream_t s);
+cudaError_t launch_gather_diff(const double* y, const double* x, const int* idx, double* out, long long n,
+                               cudaStream_t s);
+cudaError_t launch_scatter_base(double* y, const double* base, const int* idx, const double* d, long long n,
+                                cudaStream_t s);
+cudaError_t launch_mask(double* y, const unsigned char* owned, long long n, cudaStream_t s);
 
 
 // ---------------------------------------------------------------------------

@@ -52,6 +52,7 @@ class DeviceCSR(object):
         h = C.c_void_p()
         if A is not None:
             A = sp.csr_matrix(A)
+            self._host = A  # the pattern, for callers that plan on it (sharded.pcg_sharded)
             if A.shape[0] != A.shape[1]:
                 raise ShapeMismatchError(f"operator must be square, got {A.shape}")
             self.shape = A.shape

@@ -97,8 +97,24 @@ def solve_mode(args):
                                   zip(reps.residual_history[:-1], rep1.residual_history[:-1]))) if
             len(rep1.residual_history) > 1 else 0.0,
             "local_factors": PS.n_local_factors,
-            "top_unknowns": int(PS.top_idx.numel()),
+            "local_levels": sorted({f.level for f in PS.pre.factors[:PS.n_local_factors]}),
+            "local_big": sum(1 for f in PS.pre.factors[:PS.n_local_factors] if f.m >= 1024),
+            "top_unknowns": int(len(PS.top_idx)),
+            "stop": PS.plan.get("stop"),
+            "partition_level": PS.plan.get("partition_level"),
         }
+        log = PS.exchange_log
+        if log:
+            meta = np.asarray(log["sent_meta"]).reshape(-1, 4)
+            # a rank != 0 sends only blocks touching its own cells, or shared
+            # (top-separator x top-separator) blocks carrying its Schur sums
+            if rank != 0 and len(meta):
+                ok = (meta[:, 2] == rank) | (meta[:, 3] == rank) | ((meta[:, 2] < 0) & (meta[:, 3] < 0))
+            else:
+                ok = np.ones(len(meta), bool)
+            r.update(exchange_blocks=int(log["nblocks"]), sent_blocks=int(log["sent_blocks"]),
+                     sent_bytes=int(log["sent_bytes"]), exchange_ok=bool(ok.all()),
+                     sent_foreign=int((~ok).sum()), per_rank=log["per_rank"])
         if args.free:
             # free-running pivots: iteration count within +-1 (SURVEY.md 8c gate 5)
             PF = S.factorize_sharded(prob, device=dev, **opts)

@@ -47,7 +47,9 @@ def test_shard_plan_two_ranks_gloo():
         assert r0[k] == r1[k]
     assert r0["(128, 128, 128)-9-True-8"] == {"stop": 3, "p": 4, "ranks_used": list(range(8)), "shared": 2437,
                                               "cells": 24389}
-    assert r0["(40, 40, 40)-9-True-2"]["stop"] == 2
+    # cfg2-like (3 levels): the level-3 interiors are the partition cells, so
+    # their eliminations (the big nodes) run on their owners
+    assert r0["(40, 40, 40)-9-True-2"]["stop"] == 3 and r0["(40, 40, 40)-9-True-2"]["p"] == 3
     assert r0["reduce"] == [3.0] * 5 and r1["reduce"] is None
     assert r0["bcast"] == r1["bcast"] == [7.0] * 3
     assert r0["allreduce"] == r1["allreduce"] == [0.5, 1.5]
@@ -65,6 +67,11 @@ def _check_solve(res, cases):
         r = res["ranks"][0][name]
         assert r["stats_equal"], (name, r["stats_diff"])
         assert r["trace_equal"], name
+        # the exchange moves only what each rank holds: its own cells' blocks and
+        # its partial sums of shared blocks, never another rank's blocks
+        for rk in res["ranks"]:
+            if "exchange_ok" in rk[name]:
+                assert rk[name]["exchange_ok"], (name, rk[name]["sent_foreign"])
 
 
 @pytest.mark.gpu
@@ -110,3 +117,12 @@ def test_sharded_cfg2_two_ranks():
     # run the INT8-emulated products inside the rank-local phase / on rank 0
     res = _launch(2, "--mode", "solve", "--backend", "gloo", "--cases", "cfg2", timeout=1500)
     _check_solve(res, ["cfg2"])
+    # the level-3 eliminations (2654-3571 unknowns, 71.5% of the flops) run
+    # on their owners: 4 on each rank
+    for rk in res["ranks"]:
+        r = rk["cfg2"]
+        assert r["stop"] == 3 and 3 in r["local_levels"], r
+        assert r["local_big"] == 4, r
+    # rank 1 sends only part of the trailing matrix
+    r1 = res["ranks"][1]["cfg2"]
+    assert 0 < r1["sent_blocks"] < r1["exchange_blocks"], r1
