@@ -4,18 +4,24 @@
 // tcgen05 has no f64 kind; DMMA (mma.sync f64) tops out at ~37 TFLOP/s.  The
 // 5th-generation tensor cores run kind::i8 at ~4.5 POPS with exact int32
 // accumulation in TMEM, so an FP64 product can be assembled from int8 ones:
-// every row of an operand is scaled by a power of two (|x| < 1) and cut into
-// S = 8 signed 7-bit slices, x = 2^e sum_t d_t 2^-7t (truncation: exact), and
-//   (A B^T)_ij = 2^(ea_i + eb_j) sum_{t,u} 2^-7(t+u) (A_t B_u^T)_ij .
-// Pairs with t + u <= S + 1 are kept (56 bits relative to the row maxima);
-// pairs of one diagonal d = t + u accumulate exactly in one int32 TMEM
-// accumulator.  The MMA shape is M=128, N=128 (tools/i8_peak.cu: N=64 issues
-// at only 61% of the 4.5 POPS reached from N=128 on), so the 8 diagonals
-// x 128 columns do not fit the 512 TMEM columns at once: a product runs in two
-// passes over K, diagonals d = 2..5 (slices 1..4 only) then d = 6..9, each
-// pass draining its 4 accumulators into the FP64 output.  The epilogue sums
-// 2^-7d S_d in FP64.  Error ~1e-14 of sum |a||b| (tools/ozaki_test.cu,
-// tools/oz_batch_test.cu).
+// every row of an operand is scaled by a power of two (|x| < 1), truncated to
+// a 62-bit fixed-point integer F = trunc(|x| 2^62) (sign applied) and written
+// as S = 8 balanced base-256 digits d_t in [-128, 127] (two's-complement
+// bytes with carries: exact), x = 2^e sum_t d_t 2^-(8t+6), so
+//   (A B^T)_ij = 2^(ea_i + eb_j) sum_{t,u} 2^-(8(t+u)+12) (A_t B_u^T)_ij .
+// Pairs with t + u <= S - 1 are kept (36 of 64; the dropped ones weigh
+// <= 2^-62 of the row maxima, like the truncation); pairs of one diagonal
+// d = t + u accumulate exactly in one int32 TMEM accumulator (<= 8 pairs x
+// K x 2^14 < 2^31 for K <= 16384).  The MMA shape is M=128, N=128
+// (tools/i8_peak.cu: N=64 issues at only 61% of the 4.5 POPS reached from
+// N=128 on), so the 8 diagonals x 128 columns do not fit the 512 TMEM columns
+// at once: a product runs in two passes over K, diagonals d = 0..3 (slices
+// 0..3 only) then d = 4..7, each pass draining its 4 accumulators into the
+// FP64 output.  The epilogue sums 2^-(8d+12) S_d in FP64.  Error <= ~2 K
+// 2^-62 max|A_i| max|B_j| (tools/oz_batch_test.cu, graded rows included).
+// (A first version used 7-bit sign-magnitude slices, 56 bits: on BASELINE
+// cfg5 its level-3 Schur updates moved apply_inverse by 5.6e-10 against the
+// reference, over the 1e-10 gate; the balanced 8-bit digits cost nothing.)
 //
 // Operand layout (written by oz_split_kernel): for an R-row operand padded to
 // Rp rows (multiple of 128) and Kp columns (multiple of 32),
@@ -71,6 +77,27 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
 }
 
+// the S balanced base-256 digits of x 2^-ex (|x| 2^-ex < 1), most
+// significant first: F = trunc(|x| 2^(62-ex)) with x's sign, then
+// d = F mod 256 in [-128, 127], F = (F - d) / 256, least significant first
+__device__ __forceinline__ void oz_digits(double x, int ex, int (&dg)[OZ_S]) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int bexp = (int)((bits >> 52) & 0x7FF);
+  unsigned long long F = 0;
+  if (bexp != 0) {  // zero (and subnormals, far below any row maximum) give 0
+    const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+    const int sh = bexp - 1075 + 62 - ex;  // F = |x| 2^(62-ex) < 2^62 (sh <= 9)
+    F = sh >= 0 ? (sh < 10 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
+  }
+  long long v = ((long long)bits < 0) ? -(long long)F : (long long)F;
+#pragma unroll
+  for (int t = OZ_S - 1; t >= 0; --t) {
+    const int d = (int)(signed char)(v & 0xFF);
+    dg[t] = d;
+    v = (v - d) >> 8;
+  }
+}
+
 // One warp per group of 8 operand rows: lane l works on row (l & 7) and on
 // the 16-element K chunks c = (l >> 3) + 4 i, so for every slice the warp
 // stores two contiguous 256-byte runs (the core matrices of two K tiles).
@@ -111,24 +138,10 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
     for (int q = 0; q < 16; ++q) {
       const int k = k0 + q;
       const double x = (live && k < J.K) ? row[(long long)k * J.cs] : 0.0;
-      // integer slicing: |x| 2^-ex as a 56-bit fixed-point F (truncated, as the
-      // FP64 recurrence v *= 128, d = trunc(v), v -= d would give), its 7-bit
-      // groups are the digits, the sign applies to all of them
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-      const int bexp = (int)((bits >> 52) & 0x7FF);
-      unsigned long long F = 0;
-      if (bexp != 0) {  // zero (and subnormals, far below any row maximum) give 0
-        const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-        const int sh = bexp - 1075 + 56 - ex;  // F = |x| 2^(56-ex)
-        F = sh >= 0 ? (sh < 11 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
-      }
-      const bool neg = (long long)bits < 0;
+      int dg[OZ_S];
+      oz_digits(x, ex, dg);
 #pragma unroll
-      for (int t = 0; t < OZ_S; ++t) {
-        int d = (int)((F >> (7 * (OZ_S - 1 - t))) & 0x7F);
-        if (neg) d = -d;
-        w[t][q >> 2] |= ((unsigned)d & 0xFFu) << (8 * (q & 3));
-      }
+      for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= ((unsigned)dg[t] & 0xFFu) << (8 * (q & 3));
     }
     const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
     const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
@@ -229,21 +242,10 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const double x = tile[rl * OZS_PITCH + ci * 16 + q];
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-        const int bexp = (int)((bits >> 52) & 0x7FF);
-        unsigned long long F = 0;
-        if (bexp != 0) {
-          const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-          const int sh = bexp - 1075 + 56 - ex;  // F = |x| 2^(56-ex)
-          F = sh >= 0 ? (sh < 11 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
-        }
-        const bool neg = (long long)bits < 0;
+        int dg[OZ_S];
+        oz_digits(x, ex, dg);
 #pragma unroll
-        for (int t = 0; t < OZ_S; ++t) {
-          int d = (int)((F >> (7 * (OZ_S - 1 - t))) & 0x7F);
-          if (neg) d = -d;
-          w[t][q >> 2] |= ((unsigned)d & 0xFFu) << (8 * (q & 3));
-        }
+        for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= ((unsigned)dg[t] & 0xFFu) << (8 * (q & 3));
       }
       const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
       const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           for (int j = 0; j < 32; ++j) acc[j] = 0.0;
 #pragma unroll
           for (int dd = OZ_H - 1; dd >= 0; --dd) {  // smallest terms first
-            const double sc = ldexp(1.0, -7 * (dd + pass * OZ_H + 2));
+            const double sc = ldexp(1.0, -(8 * (dd + pass * OZ_H) + 12));
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               uint32_t v[16];
