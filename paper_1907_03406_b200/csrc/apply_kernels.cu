@@ -258,12 +258,9 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
   static const int bulk = getenv("SGF_GEMV_BULK") ? atoi(getenv("SGF_GEMV_BULK")) : 1;
   if (mode == 0 && lpr == 64 && bulk) {
     const size_t smem = ((size_t)8 * GB_S * GB_CH + GB_XCAP) * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(gemv_n_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    static FuncAttrs fa;
+    cudaError_t e = ensure_smem(gemv_n_bulk_kernel, smem, fa);
+    if (e != cudaSuccess) return e;
     gemv_n_bulk_kernel<<<ntasks, 256, smem, s>>>(d_tasks);
     return cudaGetLastError();
   }
@@ -491,13 +488,9 @@ static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t
   // ring (8 warps x S slots) also holds the 8 x MP column partials at the end
   const size_t ring = (size_t)8 * std::max(S * (64 * Q + 2), 64 * Q);
   const size_t smem = (2 * (size_t)64 * Q + ring) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(symv_bulk_kernel<Q, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(symv_bulk_kernel<Q, S>, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch(); symv_bulk_kernel<Q, S><<<ntasks, 256, smem, s>>>(d_tasks, v);
   return cudaGetLastError();
 }
@@ -505,12 +498,9 @@ static cudaError_t symv_bulk_q(const SymvTask* d_tasks, int ntasks, cudaStream_t
 template <int Q>
 static cudaError_t symv_q(const SymvTask* d_tasks, int ntasks, cudaStream_t s) {
   const size_t smem = (size_t)10 * 64 * Q * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(symv_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(symv_kernel<Q>, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch(); symv_kernel<Q><<<ntasks, 256, smem, s>>>(d_tasks);
   return cudaGetLastError();
 }

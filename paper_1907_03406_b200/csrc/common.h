@@ -8,10 +8,50 @@
 //   * triangular matrices (L, L^{-1}) are stored as full squares with exact
 //     zeros in the unused triangle, so K-range limits are optimisations only.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace sgf {
+
+// ---- kernel function attributes (per device) ----------------------------------
+// cudaFuncSetAttribute applies to the current device only, so a process with
+// contexts on several GPUs must configure each one.  A FuncAttrs instance
+// (one static per kernel) remembers, per device ordinal, the largest dynamic
+// shared-memory size already set and whether non-portable cluster sizes were
+// enabled.  The entry points select the context's device before launching.
+struct FuncAttrs {
+  std::atomic<int> smem[64];
+  std::atomic<unsigned long long> nonportable;
+  FuncAttrs() : nonportable(0) {
+    for (auto& v : smem) v.store(0, std::memory_order_relaxed);
+  }
+};
+template <class K>
+inline cudaError_t ensure_smem(K kern, size_t bytes, FuncAttrs& fa) {
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return e;
+  std::atomic<int>& cur = fa.smem[d & 63];
+  if ((int)bytes <= cur.load(std::memory_order_acquire)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int seen = cur.load(std::memory_order_relaxed);
+  while (seen < (int)bytes && !cur.compare_exchange_weak(seen, (int)bytes)) {
+  }
+  return cudaSuccess;
+}
+template <class K>
+inline cudaError_t ensure_nonportable_cluster(K kern, FuncAttrs& fa) {
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (d & 63);
+  if (fa.nonportable.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) fa.nonportable.fetch_or(bit);
+  return e;
+}
 
 // ---- batched FP64 GEMM (DMMA) ------------------------------------------------
 // C(i,j) = beta*C(i,j) + alpha * sum_seg sum_{k in seg range} A(i,k) * B(j,k)

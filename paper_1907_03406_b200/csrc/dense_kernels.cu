@@ -151,24 +151,16 @@ cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_stat
                                 double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   const size_t smem = (2 * 64 * 65 + 64) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(diag_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static FuncAttrs fa, fa_rl;
   static const int variant = getenv("SGF_DIAG_CHOL") ? atoi(getenv("SGF_DIAG_CHOL")) : 1;
-  static bool configured_rl = false;
   if (variant == 1) {
-    if (!configured_rl) {
-      cudaError_t e =
-          cudaFuncSetAttribute(diag_chol_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured_rl = true;
-    }
+    cudaError_t e = ensure_smem(diag_chol_rl_kernel, smem, fa_rl);
+    if (e != cudaSuccess) return e;
     count_launch(); diag_chol_rl_kernel<<<ntasks, 256, smem, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
     return cudaGetLastError();
   }
+  cudaError_t e = ensure_smem(diag_chol_kernel, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch(); diag_chol_kernel<<<ntasks, 256, smem, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
   return cudaGetLastError();
 }

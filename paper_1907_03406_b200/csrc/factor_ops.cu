@@ -175,10 +175,9 @@ cudaError_t launch_trsv(const double* L, long long ldl, int m, int nvec, const d
                         long long bes, double* X, long long xvs, long long xes, int trans, cudaStream_t s) {
   if (m <= 0 || nvec <= 0) return cudaSuccess;
   const size_t smem = (size_t)m * sizeof(double);
-  if (smem > (48u << 10)) {
-    cudaError_t e = cudaFuncSetAttribute(trsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(trsv_kernel, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch();
   trsv_kernel<<<nvec, 256, smem, s>>>(L, ldl, m, B, bvs, bes, X, xvs, xes, trans);
   return cudaGetLastError();

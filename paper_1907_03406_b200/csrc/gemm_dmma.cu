@@ -234,12 +234,9 @@ static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg
   constexpr int B_EL = BN * (BK + 4);
   const size_t smem = (size_t)STAGES * (A_EL + B_EL) * sizeof(double);
   auto kern = gemm_f64_kernel<BM, BN, WM, WN, NT, STAGES, BK>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(kern, smem, fa);
+  if (e != cudaSuccess) return e;
   // gridDim.x is limited to 2^31-1; tasks are launched in chunks of 1<<30
   for (int off = 0; off < ntasks; off += (1 << 30)) {
     int cnt = ntasks - off < (1 << 30) ? ntasks - off : (1 << 30);

@@ -169,12 +169,9 @@ cudaError_t launch_l1_e(const L1ETask* d_tasks, int ntasks, int max_m, int max_c
   const size_t smem = (size_t)L1E_TJ * (max_m | 1) * sizeof(double) +
                       (size_t)max_c * (L1_KMAX * (sizeof(double) + sizeof(int)) + sizeof(int));
   if (smem > (size_t)220 << 10) return cudaErrorInvalidValue;  // caller checks l1_e_fits
-  static size_t configured = 48 << 10;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(l1_e_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(l1_e_kernel, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch();
   l1_e_kernel<<<dim3(ntasks, (max_m + L1E_TJ - 1) / L1E_TJ), 256, smem, s>>>(d_tasks, rl_n, rl_k, rl_a, max_m);
   return cudaGetLastError();

@@ -472,12 +472,9 @@ cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_p
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE) + 4 * 32 * 33 * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(oz_gemm_kernel, smem, fa);
+  if (e != cudaSuccess) return e;
   count_launch();
   oz_gemm_kernel<<<ntasks, OZ_THREADS, smem, s>>>(d_tasks, d_segs);
   return cudaGetLastError();

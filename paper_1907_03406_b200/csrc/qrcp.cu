@@ -721,19 +721,10 @@ static size_t qrcp_smem_bytes(int m, int c) {
 
 template <int CS>
 static cudaError_t qr_configure(size_t sb) {
-  static size_t conf = 0;
-  static bool np = false;
-  if (!np) {
-    cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    np = true;
-  }
-  if (sb > conf) {
-    cudaError_t e = cudaFuncSetAttribute(qrcp_smem_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    if (e != cudaSuccess) return e;
-    conf = sb;
-  }
-  return cudaSuccess;
+  static FuncAttrs fa;
+  cudaError_t e = ensure_nonportable_cluster(qrcp_smem_kernel<CS>, fa);
+  if (e != cudaSuccess) return e;
+  return ensure_smem(qrcp_smem_kernel<CS>, sb, fa);
 }
 
 template <int CS>
@@ -783,20 +774,12 @@ static int qr_active_clusters(int cs, size_t sb) {
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = (size_t)max_m * sizeof(double) + (size_t)max_c * sizeof(int);
-  static size_t configured = 48 * 1024;
-  static bool nonportable = false;
-  if (!nonportable) {
-    cudaError_t e = cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  static FuncAttrs fa_cluster, fa_single;
+  {
+    cudaError_t e = ensure_nonportable_cluster(qrcp_cluster_kernel, fa_cluster);
+    if (e == cudaSuccess) e = ensure_smem(qrcp_cluster_kernel, smem, fa_cluster);
+    if (e == cudaSuccess) e = ensure_smem(qrcp_kernel, smem, fa_single);
     if (e != cudaSuccess) return e;
-    nonportable = true;
-  }
-  if (smem > configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
   }
   static int single = getenv("SGF_QR_SINGLE_CTA") ? 1 : 0;
   static int smem_ok = getenv("SGF_QR_SMEM") ? atoi(getenv("SGF_QR_SMEM")) : 1;
@@ -921,12 +904,9 @@ cudaError_t launch_qr_finish(const void* d_tasks, int ntasks, int phase, cudaStr
       qr_larft_global_kernel<<<ntasks, QR_THREADS, 0, s>>>((const QrFinishTask*)d_tasks);
       return cudaGetLastError();
     }
-    static size_t configured = 48 << 10;
-    if (smem > configured) {
-      cudaError_t e = cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = smem;
-    }
+    static FuncAttrs fa;
+    cudaError_t e = ensure_smem(qr_larft_kernel, smem, fa);
+    if (e != cudaSuccess) return e;
     qr_larft_kernel<<<ntasks, QR_THREADS, smem, s>>>((const QrFinishTask*)d_tasks);
   }
   return cudaGetLastError();

@@ -15,6 +15,23 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libsgf.so")
 
 
+@pytest.fixture(autouse=True)
+def _release_failed_test_frames(request):
+    """pytest keeps a failed test's traceback in sys.last_traceback (for
+    post-mortem debugging); its frames hold the test's locals, e.g. a
+    full-size Preconditioner with tens of GB of factors in HBM, which would
+    make every later full-size test fail with out-of-memory.  Drop it after
+    each test."""
+    yield
+    import gc
+
+    for k in ("last_type", "last_value", "last_traceback", "last_exc"):
+        if hasattr(sys, k):
+            setattr(sys, k, None)
+    if request.node.get_closest_marker("gpu") is not None:
+        gc.collect()
+
+
 class Golden:
     """One reference-generated fixture (tests/golden/make_golden.py)."""
 
