@@ -147,12 +147,142 @@ __global__ void __launch_bounds__(256) diag_chol_rl_kernel(const DiagTask* __res
   }
 }
 
+// Register-resident form of the right-looking sweep above (the default).
+// Threads 0-127 hold the factor by columns: column x = t & 63, rows
+// [32h, 32h + 32), h = t >> 6.  Threads 128-255 hold the inverse by rows:
+// row i = t & 63, columns [32h, 32h + 32).  Step j is one uniform rank-1
+// update of both with no per-element branches:
+//   S[i][x] -= S[i][j] (S[x][j] / S[j][j])  for x > j   (trailing matrix)
+//   D[i][x] -= (S[i][j] / S[j][j]) D[j][x]  for i > j   (inverse rows)
+// with S[.][j] and D[j][.] the raw (unscaled) pivot column and row, which the
+// owners publish to shared memory at the end of step j - 1 (double-buffered
+// by the parity of j: one barrier per column).  Finished columns / rows
+// (p <= j) skip the step.  The S update runs over whole columns: rows above
+// the pivot only touch the unused upper triangle of the active columns, so
+// the published column's rows < j (upper-triangle values) never reach the
+// lower triangle or the inverse; the upper triangle of D stays exactly zero
+// (D[j][x] = 0 for x > j), so its published rows need no masking either.
+// The coefficients need only S[.][j] / S[j][j] (one division per thread and
+// column); columns of L and rows of L^{-1} stay raw once final and are
+// divided by sqrt(S[j][j]) when written out (no square root on the column
+// chain).  Per column a thread issues 16 paired shared loads and 32 FMAs,
+// the publishers (the owners of column and row j + 1) 16 paired stores.
+// Same breakdown rule and outputs as the kernels above (the rounding
+// differs at the last bits).
+__global__ void __launch_bounds__(256, 2) diag_chol_reg_kernel(const DiagTask* __restrict__ tasks,
+                                                               int* __restrict__ status,
+                                                               double* __restrict__ pivval,
+                                                               double* const* __restrict__ xdiag,
+                                                               const int* __restrict__ ldx) {
+  __shared__ __align__(16) double colraw[2][64];  // S[.][j], rows < j zero
+  __shared__ __align__(16) double rowraw[2][64];  // D[j][.], columns > j zero
+  __shared__ double piv_s[64];                    // raw pivots S[j][j]
+  __shared__ double sD[64][65];                   // output staging (coalesced stores)
+  const DiagTask T = tasks[blockIdx.x];
+  const int nb = T.nb, tid = threadIdx.x;
+  const bool isD = tid >= 128;
+  const int p = tid & 63, h = (tid >> 6) & 1, base = 32 * h;  // column (S) or row (D) p
+  double* W = T.W + (long long)T.k0 * T.ld + T.k0;
+  double v[32];
+  if (!isD) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int i = base + q;
+      v[q] = (i < nb && p <= i && p < nb) ? W[(long long)i * T.ld + p] : 0.0;
+    }
+    if (p == 0) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) colraw[0][base + q] = v[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = (base + q == p) ? 1.0 : 0.0;
+    if (p == 0) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) rowraw[0][base + q] = v[q];
+    }
+  }
+  const double floor_ = *T.floor;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const int b = j & 1;
+    const double piv = colraw[b][j];
+    if (!(piv > floor_) || !isfinite(piv)) {
+      if (tid == 0 && status[T.node] == 0) {
+        status[T.node] = T.k0 + j + 1;
+        pivval[T.node] = piv;
+      }
+      return;  // uniform: every thread saw the same pivot
+    }
+    const double2* c2 = reinterpret_cast<const double2*>(colraw[b] + base);
+    if (p <= j) {
+      // finished column of L / row of L^{-1}: nothing to update
+    } else if (!isD) {
+      const double f = colraw[b][p] / piv;  // S[x][j] / S[j][j]
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 l = c2[q];
+        v[2 * q] = fma(-l.x, f, v[2 * q]);
+        v[2 * q + 1] = fma(-l.y, f, v[2 * q + 1]);
+      }
+    } else {
+      const double l = colraw[b][p] / piv;
+      const double2* r2v = reinterpret_cast<const double2*>(rowraw[b] + base);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 dj = r2v[q];
+        v[2 * q] = fma(-l, dj.x, v[2 * q]);
+        v[2 * q + 1] = fma(-l, dj.y, v[2 * q + 1]);
+      }
+    }
+    if (tid == 0) piv_s[j] = piv;
+    // publish column j + 1 of S (rows >= j + 1) and row j + 1 of D (columns <= j + 1)
+    const int jn = j + 1;
+    if (p == jn) {
+      double2* dst = reinterpret_cast<double2*>((isD ? rowraw[b ^ 1] : colraw[b ^ 1]) + base);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) dst[q] = make_double2(v[2 * q], v[2 * q + 1]);
+    }
+    __syncthreads();
+  }
+  // scaled outputs: L[i][x] = raw * rinv_x (i > x), sqrt pivot on the
+  // diagonal; L^{-1}[i][x] = raw * rinv_i (x <= i)
+  if (!isD) {
+    const double dp = p < nb ? sqrt(piv_s[p]) : 1.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int i = base + q;
+      if (i < nb && p < nb) W[(long long)i * T.ld + p] = i > p ? v[q] / dp : (i == p ? dp : 0.0);
+    }
+  } else {
+    const double dp = p < nb ? sqrt(piv_s[p]) : 1.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int x = base + q;
+      sD[p][x] = (p < nb && x < nb && x <= p) ? v[q] / dp : 0.0;
+    }
+  }
+  __syncthreads();
+  double* X = xdiag ? xdiag[blockIdx.x] : nullptr;
+  const int lx = ldx ? ldx[blockIdx.x] : 0;
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int r = idx >> 6, c = idx & 63;
+    const double dv = sD[r][c];
+    T.Dinv[idx] = dv;
+    if (X && r < nb && c < nb) X[(long long)(T.k0 + r) * lx + T.k0 + c] = dv;
+  }
+}
+
 cudaError_t launch_diag_chol_ex(const DiagTask* d_tasks, int ntasks, int* d_status, double* d_pivval,
                                 double* const* d_xdiag, const int* d_ldx, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   const size_t smem = (2 * 64 * 65 + 64) * sizeof(double);
   static FuncAttrs fa, fa_rl;
-  static const int variant = getenv("SGF_DIAG_CHOL") ? atoi(getenv("SGF_DIAG_CHOL")) : 1;
+  static const int variant = getenv("SGF_DIAG_CHOL") ? atoi(getenv("SGF_DIAG_CHOL")) : 2;
+  if (variant == 2) {
+    count_launch(); diag_chol_reg_kernel<<<ntasks, 256, 0, s>>>(d_tasks, d_status, d_pivval, d_xdiag, d_ldx);
+    return cudaGetLastError();
+  }
   if (variant == 1) {
     cudaError_t e = ensure_smem(diag_chol_rl_kernel, smem, fa_rl);
     if (e != cudaSuccess) return e;

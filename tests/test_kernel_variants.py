@@ -28,6 +28,7 @@ VARIANTS = {
     "l1_dense": {"SGF_NO_L1SPARSE": "1"},              # level-1 E and Schur as dense DMMA GEMMs
     "l1_e_eager": {"SGF_L1E_EAGER": "1"},              # level-1 couplings E formed during the factorization
     "diag_left_looking": {"SGF_DIAG_CHOL": "0"},       # left-looking 64x64 diagonal Cholesky
+    "diag_shared_rl": {"SGF_DIAG_CHOL": "1"},          # right-looking diagonal Cholesky in shared memory
     "split_warp": {"SGF_OZ_SPLIT_WARP": "1"},          # warp-per-group operand split
     "l2_schur_dmma": {"SGF_OZAKI_SCHUR_MIN_M": "0"},   # level-2 Schur on DMMA
     "no_emulation": {"SGF_OZAKI_MIN_M": "0"},          # every product on DMMA
