@@ -132,6 +132,7 @@ struct OzSplitJob {
   int R, K, Rp, Kp;
   int8_t* out;
   int* exps;
+  uint8_t* nz;  // optional: nz[(r / 128) * (Kp / 32) + k / 32] = 1 where the 128 x 32 tile has a nonzero
 };
 // one product term C += alpha * A B^T of split operands (rows of A = rows of C)
 struct OzSeg {
@@ -142,6 +143,8 @@ struct OzSeg {
   int a_rp, b_rp;
   int nk;  // K tiles of 32
   double alpha;
+  const uint8_t* a_nz;  // optional nonzero flags of A's 128 x 32 tiles (row tile-major, nk per row tile):
+                        // all-zero K tiles are skipped (their products are exact zeros)
 };
 // one 128 x 128 output tile: C = beta*C + sum of its segments (in order)
 struct OzTask {
@@ -286,6 +289,8 @@ cudaError_t launch_symv_fused(const SymvTask* d_tasks, int ntasks, int max_m, do
 // sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
 cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,
                             double* out, int mode, cudaStream_t s);
+cudaError_t launch_zero_tiles(const double* p, long long rs, long long cs, int rows, int cols, int tr, int tk,
+                              unsigned long long* counters, cudaStream_t s);
 cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, const int* d_ld, int n,
                             double* d_out, cudaStream_t s);
 }  // namespace sgf

@@ -518,4 +518,30 @@ cudaError_t launch_max_diag(const double* const* d_ptrs, const int* d_sizes, con
   return cudaGetLastError();
 }
 
+// Diagnostics (SGF_ZERO_STATS): number of all-zero tr x tk tiles of a strided
+// view; one CTA per tile, counters[0] += zero tiles, counters[1] += tiles.
+__global__ void zero_tiles_kernel(const double* __restrict__ p, long long rs, long long cs, int rows, int cols,
+                                  int tr, int tk, unsigned long long* counters) {
+  const int ntc = (cols + tk - 1) / tk;
+  const int r0 = (blockIdx.x / ntc) * tr, c0 = (blockIdx.x % ntc) * tk;
+  int nz = 0;
+  for (int e = threadIdx.x; e < tr * tk; e += blockDim.x) {
+    const int r = r0 + e / tk, c = c0 + e % tk;
+    if (r < rows && c < cols && p[(long long)r * rs + (long long)c * cs] != 0.0) nz = 1;
+  }
+  nz = __syncthreads_or(nz);
+  if (threadIdx.x == 0) {
+    if (!nz) atomicAdd(&counters[0], 1ull);
+    atomicAdd(&counters[1], 1ull);
+  }
+}
+
+cudaError_t launch_zero_tiles(const double* p, long long rs, long long cs, int rows, int cols, int tr, int tk,
+                              unsigned long long* counters, cudaStream_t s) {
+  const long long nt = (long long)((rows + tr - 1) / tr) * ((cols + tk - 1) / tk);
+  if (nt <= 0) return cudaSuccess;
+  zero_tiles_kernel<<<(unsigned)nt, 128, 0, s>>>(p, rs, cs, rows, cols, tr, tk, counters);
+  return cudaGetLastError();
+}
+
 }  // namespace sgf

@@ -644,7 +644,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
                                   rl_base[qi] + e.off[q]});
           if (q == 0) l1e.push_back(L1ETask{e.X, (long long)e.ld, e.E, (long long)e.ld, e.m, e.c, rl_base[qi]});
         } else if (use_oz) {
-          OzOperand aop = oz.split(S.scratch, v.p, v.rs, v.cs, v.rows, e.m);
+          OzOperand aop = oz.split(S.scratch, v.p, v.rs, v.cs, v.rows, e.m, true);  // block-sparse A_NB
           oz.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 0.0, {{{aop, xop}, 1.0}}, false, true);
         } else {
           ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
@@ -662,6 +662,23 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       fl_e += f - (long long)e.m * e.m * e.m / 3;
       fl_s += fs;
     }
+  }
+  static const bool zero_stats = getenv("SGF_ZERO_STATS") != nullptr;
+  if (zero_stats) {  // diagnostics: all-zero 128 x 32 tiles of the A_NB operands of E
+    unsigned long long* cnt = S.scratch.alloc_t<unsigned long long>(2);
+    SGF_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), st));
+    for (size_t qi = 0; qi < info.size(); ++qi) {
+      if (!own[qi]) continue;
+      for (size_t q = 0; q < info[qi].nb.size(); ++q) {
+        View v = view_of(M, info[qi].nb[q], info[qi].x);
+        SGF_CUDA(launch_zero_tiles(v.p, v.rs, v.cs, v.rows, v.cols, 128, 32, cnt, st));
+      }
+    }
+    unsigned long long h[2];
+    SGF_CUDA(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[sgf] L%d A_NB 128x32 tiles: %llu of %llu all zero (%.1f%%)\n", level, h[0], h[1],
+            100.0 * h[0] / std::max(1ull, h[1]));
   }
   if (Phase::mode())
     fprintf(stderr, "[sgf] L%d eliminate: %zu nodes, max m %d, flops chol %.3e E %.3e schur %.3e (%s)\n", level,

@@ -298,6 +298,8 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
+  for (auto& z : nz_clear) SGF_CUDA(cudaMemsetAsync(z.first, 0, z.second, st));
+  nz_clear.clear();
   // row-contiguous operands (coalesced CTA kernel) and the others, one launch each
   std::vector<OzSplitJob> part[2];
   for (auto& j : jobs) part[(j.cs == 1 || j.rs == 1) ? 0 : 1].push_back(j);  // the CTA kernel reads both
@@ -457,7 +459,7 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
   for (int i = 0; i < nb; ++i) {
     const CholJob& j = big[i];
     const long long ld = j.ld;
-    a21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i]);
+    a21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i], true);  // block-sparse A21
     x11[i] = oz.split(scratch, j.X, ld, 1, m1[i], m1[i]);
   }
   oz.launch_splits(scratch, st);
