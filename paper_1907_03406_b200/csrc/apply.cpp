@@ -121,7 +121,7 @@ static void add_gemv_tri_pairs(std::vector<GemvTask>& v, const double* A, long l
 }
 
 static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y, int rows,
-                       int cols, int tri, int rows_per = GN_ROWS) {
+                       int cols, int tri, int rows_per = GN_ROWS, const int* kfirst = nullptr) {
   for (int r0 = 0; r0 < rows; r0 += rows_per) {
     GemvTask t;
     t.A = A;
@@ -133,13 +133,14 @@ static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda,
     t.c0 = 0;
     t.c1 = cols;
     t.tri = tri;
+    t.kfirst = kfirst;
     v.push_back(t);
   }
 }
 
 // partials part[rb*cols + k] = sum_{i in rb} A[i,k] x[i]; returns #row blocks
 static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* part,
-                      int rows, int cols, int tri, int rows_per = GT_ROWS) {
+                      int rows, int cols, int tri, int rows_per = GT_ROWS, const int* kfirst = nullptr) {
   int nrb = 0;
   for (int r0 = 0; r0 < rows; r0 += rows_per, ++nrb)
     for (int c0 = 0; c0 < cols; c0 += GT_COLS) {
@@ -153,6 +154,7 @@ static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, 
       t.c0 = c0;
       t.c1 = std::min(cols, c0 + GT_COLS);
       t.tri = tri;
+      t.kfirst = kfirst;
       v.push_back(t);
     }
   return nrb;
@@ -233,9 +235,9 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       else add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
-        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows, f.ekfirst);
         for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
-        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0, g.gt_rows) : 0;
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0, g.gt_rows, f.ekfirst) : 0;
         r1.push_back(RedSeg{g.part + op, g.xb + om, g.acc + om, f.m, nrb, f.m, -1.0});
         // second stage reuses the partial buffer after red1 consumed it
         int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1, g.gt_rows);

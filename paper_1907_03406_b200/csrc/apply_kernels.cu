@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restri
       const int ke = T.tri ? min(T.c1, i + 1) : T.c1;  // c0 == 0 for every task
       const int k2 = ke >> 1;
       const double* x = T.x;
-      int k = sub;
+      // leading zeros of the row (couplings E): start at the first nonzero
+      // 16-byte word
+      int k = (T.kfirst ? min(T.kfirst[i], ke) >> 1 : 0) + sub;
       for (; k + 3 * LPR < k2; k += 4 * LPR) {
         const double2 a0 = __ldcs(a + k), a1 = __ldcs(a + k + LPR), a2 = __ldcs(a + k + 2 * LPR),
                       a3 = __ldcs(a + k + 3 * LPR);
@@ -131,6 +133,23 @@ __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restri
 __global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
   const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
+  if (T.kfirst) {
+    // rows with leading zeros (couplings E): columns left of every row's
+    // first nonzero have an exact zero partial, written without reading A
+    __shared__ int kmin;
+    if (threadIdx.x == 0) kmin = T.c1;
+    __syncthreads();
+    int km = T.c1;
+    for (int i = T.r0 + threadIdx.x; i < T.r1; i += blockDim.x) km = min(km, T.kfirst[i]);
+    if (km < T.c1) atomicMin(&kmin, km);
+    __syncthreads();
+    if (k >= T.c1) return;
+    if (k + 1 < kmin) {
+      T.y[k] = 0.0;
+      if (k + 1 < T.c1) T.y[k + 1] = 0.0;
+      return;
+    }
+  }
   if (k >= T.c1) return;
   int i0 = T.r0;
   // lower triangular: column k starts at row k; A[k][k+1] is a stored zero
@@ -168,16 +187,22 @@ constexpr int GB_CH = 256, GB_S = 4, GB_XCAP = 4096;
 struct GbCursor {
   int n = 0, sub = 0, off = 0;  // row (or pair) counter of the warp, row of the pair, offset in the row
 };
-// row index and its length for the cursor; false when the warp has no more rows
-__device__ __forceinline__ bool gb_row(const GemvTask& T, int warp, const GbCursor& c, int& row, int& len) {
+// row index, its first column (even: 16-byte aligned; the leading zeros of a
+// coupling row are skipped) and its length counted from there, for the
+// cursor; false when the warp has no more rows
+__device__ __forceinline__ bool gb_row(const GemvTask& T, int warp, const GbCursor& c, int& row, int& start,
+                                       int& len) {
   const int q = T.r0 + warp + 8 * c.n;
   if (q >= T.r1) return false;
+  start = 0;
   if (T.tri == 2) {
     row = c.sub ? T.c1 - 1 - q : q;
     len = row + 1;
   } else {
     row = q;
     len = T.tri ? min(T.c1, q + 1) : T.c1;
+    if (T.kfirst) start = min(T.kfirst[row], len) & ~1;
+    len -= start;
   }
   return true;
 }
@@ -202,12 +227,16 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
   uint64_t* wbar = bar + warp * GB_S;
   GbCursor pc;  // producer cursor (lane 0)
   auto issue = [&](int slot) -> bool {
-    int row, len;
-    if (!gb_row(T, warp, pc, row, len)) return false;
-    const int cl = min(GB_CH, len - pc.off);
-    const uint32_t bytes = (uint32_t)((cl + 1) & ~1) * 8u;  // even count: 16-byte multiple (ld even)
-    ptx::mbar_expect_tx(&wbar[slot], bytes);
-    ptx::bulk_g2s(wring + slot * GB_CH, T.A + (long long)row * T.lda + pc.off, bytes, &wbar[slot]);
+    int row, start, len;
+    if (!gb_row(T, warp, pc, row, start, len)) return false;
+    if (len > 0) {
+      const int cl = min(GB_CH, len - pc.off);
+      const uint32_t bytes = (uint32_t)((cl + 1) & ~1) * 8u;  // even count: 16-byte multiple (ld even)
+      ptx::mbar_expect_tx(&wbar[slot], bytes);
+      ptx::bulk_g2s(wring + slot * GB_CH, T.A + (long long)row * T.lda + start + pc.off, bytes, &wbar[slot]);
+    } else {
+      ptx::mbar_arrive(&wbar[slot]);  // an all-zero row: an empty chunk
+    }
     gb_advance(T, warp, pc, len);
     return true;
   };
@@ -224,19 +253,20 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
   GbCursor cc;  // consumer cursor
   double acc = 0.0;
   for (int it = 0;; ++it) {
-    int row, len;
-    if (!gb_row(T, warp, cc, row, len)) break;
+    int row, start, len;
+    if (!gb_row(T, warp, cc, row, start, len)) break;
     const int slot = it % GB_S;
     const int off = cc.off, cl = min(GB_CH, len - off);
     ptx::mbar_wait(&wbar[slot], (it / GB_S) & 1);
     const double* ch = wring + slot * GB_CH;
+    const double* xo = xv + start + off;
 #pragma unroll
     for (int t = 0; t < GB_CH / 64; ++t) {
       const int j = 64 * t + 2 * lane;
       if (j < cl) {
         const double2 g = *reinterpret_cast<const double2*>(ch + j);
-        acc = fma(g.x, xv[off + j], acc);
-        if (j + 1 < cl) acc = fma(g.y, xv[off + j + 1], acc);
+        acc = fma(g.x, xo[j], acc);
+        if (j + 1 < cl) acc = fma(g.y, xo[j + 1], acc);
       }
     }
     __syncwarp();

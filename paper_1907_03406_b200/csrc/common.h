@@ -133,6 +133,7 @@ struct OzSplitJob {
   int8_t* out;
   int* exps;
   uint8_t* nz;  // optional: nz[(r / 128) * (Kp / 32) + k / 32] = 1 where the 128 x 32 tile has a nonzero
+  int* kfirst;  // optional: per row r < R, the first column k with x(r, k) != 0 (K when none)
 };
 // one product term C += alpha * A B^T of split operands (rows of A = rows of C)
 struct OzSeg {
@@ -172,6 +173,7 @@ struct GemvTask {
   int c0, c1;
   int tri;             // 1: lower-triangular A (row i uses k <= i); 2 (mode N): rows in pairs
                        //    (p, c1-1-p) for pair indices p in [r0, r1)
+  const int* kfirst = nullptr;  // optional (tri == 0): row i is zero in columns < kfirst[i] (skipped)
 };
 
 struct TriTask { double* p; int m; int ld; };

@@ -71,6 +71,7 @@ struct State {
   int oz_min_m = 1024;         // eliminations with a node this large use the INT8-emulated FP64 products (0: off)
   int oz_schur_min_m = 640;    // nodes this large (below oz_min_m) take only the Schur updates emulated
   int chol_oz_min_m = 1024;    // Cholesky/inverse of nodes this large split recursively onto those products (0: off)
+  bool ekfirst = true;         // record the couplings' leading zeros for the apply (SGF_NO_EKFIRST=1: off)
   int qr_full_steps = 0;       // 1: QR past the rank as the reference does (its Q_2 is rounding-determined
                                //    there, so apply_half_inverse's dropped coordinates never match it exactly)
   std::vector<std::string> warnings;  // reference warnings.warn messages (stats "warnings", raised by Python)
@@ -717,15 +718,55 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     oz.launch_splits(S.scratch, st);
     oz.launch(S.scratch, st);
   }
-  if (oz_schur) {
-    // the couplings as Schur operands, one split per neighbour block
+  if (zero_stats && tot_e) {  // diagnostics: all-zero 128 x 32 tiles of the couplings E
+    unsigned long long* cnt = S.scratch.alloc_t<unsigned long long>(2);
+    SGF_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), st));
     for (size_t qi = 0; qi < info.size(); ++qi) {
       if (!own[qi]) continue;
       const EI& e = info[qi];
       for (size_t q = 0; q < e.nb.size(); ++q)
-        eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m));
+        SGF_CUDA(launch_zero_tiles(e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m, 128, 32, cnt, st));
+    }
+    unsigned long long h[2];
+    SGF_CUDA(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[sgf] L%d E 128x32 tiles: %llu of %llu all zero (%.1f%%)%s\n", level, h[0], h[1],
+            100.0 * h[0] / std::max(1ull, h[1]), sparse1 ? " (level-1 E formed later: not yet written)" : "");
+  }
+  // per row of E, its first nonzero column (apply: the leading zeros of the
+  // couplings are skipped; written by the operand split below)
+  std::vector<int*> ekf(info.size(), nullptr);
+  if (oz_schur) {
+    // the couplings as Schur operands, one split per neighbour block
+    long long tot_c = 0;
+    for (size_t qi = 0; qi < info.size(); ++qi)
+      if (own[qi]) tot_c += info[qi].c;
+    int* kf_all = (S.ekfirst && tot_c) ? P->store.alloc_t<int>(tot_c) : nullptr;
+    long long okf = 0;
+    for (size_t qi = 0; qi < info.size(); ++qi) {
+      if (!own[qi]) continue;
+      const EI& e = info[qi];
+      if (kf_all) ekf[qi] = kf_all + okf;
+      okf += e.c;
+      for (size_t q = 0; q < e.nb.size(); ++q)
+        eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m, false,
+                                   kf_all ? ekf[qi] + e.off[q] : nullptr));
     }
     oz.launch_splits(S.scratch, st);
+    if (zero_stats && kf_all) {  // diagnostics: leading zeros of the couplings' rows
+      std::vector<int> h(tot_c);
+      SGF_CUDA(cudaMemcpyAsync(h.data(), kf_all, tot_c * sizeof(int), cudaMemcpyDeviceToHost, st));
+      SGF_CUDA(cudaStreamSynchronize(st));
+      double lead = 0, tot = 0;
+      long long o = 0;
+      for (size_t qi = 0; qi < info.size(); ++qi) {
+        if (!own[qi]) continue;
+        for (int r = 0; r < info[qi].c; ++r) lead += std::min(h[o + r], info[qi].m);
+        tot += (double)info[qi].c * info[qi].m;
+        o += info[qi].c;
+      }
+      fprintf(stderr, "[sgf] L%d E rows: %.1f%% of the entries are leading zeros\n", level, 100.0 * lead / tot);
+    }
   }
 
   // Schur targets in the reference's insertion order (ascending interior id,
@@ -865,6 +906,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       f.L = e.W;
       f.inv = e.X;
       f.E = e.E;
+      f.ekfirst = ekf[q];
       if (Gall) f.G = Gall + (e.X - Xall);
     }
     // replay the reference sequence for the table and its byte accounting:
@@ -1659,6 +1701,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   const bool compression = a.compression && a.mode != SGF_MODE_EXACT;
   S.l1_sym = !getenv("SGF_NO_L1SYM") && a.nnz <= (int64_t)INT32_MAX;
   if (getenv("SGF_OZAKI_MIN_M")) S.oz_min_m = atoi(getenv("SGF_OZAKI_MIN_M"));
+  if (getenv("SGF_NO_EKFIRST")) S.ekfirst = false;
   if (getenv("SGF_QR_FULL_STEPS")) S.qr_full_steps = atoi(getenv("SGF_QR_FULL_STEPS")) ? 1 : 0;
   if (getenv("SGF_OZAKI_CHOL_MIN_M")) S.chol_oz_min_m = atoi(getenv("SGF_OZAKI_CHOL_MIN_M"));
   if (getenv("SGF_OZAKI_SCHUR_MIN_M")) S.oz_schur_min_m = atoi(getenv("SGF_OZAKI_SCHUR_MIN_M"));

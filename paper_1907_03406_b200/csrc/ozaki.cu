@@ -119,16 +119,24 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
   const bool live = r < J.R;
   const double* row = J.x + (long long)r * J.rs;
   double mx = 0.0;
+  int kf = J.K;  // first nonzero column of the row seen by this lane
   if (live)
     for (int k0 = c0 * 16; k0 < J.K; k0 += 64)
 #pragma unroll
       for (int q = 0; q < 16; ++q)
-        if (k0 + q < J.K) mx = fmax(mx, fabs(row[(long long)(k0 + q) * J.cs]));
+        if (k0 + q < J.K) {
+          const double x = row[(long long)(k0 + q) * J.cs];
+          mx = fmax(mx, fabs(x));
+          if (x != 0.0) kf = min(kf, k0 + q);
+        }
   mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
   mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, 8));
+  kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, 16));
   int ex = 0;
   if (mx > 0.0) frexp(mx, &ex);  // |x| 2^-ex < 1
   if (lane < 8) J.exps[r] = live ? ex : 0;
+  if (lane < 8 && live && J.kfirst) J.kfirst[r] = kf;
   const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
   for (int k0 = c0 * 16; k0 < J.Kp; k0 += 64) {
     unsigned w[OZ_S][4];
@@ -180,38 +188,65 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
   // trans: the 8 rows of a group are contiguous for every k (rs == 1): thread
   // t reads row t & 7 at k = t >> 3 (+32 i), 64-byte runs per k
   const bool trans = J.cs != 1;
-  if (!trans) {  // pass 1: row maxima, warp w = row g0 + w
+  if (!trans) {  // pass 1: row maxima (and first nonzero), warp w = row g0 + w
     const int r = g0 + warp;
     double mx = 0.0;
+    int kf = J.K;
     if (r < J.R) {
       const double* row = J.x + (long long)r * J.rs;
-      for (int k = lane; k < J.K; k += 32) mx = fmax(mx, fabs(__ldg(row + k)));
+      for (int k = lane; k < J.K; k += 32) {
+        const double x = __ldg(row + k);
+        mx = fmax(mx, fabs(x));
+        if (x != 0.0) kf = min(kf, k);
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, o));
+    }
     if (lane == 0) {
       int e = 0;
       if (mx > 0.0) frexp(mx, &e);  // |x| 2^-ex < 1
       sex[warp] = e;
       if (r < J.R) J.exps[r] = e;
+      if (r < J.R && J.kfirst) J.kfirst[r] = kf;
     }
   } else {
     const int r = g0 + (threadIdx.x & 7);
     double mx = 0.0;
+    int kf = J.K;
     if (r < J.R)
-      for (int k = threadIdx.x >> 3; k < J.K; k += 32) mx = fmax(mx, fabs(__ldg(J.x + r + (long long)k * J.cs)));
+      for (int k = threadIdx.x >> 3; k < J.K; k += 32) {
+        const double x = __ldg(J.x + r + (long long)k * J.cs);
+        mx = fmax(mx, fabs(x));
+        if (x != 0.0) kf = min(kf, k);
+      }
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, 8));
+    kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, 16));
     __shared__ double wm[8][8];
-    if (lane < 8) wm[warp][lane] = mx;
+    __shared__ int wk[8][8];
+    if (lane < 8) {
+      wm[warp][lane] = mx;
+      wk[warp][lane] = kf;
+    }
     __syncthreads();
     if (threadIdx.x < 8) {
       double m = 0.0;
-      for (int w = 0; w < 8; ++w) m = fmax(m, wm[w][threadIdx.x]);
+      int kmin = J.K;
+      for (int w = 0; w < 8; ++w) {
+        m = fmax(m, wm[w][threadIdx.x]);
+        kmin = min(kmin, wk[w][threadIdx.x]);
+      }
       int e = 0;
       if (m > 0.0) frexp(m, &e);
       sex[threadIdx.x] = e;
-      if (g0 + (int)threadIdx.x < J.R) J.exps[g0 + threadIdx.x] = e;
+      if (g0 + (int)threadIdx.x < J.R) {
+        J.exps[g0 + threadIdx.x] = e;
+        if (J.kfirst) J.kfirst[g0 + threadIdx.x] = kmin;
+      }
     }
   }
   __syncthreads();

@@ -21,6 +21,8 @@ struct Factor {
   double* L = nullptr;        // m x m lower (row-major)
   double* inv = nullptr;      // m x m: L^{-1} (elim/dense) or Q^T L^{-1} (compression)
   double* E = nullptr;        // c x m couplings E_N = A_NB L^{-T}, stacked
+  int* ekfirst = nullptr;     // per row of E: first nonzero column (leading zeros: E = A_NB L^{-T} with
+                              // L^{-T} upper triangular keeps the leading zero columns of A_NB's rows)
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator
