@@ -36,6 +36,7 @@ struct Group {
   long long ntgt = 0;
   GemvTask* bwd1 = nullptr;
   int nb1 = 0;
+  int b1_mode = 1;  // 2: every task carries the rows' leading-zero offsets (gemv_t_lead_kernel)
   RedSeg* red1 = nullptr;
   int nred1 = 0, maxn1 = 0;
   GemvTask* bwd2 = nullptr;
@@ -299,6 +300,11 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.nf2 = (int)f2.size();
     g.bwd1 = plan->mem.upload(b1);
     g.nb1 = (int)b1.size();
+    {
+      bool lead = !b1.empty();
+      for (const auto& t : b1) lead = lead && t.kfirst && t.r1 - t.r0 <= GT_ROWS;
+      g.b1_mode = lead ? 2 : 1;
+    }
     g.bwd2 = plan->mem.upload(b2);
     g.nb2 = (int)b2.size();
     // the group's final reduction scatters straight into the full vector
@@ -403,12 +409,12 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
   SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) {
     SGF_CUDA(launch_gather(y, g.nidx, g.xn, g.nc, st));
-    gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
+    gemv(g.bwd1, g.nb1, g.b1_mode, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
     gemv(g.bwd2, g.nb2, 1, g.bytes_b2, st);
     SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st, y));  // + scatter into y
   } else {
-    gemv(g.bwd1, g.nb1, 1, g.bytes_b1, st);
+    gemv(g.bwd1, g.nb1, g.b1_mode, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st, y));  // + scatter into y
   }
 }

@@ -126,30 +126,69 @@ __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restri
   }
 }
 
+constexpr int GT_MAXROWS = 256;  // rows of a transposed task with leading-zero rows (apply.cpp GT_ROWS)
+
 // ---------------------------------------------------------------------------
 // part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T): each thread owns two
 // adjacent columns (one 16-byte load per row), 512 columns per CTA.
 // ---------------------------------------------------------------------------
+// Rows with leading zeros (couplings E, task.kfirst): row i holds zeros left
+// of kfirst[i]; the task's first nonzero columns are staged in shared memory
+// and each row's entries are loaded only where a thread's column pair can
+// reach them (columns left of every row's first nonzero get an exact zero
+// partial without reading A).  Same sums as the dense form: the skipped
+// entries are exact zeros.
+__global__ void __launch_bounds__(256, 6) gemv_t_lead_kernel(const GemvTask* __restrict__ tasks) {
+  const GemvTask T = tasks[blockIdx.x];
+  __shared__ int skf[GT_MAXROWS];
+  __shared__ int kmin;
+  const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
+  const int nr = T.r1 - T.r0;
+  if (threadIdx.x == 0) kmin = T.c1;
+  __syncthreads();
+  int km = T.c1;
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    const int kf = T.kfirst[T.r0 + i];
+    skf[i] = kf;
+    km = min(km, kf);
+  }
+  if (km < T.c1) atomicMin(&kmin, km);
+  __syncthreads();
+  if (k >= T.c1) return;
+  if (k + 1 < kmin) {
+    T.y[k] = 0.0;
+    if (k + 1 < T.c1) T.y[k + 1] = 0.0;
+    return;
+  }
+  const long long ld = T.lda;
+  const double2* a = reinterpret_cast<const double2*>(T.A + k + (long long)T.r0 * ld);
+  const long long ld2 = ld >> 1;
+  const double2 z = make_double2(0.0, 0.0);
+  double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+  int i = 0;
+  for (; i + 3 < nr; i += 4, a += 4 * ld2) {
+    const double2 a0 = k + 1 >= skf[i] ? __ldcs(a) : z, a1 = k + 1 >= skf[i + 1] ? __ldcs(a + ld2) : z,
+                  a2 = k + 1 >= skf[i + 2] ? __ldcs(a + 2 * ld2) : z,
+                  a3 = k + 1 >= skf[i + 3] ? __ldcs(a + 3 * ld2) : z;
+    const double* xr = T.x + T.r0 + i;
+    const double x0 = xr[0], x1 = xr[1], x2 = xr[2], x3 = xr[3];
+    s0 = fma(a0.x, x0, fma(a1.x, x1, s0));
+    t0 = fma(a0.y, x0, fma(a1.y, x1, t0));
+    s1 = fma(a2.x, x2, fma(a3.x, x3, s1));
+    t1 = fma(a2.y, x2, fma(a3.y, x3, t1));
+  }
+  for (; i < nr; ++i, a += ld2) {
+    const double2 a0 = k + 1 >= skf[i] ? __ldcs(a) : z;
+    s0 = fma(a0.x, T.x[T.r0 + i], s0);
+    t0 = fma(a0.y, T.x[T.r0 + i], t0);
+  }
+  T.y[k] = s0 + s1;
+  if (k + 1 < T.c1) T.y[k + 1] = t0 + t1;
+}
+
 __global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
   const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
-  if (T.kfirst) {
-    // rows with leading zeros (couplings E): columns left of every row's
-    // first nonzero have an exact zero partial, written without reading A
-    __shared__ int kmin;
-    if (threadIdx.x == 0) kmin = T.c1;
-    __syncthreads();
-    int km = T.c1;
-    for (int i = T.r0 + threadIdx.x; i < T.r1; i += blockDim.x) km = min(km, T.kfirst[i]);
-    if (km < T.c1) atomicMin(&kmin, km);
-    __syncthreads();
-    if (k >= T.c1) return;
-    if (k + 1 < kmin) {
-      T.y[k] = 0.0;
-      if (k + 1 < T.c1) T.y[k + 1] = 0.0;
-      return;
-    }
-  }
   if (k >= T.c1) return;
   int i0 = T.r0;
   // lower triangular: column k starts at row k; A[k][k+1] is a stored zero
@@ -299,6 +338,8 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
     if (lpr == 8) gemv_n_kernel<8><<<ntasks, 256, 0, s>>>(d_tasks);
     else if (lpr == 16) gemv_n_kernel<16><<<ntasks, 256, 0, s>>>(d_tasks);
     else gemv_n_kernel<32><<<ntasks, 256, 0, s>>>(d_tasks);
+  } else if (mode == 2) {  // transposed, rows with leading zeros (task.kfirst, <= GT_MAXROWS rows)
+    gemv_t_lead_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
   } else {
     gemv_t_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
   }

@@ -146,6 +146,7 @@ struct OzSeg {
   double alpha;
   const uint8_t* a_nz;  // optional nonzero flags of A's 128 x 32 tiles (row tile-major, nk per row tile):
                         // all-zero K tiles are skipped (their products are exact zeros)
+  const uint8_t* b_nz;  // same for B (its K padding equals A's)
 };
 // one 128 x 128 output tile: C = beta*C + sum of its segments (in order)
 struct OzTask {

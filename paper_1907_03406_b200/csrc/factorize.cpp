@@ -748,8 +748,11 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       const EI& e = info[qi];
       if (kf_all) ekf[qi] = kf_all + okf;
       okf += e.c;
+      // nonzero tile flags: the Schur products E_a E_b^T skip the K tiles
+      // where E_a or E_b is zero (the couplings are block-sparse: 30-50% of
+      // their 128 x 32 tiles are zero at levels 2-3 of 128^3)
       for (size_t q = 0; q < e.nb.size(); ++q)
-        eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m, false,
+        eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m, true,
                                    kf_all ? ekf[qi] + e.off[q] : nullptr));
     }
     oz.launch_splits(S.scratch, st);
@@ -766,6 +769,18 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         o += info[qi].c;
       }
       fprintf(stderr, "[sgf] L%d E rows: %.1f%% of the entries are leading zeros\n", level, 100.0 * lead / tot);
+      const bool pat = atoi(getenv("SGF_ZERO_STATS")) == 2;
+      for (size_t q = 0; pat && q < eop[0].size() && eop[0][q].nz; ++q) {  // SGF_ZERO_STATS=2: first node's tiles
+        const OzOperand& o = eop[0][q];
+        const int nr = o.Rp / 128, nk = o.Kp / 32;
+        std::vector<uint8_t> f((size_t)nr * nk);
+        SGF_CUDA(cudaMemcpy(f.data(), o.nz, f.size(), cudaMemcpyDeviceToHost));
+        for (int r = 0; r < nr; ++r) {
+          std::string line;
+          for (int k = 0; k < nk; ++k) line += f[(size_t)r * nk + k] ? '#' : '.';
+          fprintf(stderr, "[sgf] L%d nb %zu rt %d %s\n", level, q, r, line.c_str());
+        }
+      }
     }
   }
 

@@ -300,16 +300,18 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
   }
 }
 
-// K tiles of one segment: for the first segment of a tile whose A operand
-// carries nonzero flags, the list of the K tiles whose A tile holds a
-// nonzero (built once per CTA in shared memory; all-zero tiles contribute
-// exact zeros and are skipped), otherwise the range [kstart, nk) (flags of
-// later segments are not used).  The producer and MMA loops stay simple
-// counted loops either way (a data-dependent skip inside the MMA issue loop
-// cost 7-9% on dense products).
-constexpr int OZ_KLIST = 512;  // K <= 16384
+// K tiles of one segment: for the first two segments of a tile whose
+// operands carry nonzero flags, the list of the K tiles where both the A
+// tile and the B tile hold a nonzero (an absent flag array counts as all
+// nonzero; built once per CTA in shared memory; every other K tile is a
+// product with an all-zero operand tile, an exact zero, and is skipped),
+// otherwise the range [kstart, nk) (flags of later segments, or of
+// products with more than 256 K tiles, are not used).  The producer and MMA
+// loops stay simple counted loops either way (a data-dependent skip inside
+// the MMA issue loop cost 7-9% on dense products).
+constexpr int OZ_KLIST = 256, OZ_KLSEG = 2;
 struct OzKRange {
-  const uint16_t* list;  // nullptr: dense range
+  const uint8_t* list;  // nullptr: dense range
   int kstart, count;
   __device__ __forceinline__ int k(int idx) const { return list ? (int)list[idx] : kstart + idx; }
 };
@@ -321,24 +323,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint8_t* sB = smem + OZ_STAGES * OZ_A_STAGE;
   __shared__ __align__(8) uint64_t full[OZ_STAGES], empty[OZ_STAGES], tmem_full, tmem_empty;
   __shared__ uint32_t tmem_base;
-  __shared__ uint16_t klist[OZ_KLIST];
-  __shared__ int kcount;
+  __shared__ uint8_t klist[OZ_KLSEG][OZ_KLIST];
+  __shared__ int kcount[OZ_KLSEG];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const OzTask T = tasks[blockIdx.x];
-  if (warp == 0) {  // K-tile list of the first segment when A carries nonzero flags
-    const OzSeg G0 = segs[T.seg0];
-    if (G0.a_nz && min(G0.nk, T.klim) <= OZ_KLIST) {
-      const uint8_t* nzr = G0.a_nz + (size_t)(T.m0 / OZ_BM) * G0.nk;
-      const int nk = min(G0.nk, T.klim);
+  if (warp < OZ_KLSEG && warp < T.nseg) {  // K-tile lists of segments 0 and 1 (warp w: segment w)
+    const OzSeg G = segs[T.seg0 + warp];
+    const int nk = min(G.nk, T.klim);
+    if ((G.a_nz || G.b_nz) && nk <= OZ_KLIST) {
+      const uint8_t* fa = G.a_nz ? G.a_nz + (size_t)(T.m0 / OZ_BM) * G.nk : nullptr;
+      const uint8_t* fb = G.b_nz ? G.b_nz + (size_t)(T.n0 / OZ_BN) * G.nk : nullptr;
       int cnt = 0;
       for (int k0 = T.kstart; k0 < nk; k0 += 32) {
         const int k = k0 + lane;
-        const bool f = k < nk && nzr[k] != 0;
+        const bool f = k < nk && (!fa || fa[k] != 0) && (!fb || fb[k] != 0);
         const unsigned m = __ballot_sync(0xffffffffu, f);
-        if (f) klist[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)k;
+        if (f) klist[warp][cnt + __popc(m & ((1u << lane) - 1u))] = (uint8_t)k;
         cnt += __popc(m);
       }
-      if (lane == 0) kcount = cnt;
+      if (lane == 0) kcount[warp] = cnt;
     }
   }
   if (threadIdx.x == 0) {
@@ -364,9 +367,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     r.kstart = T.kstart;
     r.list = nullptr;
     r.count = max(0, nk - T.kstart);
-    if (G.a_nz && si == 0 && nk <= OZ_KLIST) {
-      r.list = klist;
-      r.count = kcount;
+    if ((G.a_nz || G.b_nz) && si < OZ_KLSEG && nk <= OZ_KLIST) {
+      r.list = klist[si];
+      r.count = kcount[si];
     }
     return r;
   };

@@ -573,7 +573,8 @@ struct OzBatch {
     for (auto& tm : terms) {
       const OzOperand& A = tm.first.first;
       const OzOperand& B = tm.first.second;
-      segs.push_back(OzSeg{A.data, B.data, A.e, B.e, A.Rp, B.Rp, A.Kp / 32, tm.second, A.nz});
+      segs.push_back(OzSeg{A.data, B.data, A.e, B.e, A.Rp, B.Rp, A.Kp / 32, tm.second, A.nz,
+                           B.Kp == A.Kp ? B.nz : nullptr});
     }
     for (int m0 = 0; m0 < M; m0 += 128)
       for (int n0 = 0; n0 < N; n0 += 128) {
