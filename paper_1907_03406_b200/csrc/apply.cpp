@@ -37,6 +37,7 @@ struct Group {
   GemvTask* bwd1 = nullptr;
   int nb1 = 0;
   int b1_mode = 1;  // 2: every task carries the rows' leading-zero offsets (gemv_t_lead_kernel)
+  int f2_mode = 0;  // 3: the couplings' rows are block-sparse (task.kfirst / task.rmask)
   RedSeg* red1 = nullptr;
   int nred1 = 0, maxn1 = 0;
   GemvTask* bwd2 = nullptr;
@@ -122,7 +123,8 @@ static void add_gemv_tri_pairs(std::vector<GemvTask>& v, const double* A, long l
 }
 
 static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* y, int rows,
-                       int cols, int tri, int rows_per = GN_ROWS, const int* kfirst = nullptr) {
+                       int cols, int tri, int rows_per = GN_ROWS, const int* kfirst = nullptr,
+                       const uint32_t* rmask = nullptr, int mwords = 0) {
   for (int r0 = 0; r0 < rows; r0 += rows_per) {
     GemvTask t;
     t.A = A;
@@ -135,13 +137,16 @@ static void add_gemv_n(std::vector<GemvTask>& v, const double* A, long long lda,
     t.c1 = cols;
     t.tri = tri;
     t.kfirst = kfirst;
+    t.rmask = rmask;
+    t.mwords = mwords;
     v.push_back(t);
   }
 }
 
 // partials part[rb*cols + k] = sum_{i in rb} A[i,k] x[i]; returns #row blocks
 static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, const double* x, double* part,
-                      int rows, int cols, int tri, int rows_per = GT_ROWS, const int* kfirst = nullptr) {
+                      int rows, int cols, int tri, int rows_per = GT_ROWS, const int* kfirst = nullptr,
+                      const uint32_t* rmask = nullptr, int mwords = 0) {
   int nrb = 0;
   for (int r0 = 0; r0 < rows; r0 += rows_per, ++nrb)
     for (int c0 = 0; c0 < cols; c0 += GT_COLS) {
@@ -156,6 +161,8 @@ static int add_gemv_t(std::vector<GemvTask>& v, const double* A, long long lda, 
       t.c1 = std::min(cols, c0 + GT_COLS);
       t.tri = tri;
       t.kfirst = kfirst;
+      t.rmask = rmask;
+      t.mwords = mwords;
       v.push_back(t);
     }
   return nrb;
@@ -236,9 +243,11 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       else add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
-        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows, f.ekfirst);
+        if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows, f.ekfirst, f.emask, f.emw);
         for (int p = 0; p < f.c; ++p) contrib.push_back({f.nidx[p], oc + p});
-        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0, g.gt_rows, f.ekfirst) : 0;
+        int nrb = f.c > 0 ? add_gemv_t(b1, f.E, f.ld, g.xn + oc, g.part + op, f.c, f.m, 0, g.gt_rows, f.ekfirst,
+                                       f.emask, f.emw)
+                          : 0;
         r1.push_back(RedSeg{g.part + op, g.xb + om, g.acc + om, f.m, nrb, f.m, -1.0});
         // second stage reuses the partial buffer after red1 consumed it
         int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1, g.gt_rows);
@@ -302,8 +311,11 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.nb1 = (int)b1.size();
     {
       bool lead = !b1.empty();
-      for (const auto& t : b1) lead = lead && t.kfirst && t.r1 - t.r0 <= GT_ROWS;
+      for (const auto& t : b1) lead = lead && (t.kfirst || t.rmask) && t.r1 - t.r0 <= GT_ROWS;
       g.b1_mode = lead ? 2 : 1;
+      bool sp = !f2.empty();
+      for (const auto& t : f2) sp = sp && (t.kfirst || t.rmask);
+      g.f2_mode = sp ? 3 : 0;
     }
     g.bwd2 = plan->mem.upload(b2);
     g.nb2 = (int)b2.size();
@@ -399,7 +411,7 @@ static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t
   (void)pl;
   SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
   gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st, g.lpr1);
-  if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, 0, g.bytes_f2, st, g.lpr2);
+  if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, g.f2_mode, g.bytes_f2, st, g.lpr2);
   SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, g.t, g.ntgt, st));
 }

@@ -76,8 +76,11 @@ __device__ __forceinline__ void gemv_tri_pairs(const GemvTask& T) {
   }
 }
 
-template <int LPR>
-__global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
+// SPARSE: the rows' leading zeros / all-zero 256-column chunks (task.kfirst,
+// task.rmask) are skipped; its own instantiation keeps the dense kernel at
+// 32 registers.
+template <int LPR, bool SPARSE = false>
+__global__ void __launch_bounds__(256, SPARSE ? 6 : 8) gemv_n_kernel(const GemvTask* __restrict__ tasks) {
   constexpr int RPW = 32 / LPR;  // rows per warp pass
   const GemvTask T = tasks[blockIdx.x];
   if (LPR == 32 && T.tri == 2) {
@@ -96,8 +99,9 @@ __global__ void __launch_bounds__(256, 8) gemv_n_kernel(const GemvTask* __restri
       const int k2 = ke >> 1;
       const double* x = T.x;
       // leading zeros of the row (couplings E): start at the first nonzero
-      // 16-byte word
-      int k = (T.kfirst ? min(T.kfirst[i], ke) >> 1 : 0) + sub;
+      // 16-byte word (the interior zero runs are left to the bulk kernel of
+      // the long rows: per-iteration skips cost more than they save here)
+      int k = (SPARSE && T.kfirst ? min(T.kfirst[i], ke) >> 1 : 0) + sub;
       for (; k + 3 * LPR < k2; k += 4 * LPR) {
         const double2 a0 = __ldcs(a + k), a1 = __ldcs(a + k + LPR), a2 = __ldcs(a + k + 2 * LPR),
                       a3 = __ldcs(a + k + 3 * LPR);
@@ -132,30 +136,44 @@ constexpr int GT_MAXROWS = 256;  // rows of a transposed task with leading-zero 
 // part[k] = sum_{i in [r0,r1)} A[i,k] x[i] (mode T): each thread owns two
 // adjacent columns (one 16-byte load per row), 512 columns per CTA.
 // ---------------------------------------------------------------------------
-// Rows with leading zeros (couplings E, task.kfirst): row i holds zeros left
-// of kfirst[i]; the task's first nonzero columns are staged in shared memory
-// and each row's entries are loaded only where a thread's column pair can
-// reach them (columns left of every row's first nonzero get an exact zero
-// partial without reading A).  Same sums as the dense form: the skipped
-// entries are exact zeros.
-__global__ void __launch_bounds__(256, 6) gemv_t_lead_kernel(const GemvTask* __restrict__ tasks) {
+// Block-sparse rows (couplings E): with task.rmask, row i's all-zero
+// 32-column tiles (16 per CTA: c0 is a multiple of 512) are staged in
+// shared memory as a 16-bit mask per row; with only task.kfirst, row i
+// holds zeros left of kfirst[i].  A thread loads a row's entries only where
+// its column pair can be nonzero; columns that are zero in every row of the
+// task get an exact zero partial without reading A.  Same sums as the dense
+// form: the skipped entries are exact zeros.
+__global__ void __launch_bounds__(256, 5) gemv_t_lead_kernel(const GemvTask* __restrict__ tasks) {
   const GemvTask T = tasks[blockIdx.x];
-  __shared__ int skf[GT_MAXROWS];
-  __shared__ int kmin;
+  __shared__ int skf[GT_MAXROWS];  // per row: first nonzero column, or (rmask) the CTA's 16 tile bits
+  __shared__ int cany;             // OR of the tile bits / min of the first nonzero columns
+  const bool tiles = T.rmask != nullptr;
   const int k = T.c0 + 2 * threadIdx.x;  // c0 is even
   const int nr = T.r1 - T.r0;
-  if (threadIdx.x == 0) kmin = T.c1;
+  const int tb = T.c0 >> 5;              // first 32-column tile of the CTA (a multiple of 16)
+  if (threadIdx.x == 0) cany = tiles ? 0 : T.c1;
   __syncthreads();
-  int km = T.c1;
+  int acc = tiles ? 0 : T.c1;
   for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-    const int kf = T.kfirst[T.r0 + i];
-    skf[i] = kf;
-    km = min(km, kf);
+    int v;
+    if (tiles) {
+      v = (int)((T.rmask[(size_t)(T.r0 + i) * T.mwords + (tb >> 5)] >> (tb & 31)) & 0xFFFFu);
+      acc |= v;
+    } else {
+      v = T.kfirst[T.r0 + i];
+      acc = min(acc, v);
+    }
+    skf[i] = v;
   }
-  if (km < T.c1) atomicMin(&kmin, km);
+  if (tiles) {
+    if (acc) atomicOr(&cany, acc);
+  } else if (acc < T.c1) {
+    atomicMin(&cany, acc);
+  }
   __syncthreads();
   if (k >= T.c1) return;
-  if (k + 1 < kmin) {
+  const int bit = 1 << (threadIdx.x >> 4);  // this thread's tile among the CTA's 16
+  if (tiles ? !(cany & bit) : k + 1 < cany) {
     T.y[k] = 0.0;
     if (k + 1 < T.c1) T.y[k + 1] = 0.0;
     return;
@@ -165,11 +183,11 @@ __global__ void __launch_bounds__(256, 6) gemv_t_lead_kernel(const GemvTask* __r
   const long long ld2 = ld >> 1;
   const double2 z = make_double2(0.0, 0.0);
   double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+  auto live = [&](int i) { return tiles ? (skf[i] & bit) != 0 : k + 1 >= skf[i]; };
   int i = 0;
   for (; i + 3 < nr; i += 4, a += 4 * ld2) {
-    const double2 a0 = k + 1 >= skf[i] ? __ldcs(a) : z, a1 = k + 1 >= skf[i + 1] ? __ldcs(a + ld2) : z,
-                  a2 = k + 1 >= skf[i + 2] ? __ldcs(a + 2 * ld2) : z,
-                  a3 = k + 1 >= skf[i + 3] ? __ldcs(a + 3 * ld2) : z;
+    const double2 a0 = live(i) ? __ldcs(a) : z, a1 = live(i + 1) ? __ldcs(a + ld2) : z,
+                  a2 = live(i + 2) ? __ldcs(a + 2 * ld2) : z, a3 = live(i + 3) ? __ldcs(a + 3 * ld2) : z;
     const double* xr = T.x + T.r0 + i;
     const double x0 = xr[0], x1 = xr[1], x2 = xr[2], x3 = xr[3];
     s0 = fma(a0.x, x0, fma(a1.x, x1, s0));
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(256, 6) gemv_t_lead_kernel(const GemvTask* __r
     t1 = fma(a2.y, x2, fma(a3.y, x3, t1));
   }
   for (; i < nr; ++i, a += ld2) {
-    const double2 a0 = k + 1 >= skf[i] ? __ldcs(a) : z;
+    const double2 a0 = live(i) ? __ldcs(a) : z;
     s0 = fma(a0.x, T.x[T.r0 + i], s0);
     t0 = fma(a0.y, T.x[T.r0 + i], t0);
   }
@@ -225,12 +243,29 @@ __global__ void __launch_bounds__(256, 6) gemv_t_kernel(const GemvTask* __restri
 constexpr int GB_CH = 256, GB_S = 4, GB_XCAP = 4096;
 struct GbCursor {
   int n = 0, sub = 0, off = 0;  // row (or pair) counter of the warp, row of the pair, offset in the row
+  bool fresh = true;            // off not yet moved past the row's leading all-zero chunks
 };
+// block-sparse rows (task.rmask, staged in shared memory per task row): the
+// 256-column chunk at column col (a multiple of 32) holds no nonzero
+constexpr int GB_MW = 16;  // mask words per row (K <= 16384)
+__device__ __forceinline__ bool gb_zero_chunk(const uint32_t* smk, int mw, int lrow, int col) {
+  const int t = col >> 5, w = t >> 5, sh = t & 31;
+  const uint32_t* m = smk + lrow * mw;
+  uint32_t bits = m[w] >> sh;
+  if (sh > 24 && w + 1 < mw) bits |= m[w + 1] << (32 - sh);
+  return (bits & 0xFFu) == 0u;
+}
+// skip all-zero chunks, keeping the row's last chunk (every row ends with a
+// chunk, whose completion writes y[row])
+__device__ __forceinline__ void gb_skip(const GemvTask& T, const uint32_t* smk, int row, int start, int len,
+                                        int& off) {
+  while (off + GB_CH < len && gb_zero_chunk(smk, T.mwords, row - T.r0, start + off)) off += GB_CH;
+}
 // row index, its first column (even: 16-byte aligned; the leading zeros of a
 // coupling row are skipped) and its length counted from there, for the
 // cursor; false when the warp has no more rows
-__device__ __forceinline__ bool gb_row(const GemvTask& T, int warp, const GbCursor& c, int& row, int& start,
-                                       int& len) {
+__device__ __forceinline__ bool gb_row(const GemvTask& T, const uint32_t* smk, int warp, GbCursor& c, int& row,
+                                       int& start, int& len) {
   const int q = T.r0 + warp + 8 * c.n;
   if (q >= T.r1) return false;
   start = 0;
@@ -240,15 +275,22 @@ __device__ __forceinline__ bool gb_row(const GemvTask& T, int warp, const GbCurs
   } else {
     row = q;
     len = T.tri ? min(T.c1, q + 1) : T.c1;
-    if (T.kfirst) start = min(T.kfirst[row], len) & ~1;
+    if (T.kfirst) start = min(T.kfirst[row], len) & (smk ? ~31 : ~1);  // tile-aligned with masks
     len -= start;
+    if (smk && c.fresh) gb_skip(T, smk, row, start, len, c.off);
   }
+  c.fresh = false;
   return true;
 }
-__device__ __forceinline__ void gb_advance(const GemvTask& T, int warp, GbCursor& c, int len) {
+__device__ __forceinline__ void gb_advance(const GemvTask& T, const uint32_t* smk, int warp, GbCursor& c,
+                                           int start, int len, int row) {
   c.off += GB_CH;
-  if (c.off < len) return;
+  if (c.off < len) {
+    if (smk && !T.tri) gb_skip(T, smk, row, start, len, c.off);
+    return;
+  }
   c.off = 0;
+  c.fresh = true;
   if (T.tri == 2 && c.sub == 0 && T.c1 - 1 - (T.r0 + warp + 8 * c.n) != T.r0 + warp + 8 * c.n) {
     c.sub = 1;
     return;
@@ -264,10 +306,11 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
   double* wring = sm + warp * GB_S * GB_CH;
   double* xs = sm + 8 * GB_S * GB_CH;
   uint64_t* wbar = bar + warp * GB_S;
+  const uint32_t* smk = nullptr;  // (block-sparse rows: gemv_n_bulk_sparse_kernel)
   GbCursor pc;  // producer cursor (lane 0)
   auto issue = [&](int slot) -> bool {
     int row, start, len;
-    if (!gb_row(T, warp, pc, row, start, len)) return false;
+    if (!gb_row(T, smk, warp, pc, row, start, len)) return false;
     if (len > 0) {
       const int cl = min(GB_CH, len - pc.off);
       const uint32_t bytes = (uint32_t)((cl + 1) & ~1) * 8u;  // even count: 16-byte multiple (ld even)
@@ -276,7 +319,7 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
     } else {
       ptx::mbar_arrive(&wbar[slot]);  // an all-zero row: an empty chunk
     }
-    gb_advance(T, warp, pc, len);
+    gb_advance(T, smk, warp, pc, start, len, row);
     return true;
   };
   if (lane == 0) {
@@ -293,7 +336,7 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
   double acc = 0.0;
   for (int it = 0;; ++it) {
     int row, start, len;
-    if (!gb_row(T, warp, cc, row, start, len)) break;
+    if (!gb_row(T, smk, warp, cc, row, start, len)) break;
     const int slot = it % GB_S;
     const int off = cc.off, cl = min(GB_CH, len - off);
     ptx::mbar_wait(&wbar[slot], (it / GB_S) & 1);
@@ -317,7 +360,125 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_kernel(const GemvTask* __r
       if (lane == 0) T.y[row] = s;
       acc = 0.0;
     }
-    gb_advance(T, warp, cc, len);
+    gb_advance(T, smk, warp, cc, start, len, row);
+  }
+}
+
+// Mode N over block-sparse rows (couplings E: task.kfirst, task.rmask) with
+// the rows staged by the bulk copy engine.  A row starts at its first
+// nonzero 32-column tile and skips its all-zero 256-column chunks (the mask
+// byte of 8 tiles; the last chunk of a row is always read, its completion
+// writes y[row]).  Rows then differ widely in length, so the warps of a CTA
+// take rows from a shared counter instead of a fixed stride (a fixed
+// assignment left warps idle behind the longest row), and the producer lane
+// passes each slot's (row, column, count, last) to the consumer in shared
+// memory next to the data.  A row is reduced by one warp in chunk order, so
+// the sums do not depend on which warp takes it.
+struct GbMeta {
+  int row, col, cl, last;
+};
+__global__ void __launch_bounds__(256, 2) gemv_n_bulk_sparse_kernel(const GemvTask* __restrict__ tasks) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar[8 * GB_S];
+  __shared__ GbMeta meta[8 * GB_S];
+  __shared__ uint32_t smk[64 * GB_MW];
+  __shared__ int next_row;
+  const GemvTask T = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* wring = sm + warp * GB_S * GB_CH;
+  double* xs = sm + 8 * GB_S * GB_CH;
+  uint64_t* wbar = bar + warp * GB_S;
+  GbMeta* wmeta = meta + warp * GB_S;
+  const int nr = T.r1 - T.r0, mw = T.mwords;
+  const bool masked = T.rmask && nr <= 64 && mw <= GB_MW;
+  if (masked)
+    for (int i = threadIdx.x; i < nr * mw; i += 256) smk[i] = T.rmask[(size_t)T.r0 * mw + i];
+  if (threadIdx.x == 0) next_row = 0;
+  __syncthreads();
+  // producer state (lane 0): the current row and the next chunk's offset
+  int prow = -1, pstart = 0, plen = 0, poff = 0;
+  auto skip = [&]() {
+    if (masked)
+      while (poff + GB_CH < plen && gb_zero_chunk(smk, mw, prow, pstart + poff)) poff += GB_CH;
+  };
+  auto issue = [&](int slot) {
+    GbMeta& md = wmeta[slot];
+    bool have = false;
+    if (prow >= 0) {
+      poff += GB_CH;
+      if (poff < plen) {
+        skip();
+        have = true;
+      }
+    }
+    if (!have) {
+      const int r = atomicAdd(&next_row, 1);
+      if (r < nr) {
+        prow = r;
+        pstart = T.kfirst ? min(T.kfirst[T.r0 + r], T.c1) & ~31 : 0;
+        plen = T.c1 - pstart;
+        poff = 0;
+        skip();
+        have = true;
+      } else {
+        prow = -1;
+        plen = 0;
+      }
+    }
+    if (!have) {  // no rows left: a sentinel slot
+      md.row = -1;
+      ptx::mbar_arrive(&wbar[slot]);
+      return;
+    }
+    const int cl = min(GB_CH, plen - poff);
+    md.row = prow;
+    md.col = pstart + poff;
+    md.cl = cl;
+    md.last = poff + GB_CH >= plen;
+    if (cl > 0) {
+      const uint32_t bytes = (uint32_t)((cl + 1) & ~1) * 8u;  // even count: 16-byte multiple (ld even)
+      ptx::mbar_expect_tx(&wbar[slot], bytes);
+      ptx::bulk_g2s(wring + slot * GB_CH, T.A + (long long)(T.r0 + prow) * T.lda + pstart + poff, bytes,
+                    &wbar[slot]);
+    } else {
+      ptx::mbar_arrive(&wbar[slot]);  // an all-zero row: an empty chunk
+    }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < GB_S; ++s) ptx::mbar_init(&wbar[s], 1);
+    ptx::mbar_init_fence();
+    for (int s = 0; s < GB_S; ++s) issue(s);
+  }
+  const bool sx = T.c1 <= GB_XCAP;
+  for (int i = threadIdx.x; i < T.c1 && sx; i += 256) xs[i] = T.x[i];
+  __syncthreads();
+  const double* xv = sx ? xs : T.x;
+  double acc = 0.0;
+  for (int it = 0;; ++it) {
+    const int slot = it % GB_S;
+    ptx::mbar_wait(&wbar[slot], (it / GB_S) & 1);
+    const GbMeta md = wmeta[slot];
+    if (md.row < 0) break;
+    const double* ch = wring + slot * GB_CH;
+    const double* xo = xv + md.col;
+#pragma unroll
+    for (int t = 0; t < GB_CH / 64; ++t) {
+      const int j = 64 * t + 2 * lane;
+      if (j < md.cl) {
+        const double2 g = *reinterpret_cast<const double2*>(ch + j);
+        acc = fma(g.x, xo[j], acc);
+        if (j + 1 < md.cl) acc = fma(g.y, xo[j + 1], acc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) issue(slot);
+    if (md.last) {  // row complete
+      double sum = acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) T.y[T.r0 + md.row] = sum;
+      acc = 0.0;
+    }
   }
 }
 
@@ -325,9 +486,15 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
   if (ntasks <= 0) return cudaSuccess;
   count_launch();
   static const int bulk = getenv("SGF_GEMV_BULK") ? atoi(getenv("SGF_GEMV_BULK")) : 1;
-  if (mode == 0 && lpr == 64 && bulk) {
+  if ((mode == 0 || mode == 3) && lpr == 64 && bulk) {
     const size_t smem = ((size_t)8 * GB_S * GB_CH + GB_XCAP) * sizeof(double);
-    static FuncAttrs fa;
+    static FuncAttrs fa, fa_sp;
+    if (mode == 3) {  // block-sparse coupling rows
+      cudaError_t e = ensure_smem(gemv_n_bulk_sparse_kernel, smem, fa_sp);
+      if (e != cudaSuccess) return e;
+      gemv_n_bulk_sparse_kernel<<<ntasks, 256, smem, s>>>(d_tasks);
+      return cudaGetLastError();
+    }
     cudaError_t e = ensure_smem(gemv_n_bulk_kernel, smem, fa);
     if (e != cudaSuccess) return e;
     gemv_n_bulk_kernel<<<ntasks, 256, smem, s>>>(d_tasks);
@@ -338,6 +505,10 @@ cudaError_t launch_gemv(const GemvTask* d_tasks, int ntasks, int mode, cudaStrea
     if (lpr == 8) gemv_n_kernel<8><<<ntasks, 256, 0, s>>>(d_tasks);
     else if (lpr == 16) gemv_n_kernel<16><<<ntasks, 256, 0, s>>>(d_tasks);
     else gemv_n_kernel<32><<<ntasks, 256, 0, s>>>(d_tasks);
+  } else if (mode == 3) {  // mode N, block-sparse rows (task.kfirst / task.rmask)
+    if (lpr == 8) gemv_n_kernel<8, true><<<ntasks, 256, 0, s>>>(d_tasks);
+    else if (lpr == 16) gemv_n_kernel<16, true><<<ntasks, 256, 0, s>>>(d_tasks);
+    else gemv_n_kernel<32, true><<<ntasks, 256, 0, s>>>(d_tasks);
   } else if (mode == 2) {  // transposed, rows with leading zeros (task.kfirst, <= GT_MAXROWS rows)
     gemv_t_lead_kernel<<<ntasks, 256, 0, s>>>(d_tasks);
   } else {

@@ -134,6 +134,9 @@ struct OzSplitJob {
   int* exps;
   uint8_t* nz;  // optional: nz[(r / 128) * (Kp / 32) + k / 32] = 1 where the 128 x 32 tile has a nonzero
   int* kfirst;  // optional: per row r < R, the first column k with x(r, k) != 0 (K when none)
+  uint32_t* rmask;  // optional: per row r < R, mwords words; bit t: columns [32t, 32t+32) hold a nonzero
+                    // value (must be zeroed beforehand when the warp kernel runs)
+  int mwords;
 };
 // one product term C += alpha * A B^T of split operands (rows of A = rows of C)
 struct OzSeg {
@@ -175,6 +178,8 @@ struct GemvTask {
   int tri;             // 1: lower-triangular A (row i uses k <= i); 2 (mode N): rows in pairs
                        //    (p, c1-1-p) for pair indices p in [r0, r1)
   const int* kfirst = nullptr;  // optional (tri == 0): row i is zero in columns < kfirst[i] (skipped)
+  const uint32_t* rmask = nullptr;  // optional (tri == 0): row i's 32-column tiles holding a nonzero
+  int mwords = 0;                   // (mwords words per row; all-zero tiles are skipped)
 };
 
 struct TriTask { double* p; int m; int ld; };

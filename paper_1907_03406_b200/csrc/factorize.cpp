@@ -736,24 +736,32 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
   // per row of E, its first nonzero column (apply: the leading zeros of the
   // couplings are skipped; written by the operand split below)
   std::vector<int*> ekf(info.size(), nullptr);
+  std::vector<uint32_t*> emk(info.size(), nullptr);
+  int emw = 0;
   if (oz_schur) {
     // the couplings as Schur operands, one split per neighbour block
     long long tot_c = 0;
     for (size_t qi = 0; qi < info.size(); ++qi)
       if (own[qi]) tot_c += info[qi].c;
     int* kf_all = (S.ekfirst && tot_c) ? P->store.alloc_t<int>(tot_c) : nullptr;
+    // row masks of the couplings' 32-column tiles (apply: all-zero tiles skipped)
+    const int mw = (maxm + 1023) / 1024;
+    emw = mw;
+    uint32_t* mk_all = (S.ekfirst && tot_c && maxm <= 16384) ? P->store.alloc_t<uint32_t>(tot_c * mw) : nullptr;
     long long okf = 0;
     for (size_t qi = 0; qi < info.size(); ++qi) {
       if (!own[qi]) continue;
       const EI& e = info[qi];
       if (kf_all) ekf[qi] = kf_all + okf;
+      if (mk_all) emk[qi] = mk_all + okf * mw;
       okf += e.c;
       // nonzero tile flags: the Schur products E_a E_b^T skip the K tiles
       // where E_a or E_b is zero (the couplings are block-sparse: 30-50% of
       // their 128 x 32 tiles are zero at levels 2-3 of 128^3)
       for (size_t q = 0; q < e.nb.size(); ++q)
         eop[qi].push_back(oz.split(S.scratch, e.E + (long long)e.off[q] * e.ld, e.ld, 1, M.size[e.nb[q]], e.m, true,
-                                   kf_all ? ekf[qi] + e.off[q] : nullptr));
+                                   kf_all ? ekf[qi] + e.off[q] : nullptr,
+                                   mk_all ? emk[qi] + (long long)e.off[q] * mw : nullptr, mw));
     }
     oz.launch_splits(S.scratch, st);
     if (zero_stats && kf_all) {  // diagnostics: leading zeros of the couplings' rows
@@ -922,6 +930,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       f.inv = e.X;
       f.E = e.E;
       f.ekfirst = ekf[q];
+      f.emask = emk[q];
+      f.emw = emk[q] ? emw : 0;
       if (Gall) f.G = Gall + (e.X - Xall);
     }
     // replay the reference sequence for the table and its byte accounting:

@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
     unsigned w[OZ_S][4];
 #pragma unroll
     for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+    bool nzv = false;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int k = k0 + q;
       const double x = (live && k < J.K) ? row[(long long)k * J.cs] : 0.0;
+      nzv |= x != 0.0;
       int dg[OZ_S];
       oz_digits(x, ex, dg);
 #pragma unroll
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
       *reinterpret_cast<uint4*>(J.out + ((size_t)kt * OZ_S + t) * blk + off) = v4;
     }
     if (J.nz && any) J.nz[(size_t)(r >> 7) * (J.Kp / OZ_KT) + kt] = 1;  // benign race: every writer stores 1
+    if (J.rmask && nzv) atomicOr(&J.rmask[(size_t)r * J.mwords + (kt >> 5)], 1u << (kt & 31));
   }
 }
 
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
 // group form reads 16-element runs per lane and fetched ~2x the operand bytes
 // from HBM.)  Identical output.
 constexpr int OZS_TK = 512, OZS_PITCH = OZS_TK + 4;
+constexpr int OZS_MW = 16;  // row-mask words (K <= 16384)
 __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __restrict__ jobs,
                                                            const long long* __restrict__ group_prefix, int njobs) {
   __shared__ double tile[8 * OZS_PITCH];
@@ -249,6 +253,9 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
       }
     }
   }
+  __shared__ uint32_t smask[8][OZS_MW];  // per row: bit kt = 32-column tile kt holds a nonzero value
+  if (J.rmask)
+    for (int i = threadIdx.x; i < 8 * OZS_MW; i += 256) smask[i / OZS_MW][i % OZS_MW] = 0u;
   __syncthreads();
   const int rl = lane & 7, r = g0 + rl;
   const int ex = sex[rl];
@@ -277,15 +284,18 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
       unsigned w[OZ_S][4];
 #pragma unroll
       for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+      bool nzv = false;  // a nonzero value (not digit) in this 16-column chunk of the row
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const double x = tile[rl * OZS_PITCH + ci * 16 + q];
+        nzv |= x != 0.0;
         int dg[OZ_S];
         oz_digits(x, ex, dg);
 #pragma unroll
         for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= ((unsigned)dg[t] & 0xFFu) << (8 * (q & 3));
       }
       const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
+      if (J.rmask && nzv) atomicOr(&smask[rl][kt >> 5], 1u << (kt & 31));
       const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
       unsigned any = 0u;
 #pragma unroll
@@ -298,6 +308,11 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
     }
     __syncthreads();
   }
+  if (J.rmask)
+    for (int i = threadIdx.x; i < 8 * J.mwords; i += 256) {
+      const int rr = g0 + i / J.mwords, wi = i % J.mwords;
+      if (rr < J.R) J.rmask[(size_t)rr * J.mwords + wi] = smask[i / J.mwords][wi];
+    }
 }
 
 // K tiles of one segment: for the first two segments of a tile whose

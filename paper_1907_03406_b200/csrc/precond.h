@@ -23,6 +23,8 @@ struct Factor {
   double* E = nullptr;        // c x m couplings E_N = A_NB L^{-T}, stacked
   int* ekfirst = nullptr;     // per row of E: first nonzero column (leading zeros: E = A_NB L^{-T} with
                               // L^{-T} upper triangular keeps the leading zero columns of A_NB's rows)
+  uint32_t* emask = nullptr;  // per row of E: bit t = 32-column tile t holds a nonzero (emw words per row;
+  int emw = 0;                // E is block-sparse: zero runs at the interior's pieces, not only leading)
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator

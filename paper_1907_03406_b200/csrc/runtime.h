@@ -542,7 +542,7 @@ struct OzBatch {
   // products with it as the A operand skip the all-zero K tiles (block-sparse
   // couplings A_NB: 54-69% of their tiles are zero at levels 2-3 of 128^3)
   OzOperand split(Arena& mem, const double* x, long long rs, long long cs, int R, int K, bool nz_flags = false,
-                  int* kfirst = nullptr) {
+                  int* kfirst = nullptr, uint32_t* rmask = nullptr, int mwords = 0) {
     OzOperand o;
     o.R = R;
     o.K = K;
@@ -556,7 +556,8 @@ struct OzBatch {
       o.nz = mem.alloc_t<uint8_t>(nb);
       nz_clear.push_back({o.nz, nb});
     }
-    jobs.push_back(OzSplitJob{x, rs, cs, R, K, o.Rp, o.Kp, o.data, o.e, o.nz, kfirst});
+    if (rmask) nz_clear.push_back({(uint8_t*)rmask, (size_t)R * mwords * sizeof(uint32_t)});
+    jobs.push_back(OzSplitJob{x, rs, cs, R, K, o.Rp, o.Kp, o.data, o.e, o.nz, kfirst, rmask, mwords});
     return o;
   }
   void launch_splits(Arena& scratch, cudaStream_t st);
