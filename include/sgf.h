@@ -162,6 +162,12 @@ int64_t sgf_precond_n(const sgf_precond* p);
 const char* sgf_precond_stats_json(const sgf_precond* p);
 int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap);  /* returns #entries */
 int sgf_precond_num_factors(const sgf_precond* p);
+
+/* Measurement helper (bench.py's apply roofline; no reference counterpart):
+ * bytes of the stored couplings E per sweep, out[0] dense (sum c*m*8) and
+ * out[1] in the 32-column tiles that hold a nonzero -- the part the apply
+ * kernels stream (all-zero tiles are skipped; apply.cpp).  Synchronises. */
+int sgf_precond_coupling_bytes(const sgf_precond* p, double* out);
 /* info[0..7] = type, node, m (idx size), c (coupling rows), retained, level, reflectors, QR columns */
 int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info);
 /* what: 0 idx (int64 m), 1 L (m*m), 2 couplings E (c*m), 3 coupling idx (int64 c),

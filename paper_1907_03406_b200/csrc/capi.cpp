@@ -1,5 +1,6 @@
 // extern "C" boundary (include/sgf.h).  Every entry point converts internal
 // errors to an sgf_status and records the message on the context.
+#include <algorithm>
 #include <cstdio>
 
 #include "precond.h"
@@ -125,6 +126,39 @@ int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap) {
 }
 
 int sgf_precond_num_factors(const sgf_precond* p) { return p ? (int)p->p->factors.size() : 0; }
+
+int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) {
+  if (!p || !out) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = p->ctx;
+  return guarded(ctx, [&] {
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    double dense = 0.0, nz = 0.0;
+    std::vector<uint32_t> mk;
+    std::vector<int> kf;
+    for (const Factor& f : p->p->factors) {
+      if (f.type != SGF_FACTOR_ELIMINATION || !f.E || f.c <= 0) continue;
+      dense += 8.0 * f.c * f.m;
+      if (f.emask) {
+        mk.resize((size_t)f.c * f.emw);
+        SGF_CUDA(cudaMemcpy(mk.data(), f.emask, mk.size() * 4, cudaMemcpyDeviceToHost));
+        for (int r = 0; r < f.c; ++r)
+          for (int w = 0; w < f.emw; ++w) {
+            const uint32_t b = mk[(size_t)r * f.emw + w];
+            for (int t = 0; t < 32; ++t)
+              if ((b >> t) & 1u) nz += 8.0 * std::max(0, std::min(32, f.m - 32 * (32 * w + t)));
+          }
+      } else if (f.ekfirst) {
+        kf.resize(f.c);
+        SGF_CUDA(cudaMemcpy(kf.data(), f.ekfirst, kf.size() * 4, cudaMemcpyDeviceToHost));
+        for (int r = 0; r < f.c; ++r) nz += 8.0 * std::max(0, f.m - kf[r]);
+      } else {
+        nz += 8.0 * f.c * f.m;
+      }
+    }
+    out[0] = dense;
+    out[1] = nz;
+  });
+}
 
 int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info) {
   if (!p || k < 0 || k >= (int)p->p->factors.size() || !info) return SGF_INVALID_ARG;
