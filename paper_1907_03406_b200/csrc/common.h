@@ -163,6 +163,12 @@ struct OzTask {
 };
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
                             long long total_groups, cudaStream_t s, bool all_rowc = false);
+// row-contiguous operands (oz_split_rows_ok): groups of
+// oz_split_rows_per_cta(max Kp) rows per CTA (the prefix counts those groups), rows staged once
+bool oz_split_rows_ok(const OzSplitJob& j);
+int oz_split_rows_per_cta(int max_kp);
+cudaError_t launch_oz_split_rows(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
+                                 long long total_groups, int max_kp, cudaStream_t s);
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s);
 
 // ---- apply / GEMV -----------------------------------------------------------------

@@ -77,10 +77,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
 }
 
-// the S balanced base-256 digits of x 2^-ex (|x| 2^-ex < 1), most
-// significant first: F = trunc(|x| 2^(62-ex)) with x's sign, then
+// The S balanced base-256 digits of x 2^-ex (|x| 2^-ex < 1), most
+// significant first: F = trunc(|x| 2^(62-ex)) with x's sign (oz_fixed), then
 // d = F mod 256 in [-128, 127], F = (F - d) / 256, least significant first
-__device__ __forceinline__ void oz_digits(double x, int ex, int (&dg)[OZ_S]) {
+// (oz_pack4).  oz_fixed: the 62-bit fixed-point integer of x 2^-ex.
+__device__ __forceinline__ long long oz_fixed(double x, int ex) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
   const int bexp = (int)((bits >> 52) & 0x7FF);
   unsigned long long F = 0;
@@ -89,12 +90,32 @@ __device__ __forceinline__ void oz_digits(double x, int ex, int (&dg)[OZ_S]) {
     const int sh = bexp - 1075 + 62 - ex;  // F = |x| 2^(62-ex) < 2^62 (sh <= 9)
     F = sh >= 0 ? (sh < 10 ? mant << sh : 0) : (sh > -53 ? mant >> (-sh) : 0);
   }
-  long long v = ((long long)bits < 0) ? -(long long)F : (long long)F;
+  return ((long long)bits < 0) ? -(long long)F : (long long)F;
+}
+
+// Slice words of 4 consecutive elements: out[t] holds the (int8) digit t of
+// elements 0..3 in its bytes 0..3.  The balanced base-256 digits of v are the
+// bytes of u = v + 0x80..80 minus 128 (adding 128 to every digit leaves them
+// in [0, 255], so no carries), i.e. as int8 bytes: byte_j(u) ^ 0x80, digit
+// t (most significant first) = byte 7 - t.  Four byte permutes per slice
+// word instead of eight dependent extract/subtract/shift steps per element
+// (d = (int8)(v & 0xFF), v = (v - d) >> 8, least significant digit first).
+__device__ __forceinline__ void oz_pack4(const double (&x)[4], int ex, uint32_t (&out)[OZ_S]) {
+  constexpr unsigned long long B = 0x8080808080808080ull;
+  uint32_t lo[4], hi[4];
 #pragma unroll
-  for (int t = OZ_S - 1; t >= 0; --t) {
-    const int d = (int)(signed char)(v & 0xFF);
-    dg[t] = d;
-    v = (v - d) >> 8;
+  for (int e = 0; e < 4; ++e) {
+    const unsigned long long u = ((unsigned long long)oz_fixed(x[e], ex) + B) ^ B;
+    lo[e] = (uint32_t)u;
+    hi[e] = (uint32_t)(u >> 32);
+  }
+#pragma unroll
+  for (int t = 0; t < OZ_S; ++t) {
+    const int j = 3 - (t & 3);  // byte within the word: t = 0..3 from hi, 4..7 from lo
+    const uint32_t* W = t < 4 ? hi : lo;
+    const uint32_t a01 = __byte_perm(W[0], W[1], (uint32_t)(j | ((j + 4) << 4)));
+    const uint32_t a23 = __byte_perm(W[2], W[3], (uint32_t)(j | ((j + 4) << 4)));
+    out[t] = __byte_perm(a01, a23, 0x5410);
   }
 }
 
@@ -140,18 +161,20 @@ __global__ void __launch_bounds__(256) oz_split_kernel(const OzSplitJob* __restr
   const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
   for (int k0 = c0 * 16; k0 < J.Kp; k0 += 64) {
     unsigned w[OZ_S][4];
-#pragma unroll
-    for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
     bool nzv = false;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int k = k0 + q;
-      const double x = (live && k < J.K) ? row[(long long)k * J.cs] : 0.0;
-      nzv |= x != 0.0;
-      int dg[OZ_S];
-      oz_digits(x, ex, dg);
+    for (int p = 0; p < 4; ++p) {
+      double x4[4];
 #pragma unroll
-      for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= ((unsigned)dg[t] & 0xFFu) << (8 * (q & 3));
+      for (int e = 0; e < 4; ++e) {
+        const int k = k0 + 4 * p + e;
+        x4[e] = (live && k < J.K) ? row[(long long)k * J.cs] : 0.0;
+        nzv |= x4[e] != 0.0;
+      }
+      uint32_t o[OZ_S];
+      oz_pack4(x4, ex, o);
+#pragma unroll
+      for (int t = 0; t < OZ_S; ++t) w[t][p] = o[t];
     }
     const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
     const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
@@ -282,17 +305,19 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
     const int k0 = kb + ci * 16;
     if (k0 < J.Kp) {
       unsigned w[OZ_S][4];
-#pragma unroll
-      for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
       bool nzv = false;  // a nonzero value (not digit) in this 16-column chunk of the row
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const double x = tile[rl * OZS_PITCH + ci * 16 + q];
-        nzv |= x != 0.0;
-        int dg[OZ_S];
-        oz_digits(x, ex, dg);
+      for (int p = 0; p < 4; ++p) {
+        double x4[4];
 #pragma unroll
-        for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= ((unsigned)dg[t] & 0xFFu) << (8 * (q & 3));
+        for (int e = 0; e < 4; ++e) {
+          x4[e] = tile[rl * OZS_PITCH + ci * 16 + 4 * p + e];
+          nzv |= x4[e] != 0.0;
+        }
+        uint32_t o[OZ_S];
+        oz_pack4(x4, ex, o);
+#pragma unroll
+        for (int t = 0; t < OZ_S; ++t) w[t][p] = o[t];
       }
       const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
       if (J.rmask && nzv) atomicOr(&smask[rl][kt >> 5], 1u << (kt & 31));
@@ -313,6 +338,143 @@ __global__ void __launch_bounds__(256) oz_split_cta_kernel(const OzSplitJob* __r
       const int rr = g0 + i / J.mwords, wi = i % J.mwords;
       if (rr < J.R) J.rmask[(size_t)rr * J.mwords + wi] = smask[i / J.mwords][wi];
     }
+}
+
+// Split of row-contiguous operands with rows of at most OZR_KMAX columns
+// (the couplings E and A_NB, L^{-1}, A21 ...), one CTA per R rows: the rows
+// are fetched once (by the bulk copy engine when 16-byte aligned) into shared memory
+// (pass 1 then reads them there for the row maxima; the CTA kernel above
+// streams every row twice from HBM, the second time after it was evicted
+// from L2), then cut into slices.  A CTA writes its R rows' 16-byte pieces
+// of every 8-row core matrix (the other rows of the group are other CTAs).
+// R = 2 for long rows (up to 3 CTAs per SM overlap staging and cutting),
+// 4 or 8 for short ones (per-CTA overheads).
+// Identical output to the kernels above.
+constexpr int OZR_KMAX = 6912;
+template <int OZR_ROWS>
+__global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __restrict__ jobs,
+                                                            const long long* __restrict__ group_prefix, int njobs) {
+  extern __shared__ __align__(16) double srow[];  // [OZR_ROWS][pitch]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double smx[8];
+  __shared__ int skf[8], sex[OZR_ROWS];
+  __shared__ uint32_t smask[OZR_ROWS][OZS_MW];
+  const long long gw = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lo = 0, hi = njobs - 1;  // job containing row group gw
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (group_prefix[mid] <= gw) lo = mid;
+    else hi = mid - 1;
+  }
+  const OzSplitJob J = jobs[lo];
+  const int g0 = (int)(gw - group_prefix[lo]) * OZR_ROWS;
+  const int pitch = J.Kp + 2;  // doubles; 16-byte multiple, staggers the rows' banks
+  const int nlive = max(0, min(OZR_ROWS, J.R - g0));
+  // 16-byte aligned rows: the bulk copy engine (an odd last column is loaded
+  // directly); otherwise every thread loads (coalesced along the row)
+  const bool aligned = J.rs % 2 == 0 && ((uintptr_t)J.x & 15) == 0;
+  const int kb2 = aligned ? J.K & ~1 : 0;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::mbar_init_fence();
+    ptx::mbar_expect_tx(&bar, (uint32_t)nlive * kb2 * 8u);
+    for (int i = 0; i < nlive; ++i)
+      if (kb2) ptx::bulk_g2s(srow + i * pitch, J.x + (long long)(g0 + i) * J.rs, (uint32_t)kb2 * 8u, &bar);
+  }
+  for (int i = threadIdx.x; i < OZR_ROWS * OZS_MW; i += 256) smask[i / OZS_MW][i % OZS_MW] = 0u;
+  // zero padding (columns K .. Kp) and dead rows; the odd last column
+  for (int i = threadIdx.x; i < OZR_ROWS * pitch; i += 256) {
+    const int rr = i / pitch, k = i % pitch;
+    if (rr >= nlive) srow[i] = 0.0;
+    else if (k >= kb2) srow[i] = k < J.K ? J.x[(long long)(g0 + rr) * J.rs + k] : 0.0;
+  }
+  __syncthreads();
+  ptx::mbar_wait(&bar, 0);
+  {  // pass 1: row maxima and first nonzero, warps (row w % R, part w / R of 8 / R)
+    constexpr int NP = 8 / OZR_ROWS;
+    const int rr = warp % OZR_ROWS, h = warp / OZR_ROWS;
+    const int part = (J.Kp / NP + 15) & ~15;
+    const int k0 = min(J.Kp, h * part), k1 = h == NP - 1 ? J.Kp : min(J.Kp, (h + 1) * part);
+    const double* row = srow + rr * pitch;
+    double mx = 0.0;
+    int kf = J.K;
+    for (int k = k0 + lane; k < k1; k += 32) {
+      const double x = row[k];
+      mx = fmax(mx, fabs(x));
+      if (x != 0.0) kf = min(kf, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      kf = min(kf, __shfl_xor_sync(0xffffffffu, kf, o));
+    }
+    if (lane == 0) {
+      smx[warp] = mx;
+      skf[warp] = kf;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < OZR_ROWS) {
+    const int t = threadIdx.x;
+    double m = 0.0;
+    int kf = J.K;
+    for (int p = t; p < 8; p += OZR_ROWS) {
+      m = fmax(m, smx[p]);
+      kf = min(kf, skf[p]);
+    }
+    int e = 0;
+    if (m > 0.0) frexp(m, &e);  // |x| 2^-ex < 1
+    sex[t] = e;
+    if (t < nlive) {
+      J.exps[g0 + t] = e;
+      if (J.kfirst) J.kfirst[g0 + t] = kf;
+    }
+  }
+  if (g0 + OZR_ROWS > J.R && threadIdx.x >= OZR_ROWS && threadIdx.x < 2 * OZR_ROWS) {
+    const int t = threadIdx.x - OZR_ROWS;  // padded rows of the operand: exponent 0
+    if (g0 + t >= J.R && g0 + t < J.Rp) J.exps[g0 + t] = 0;
+  }
+  __syncthreads();
+  // pass 2: items (row, 16-column chunk), 8 slices of 16 bytes each
+  const size_t blk = (size_t)J.Rp * OZ_KT;  // bytes of one (k-tile, slice) block
+  const int nch = J.Kp / 16;
+  for (int item = threadIdx.x; item < OZR_ROWS * nch; item += 256) {
+    const int rr = item % OZR_ROWS, ch = item / OZR_ROWS;
+    const int r = g0 + rr, k0 = ch * 16;
+    const int ex = sex[rr];
+    const double2* src = reinterpret_cast<const double2*>(srow + rr * pitch + k0);
+    unsigned w[OZ_S][4];
+    bool nzv = false;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const double2 v0 = src[2 * p], v1 = src[2 * p + 1];
+      const double x4[4] = {v0.x, v0.y, v1.x, v1.y};
+      nzv |= (x4[0] != 0.0) | (x4[1] != 0.0) | (x4[2] != 0.0) | (x4[3] != 0.0);
+      uint32_t o[OZ_S];
+      oz_pack4(x4, ex, o);
+#pragma unroll
+      for (int t = 0; t < OZ_S; ++t) w[t][p] = o[t];
+    }
+    const int kt = k0 / OZ_KT, kc = (k0 % OZ_KT) / 16;
+    const size_t off = (size_t)(r >> 3) * 256 + (size_t)kc * 128 + (size_t)(r & 7) * 16;
+    unsigned any = 0u;
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t) {
+      uint4 v4 = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
+      any |= v4.x | v4.y | v4.z | v4.w;
+      *reinterpret_cast<uint4*>(J.out + ((size_t)kt * OZ_S + t) * blk + off) = v4;
+    }
+    if (J.nz && any) J.nz[(size_t)(r >> 7) * (J.Kp / OZ_KT) + kt] = 1;  // benign race: every writer stores 1
+    if (J.rmask && nzv) atomicOr(&smask[rr][kt >> 5], 1u << (kt & 31));
+  }
+  if (J.rmask) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < nlive * J.mwords; i += 256) {
+      const int rr = i / J.mwords, wi = i % J.mwords;
+      J.rmask[(size_t)(g0 + rr) * J.mwords + wi] = smask[rr][wi];
+    }
+  }
 }
 
 // K tiles of one segment: for the first two segments of a tile whose
@@ -564,6 +726,29 @@ extern "C" int sgf_oz_prof_read(unsigned long long* out, int reset) {
 #endif
 
 // d_group_prefix: per job the first global 8-row group (njobs + 1 entries)
+int oz_split_rows_per_cta(int max_kp) { return max_kp <= 1024 ? 8 : (max_kp <= 2048 ? 4 : 2); }
+template <int R>
+static cudaError_t split_rows_launch(const OzSplitJob* d_jobs, const long long* d_prefix, int njobs, long long ngroups,
+                                     int max_kp, cudaStream_t s) {
+  const size_t smem = (size_t)R * (max_kp + 2) * sizeof(double);
+  static FuncAttrs fa;
+  cudaError_t e = ensure_smem(oz_split_rows_kernel<R>, smem, fa);
+  if (e != cudaSuccess) return e;
+  oz_split_rows_kernel<R><<<(unsigned)ngroups, 256, smem, s>>>(d_jobs, d_prefix, njobs);
+  return cudaGetLastError();
+}
+cudaError_t launch_oz_split_rows(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
+                                 long long total_groups, int max_kp, cudaStream_t s) {
+  if (njobs <= 0 || total_groups <= 0) return cudaSuccess;
+  count_launch();
+  switch (oz_split_rows_per_cta(max_kp)) {
+    case 8: return split_rows_launch<8>(d_jobs, d_group_prefix, njobs, total_groups, max_kp, s);
+    case 4: return split_rows_launch<4>(d_jobs, d_group_prefix, njobs, total_groups, max_kp, s);
+    default: return split_rows_launch<2>(d_jobs, d_group_prefix, njobs, total_groups, max_kp, s);
+  }
+}
+bool oz_split_rows_ok(const OzSplitJob& j) { return j.cs == 1 && j.Kp <= OZR_KMAX && j.R > 0; }
+
 cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_prefix, int njobs,
                             long long total_groups, cudaStream_t s, bool all_rowc) {
   if (njobs <= 0 || total_groups <= 0) return cudaSuccess;

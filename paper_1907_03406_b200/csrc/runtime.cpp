@@ -300,9 +300,30 @@ void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
   for (auto& z : nz_clear) SGF_CUDA(cudaMemsetAsync(z.first, 0, z.second, st));
   nz_clear.clear();
-  // row-contiguous operands (coalesced CTA kernel) and the others, one launch each
+  // row-contiguous operands with aligned rows (rows staged once), other
+  // row-contiguous or row-interleaved operands (coalesced CTA kernel) and the
+  // rest, one launch each
+  static const bool rows_off = getenv("SGF_OZ_SPLIT_ROWS") && atoi(getenv("SGF_OZ_SPLIT_ROWS")) == 0;
+  std::vector<OzSplitJob> rowsj;
   std::vector<OzSplitJob> part[2];
-  for (auto& j : jobs) part[(j.cs == 1 || j.rs == 1) ? 0 : 1].push_back(j);  // the CTA kernel reads both
+  for (auto& j : jobs) {
+    if (!rows_off && oz_split_rows_ok(j)) rowsj.push_back(j);
+    else part[(j.cs == 1 || j.rs == 1) ? 0 : 1].push_back(j);  // the CTA kernel reads both
+  }
+  if (!rowsj.empty()) {
+    int max_kp = 0;
+    for (auto& j : rowsj) max_kp = std::max(max_kp, j.Kp);
+    const int rpc = oz_split_rows_per_cta(max_kp);
+    std::vector<long long> prefix(rowsj.size() + 1, 0);  // groups of rpc rows
+    for (size_t i = 0; i < rowsj.size(); ++i) prefix[i + 1] = prefix[i] + rowsj[i].Rp / rpc;
+    OzSplitJob* d_j = scratch.upload(rowsj);
+    long long* d_p = scratch.upload(prefix);
+    double bytes = 0.0;
+    if (g_prof.on)
+      for (auto& j : rowsj) bytes += 16.0 * j.Rp * j.Kp;
+    ProfScope ps(st, PROF_OZSPLIT, bytes);
+    SGF_CUDA(launch_oz_split_rows(d_j, d_p, (int)rowsj.size(), prefix.back(), max_kp, st));
+  }
   for (int w = 0; w < 2; ++w) {
     auto& js = part[w];
     if (js.empty()) continue;
