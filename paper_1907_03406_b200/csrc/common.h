@@ -70,7 +70,21 @@ struct GemmSeg {
   long long b_rs, b_ks;
   int K;
   int flags;
+  // optional (single-segment tasks): one byte per 64 x 16 tile of A (row tile
+  // i / 64, K chunk k / 16; a_nzk chunks per row tile), nonzero where the tile
+  // holds a nonzero: K steps over all-zero A tiles are skipped (exact zeros)
+  const uint8_t* a_nz = nullptr;
+  int a_nzk = 0;
 };
+// nonzero flags of the 64 x 16 tiles of strided views (gemm_dmma.cu), one per job
+struct NzFlagJob {
+  const double* p;
+  long long rs, cs;
+  int rows, cols;
+  uint8_t* out;  // (rows / 64 rounded up) x (cols / 16 rounded up)
+};
+cudaError_t launch_nz_flags64(const NzFlagJob* d_jobs, const long long* d_tile_prefix, int njobs, long long ntiles,
+                              cudaStream_t s);
 
 struct GemmTask {
   double* C;

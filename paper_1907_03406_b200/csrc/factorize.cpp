@@ -629,6 +629,8 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
         rl_rows += info[qi].c;
       }
   long long fl_chol = 0, fl_e = 0, fl_s = 0;
+  static const bool dmma_skip = !getenv("SGF_NO_DMMA_SKIP");
+  std::vector<NzFlagJob> nzjobs;
   for (size_t qi = 0; qi < info.size(); ++qi) {
     const EI& e = info[qi];
     long long f = (long long)e.m * e.m * e.m / 3;
@@ -648,8 +650,14 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
           OzOperand aop = oz.split(S.scratch, v.p, v.rs, v.cs, v.rows, e.m, true);  // block-sparse A_NB
           oz.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 0.0, {{{aop, xop}, 1.0}}, false, true);
         } else {
-          ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0,
-                 {seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N)});
+          GemmSeg sg = seg(v.p, v.rs, v.cs, e.X, e.ld, 1, e.m, SEG_KLIM_N);
+          if (dmma_skip && e.m <= 8192) {  // block-sparse A_NB: K steps over its all-zero tiles skipped
+            sg.a_nzk = (e.m + 15) / 16;
+            uint8_t* fl = S.scratch.alloc_t<uint8_t>((size_t)((v.rows + 63) / 64) * sg.a_nzk);
+            nzjobs.push_back(NzFlagJob{v.p, v.rs, v.cs, v.rows, e.m, fl});
+            sg.a_nz = fl;
+          }
+          ge.add(e.E + (long long)e.off[q] * e.ld, e.ld, 1, v.rows, e.m, 1.0, 0.0, sg);
         }
       }
       f += (long long)e.m * e.m * rows;
@@ -685,6 +693,13 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     fprintf(stderr, "[sgf] L%d eliminate: %zu nodes, max m %d, flops chol %.3e E %.3e schur %.3e (%s)\n", level,
             info.size(), maxm, (double)fl_chol, (double)fl_e, (double)fl_s,
             use_oz ? "int8-emulated" : (oz_schur ? "E dmma, schur int8-emulated" : "dmma"));
+  if (!nzjobs.empty()) {
+    std::vector<long long> tp(nzjobs.size() + 1, 0);
+    for (size_t i = 0; i < nzjobs.size(); ++i)
+      tp[i + 1] = tp[i] + (long long)((nzjobs[i].rows + 63) / 64) * ((nzjobs[i].cols + 15) / 16);
+    ProfScope ps(st, PROF_MOVE, 0.0);
+    SGF_CUDA(launch_nz_flags64(S.scratch.upload(nzjobs), S.scratch.upload(tp), (int)nzjobs.size(), tp.back(), st));
+  }
   ge.launch(S.scratch, st);
   int *rl_n = nullptr, *rl_k = nullptr;
   double* rl_a = nullptr;

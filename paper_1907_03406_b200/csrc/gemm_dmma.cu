@@ -38,6 +38,8 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
+constexpr int GEMM_KLIST = 512;  // listed K steps (K <= 8192 at BK 16)
+
 template <int BM, int BN, int BK>
 __device__ __forceinline__ void seg_krange(const GemmSeg& S, int m0, int n0, int& kb, int& ke) {
   kb = 0;
@@ -136,11 +138,44 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
 
-  int njobs = 0;
-  for (int s = 0; s < T.nseg; ++s) {
+  // single-segment tasks whose A carries tile flags: the K steps over a
+  // nonzero A tile, listed once in shared memory (all-zero tiles skipped)
+  __shared__ short klist[GEMM_KLIST];
+  __shared__ int klist_n;
+  bool use_list = false;
+  if (T.nseg == 1 && segs[T.seg0].a_nz) {
+    const GemmSeg S0 = segs[T.seg0];
     int kb, ke;
-    seg_krange<BM, BN, BK>(segs[T.seg0 + s], T.m0, T.n0, kb, ke);
-    if (ke > kb) njobs += (ke - kb + BK - 1) / BK;
+    seg_krange<BM, BN, BK>(S0, T.m0, T.n0, kb, ke);
+    const int nsteps = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+    use_list = nsteps <= GEMM_KLIST && BM % 64 == 0;
+    if (use_list && warp == 0) {
+      int cnt = 0;
+      for (int j0 = 0; j0 < nsteps; j0 += 32) {
+        const int j = j0 + lane;
+        bool f = false;
+        if (j < nsteps) {
+          const int k = kb + j * BK, kend = min(ke, k + BK);
+          for (int rt = T.m0 / 64; rt < (T.m0 + BM) / 64; ++rt)
+            for (int c = k / 16; c * 16 < kend; ++c) f |= S0.a_nz[(size_t)rt * S0.a_nzk + c] != 0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) klist[cnt + __popc(m & ((1u << lane) - 1u))] = (short)(kb + j * BK);
+        cnt += __popc(m);
+      }
+      if (lane == 0) klist_n = cnt;
+    }
+    __syncthreads();
+  }
+  int njobs = 0;
+  if (use_list) {
+    njobs = klist_n;
+  } else {
+    for (int s = 0; s < T.nseg; ++s) {
+      int kb, ke;
+      seg_krange<BM, BN, BK>(segs[T.seg0 + s], T.m0, T.n0, kb, ke);
+      if (ke > kb) njobs += (ke - kb + BK - 1) / BK;
+    }
   }
 
   double acc[FM][FN][2];
@@ -170,7 +205,14 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
     }
   };
   next_seg(0);
+  int l_j = 0;  // next job (listed K step) to load
   auto load_stage = [&](int st) {
+    if (use_list) {
+      const int k = klist[l_j++];
+      la.issue(sA0 + st * A_EL * 8, k, l_ke);
+      lb.issue(sB0 + st * B_EL * 8, k, l_ke);
+      return;
+    }
     la.issue(sA0 + st * A_EL * 8, l_k, l_ke);
     lb.issue(sB0 + st * B_EL * 8, l_k, l_ke);
     l_k += BK;
@@ -226,6 +268,43 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
       }
     }
   }
+}
+
+// nonzero flags of 64 x 16 tiles, one warp per tile (32 elements per lane,
+// coalesced along the view's contiguous dimension)
+__global__ void __launch_bounds__(256) nz_flags64_kernel(const NzFlagJob* __restrict__ jobs,
+                                                         const long long* __restrict__ tile_prefix, int njobs) {
+  const long long gt = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gt >= tile_prefix[njobs]) return;
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile_prefix[mid] <= gt) lo = mid;
+    else hi = mid - 1;
+  }
+  const NzFlagJob J = jobs[lo];
+  const int nkc = (J.cols + 15) / 16;
+  const long long t = gt - tile_prefix[lo];
+  const int r0 = (int)(t / nkc) * 64, c0 = (int)(t % nkc) * 16;
+  const bool rowc = J.cs == 1;
+  bool nz = false;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int e = lane + 32 * i;
+    const int r = r0 + (rowc ? e / 16 : e % 64), c = c0 + (rowc ? e % 16 : e / 64);
+    if (r < J.rows && c < J.cols) nz |= J.p[(long long)r * J.rs + (long long)c * J.cs] != 0.0;
+  }
+  nz = __any_sync(0xffffffffu, nz);
+  if (lane == 0) J.out[t] = nz ? 1 : 0;
+}
+
+cudaError_t launch_nz_flags64(const NzFlagJob* d_jobs, const long long* d_tile_prefix, int njobs, long long ntiles,
+                              cudaStream_t s) {
+  if (njobs <= 0 || ntiles <= 0) return cudaSuccess;
+  count_launch();
+  nz_flags64_kernel<<<(unsigned)((ntiles * 32 + 255) / 256), 256, 0, s>>>(d_jobs, d_tile_prefix, njobs);
+  return cudaGetLastError();
 }
 
 template <int BM, int BN, int WM, int WN, int NT, int STAGES, int BK>
