@@ -328,7 +328,11 @@ cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_se
                         cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   static int variant = getenv("SGF_GEMM_VARIANT") ? atoi(getenv("SGF_GEMM_VARIANT")) : 0;
-  if (big_tiles) return launch_cfg<128, 128, 64, 32, 256, 3, 32>(d_tasks, ntasks, d_segs, s);
+  if (big_tiles == 1) return launch_cfg<128, 128, 64, 32, 256, 3, 32>(d_tasks, ntasks, d_segs, s);
+  // narrow products (N <= 16: the compression's basis columns, pi = 4): a
+  // 64 x 16 tile (4 warps of 16 x 16) instead of 64 x 64, 4x less wasted
+  // DMMA work and B traffic per useful column
+  if (big_tiles == 2) return launch_cfg<64, 16, 16, 16, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
   switch (variant) {
     case 1: return launch_cfg<64, 64, 32, 32, 128, 4, 16>(d_tasks, ntasks, d_segs, s);
     case 2: return launch_cfg<64, 64, 32, 32, 128, 3, 16>(d_tasks, ntasks, d_segs, s);

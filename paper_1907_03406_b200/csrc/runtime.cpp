@@ -256,7 +256,7 @@ static int trace_level() {
 // SGF_TRACE=2: time every GEMM launch (synchronising) and print its rate
 static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const GemmSeg* d_segs,
                         const std::vector<GemmSeg>& segs, int big, cudaStream_t st) {
-  const int bm = big ? 128 : 64;
+  const int bm = big == 1 ? 128 : 64;  // (big 2: 64 x 16 tiles; N <= 16 bounds the columns)
   ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(h, segs, bm) : 0.0);
   if (trace_level() != 2) {
     SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
@@ -294,6 +294,7 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
   GemmSeg* d_segs = scratch.upload(segs);
   if (!big.empty()) traced_gemm(scratch.upload(big), big, d_segs, segs, 1, st);
   if (!small.empty()) traced_gemm(scratch.upload(small), small, d_segs, segs, 0, st);
+  if (!narrow.empty()) traced_gemm(scratch.upload(narrow), narrow, d_segs, segs, 2, st);
 }
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {

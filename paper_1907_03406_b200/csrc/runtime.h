@@ -470,7 +470,7 @@ inline View view_of(BlockTable& M, int a, int b) {
 // Batched launch builders
 // ---------------------------------------------------------------------------
 struct GemmBatch {
-  std::vector<GemmTask> big, small;
+  std::vector<GemmTask> big, small, narrow;  // 128x128, 64x64, 64x16 tiles
   std::vector<GemmSeg> segs;
   long long flops = 0;  // executed flops (information)
 
@@ -494,11 +494,13 @@ struct GemmBatch {
     // the 64x64 configuration is the fastest on B200 for every shape measured
     // (tools/gemm_bench.cu); the 128x128 path stays available via force = 1
     bool use_big = force == 1;
-    int bm = use_big ? 128 : 64, bn = bm;
-    auto& dst = use_big ? big : small;
+    static const bool narrow_off = getenv("SGF_NO_NARROW") != nullptr;
+    const bool use_narrow = !use_big && N <= 16 && !narrow_off;  // basis-column products
+    int bm = use_big ? 128 : 64, bn = use_narrow ? 16 : bm;
+    auto& dst = use_big ? big : (use_narrow ? narrow : small);
     for (int m0 = 0; m0 < M; m0 += bm)
       for (int n0 = 0; n0 < N; n0 += bn) {
-        if (lower_only && n0 >= m0 + bm) continue;
+        if (lower_only && n0 >= m0 + bm) continue;  // (64x16 tiles: n0 = 0 < m0 + 64)
         GemmTask t;
         t.C = C;
         t.c_rs = c_rs;
@@ -515,11 +517,12 @@ struct GemmBatch {
       }
     for (int i = 0; i < nsg; ++i) flops += 2LL * M * N * sg[i].K;
   }
-  bool empty() const { return big.empty() && small.empty(); }
+  bool empty() const { return big.empty() && small.empty() && narrow.empty(); }
   void launch(Arena& scratch, cudaStream_t st);
   void clear() {
     big.clear();
     small.clear();
+    narrow.clear();
     segs.clear();
   }
 };
