@@ -436,7 +436,9 @@ void zero_upper(Arena& scratch, cudaStream_t st, const std::vector<TriTask>& tas
 // Recursive split of the large nodes: with W = [A11 .; A21 A22] (lower part),
 //   (L11, X11) = chol_inv(A11);  L21 = A21 X11^T;  A22 -= L21 L21^T;
 //   (L22, X22) = chol_inv(A22);  X21 = -X22 (L21 X11)
-// The three products of each split run on the INT8 tensor cores (ozaki.cu);
+// The products of each split run on the INT8 tensor cores (ozaki.cu), every
+// operand with its nonzero tile flags (A_BB is block-sparse, and so are its
+// factor blocks: the products skip all-zero operand tiles);
 // halves below min_m, and small nodes, take the blocked kernel above.  The
 // pivot floor of every half is the enclosing node's (densela.py:105-110).
 void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCheck* check, int min_m) {
@@ -482,7 +484,7 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
     const CholJob& j = big[i];
     const long long ld = j.ld;
     a21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i], true);  // block-sparse A21
-    x11[i] = oz.split(scratch, j.X, ld, 1, m1[i], m1[i]);
+    x11[i] = oz.split(scratch, j.X, ld, 1, m1[i], m1[i], true);
   }
   oz.launch_splits(scratch, st);
   for (int i = 0; i < nb; ++i) {
@@ -495,7 +497,7 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
   for (int i = 0; i < nb; ++i) {
     const CholJob& j = big[i];
     const long long ld = j.ld;
-    l21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i]);
+    l21[i] = oz.split(scratch, j.W + (long long)m1[i] * ld, ld, 1, m2[i], m1[i], true);
   }
   oz.launch_splits(scratch, st);
   for (int i = 0; i < nb; ++i) {
@@ -523,7 +525,7 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
     const CholJob& j = big[i];
     ldt[i] = pad_ld(m1[i]);
     T[i] = scratch.alloc((size_t)m2[i] * ldt[i]);
-    x11t[i] = oz.split(scratch, j.X, 1, j.ld, m1[i], m1[i]);
+    x11t[i] = oz.split(scratch, j.X, 1, j.ld, m1[i], m1[i], true);
   }
   oz.launch_splits(scratch, st);
   for (int i = 0; i < nb; ++i)
@@ -533,8 +535,8 @@ void chol_inv_rec(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholChec
   for (int i = 0; i < nb; ++i) {
     const CholJob& j = big[i];
     const long long ld = j.ld;
-    x22[i] = oz.split(scratch, j.X + (long long)m1[i] * ld + m1[i], ld, 1, m2[i], m2[i]);
-    tt[i] = oz.split(scratch, T[i], 1, ldt[i], m1[i], m2[i]);
+    x22[i] = oz.split(scratch, j.X + (long long)m1[i] * ld + m1[i], ld, 1, m2[i], m2[i], true);
+    tt[i] = oz.split(scratch, T[i], 1, ldt[i], m1[i], m2[i], true);
   }
   oz.launch_splits(scratch, st);
   for (int i = 0; i < nb; ++i) {
