@@ -23,8 +23,10 @@ CPU reference (never extrapolated): `--impl reference` runs the reference
 package itself (oracle/_ref, built from /root/reference by
 oracle/build_ref.sh) on the full cfg4 problem, one factorize + pcg with one
 BLAS thread, timed as the reference's own harness does (reference
-bench.py:157-166); the GPU arm's `cpu_baseline` runs the same with every
-host core as BLAS threads, after the GPU measurements.
+bench.py:157-166); the GPU arm's `cpu_baseline` is a bounded sample (the
+same package and operator at 40^3 with every host core as BLAS threads,
+after the GPU measurements; `--cpu-baseline full` runs the whole cfg4
+problem instead, ~15 min).
 
 Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sgf|reference]
 N > 1 (torchrun, NCCL): the one 128^3 problem is sharded across the ranks
@@ -425,7 +427,7 @@ def run_sgf(args, ws, rank, local):
     if rank == 0 and ws == 1 and args.cpu_baseline != "none":
         left = BENCH_BUDGET_S - (time.perf_counter() - T_START)
         threads = os.cpu_count() or 1
-        n_sample = None if args.cpu_baseline == "full" else 48
+        n_sample = None if args.cpu_baseline == "full" else 40
         res, err, wall = run_reference_subprocess(CFG, threads, left, n=n_sample)
         if res is not None:
             cpu = {"value": res["t_factor_s"] + res["t_solve_s"], "unit": "s", "cores": threads, "kind": "reference",
@@ -565,9 +567,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sgf", choices=["sgf", "reference"])
-    ap.add_argument("--cpu-baseline", default="full", choices=["full", "sample", "none"],
-                    help="GPU arm's CPU reference leg: the whole cfg4 run on all host cores (default, ~10-15 min), "
-                         "a 48^3 sample, or none")
+    ap.add_argument("--cpu-baseline", default="sample", choices=["full", "sample", "none"],
+                    help="GPU arm's CPU reference leg: a bounded sample, the reference package on the cfg4 "
+                         "operator at 40^3 with all host cores (default, ~15-20 s); the whole cfg4 run on all "
+                         "host cores (~15 min; profiles/r02_bench_cpu_full.jsonl); or none.  The full-size "
+                         "single-thread reference is the --impl reference arm")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-config and IEEE-FP64 lines")
     # code-path checks only (numbers from these are not bench values): another
     # config, gloo collectives, every rank on GPU 0
