@@ -452,9 +452,9 @@ def run_sgf(args, ws, rank, local):
                        "b": c["b"], "rank_tol": c["rank_tol"], "scheme": "nest-2-2", "degree": 1,
                        "pcg_rtol": 1e-12, "parallelism": f"shard{ws}" if ws > 1 else "single",
                        "l2": "inputs and factors (>60 GB) exceed the 126 MB L2",
-                       "fp64_products": "DMMA (mma.sync f64) for nodes < 1024 unknowns; FP64 emulated on the "
-                                        "tcgen05 INT8 tensor cores (Ozaki scheme, 8 x 7-bit slices, 56-bit, exact "
-                                        "int32 accumulation) for larger nodes"},
+                       "fp64_products": "DMMA (mma.sync f64) for nodes < 640 unknowns; FP64 emulated on the "
+                                        "tcgen05 INT8 tensor cores (Ozaki scheme, 8 balanced 8-bit digits, 62-bit, exact "
+                                        "int32 accumulation; all-zero operand tiles skipped) for larger nodes"},
             "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu,
             "ieee_fp64": ieee, "configs": configs,
