@@ -90,9 +90,16 @@ struct GemmTask {
   double* C;
   long long c_rs, c_cs;
   int M, N;      // extents of C (bounds for the tile)
-  int m0, n0;    // tile origin
+  int m0, n0;    // tile origin (set per tile from its GemmTile record)
   int seg0, nseg;
   double alpha, beta;
+};
+// one output tile of a product: the product's GemmTask and the tile's
+// coordinates in units of the launch's tile shape (8 bytes per tile: the
+// host writes one record per tile instead of a whole task)
+struct GemmTile {
+  uint32_t desc;
+  uint16_t mt, nt;
 };
 
 // ---- Cholesky of diagonal tiles ------------------------------------------------
@@ -268,7 +275,7 @@ namespace sgf {
 extern unsigned long long g_kernel_launches;
 inline void count_launch(unsigned long long k = 1) { g_kernel_launches += k; }
 
-cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, int big_tiles,
+cudaError_t launch_gemm(const GemmTask* d_descs, const GemmTile* d_tiles, int ntiles, const GemmSeg* d_segs, int big_tiles,
                         cudaStream_t s);
 cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s);
 cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,

@@ -119,7 +119,8 @@ struct LoadPlan {
 };
 
 template <int BM, int BN, int WM, int WN, int NT, int STAGES, int BK>
-__global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict__ tasks,
+__global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict__ descs,
+                                                      const GemmTile* __restrict__ tiles,
                                                       const GemmSeg* __restrict__ segs) {
   using LA = LoadPlan<BM, BK, NT>;
   using LB = LoadPlan<BN, BK, NT>;
@@ -132,7 +133,11 @@ __global__ void __launch_bounds__(NT) gemm_f64_kernel(const GemmTask* __restrict
   const unsigned sA0 = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned sB0 = sA0 + STAGES * A_EL * 8;
 
-  const GemmTask T = tasks[blockIdx.x];
+  const GemmTile tr = tiles[blockIdx.x];
+  GemmTask Tt = descs[tr.desc];
+  Tt.m0 = (int)tr.mt * BM;
+  Tt.n0 = (int)tr.nt * BN;
+  const GemmTask& T = Tt;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
@@ -308,7 +313,8 @@ cudaError_t launch_nz_flags64(const NzFlagJob* d_jobs, const long long* d_tile_p
 }
 
 template <int BM, int BN, int WM, int WN, int NT, int STAGES, int BK>
-static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, cudaStream_t s) {
+static cudaError_t launch_cfg(const GemmTask* d_descs, const GemmTile* d_tiles, int ntasks, const GemmSeg* d_segs,
+                              cudaStream_t s) {
   constexpr int A_EL = BM * (BK + 4);
   constexpr int B_EL = BN * (BK + 4);
   const size_t smem = (size_t)STAGES * (A_EL + B_EL) * sizeof(double);
@@ -319,34 +325,33 @@ static cudaError_t launch_cfg(const GemmTask* d_tasks, int ntasks, const GemmSeg
   // gridDim.x is limited to 2^31-1; tasks are launched in chunks of 1<<30
   for (int off = 0; off < ntasks; off += (1 << 30)) {
     int cnt = ntasks - off < (1 << 30) ? ntasks - off : (1 << 30);
-    count_launch(); kern<<<cnt, NT, smem, s>>>(d_tasks + off, d_segs);
+    count_launch(); kern<<<cnt, NT, smem, s>>>(d_descs, d_tiles + off, d_segs);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(const GemmTask* d_tasks, int ntasks, const GemmSeg* d_segs, int big_tiles,
-                        cudaStream_t s) {
+cudaError_t launch_gemm(const GemmTask* d_descs, const GemmTile* d_tiles, int ntasks, const GemmSeg* d_segs,
+                        int big_tiles, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   static int variant = getenv("SGF_GEMM_VARIANT") ? atoi(getenv("SGF_GEMM_VARIANT")) : 0;
-  if (big_tiles == 1) return launch_cfg<128, 128, 64, 32, 256, 3, 32>(d_tasks, ntasks, d_segs, s);
+  if (big_tiles == 1) return launch_cfg<128, 128, 64, 32, 256, 3, 32>(d_descs, d_tiles, ntasks, d_segs, s);
   // narrow products (N <= 16: the compression's basis columns, pi = 4): a
   // 64 x 16 tile (4 warps of 16 x 16) instead of 64 x 64, 4x less wasted
   // DMMA work and B traffic per useful column
-  if (big_tiles == 2) return launch_cfg<64, 16, 16, 16, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
+  if (big_tiles == 2) return launch_cfg<64, 16, 16, 16, 128, 2, 16>(d_descs, d_tiles, ntasks, d_segs, s);
   switch (variant) {
-    case 1: return launch_cfg<64, 64, 32, 32, 128, 4, 16>(d_tasks, ntasks, d_segs, s);
-    case 2: return launch_cfg<64, 64, 32, 32, 128, 3, 16>(d_tasks, ntasks, d_segs, s);
-    case 3: return launch_cfg<64, 64, 32, 32, 128, 2, 32>(d_tasks, ntasks, d_segs, s);
-    case 4: return launch_cfg<64, 64, 32, 64, 64, 3, 32>(d_tasks, ntasks, d_segs, s);
-    case 5: return launch_cfg<64, 64, 64, 32, 64, 3, 32>(d_tasks, ntasks, d_segs, s);
-    case 6: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
-    case 7: return launch_cfg<128, 64, 32, 32, 256, 3, 16>(d_tasks, ntasks, d_segs, s);
-    case 8: return launch_cfg<64, 64, 32, 32, 128, 4, 8>(d_tasks, ntasks, d_segs, s);
-    case 9: return launch_cfg<64, 64, 32, 32, 128, 3, 32>(d_tasks, ntasks, d_segs, s);
+    case 1: return launch_cfg<64, 64, 32, 32, 128, 4, 16>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 2: return launch_cfg<64, 64, 32, 32, 128, 3, 16>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 3: return launch_cfg<64, 64, 32, 32, 128, 2, 32>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 4: return launch_cfg<64, 64, 32, 64, 64, 3, 32>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 5: return launch_cfg<64, 64, 64, 32, 64, 3, 32>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 6: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 8: return launch_cfg<64, 64, 32, 32, 128, 4, 8>(d_descs, d_tiles, ntasks, d_segs, s);
+    case 9: return launch_cfg<64, 64, 32, 32, 128, 3, 32>(d_descs, d_tiles, ntasks, d_segs, s);
     // default: 64x64 tile, 4 warps of 32x32, BK=16, 2 stages (41 KB smem -> 4 CTAs
     // = 16 warps per SM): 33.9 TFLOP/s = 91% of the measured DMMA peak on a
     // 7680^2 x 3584 NT problem (tools/gemm_bench.cu)
-    default: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_tasks, ntasks, d_segs, s);
+    default: return launch_cfg<64, 64, 32, 32, 128, 2, 16>(d_descs, d_tiles, ntasks, d_segs, s);
   }
 }
 

@@ -1,6 +1,8 @@
 // Runtime utilities: arena allocator, batched launch builders, and the
 // batched blocked Cholesky + explicit inverse used by elimination,
 // compression and the final dense factor.
+#include <omp.h>
+
 #include "runtime.h"
 
 #include <chrono>
@@ -231,17 +233,20 @@ void chunk_trim() {
 
 // flops the tiles actually multiply (k range per segment after the
 // triangular limits), for the roofline accounting
-static double useful_flops(const std::vector<GemmTask>& ts, const std::vector<GemmSeg>& segs, int bm) {
+static double useful_flops(const GemmBatch::Set& st, const std::vector<GemmSeg>& segs, int bm, int bn,
+                           bool padded = false) {
   double f = 0.0;
-  for (const auto& t : ts) {
-    const int rows = std::min(bm, t.M - t.m0), cols = std::min(bm, t.N - t.n0);
+  for (const auto& tr : st.tiles) {
+    const GemmTask& t = st.desc[tr.desc];
+    const int m0 = tr.mt * bm, n0 = tr.nt * bn;
+    const int rows = padded ? bm : std::min(bm, t.M - m0), cols = padded ? bn : std::min(bn, t.N - n0);
     for (int s = 0; s < t.nseg; ++s) {
       const GemmSeg& g = segs[t.seg0 + s];
       int kb = 0, ke = g.K;
-      if (g.flags & SEG_KLIM_M) ke = std::min(ke, t.m0 + bm);
-      if (g.flags & SEG_KLIM_N) ke = std::min(ke, t.n0 + bm);
-      if (g.flags & SEG_KSTART_M) kb = std::max(kb, t.m0);
-      if (g.flags & SEG_KSTART_N) kb = std::max(kb, t.n0);
+      if (g.flags & SEG_KLIM_M) ke = std::min(ke, m0 + bm);
+      if (g.flags & SEG_KLIM_N) ke = std::min(ke, n0 + bn);
+      if (g.flags & SEG_KSTART_M) kb = std::max(kb, m0);
+      if (g.flags & SEG_KSTART_N) kb = std::max(kb, n0);
       if (ke > kb) f += 2.0 * rows * cols * (ke - kb);
     }
   }
@@ -254,36 +259,35 @@ static int trace_level() {
 }
 
 // SGF_TRACE=2: time every GEMM launch (synchronising) and print its rate
-static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const GemmSeg* d_segs,
+static void traced_gemm(Arena& scratch, const GemmBatch::Set& h, const GemmSeg* d_segs,
                         const std::vector<GemmSeg>& segs, int big, cudaStream_t st) {
-  const int bm = big == 1 ? 128 : 64;  // (big 2: 64 x 16 tiles; N <= 16 bounds the columns)
-  ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(h, segs, bm) : 0.0);
+  const int bm = big == 1 ? 128 : 64, bn = big == 1 ? 128 : (big == 2 ? 16 : 64);
+  ProfScope ps(st, PROF_GEMM, g_prof.on ? useful_flops(h, segs, bm, bn) : 0.0);
+  const GemmTask* d_desc = scratch.upload(h.desc);
+  const GemmTile* d_tiles = scratch.upload(h.tiles);
+  const int nt = (int)h.tiles.size();
   if (trace_level() != 2) {
-    SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
+    SGF_CUDA(launch_gemm(d_desc, d_tiles, nt, d_segs, big, st));
     return;
   }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a, st);
-  SGF_CUDA(launch_gemm(d, (int)h.size(), d_segs, big, st));
+  SGF_CUDA(launch_gemm(d_desc, d_tiles, nt, d_segs, big, st));
   cudaEventRecord(b, st);
   cudaEventSynchronize(b);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
-  const double f = useful_flops(h, segs, bm);
-  // executed: full bm x bm tiles over the same K ranges (padding included)
-  std::vector<GemmTask> hp(h);
-  for (auto& t : hp) {
-    t.M = t.m0 + bm;
-    t.N = t.n0 + bm;
-  }
-  const double fx = useful_flops(hp, segs, bm);
+  const double f = useful_flops(h, segs, bm, bn);
+  const double fx = useful_flops(h, segs, bm, bn, true);  // executed: full tiles over the same K ranges
   long long ksum = 0;
-  for (auto& t : h)
+  for (auto& tr : h.tiles) {
+    const GemmTask& t = h.desc[tr.desc];
     for (int s = 0; s < t.nseg; ++s) ksum += segs[t.seg0 + s].K;
-  fprintf(stderr, "[gemm] %s tiles=%7zu avgK=%7.0f gflop=%9.3f ms=%8.3f tflops=%6.2f executed/useful=%5.2f\n",
-          big ? "128" : " 64", h.size(), h.empty() ? 0.0 : (double)ksum / h.size(), f / 1e9, ms,
+  }
+  fprintf(stderr, "[gemm] %s tiles=%7d avgK=%7.0f gflop=%9.3f ms=%8.3f tflops=%6.2f executed/useful=%5.2f\n",
+          big == 1 ? "128" : (big == 2 ? " 16" : " 64"), nt, nt ? (double)ksum / nt : 0.0, f / 1e9, ms,
           f / (ms * 1e-3) / 1e12, fx / std::max(f, 1.0));
   cudaEventDestroy(a);
   cudaEventDestroy(b);
@@ -292,9 +296,9 @@ static void traced_gemm(const GemmTask* d, const std::vector<GemmTask>& h, const
 void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
   if (empty()) return;
   GemmSeg* d_segs = scratch.upload(segs);
-  if (!big.empty()) traced_gemm(scratch.upload(big), big, d_segs, segs, 1, st);
-  if (!small.empty()) traced_gemm(scratch.upload(small), small, d_segs, segs, 0, st);
-  if (!narrow.empty()) traced_gemm(scratch.upload(narrow), narrow, d_segs, segs, 2, st);
+  if (!big.empty()) traced_gemm(scratch, big, d_segs, segs, 1, st);
+  if (!small.empty()) traced_gemm(scratch, small, d_segs, segs, 0, st);
+  if (!narrow.empty()) traced_gemm(scratch, narrow, d_segs, segs, 2, st);
 }
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
@@ -624,12 +628,30 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
     tk[i] = scratch.alloc((size_t)64 * std::max(jobs[i].m, 1));
   }
 
+  // task lists of a panel built by host threads over contiguous job ranges,
+  // concatenated in range order (3375 level-1 nodes at 128^3: the serial
+  // loop kept the device waiting)
+  const int nthr = std::max(1, std::min(omp_get_max_threads(), nj / 8));
+  double t_build = 0.0, t_launch = 0.0;
   for (int k0 = 0; k0 < mmax; k0 += 64) {
+    auto tb0 = std::chrono::steady_clock::now();
     GemmBatch ga, gc;
     std::vector<DiagTask> dt;
     std::vector<double*> xd;
     std::vector<int> xl;
-    for (int i = 0; i < nj; ++i) {
+    std::vector<GemmBatch> tga(nthr), tgc(nthr);
+    std::vector<std::vector<DiagTask>> tdt(nthr);
+    std::vector<std::vector<double*>> txd(nthr);
+    std::vector<std::vector<int>> txl(nthr);
+#pragma omp parallel for num_threads(nthr) schedule(static, 1)
+    for (int th = 0; th < nthr; ++th) {
+      GemmBatch& ga = tga[th];
+      GemmBatch& gc = tgc[th];
+      std::vector<DiagTask>& dt = tdt[th];
+      std::vector<double*>& xd = txd[th];
+      std::vector<int>& xl = txl[th];
+      const int i0 = (int)((long long)nj * th / nthr), i1 = (int)((long long)nj * (th + 1) / nthr);
+    for (int i = i0; i < i1; ++i) {
       const int m = jobs[i].m;
       const long long ld = jobs[i].ld;
       if (m <= k0) continue;
@@ -666,6 +688,16 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
       if (k0 > 0)
         gc.add(X + k0 * ld, ld, 1, nb, k0, -1.0, 0.0, {seg(dinv[i], 64, 1, tk[i], 1, m, nb, SEG_KLIM_M)}, 0);
     }
+    }
+    for (int th = 0; th < nthr; ++th) {
+      ga.append(tga[th]);
+      gc.append(tgc[th]);
+      dt.insert(dt.end(), tdt[th].begin(), tdt[th].end());
+      xd.insert(xd.end(), txd[th].begin(), txd[th].end());
+      xl.insert(xl.end(), txl[th].begin(), txl[th].end());
+    }
+    auto tb1 = std::chrono::steady_clock::now();
+    t_build += std::chrono::duration<double, std::milli>(tb1 - tb0).count();
     ga.launch(scratch, st);
     {
       DiagTask* d_dt = scratch.upload(dt);
@@ -675,7 +707,11 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
       SGF_CUDA(launch_diag_chol_ex(d_dt, (int)dt.size(), d_status, d_piv, d_xd, d_xl, st));
     }
     gc.launch(scratch, st);
+    t_launch += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb1).count();
   }
+  if (HostTimer::on())
+    fprintf(stderr, "[host] chol_inv_batch: %d jobs, %d threads, task build %.2f ms, uploads+launches %.2f ms\n", nj,
+            nthr, t_build, t_launch);
   std::vector<TriTask> tri;
   for (auto& j : jobs)
     if (!j.upper_zero) tri.push_back(TriTask{j.W, j.m, j.ld});

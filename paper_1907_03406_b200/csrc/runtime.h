@@ -470,7 +470,18 @@ inline View view_of(BlockTable& M, int a, int b) {
 // Batched launch builders
 // ---------------------------------------------------------------------------
 struct GemmBatch {
-  std::vector<GemmTask> big, small, narrow;  // 128x128, 64x64, 64x16 tiles
+  // per tile shape (128x128, 64x64, 64x16): the products and one 8-byte
+  // record per output tile
+  struct Set {
+    std::vector<GemmTask> desc;
+    std::vector<GemmTile> tiles;
+    bool empty() const { return tiles.empty(); }
+    void clear() {
+      desc.clear();
+      tiles.clear();
+    }
+  };
+  Set big, small, narrow;
   std::vector<GemmSeg> segs;
   long long flops = 0;  // executed flops (information)
 
@@ -497,27 +508,47 @@ struct GemmBatch {
     static const bool narrow_off = getenv("SGF_NO_NARROW") != nullptr;
     const bool use_narrow = !use_big && N <= 16 && !narrow_off;  // basis-column products
     int bm = use_big ? 128 : 64, bn = use_narrow ? 16 : bm;
-    auto& dst = use_big ? big : (use_narrow ? narrow : small);
-    for (int m0 = 0; m0 < M; m0 += bm)
-      for (int n0 = 0; n0 < N; n0 += bn) {
-        if (lower_only && n0 >= m0 + bm) continue;  // (64x16 tiles: n0 = 0 < m0 + 64)
-        GemmTask t;
-        t.C = C;
-        t.c_rs = c_rs;
-        t.c_cs = c_cs;
-        t.M = M;
-        t.N = N;
-        t.m0 = m0;
-        t.n0 = n0;
-        t.seg0 = seg0;
-        t.nseg = nsg;
-        t.alpha = alpha;
-        t.beta = beta;
-        dst.push_back(t);
+    Set& dst = use_big ? big : (use_narrow ? narrow : small);
+    GemmTask t;
+    t.C = C;
+    t.c_rs = c_rs;
+    t.c_cs = c_cs;
+    t.M = M;
+    t.N = N;
+    t.m0 = 0;
+    t.n0 = 0;
+    t.seg0 = seg0;
+    t.nseg = nsg;
+    t.alpha = alpha;
+    t.beta = beta;
+    const uint32_t di = (uint32_t)dst.desc.size();
+    dst.desc.push_back(t);
+    const int ntm = (M + bm - 1) / bm, ntn = (N + bn - 1) / bn;
+    for (int mt = 0; mt < ntm; ++mt)
+      for (int nt = 0; nt < ntn; ++nt) {
+        if (lower_only && nt * bn >= (mt + 1) * bm) continue;  // (64x16 tiles: n0 = 0 < m0 + 64)
+        dst.tiles.push_back(GemmTile{di, (uint16_t)mt, (uint16_t)nt});
       }
     for (int i = 0; i < nsg; ++i) flops += 2LL * M * N * sg[i].K;
   }
   bool empty() const { return big.empty() && small.empty() && narrow.empty(); }
+  // append another batch's products (segment and product indices shifted past ours)
+  void append(const GemmBatch& o) {
+    const int off = (int)segs.size();
+    segs.insert(segs.end(), o.segs.begin(), o.segs.end());
+    auto cat = [off](Set& d, const Set& src) {
+      const uint32_t doff = (uint32_t)d.desc.size();
+      const size_t b = d.desc.size(), bt = d.tiles.size();
+      d.desc.insert(d.desc.end(), src.desc.begin(), src.desc.end());
+      for (size_t i = b; i < d.desc.size(); ++i) d.desc[i].seg0 += off;
+      d.tiles.insert(d.tiles.end(), src.tiles.begin(), src.tiles.end());
+      for (size_t i = bt; i < d.tiles.size(); ++i) d.tiles[i].desc += doff;
+    };
+    cat(big, o.big);
+    cat(small, o.small);
+    cat(narrow, o.narrow);
+    flops += o.flops;
+  }
   void launch(Arena& scratch, cudaStream_t st);
   void clear() {
     big.clear();

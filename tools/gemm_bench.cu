@@ -31,22 +31,32 @@ __global__ void dmma_rate(double* out, int iters) {
 }
 
 static float time_gemm(std::vector<GemmTask>& tasks, std::vector<GemmSeg>& segs, int big, int reps) {
-  GemmTask* dt; GemmSeg* ds;
+  // one product per task, one tile record per task (tile coordinates from
+  // the task's origin, in units of the launch's tile shape)
+  const int bm = big == 1 ? 128 : 64, bn = big == 1 ? 128 : (big == 2 ? 16 : 64);
+  std::vector<GemmTile> tiles(tasks.size());
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    tiles[i] = GemmTile{(uint32_t)i, (uint16_t)(tasks[i].m0 / bm), (uint16_t)(tasks[i].n0 / bn)};
+    tasks[i].m0 = tasks[i].n0 = 0;
+  }
+  GemmTask* dt; GemmSeg* ds; GemmTile* dtl;
   cudaMalloc(&dt, tasks.size() * sizeof(GemmTask));
+  cudaMalloc(&dtl, tiles.size() * sizeof(GemmTile));
   cudaMalloc(&ds, segs.size() * sizeof(GemmSeg));
   cudaMemcpy(dt, tasks.data(), tasks.size() * sizeof(GemmTask), cudaMemcpyHostToDevice);
+  cudaMemcpy(dtl, tiles.data(), tiles.size() * sizeof(GemmTile), cudaMemcpyHostToDevice);
   cudaMemcpy(ds, segs.data(), segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice);
-  launch_gemm(dt, (int)tasks.size(), ds, big, 0);
+  launch_gemm(dt, dtl, (int)tasks.size(), ds, big, 0);
   cudaDeviceSynchronize();
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   float best = 1e30f;
   for (int r = 0; r < reps; r++) {
     cudaEventRecord(a);
-    launch_gemm(dt, (int)tasks.size(), ds, big, 0);
+    launch_gemm(dt, dtl, (int)tasks.size(), ds, big, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
   }
-  cudaFree(dt); cudaFree(ds);
+  cudaFree(dt); cudaFree(ds); cudaFree(dtl);
   return best;
 }
 
