@@ -164,9 +164,10 @@ int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap);  /* ret
 int sgf_precond_num_factors(const sgf_precond* p);
 
 /* Measurement helper (bench.py's apply roofline; no reference counterpart):
- * bytes of the stored couplings E per sweep, out[0] dense (sum c*m*8) and
- * out[1] in the 32-column tiles that hold a nonzero -- the part the apply
- * kernels stream (all-zero tiles are skipped; apply.cpp).  Synchronises. */
+ * bytes per sweep of the stored couplings E and of the L^{-1} triangles that
+ * carry tile masks, out[0] dense (c*m*8, and m(m+1)/2*8) and out[1] in the
+ * 32-column tiles that hold a nonzero -- the part the apply kernels stream
+ * (all-zero tiles are skipped; apply.cpp).  Synchronises. */
 int sgf_precond_coupling_bytes(const sgf_precond* p, double* out);
 /* info[0..7] = type, node, m (idx size), c (coupling rows), retained, level, reflectors, QR columns */
 int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info);

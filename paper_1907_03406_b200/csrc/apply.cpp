@@ -38,6 +38,7 @@ struct Group {
   int nb1 = 0;
   int b1_mode = 1;  // 2: every task carries the rows' leading-zero offsets (gemv_t_lead_kernel)
   int f2_mode = 0;  // 3: the couplings' rows are block-sparse (task.kfirst / task.rmask)
+  int f1_mode = 0, b2_mode = 1;  // 3 / 2: L^{-1}'s rows carry tile masks
   RedSeg* red1 = nullptr;
   int nred1 = 0, maxn1 = 0;
   GemvTask* bwd2 = nullptr;
@@ -239,8 +240,13 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       const Factor& f = *fs[i];
       for (auto u : f.idx) idx.push_back((int)u);
       const int tri = (g.type != SGF_FACTOR_COMPRESSION);
-      if (tri && g.gn_rows == GN_ROWS) add_gemv_tri_pairs(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m);
-      else add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
+      if (f.xmask) {  // block-sparse L^{-1} rows: zero tiles skipped (rows taken dynamically)
+        add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, 1, g.gn_rows, f.xkfirst, f.xmask, f.xmw);
+      } else if (tri && g.gn_rows == GN_ROWS) {
+        add_gemv_tri_pairs(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m);
+      } else {
+        add_gemv_n(f1, f.inv, f.ld, g.xb + om, g.zb + om, f.m, f.m, tri, g.gn_rows);
+      }
       if (g.type == SGF_FACTOR_ELIMINATION) {
         for (auto u : f.nidx) nidx.push_back((int)u);
         if (f.c > 0) add_gemv_n(f2, f.E, f.ld, g.zb + om, g.t + oc, f.c, f.m, 0, g.gn_rows, f.ekfirst, f.emask, f.emw);
@@ -249,8 +255,12 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
                                        f.emask, f.emw)
                           : 0;
         r1.push_back(RedSeg{g.part + op, g.xb + om, g.acc + om, f.m, nrb, f.m, -1.0});
-        // second stage reuses the partial buffer after red1 consumed it
-        int nrb2 = add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1, g.gt_rows);
+        // second stage reuses the partial buffer after red1 consumed it (masked
+        // L^{-1}: every row of the square with its tile mask; the zero upper
+        // triangle is skipped by the mask)
+        int nrb2 = f.xmask ? add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 0, g.gt_rows, f.xkfirst,
+                                        f.xmask, f.xmw)
+                           : add_gemv_t(b2, f.inv, f.ld, g.acc + om, g.part + op, f.m, f.m, 1, g.gt_rows);
         r2.push_back(RedSeg{g.part + op, nullptr, g.zb + om, f.m, nrb2, f.m, 1.0});
         op += std::max<long long>(nrb, nrb2) * f.m;
       } else {
@@ -302,7 +312,12 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       if (r2n) g.lpr2 = lanes_for(g.bytes_f2 / 16.0 / r2n);
     }
     g.bytes_b1 = gemv_bytes(b1, 1);
-    g.bytes_b2 = gemv_bytes(b2, 1);
+    {  // (masked L^{-1} tasks run over the square; their dense work is the triangle)
+      std::vector<GemvTask> tb(b2);
+      for (auto& t : tb)
+        if (t.rmask) t.tri = 1;
+      g.bytes_b2 = gemv_bytes(tb, 1);
+    }
     g.fwd1 = plan->mem.upload(f1);
     g.nf1 = (int)f1.size();
     g.fwd2 = plan->mem.upload(f2);
@@ -316,6 +331,12 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       bool sp = !f2.empty();
       for (const auto& t : f2) sp = sp && (t.kfirst || t.rmask);
       g.f2_mode = sp ? 3 : 0;
+      bool s1 = !f1.empty(), s2 = !b2.empty();
+      for (const auto& t : f1) s1 = s1 && t.rmask;
+      for (const auto& t : b2) s2 = s2 && t.rmask && t.r1 - t.r0 <= GT_ROWS;
+      g.f1_mode = s1 ? 3 : 0;
+      g.b2_mode = s2 ? 2 : 1;
+      if (s1) g.lpr1 = 64;  // the bulk-copy kernel with dynamic rows
     }
     g.bwd2 = plan->mem.upload(b2);
     g.nb2 = (int)b2.size();
@@ -410,7 +431,7 @@ static void backward_group_sym(const L1Couplings& c, const Group& g, double* y, 
 static void forward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_t st) {
   (void)pl;
   SGF_CUDA(launch_gather(y, g.idx, g.xb, g.nm, st));
-  gemv(g.fwd1, g.nf1, 0, g.bytes_f1, st, g.lpr1);
+  gemv(g.fwd1, g.nf1, g.f1_mode, g.bytes_f1, st, g.lpr1);
   if (g.type == SGF_FACTOR_ELIMINATION) gemv(g.fwd2, g.nf2, g.f2_mode, g.bytes_f2, st, g.lpr2);
   SGF_CUDA(launch_scatter(g.zb, g.idx, y, g.nm, st));
   if (g.type == SGF_FACTOR_ELIMINATION) SGF_CUDA(launch_combine(y, g.tgt, g.tptr, g.tpos, g.t, g.ntgt, st));
@@ -423,7 +444,7 @@ static void backward_group(ApplyPlan* pl, const Group& g, double* y, cudaStream_
     SGF_CUDA(launch_gather(y, g.nidx, g.xn, g.nc, st));
     gemv(g.bwd1, g.nb1, g.b1_mode, g.bytes_b1, st);
     SGF_CUDA(launch_reduce_parts(g.red1, g.nred1, g.maxn1, st));
-    gemv(g.bwd2, g.nb2, 1, g.bytes_b2, st);
+    gemv(g.bwd2, g.nb2, g.b2_mode, g.bytes_b2, st);
     SGF_CUDA(launch_reduce_parts(g.red2, g.nred2, g.maxn2, st, y));  // + scatter into y
   } else {
     gemv(g.bwd1, g.nb1, g.b1_mode, g.bytes_b1, st);

@@ -415,8 +415,9 @@ __global__ void __launch_bounds__(256, 2) gemv_n_bulk_sparse_kernel(const GemvTa
       const int r = atomicAdd(&next_row, 1);
       if (r < nr) {
         prow = r;
-        pstart = T.kfirst ? min(T.kfirst[T.r0 + r], T.c1) & ~31 : 0;
-        plen = T.c1 - pstart;
+        const int rlen = T.tri ? min(T.c1, T.r0 + r + 1) : T.c1;  // lower-triangular rows end at the diagonal
+        pstart = T.kfirst ? min(T.kfirst[T.r0 + r], rlen) & ~31 : 0;
+        plen = rlen - pstart;
         poff = 0;
         skip();
         have = true;

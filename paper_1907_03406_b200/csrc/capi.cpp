@@ -155,6 +155,20 @@ int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) {
         nz += 8.0 * f.c * f.m;
       }
     }
+    // L^{-1} rows with tile masks: the lower triangle (dense) against its
+    // nonzero tiles, each tile counted up to the diagonal
+    for (const Factor& f : p->p->factors) {
+      if (!f.xmask) continue;
+      dense += 4.0 * f.m * (f.m + 1.0);
+      mk.resize((size_t)f.m * f.xmw);
+      SGF_CUDA(cudaMemcpy(mk.data(), f.xmask, mk.size() * 4, cudaMemcpyDeviceToHost));
+      for (int r = 0; r < f.m; ++r)
+        for (int w = 0; w < f.xmw; ++w) {
+          const uint32_t b = mk[(size_t)r * f.xmw + w];
+          for (int t = 0; t < 32; ++t)
+            if ((b >> t) & 1u) nz += 8.0 * std::max(0, std::min(32, r + 1 - 32 * (32 * w + t)));
+        }
+    }
     out[0] = dense;
     out[1] = nz;
   });

@@ -630,12 +630,26 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       }
   long long fl_chol = 0, fl_e = 0, fl_s = 0;
   static const bool dmma_skip = !getenv("SGF_NO_DMMA_SKIP");
+  std::vector<int*> xkf(info.size(), nullptr);
+  std::vector<uint32_t*> xmk(info.size(), nullptr);
+  std::vector<int> xmw(info.size(), 0);
   std::vector<NzFlagJob> nzjobs;
   for (size_t qi = 0; qi < info.size(); ++qi) {
     const EI& e = info[qi];
     long long f = (long long)e.m * e.m * e.m / 3;
     OzOperand xop;
-    if (use_oz && own[qi]) xop = oz.split(S.scratch, e.X, e.ld, 1, e.m, e.m);
+    if (use_oz && own[qi]) {
+      // L^{-1}'s rows: first nonzero column and 32-column tile masks for the
+      // apply (the interior's diagonal block is block-sparse, and so is its
+      // inverse factor below the diagonal)
+      if (S.ekfirst && e.m <= 16384) {
+        const int mw = (e.m + 1023) / 1024;
+        xkf[qi] = P->store.alloc_t<int>(e.m);
+        xmk[qi] = P->store.alloc_t<uint32_t>((size_t)e.m * mw);
+        xmw[qi] = mw;
+      }
+      xop = oz.split(S.scratch, e.X, e.ld, 1, e.m, e.m, false, xkf[qi], xmk[qi], xmw[qi]);
+    }
     for (size_t q = 0; q < e.nb.size(); ++q) {
       const int rows = M.size[e.nb[q]];
       if (own[qi]) {
@@ -947,6 +961,9 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       f.ekfirst = ekf[q];
       f.emask = emk[q];
       f.emw = emk[q] ? emw : 0;
+      f.xkfirst = xkf[q];
+      f.xmask = xmk[q];
+      f.xmw = xmw[q];
       if (Gall) f.G = Gall + (e.X - Xall);
     }
     // replay the reference sequence for the table and its byte accounting:

@@ -25,6 +25,9 @@ struct Factor {
                               // L^{-T} upper triangular keeps the leading zero columns of A_NB's rows)
   uint32_t* emask = nullptr;  // per row of E: bit t = 32-column tile t holds a nonzero (emw words per row;
   int emw = 0;                // E is block-sparse: zero runs at the interior's pieces, not only leading)
+  int* xkfirst = nullptr;     // the same for the rows of L^{-1} (when its operand split recorded them:
+  uint32_t* xmask = nullptr;  // the emulated levels), emw words per row
+  int xmw = 0;
   double* V = nullptr;        // m x steps reflectors (column-major, unit lower trapezoid)
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator
