@@ -631,7 +631,7 @@ void chol_inv_batch(Ctx& ctx, Arena& scratch, std::vector<CholJob>& jobs, CholCh
   // task lists of a panel built by host threads over contiguous job ranges,
   // concatenated in range order (3375 level-1 nodes at 128^3: the serial
   // loop kept the device waiting)
-  const int nthr = std::max(1, std::min(omp_get_max_threads(), nj / 8));
+  const int nthr = nj >= 1024 ? std::max(1, std::min(omp_get_max_threads(), nj / 64)) : 1;
   double t_build = 0.0, t_launch = 0.0;
   for (int k0 = 0; k0 < mmax; k0 += 64) {
     auto tb0 = std::chrono::steady_clock::now();
