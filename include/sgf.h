@@ -169,6 +169,8 @@ int sgf_precond_num_factors(const sgf_precond* p);
  * 32-column tiles that hold a nonzero -- the part the apply kernels stream
  * (all-zero tiles are skipped; apply.cpp).  Synchronises. */
 int sgf_precond_coupling_bytes(const sgf_precond* p, double* out);
+/* the same restricted to the factors of one level (level >= 1; 0: all) */
+int sgf_precond_coupling_bytes_level(const sgf_precond* p, int level, double* out);
 /* info[0..7] = type, node, m (idx size), c (coupling rows), retained, level, reflectors, QR columns */
 int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info);
 /* what: 0 idx (int64 m), 1 L (m*m), 2 couplings E (c*m), 3 coupling idx (int64 c),

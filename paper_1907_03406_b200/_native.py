@@ -30,7 +30,7 @@ SOLVE_FORWARD, SOLVE_TRANSPOSE, MULT_TRANSPOSE, MULT_FORWARD = range(4)
 EXPORTS = (
     "sgf_create", "sgf_destroy", "sgf_last_error", "sgf_stream", "sgf_sync", "sgf_factorize",
     "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
-    "sgf_precond_num_factors", "sgf_precond_coupling_bytes", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
+    "sgf_precond_num_factors", "sgf_precond_coupling_bytes", "sgf_precond_coupling_bytes_level", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read", "sgf_pcg_ops", "sgf_memcpy",
@@ -115,6 +115,7 @@ def load_library(path=LIB_PATH):
             "sgf_precond_rank_trace": (i32, [vp, vp, i32]),
             "sgf_precond_num_factors": (i32, [vp]),
             "sgf_precond_coupling_bytes": (i32, [vp, vp]),
+            "sgf_precond_coupling_bytes_level": (i32, [vp, i32, vp]),
             "sgf_precond_factor_info": (i32, [vp, i32, vp]),
             "sgf_precond_factor_copy": (i32, [vp, i32, i32, vp, i64]),
             "sgf_apply": (i32, [vp, i32, vp, vp, i32]),

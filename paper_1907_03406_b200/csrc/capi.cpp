@@ -127,7 +127,9 @@ int sgf_precond_rank_trace(const sgf_precond* p, int32_t* out, int cap) {
 
 int sgf_precond_num_factors(const sgf_precond* p) { return p ? (int)p->p->factors.size() : 0; }
 
-int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) {
+int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) { return sgf_precond_coupling_bytes_level(p, 0, out); }
+
+int sgf_precond_coupling_bytes_level(const sgf_precond* p, int level, double* out) {
   if (!p || !out) return SGF_INVALID_ARG;
   sgf_ctx* ctx = p->ctx;
   return guarded(ctx, [&] {
@@ -136,7 +138,7 @@ int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) {
     std::vector<uint32_t> mk;
     std::vector<int> kf;
     for (const Factor& f : p->p->factors) {
-      if (f.type != SGF_FACTOR_ELIMINATION || !f.E || f.c <= 0) continue;
+      if (f.type != SGF_FACTOR_ELIMINATION || !f.E || f.c <= 0 || (level > 0 && f.level != level)) continue;
       dense += 8.0 * f.c * f.m;
       if (f.emask) {
         mk.resize((size_t)f.c * f.emw);
@@ -158,7 +160,7 @@ int sgf_precond_coupling_bytes(const sgf_precond* p, double* out) {
     // L^{-1} rows with tile masks: the lower triangle (dense) against its
     // nonzero tiles, each tile counted up to the diagonal
     for (const Factor& f : p->p->factors) {
-      if (!f.xmask) continue;
+      if (!f.xmask || (level > 0 && f.level != level)) continue;
       dense += 4.0 * f.m * (f.m + 1.0);
       mk.resize((size_t)f.m * f.xmw);
       SGF_CUDA(cudaMemcpy(mk.data(), f.xmask, mk.size() * 4, cudaMemcpyDeviceToHost));
