@@ -443,42 +443,34 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
 // Shared-memory resident variant (the panels of the compression levels fit a
 // 16-CTA cluster: m x c <= 1225 x 184 at 128^3 -> ~118 KB per CTA).  CTA q
 // holds the ORIGINAL columns cj == q (mod QC) in its shared memory for the
-// whole factorization, so a step touches no global memory:
-//   B1  cluster barrier: the updates and candidates of step k-1 are final;
-//       every CTA reads the 16 candidates (DSMEM) and picks the pivot (first
-//       maximum by position, or the replayed column) and applies the position
-//       swap to its copy of the position <-> column maps;
-//   the owner of the pivot column forms the reflector (norm, sign, tau) in its
-//   reflector buffer;
-//   B2  cluster barrier: every CTA copies the reflector (DSMEM) and updates its
-//       unpivoted columns (dot, axpy, norm downdate), then forms its candidate
-//       for step k+1; the owner stores R_kk and the reflector into the column.
+// whole factorization, so a step touches no global memory, and a step costs
+// ONE cluster barrier:
+//   B   cluster barrier: the updates and candidates of step k-1 are final.
+//       A candidate carries the column's downdated norm^2 (the pivot rule),
+//       its exact norm^2 below row k (from the previous update's sweep) and
+//       its row-k entry, so every CTA picks the pivot (first maximum by
+//       position, or the replayed column), applies the position swap to its
+//       copy of the position <-> column maps and forms the reflector scalars
+//       (sign, u1, tau, R_kk) itself -- identical inputs, identical values.
+//       Every CTA then reads the pivot column from the owner (DSMEM) scaled
+//       by 1/u1 as the reflector, updates its unpivoted columns (dot, axpy,
+//       norm downdate, exact norm^2 below row k+1) and forms its candidate
+//       for step k+1.  The owner rewrites the pivot column as R_kk + the
+//       reflector after the NEXT barrier (nobody reads it remotely again).
 // Per-column arithmetic and reduction orders are those of the kernels above
-// (lane-strided FMA chains + warp_sum; block sums in fixed warp order).  At
-// the end every CTA writes its columns to their final positions in N.
+// (lane-strided FMA chains + warp_sum).  At the end every CTA writes its
+// columns to their final positions in N.
 // ---------------------------------------------------------------------------
 struct QsCand {
-  double v;   // comparison value (downdated norm^2, or 1 for the replayed column)
-  double n2;  // the column's norm^2
-  int pos;    // position (c: none)
-};
-struct QsPiv {
-  double tau, rkk, xn;
-  int stop;
+  double v;    // comparison value (downdated norm^2, or 1 for the replayed column)
+  double n2;   // the column's downdated norm^2
+  double xn2;  // the column's exact norm^2 below row k
+  double x0;   // the column's row-k entry
+  int pos;     // position (c: none)
 };
 constexpr int QST = 384;          // threads of the shared-memory variant: one warp per owned column
 constexpr int QSW = QST / 32;
-constexpr int QS_VCH = 4;         // reflector copy: 16-byte loads in flight per thread
-__device__ double sblock_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < QSW; ++i) s += red[i];
-  return s;
-}
+constexpr int QS_VCH = 4;         // reflector copy: remote loads in flight per thread
 template <int CS>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
     qrcp_smem_kernel(const QrTask* __restrict__ tasks, int cpc) {
@@ -488,24 +480,24 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
   __shared__ double red[QSW];
   __shared__ QsCand cand[2];
   __shared__ QsCand sel;
-  __shared__ QsPiv piv_s;
+  __shared__ int sel_pc;
   __shared__ double s_amax;
   __shared__ double wv[QSW];
-  __shared__ int wi[QSW];
+  __shared__ int wi[QSW], wl[QSW];
   const int q = (int)cluster.block_rank();
   const QrTask T = tasks[blockIdx.x / CS];
   const int m = T.m, c = T.c, kmax = min(m, c);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double eps = DBL_EPSILON;
-  // layout: cpc owned columns (m each) | reflector buffer (m) | local reflector (m) | nrm2, ref2 (cpc each)
+  // layout: cpc owned columns (m each) | local reflector (m) | nrm2, ref2, fn2 (cpc each)
   //         | col_of (c) | pos_of (c) | done (cpc)
   const int mp = (m + 1) & ~1;  // column stride: every buffer 16-byte aligned
   double* cols = qs;
-  double* vbuf = cols + (size_t)cpc * mp;
-  double* vloc = vbuf + mp;
+  double* vloc = cols + (size_t)cpc * mp;
   double* nrm2 = vloc + mp;
   double* ref2 = nrm2 + cpc;
-  int* col_of = reinterpret_cast<int*>(ref2 + cpc);
+  double* fn2 = ref2 + cpc;
+  int* col_of = reinterpret_cast<int*>(fn2 + cpc);
   int* pos_of = col_of + c;
   int* done = pos_of + c;
   const int nown = (c > q) ? (c - q + CS - 1) / CS : 0;  // owned columns q, q+CS, ...
@@ -532,7 +524,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     amax = fmax(amax, mx);
-    if (lane == 0) { nrm2[l] = s; ref2[l] = s; }
+    if (lane == 0) { nrm2[l] = s; ref2[l] = s; fn2[l] = s; }
   }
   if (lane == 0) red[warp] = amax;
   __syncthreads();
@@ -553,128 +545,143 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
   // this CTA's candidate for step k over its unpivoted columns: first maximum by position
   auto local_candidate = [&](int k) {
     const bool rep = T.replay && k < T.nreplay;
-    double bv = rep ? 0.0 : -1.0, bn = 0.0;
-    int bp = c;
+    double bv = rep ? 0.0 : -1.0;
+    int bp = c, bl = -1;
     for (int l = tid; l < nown; l += QST) {
       if (done[l]) continue;
       const int cj = q + CS * l, pj = pos_of[cj];
       if (rep) {
-        if (cj == T.replay[k]) { bv = 1.0; bp = pj; bn = nrm2[l]; }
+        if (cj == T.replay[k]) { bv = 1.0; bp = pj; bl = l; }
       } else {
         const double x = nrm2[l];
-        if (x > bv || (x == bv && pj < bp)) { bv = x; bp = pj; bn = x; }
+        if (x > bv || (x == bv && pj < bp)) { bv = x; bp = pj; bl = l; }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const double on = __shfl_xor_sync(0xffffffffu, bn, o);
       const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bn = on; }
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bl = ol; }
     }
-    if (lane == 0) { wv[warp] = bv; wi[warp] = bp; red[warp] = bn; }
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bp; wl[warp] = bl; }
     __syncthreads();
     if (tid == 0) {
-      double b = wv[0], n = red[0];
-      int p0 = wi[0];
+      double b = wv[0];
+      int p0 = wi[0], l0 = wl[0];
       for (int w = 1; w < QSW; ++w)
-        if (wv[w] > b || (wv[w] == b && wi[w] < p0)) { b = wv[w]; p0 = wi[w]; n = red[w]; }
-      cand[k & 1] = QsCand{b, n, p0};
+        if (wv[w] > b || (wv[w] == b && wi[w] < p0)) { b = wv[w]; p0 = wi[w]; l0 = wl[w]; }
+      QsCand r{b, 0.0, 0.0, 0.0, p0};
+      if (l0 >= 0) {
+        r.n2 = nrm2[l0];
+        r.xn2 = fn2[l0];
+        r.x0 = cols[(size_t)l0 * mp + k];
+      }
+      cand[k & 1] = r;
     }
   };
 
   const int limit = (T.forced_rank >= 0) ? min(T.forced_rank, kmax) : kmax;
   int steps = 0, rank = 0;
   double r00 = 0.0;
+  // the previous pivot column, rewritten as R_kk + reflector after the next barrier
+  int p_lp = -1, p_k = 0;
+  double p_u1 = 1.0, p_rkk = 0.0;
+  auto flush_pivot = [&]() {
+    if (p_lp < 0) return;
+    double* xk = cols + (size_t)p_lp * mp;
+    for (int i = p_k + 1 + tid; i < m; i += QST) xk[i] = xk[i] / p_u1;
+    if (tid == 0) xk[p_k] = p_rkk;
+    p_lp = -1;
+  };
   if (limit > 0) local_candidate(0);
   for (int k = 0; k < limit; ++k) {
-    cluster.sync();  // B1: candidates of k, every update of k-1
+    cluster.sync();  // candidates of k, every update of k-1; nobody reads the previous pivot column
     if (warp == 0) {   // lane r < CS fetches CTA r's candidate; (value, position) order is total
-      QsCand o{-2.0, 0.0, c};
+      QsCand o{-2.0, 0.0, 0.0, 0.0, c};
       if (lane < CS) {
         o = *cluster.map_shared_rank(&cand[k & 1], lane);
         if (o.pos >= c) o.v = -2.0;
       }
+      double bv = o.v;
+      int bp = o.pos, bl = lane;
 #pragma unroll
       for (int d = 16; d > 0; d >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, o.v, d);
-        const double on = __shfl_xor_sync(0xffffffffu, o.n2, d);
-        const int op = __shfl_xor_sync(0xffffffffu, o.pos, d);
-        if (ov > o.v || (ov == o.v && op < o.pos)) { o.v = ov; o.n2 = on; o.pos = op; }
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, d);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, d);
+        if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bl = ol; }
       }
-      if (lane == 0) sel = o;
+      const double n2 = __shfl_sync(0xffffffffu, o.n2, bl);
+      const double xn2 = __shfl_sync(0xffffffffu, o.xn2, bl);
+      const double x0 = __shfl_sync(0xffffffffu, o.x0, bl);
+      if (lane == 0) {
+        const int pp = bp < c && bv > -2.0 ? bp : c;
+        sel = QsCand{bv, n2, xn2, x0, pp};
+        if (pp < c && n2 > floor2) {
+          const int pc = col_of[pp];
+          sel_pc = pc;
+          if (pp != k) {  // position swap k <-> pp
+            const int ck = col_of[k];
+            col_of[k] = pc;
+            col_of[pp] = ck;
+            pos_of[pc] = k;
+            pos_of[ck] = pp;
+          }
+        }
+      }
+    } else {
+      flush_pivot();
     }
     __syncthreads();
-    const int pp = sel.pos < c && sel.v > -2.0 ? sel.pos : c;
-    const double pn = sel.n2;
+    if (warp == 0) flush_pivot();
+    const int pp = sel.pos;
     if (pp >= c) break;  // malformed replay
-    if (pn <= floor2) break;
-    const int pc = col_of[pp];  // pivot column (original index)
-    __syncthreads();            // every thread has read col_of[pp]
-    if (tid == 0 && pp != k) {  // position swap k <-> pp
-      const int ck = col_of[k];
-      col_of[k] = pc;
-      col_of[pp] = ck;
-      pos_of[pc] = k;
-      pos_of[ck] = pp;
-    }
-    const int owner = pc % CS;
-    if (owner == q) {
-      const int lp = pc / CS;
-      double* xk = cols + (size_t)lp * mp;
-      double ss = 0.0;
-      for (int i = k + tid; i < m; i += QST) ss = fma(xk[i], xk[i], ss);
-      const double xn = sqrt(sblock_sum(ss, red));
-      int stop = 0;
-      if (xn <= floor_) stop = 1;
-      const double r0 = (k == 0) ? xn : r00;
-      if (!stop && T.forced_rank < 0 && !T.full_steps && !(xn > T.tol * r0)) stop = 1;
-      const double x0 = xk[k];
-      const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
-      const double u1 = x0 - sgn * xn;
-      const double tau = -sgn * u1 / xn;
-      if (!stop)
-        for (int i = k + tid; i < m; i += QST) vbuf[i - k] = (i == k) ? 1.0 : xk[i] / u1;
-      if (tid == 0) piv_s = QsPiv{tau, sgn * xn, xn, stop};
-    }
-    cluster.sync();  // B2: the reflector is published
-    const QsPiv pv = *cluster.map_shared_rank(&piv_s, owner);
-    if (pv.stop) break;
-    if (k == 0) r00 = pv.xn;
-    if (pv.xn > T.tol * r00) ++rank;
+    if (sel.n2 <= floor2) break;
+    const int pc = sel_pc;
+    const int owner = pc % CS, lp = pc / CS;
+    const double xn = sqrt(sel.xn2);
+    if (xn <= floor_) break;
+    const double r0 = (k == 0) ? xn : r00;
+    if (T.forced_rank < 0 && !T.full_steps && !(xn > T.tol * r0)) break;
+    const double x0 = sel.x0;
+    const double sgn = (x0 != 0.0) ? -copysign(1.0, x0) : -1.0;
+    const double u1 = x0 - sgn * xn;
+    const double tau = -sgn * u1 / xn;
+    if (k == 0) r00 = xn;
+    if (xn > T.tol * r00) ++rank;
     const int len = m - k;
-    {  // remote reflector -> local, 16-byte loads all in flight before the stores
-      const double2* rv = reinterpret_cast<const double2*>(cluster.map_shared_rank(vbuf, owner));
-      double2* lv = reinterpret_cast<double2*>(vloc);
-      const int n2 = (len + 1) >> 1;
-      double2 t[QS_VCH];
+    {  // remote pivot column / u1 -> local reflector, the loads all in flight before the stores
+      const double* rx = cluster.map_shared_rank(cols + (size_t)lp * mp + k, owner);
+      double t[QS_VCH];
 #pragma unroll
       for (int u = 0; u < QS_VCH; ++u)
-        if (tid + QST * u < n2) t[u] = rv[tid + QST * u];
+        if (tid + QST * u < len) t[u] = rx[tid + QST * u];
 #pragma unroll
-      for (int u = 0; u < QS_VCH; ++u)
-        if (tid + QST * u < n2) lv[tid + QST * u] = t[u];
-      for (int i = tid + QST * QS_VCH; i < n2; i += QST) lv[i] = rv[i];
+      for (int u = 0; u < QS_VCH; ++u) {
+        const int i = tid + QST * u;
+        if (i < len) vloc[i] = (i == 0) ? 1.0 : t[u] / u1;
+      }
+      for (int i = tid + QST * QS_VCH; i < len; i += QST) vloc[i] = rx[i] / u1;
+    }
+    if (owner == q) {
+      if (tid == 0) {
+        done[lp] = 1;
+        T.tau[k] = tau;
+      }
+      p_lp = lp;
+      p_k = k;
+      p_u1 = u1;
+      p_rkk = sgn * xn;
     }
     __syncthreads();
-    if (owner == q) {  // the pivot column: R_kk and the reflector below it
-      const int lp = pc / CS;
-      double* xk = cols + (size_t)lp * mp;
-      for (int i = k + 1 + tid; i < m; i += QST) xk[i] = vloc[i - k];
-      if (tid == 0) {
-        xk[k] = pv.rkk;
-        done[lp] = 1;
-        T.tau[k] = pv.tau;
-      }
-    }
     for (int l = warp; l < nown; l += QSW) {
-      const int cj = q + CS * l;
-      if (cj == pc || done[l]) continue;
+      if (done[l]) continue;
       double* col = cols + (size_t)l * mp + k;
       double s = 0.0;
       for (int i = lane; i < len; i += 32) s = fma(vloc[i], col[i], s);
       s = warp_sum(s);
-      const double ts = pv.tau * s;
+      const double ts = tau * s;
       double fresh = 0.0;
       for (int i = lane; i < len; i += 32) {
         const double nv = fma(-ts, vloc[i], col[i]);
@@ -690,13 +697,16 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
           ref2[l] = fmax(fresh, floor2);
         }
         nrm2[l] = nn;
+        fn2[l] = fresh;
       }
     }
     steps = k + 1;
-    __syncthreads();  // norms and done flags of step k
+    __syncthreads();  // norms of step k
     if (k + 1 < limit) local_candidate(k + 1);
   }
   cluster.sync();  // every CTA has read its last remote data; all inputs were loaded long ago
+  flush_pivot();
+  __syncthreads();
   // columns to their final positions, permutation out
   for (int l = 0; l < nown; ++l) {
     const int cj = q + CS * l;
@@ -716,7 +726,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(QST)
 template <int CS>
 static size_t qrcp_smem_bytes(int m, int c) {
   const size_t cpc = (size_t)(c + CS - 1) / CS, mp = (size_t)((m + 1) & ~1);
-  return (cpc * mp + 2 * mp + 2 * cpc) * sizeof(double) + (2 * (size_t)c + cpc) * sizeof(int);
+  return (cpc * mp + mp + 3 * cpc) * sizeof(double) + (2 * (size_t)c + cpc) * sizeof(int);
 }
 
 template <int CS>
