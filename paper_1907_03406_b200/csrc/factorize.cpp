@@ -1010,6 +1010,13 @@ struct CompPre {
 void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int>& seqno,
                    const std::vector<int>& forced, int level, std::vector<CompOut>& out,
                    std::unordered_map<int, CompPre>& pre) {
+  HostTimer htpre("c-wave total host");
+  const auto lap0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (HostTimer::on())
+      fprintf(stderr, "[host]   cw %-16s %8.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - lap0).count());
+  };
   cudaStream_t st = S.st;
   BlockTable& M = S.M;
   Precond* P = S.P;
@@ -1052,6 +1059,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     c.perm = S.scratch.alloc_t<int>(std::max(c.cN, 1));
   }
 
+  lap("setup");
   // the filtered products M_BN Phi_N
   GemmBatch g1;
   for (auto& c : ci) {
@@ -1064,6 +1072,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     }
   }
   g1.launch(S.scratch, st);
+  lap("g1");
   // assemble N (column major): [L^T Phi_B | L^{-1} M_BN Phi_N or L^{-1} M_BN]
   GemmBatch g2;
   CopyBatch cn;
@@ -1081,6 +1090,7 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
   }
   cn.launch(S.scratch, st);
   g2.launch(S.scratch, st);
+  lap("g2");
 
   // pivoted QR (truncated at the rank), ranks read back
   std::vector<QrTask> qt(nw);
@@ -1118,9 +1128,14 @@ void compress_wave(State& S, const std::vector<int>& wave, const std::vector<int
     ProfScope ps(st, PROF_QR, 0.0);
     SGF_CUDA(launch_qrcp(d_qt, nw, max_m, st, max_c));
   }
+  lap("qr launched");
   std::vector<int> rs(2 * nw);
-  SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));
-  SGF_CUDA(cudaStreamSynchronize(st));
+  {
+    HostTimer htw("c-wave rank wait");  // (the copy to pageable memory waits for the stream)
+    SGF_CUDA(cudaMemcpyAsync(rs.data(), d_out, 2 * nw * sizeof(int), cudaMemcpyDeviceToHost, st));
+    SGF_CUDA(cudaStreamSynchronize(st));
+  }
+  HostTimer htp("c-wave post-rank host");
   S.chk.verify(st);  // a breakdown upstream must surface before ranks are used
   if (Phase::mode() == 1) {
     long long sm = 0, sc = 0, ss = 0;
