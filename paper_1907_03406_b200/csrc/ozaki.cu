@@ -384,10 +384,12 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const OzSplitJob* __
   }
   for (int i = threadIdx.x; i < OZR_ROWS * OZS_MW; i += 256) smask[i / OZS_MW][i % OZS_MW] = 0u;
   // zero padding (columns K .. Kp) and dead rows; the odd last column
-  for (int i = threadIdx.x; i < OZR_ROWS * pitch; i += 256) {
-    const int rr = i / pitch, k = i % pitch;
-    if (rr >= nlive) srow[i] = 0.0;
-    else if (k >= kb2) srow[i] = k < J.K ? J.x[(long long)(g0 + rr) * J.rs + k] : 0.0;
+  // (per row over the columns the bulk copy does not write: a flat loop over
+  // every staged element with a division each was a third of the kernel's stalls)
+  for (int rr = 0; rr < OZR_ROWS; ++rr) {
+    const bool live = rr < nlive;
+    for (int k = (live ? kb2 : 0) + threadIdx.x; k < pitch; k += 256)
+      srow[rr * pitch + k] = (live && k < J.K) ? J.x[(long long)(g0 + rr) * J.rs + k] : 0.0;
   }
   __syncthreads();
   ptx::mbar_wait(&bar, 0);

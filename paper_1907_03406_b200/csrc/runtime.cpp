@@ -329,6 +329,24 @@ void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
     ProfScope ps(st, PROF_OZSPLIT, bytes);
     SGF_CUDA(launch_oz_split_rows(d_j, d_p, (int)rowsj.size(), prefix.back(), max_kp, st));
   }
+  if (HostTimer::on()) {
+    auto desc = [](const char* what, const std::vector<OzSplitJob>& v) {
+      if (v.empty()) return;
+      long long rows = 0, el = 0;
+      int kmax = 0, ntr = 0;
+      for (auto& j : v) {
+        rows += j.R;
+        el += (long long)j.R * j.K;
+        kmax = std::max(kmax, j.Kp);
+        ntr += j.cs != 1;
+      }
+      fprintf(stderr, "[host] oz split %-5s %5zu jobs (%d col-major) rows %lld max Kp %d  %.2f GB fp64\n", what,
+              v.size(), ntr, rows, kmax, el * 8e-9);
+    };
+    desc("rows", rowsj);
+    desc("cta", part[0]);
+    desc("warp", part[1]);
+  }
   for (int w = 0; w < 2; ++w) {
     auto& js = part[w];
     if (js.empty()) continue;
