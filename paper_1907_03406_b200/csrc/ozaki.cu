@@ -46,7 +46,10 @@ constexpr int OZ_STAGES = 3;
 constexpr int OZ_A_TILE = OZ_BM * OZ_KT, OZ_B_TILE = OZ_BN * OZ_KT;
 constexpr int OZ_A_STAGE = OZ_S * OZ_A_TILE, OZ_B_STAGE = OZ_S * OZ_B_TILE;
 constexpr int OZ_H = OZ_S / 2;  // diagonals (and, in pass 0, slices) per pass
-constexpr int OZ_THREADS = 192;  // warps 0-3 epilogue (TMEM lane quadrants), 4 producer, 5 MMA
+constexpr int OZ_EPI_WARPS = 8;  // epilogue: warp w drains TMEM lane quadrant w % 4, column half w / 4
+constexpr int OZ_PROD_WARP = OZ_EPI_WARPS, OZ_MMA_WARP = OZ_EPI_WARPS + 1;
+constexpr int OZ_THREADS = 32 * (OZ_EPI_WARPS + 2);
+constexpr int OZ_EC = 16;  // epilogue chunk: columns per TMEM load / staging pass
 
 #ifdef OZ_PROFILE
 // cycles: [0] MMA waiting for operands, [1] MMA waiting for the epilogue,
@@ -529,10 +532,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tmem_full, 1);
-    mbar_init(&tmem_empty, 128);
+    mbar_init(&tmem_empty, 32 * OZ_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  if (warp == 5) {
+  if (warp == OZ_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     return r;
   };
 
-  if (warp == 4) {
+  if (warp == OZ_PROD_WARP) {
     if (lane == 0) {  // producer: stages of all segments in order
       int it = 0;
       for (int si = 0; si < T.nseg; ++si) {
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == OZ_MMA_WARP) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
@@ -637,13 +640,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else {
-    // epilogue, warps 0-3: thread = tile row (TMEM lane)
-    const int lr = warp * 32 + lane;
+    // epilogue, warps 0-7: thread = tile row (TMEM lane) of quadrant warp % 4,
+    // columns [64 (warp / 4), +64) in chunks of 16.  Two warps per SM
+    // sub-partition keep the TMEM-load -> convert -> C read-modify-write
+    // chains of one overlapping the other's (one warp per quadrant over all
+    // 128 columns ran them back to back: the drain took as long as the MMAs)
+    const int quad = warp & 3, half = warp >> 2;
+    const int lr = quad * 32 + lane;
     const int row = T.m0 + lr;
-    // staging tile of this warp: 32 rows x 32 columns (+1 pad), so the C
-    // read-modify-write runs row by row with the 32 lanes on 32 consecutive
-    // columns (coalesced) instead of one row per thread
-    double* stg = reinterpret_cast<double*>(smem + OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE)) + warp * 32 * 33;
+    // staging tile of this warp: 32 rows x 16 columns, column index XOR-swizzled
+    // by the row (conflict-free row writes and column reads of 8-byte words),
+    // so the C read-modify-write runs with the lanes on 16 consecutive
+    // columns of 2 rows (coalesced) instead of one row per thread
+    double* stg = reinterpret_cast<double*>(smem + OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE)) + warp * 32 * OZ_EC;
     int drains = 0;
     for (int si = 0; si < T.nseg; ++si) {
       const OzSeg G = segs[T.seg0 + si];
@@ -661,46 +670,50 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         OZ_T0();
         const bool first = (si == 0 && pass == 0);
 #pragma unroll 1
-        for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
-          double acc[32];
+        for (int c0 = half * (OZ_BN / 2); c0 < (half + 1) * (OZ_BN / 2); c0 += OZ_EC) {
+          // the four diagonals' 16 columns in flight together, one wait
+          uint32_t v[OZ_H][OZ_EC];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+          for (int dd = 0; dd < OZ_H; ++dd)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(v[dd][0]), "=r"(v[dd][1]), "=r"(v[dd][2]), "=r"(v[dd][3]), "=r"(v[dd][4]), "=r"(v[dd][5]),
+                  "=r"(v[dd][6]), "=r"(v[dd][7]), "=r"(v[dd][8]), "=r"(v[dd][9]), "=r"(v[dd][10]), "=r"(v[dd][11]),
+                  "=r"(v[dd][12]), "=r"(v[dd][13]), "=r"(v[dd][14]), "=r"(v[dd][15])
+                : "r"(tmem + ((uint32_t)(quad * 32) << 16) + dd * OZ_BN + c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          double acc[OZ_EC];
+#pragma unroll
+          for (int j = 0; j < OZ_EC; ++j) acc[j] = 0.0;
 #pragma unroll
           for (int dd = OZ_H - 1; dd >= 0; --dd) {  // smallest terms first
             const double sc = ldexp(1.0, -(8 * (dd + pass * OZ_H) + 12));
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t v[16];
-              asm volatile(
-                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-                  "[%16];"
-                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                    "=r"(v[15])
-                  : "r"(tmem + ((uint32_t)(warp * 32) << 16) + dd * OZ_BN + c0 + 16 * h));
-              asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-              for (int j = 0; j < 16; ++j) acc[16 * h + j] = fma((double)(int32_t)v[j], sc, acc[16 * h + j]);
-            }
+            for (int j = 0; j < OZ_EC; ++j) acc[j] = fma((double)(int32_t)v[dd][j], sc, acc[j]);
           }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = acc[j] * rs;
+          for (int j = 0; j < OZ_EC; ++j) stg[lane * OZ_EC + (j ^ (lane & 15))] = acc[j] * rs;
           __syncwarp();
-          const int col = T.n0 + c0 + lane;
+          const int cl = lane & 15, rh = lane >> 4;  // column within the chunk, row parity
+          const int col = T.n0 + c0 + cl;
           const bool cok = col < T.N && !empty_seg;
           const double cs = cok ? ldexp(1.0, G.eb[col]) : 0.0;
-          // all loads of the 32 rows first (independent), then the stores
-          const int nrow = min(32, T.M - (T.m0 + warp * 32));
-          double* cbase = T.C + (long long)(T.m0 + warp * 32) * T.c_rs + (long long)col * T.c_cs;
+          // all loads of the 16 row pairs first (independent), then the stores
+          const int nrow = min(32, T.M - (T.m0 + quad * 32));
+          double* cbase = T.C + (long long)(T.m0 + quad * 32 + rh) * T.c_rs + (long long)col * T.c_cs;
           const bool need_c = !(first && T.beta == 0.0);
-          double cv[32];
+          double cv[16];
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr)
-            cv[rr] = (need_c && rr < nrow && col < T.N) ? __ldcg(cbase + (long long)rr * T.c_rs) : 0.0;
+          for (int i = 0; i < 16; ++i)
+            cv[i] = (need_c && 2 * i + rh < nrow && col < T.N) ? __ldcg(cbase + (long long)(2 * i) * T.c_rs) : 0.0;
           const double bscale = first ? T.beta : 1.0;
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr)
-            if (rr < nrow && col < T.N) cbase[(long long)rr * T.c_rs] = fma(bscale, cv[rr], stg[rr * 33 + lane] * cs);
+          for (int i = 0; i < 16; ++i) {
+            const int r = 2 * i + rh;
+            if (r < nrow && col < T.N)
+              cbase[(long long)(2 * i) * T.c_rs] = fma(bscale, cv[i], stg[r * OZ_EC + (cl ^ (r & 15))] * cs);
+          }
           __syncwarp();
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -711,7 +724,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == OZ_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace
@@ -767,7 +780,7 @@ cudaError_t launch_oz_split(const OzSplitJob* d_jobs, const long long* d_group_p
 
 cudaError_t launch_oz_gemm(const OzTask* d_tasks, int ntasks, const OzSeg* d_segs, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE) + 4 * 32 * 33 * sizeof(double);
+  const size_t smem = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE) + OZ_EPI_WARPS * 32 * OZ_EC * sizeof(double);
   static FuncAttrs fa;
   cudaError_t e = ensure_smem(oz_gemm_kernel, smem, fa);
   if (e != cudaSuccess) return e;
