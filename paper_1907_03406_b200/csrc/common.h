@@ -278,6 +278,11 @@ inline void count_launch(unsigned long long k = 1) { g_kernel_launches += k; }
 cudaError_t launch_gemm(const GemmTask* d_descs, const GemmTile* d_tiles, int ntiles, const GemmSeg* d_segs, int big_tiles,
                         cudaStream_t s);
 cudaError_t launch_fill_identity(double* const* d_ptrs, const int* d_sizes, int n, cudaStream_t s);
+struct ZeroRange {
+  uint8_t* p;
+  size_t bytes;
+};
+cudaError_t launch_zero_ranges(const ZeroRange* d_ranges, int n, cudaStream_t s);
 cudaError_t launch_scatter_values(const double* vals, const long long* dst, long long nnz, double* base,
                                   cudaStream_t s);
 // lpr: lanes per row of the mode-N kernel (8, 16 or 32)

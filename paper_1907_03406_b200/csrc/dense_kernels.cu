@@ -569,3 +569,29 @@ cudaError_t launch_zero_tiles(const double* p, long long rs, long long cs, int r
 }
 
 }  // namespace sgf
+
+namespace sgf {
+// zero a list of byte ranges (the nonzero-flag and row-mask arrays of a
+// batch of operand splits: one launch instead of a memset call per operand,
+// ~26k calls = ~19 ms of host time at level 2 of 128^3)
+__global__ void __launch_bounds__(256) zero_ranges_kernel(const ZeroRange* __restrict__ r, int n) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    uint8_t* p = r[i].p;
+    const size_t b = r[i].bytes;
+    size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+    if (head > b) head = b;
+    for (size_t k = threadIdx.x; k < head; k += 256) p[k] = 0;
+    const size_t nv = (b - head) / 16;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    for (size_t k = threadIdx.x; k < nv; k += 256) q[k] = make_uint4(0, 0, 0, 0);
+    for (size_t k = head + nv * 16 + threadIdx.x; k < b; k += 256) p[k] = 0;
+  }
+}
+
+cudaError_t launch_zero_ranges(const ZeroRange* d_ranges, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  zero_ranges_kernel<<<(unsigned)std::min(n, 1 << 16), 256, 0, s>>>(d_ranges, n);
+  return cudaGetLastError();
+}
+}  // namespace sgf

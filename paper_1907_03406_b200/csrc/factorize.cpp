@@ -595,6 +595,12 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     gg.launch(S.scratch, st);
   }
   HostTimer hte("elim E gemm");
+  const auto elap0 = std::chrono::steady_clock::now();
+  auto elap = [&](const char* what) {
+    if (HostTimer::on())
+      fprintf(stderr, "[host]   el %-16s %8.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - elap0).count());
+  };
   // Large nodes take the FP64 products on the INT8 tensor cores (ozaki.cu):
   // E = A_NB X^T (X lower triangular) and the Schur updates E_a E_b^T, with
   // every operand split once.  Small nodes keep the DMMA GEMM.
@@ -686,6 +692,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       fl_s += fs;
     }
   }
+  elap("E products");
   static const bool zero_stats = getenv("SGF_ZERO_STATS") != nullptr;
   if (zero_stats) {  // diagnostics: all-zero 128 x 32 tiles of the A_NB operands of E
     unsigned long long* cnt = S.scratch.alloc_t<unsigned long long>(2);
@@ -714,7 +721,9 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     ProfScope ps(st, PROF_MOVE, 0.0);
     SGF_CUDA(launch_nz_flags64(S.scratch.upload(nzjobs), S.scratch.upload(tp), (int)nzjobs.size(), tp.back(), st));
   }
+  elap("nz flags");
   ge.launch(S.scratch, st);
+  elap("E launch");
   int *rl_n = nullptr, *rl_k = nullptr;
   double* rl_a = nullptr;
   if (sparse1 && rl_rows > 0) {
@@ -835,6 +844,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
     long long fill = -1;    // offset in the fill region, -1: existing block
     int head = -1, tail = -1, count = 0;
   };
+  elap("schur splits");
   HostTimer ht1("elim targets");
   std::vector<Target> targets;
   std::vector<Contrib> cbuf;

@@ -303,7 +303,13 @@ void GemmBatch::launch(Arena& scratch, cudaStream_t st) {
 
 void OzBatch::launch_splits(Arena& scratch, cudaStream_t st) {
   if (jobs.empty()) return;
-  for (auto& z : nz_clear) SGF_CUDA(cudaMemsetAsync(z.first, 0, z.second, st));
+  if (nz_clear.size() <= 2) {
+    for (auto& z : nz_clear) SGF_CUDA(cudaMemsetAsync(z.first, 0, z.second, st));
+  } else {
+    std::vector<ZeroRange> zr(nz_clear.size());
+    for (size_t i = 0; i < nz_clear.size(); ++i) zr[i] = ZeroRange{nz_clear[i].first, nz_clear[i].second};
+    SGF_CUDA(launch_zero_ranges(scratch.upload(zr), (int)zr.size(), st));
+  }
   nz_clear.clear();
   // row-contiguous operands with aligned rows (rows staged once), other
   // row-contiguous or row-interleaved operands (coalesced CTA kernel) and the
