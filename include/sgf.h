@@ -155,6 +155,10 @@ const char* sgf_last_error(const sgf_ctx* ctx);
 /* the stream all work of the context runs on (cudaStream_t as void*) */
 void* sgf_stream(sgf_ctx* ctx);
 int sgf_sync(sgf_ctx* ctx);
+/* returns the device memory the library caches for reuse (freed arena chunks
+   of this context's device) to the driver, e.g. before another process on
+   the same GPU needs it; live factors and matrices are untouched */
+int sgf_trim(sgf_ctx* ctx);
 
 int sgf_factorize(sgf_ctx* ctx, const sgf_factor_args* args, sgf_precond** out);
 int sgf_precond_free(sgf_precond* p);
@@ -171,6 +175,10 @@ int sgf_precond_num_factors(const sgf_precond* p);
 int sgf_precond_coupling_bytes(const sgf_precond* p, double* out);
 /* the same restricted to the factors of one level (level >= 1; 0: all) */
 int sgf_precond_coupling_bytes_level(const sgf_precond* p, int level, double* out);
+/* diagnostic: E bytes of a level under the forward sweeps' skipping
+   granularities (out[6]: dense, nonzero tiles, from the first nonzero tile,
+   256-column chunks, chunks trimmed to their nonzero span, nonzero-tile runs) */
+int sgf_precond_coupling_bytes_detail(const sgf_precond* p, int level, double* out);
 /* info[0..7] = type, node, m (idx size), c (coupling rows), retained, level, reflectors, QR columns */
 int sgf_precond_factor_info(const sgf_precond* p, int k, int64_t* info);
 /* what: 0 idx (int64 m), 1 L (m*m), 2 couplings E (c*m), 3 coupling idx (int64 c),

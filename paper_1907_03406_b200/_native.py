@@ -28,9 +28,9 @@ SOLVE_FORWARD, SOLVE_TRANSPOSE, MULT_TRANSPOSE, MULT_FORWARD = range(4)
 
 # functions the header declares (checked by tests/test_native_abi.py)
 EXPORTS = (
-    "sgf_create", "sgf_destroy", "sgf_last_error", "sgf_stream", "sgf_sync", "sgf_factorize",
+    "sgf_create", "sgf_destroy", "sgf_last_error", "sgf_stream", "sgf_sync", "sgf_trim", "sgf_factorize",
     "sgf_precond_free", "sgf_precond_n", "sgf_precond_stats_json", "sgf_precond_rank_trace",
-    "sgf_precond_num_factors", "sgf_precond_coupling_bytes", "sgf_precond_coupling_bytes_level", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
+    "sgf_precond_num_factors", "sgf_precond_coupling_bytes", "sgf_precond_coupling_bytes_level", "sgf_precond_coupling_bytes_detail", "sgf_precond_factor_info", "sgf_precond_factor_copy", "sgf_apply",
     "sgf_csr_create", "sgf_csr_free", "sgf_spmv", "sgf_pcg", "sgf_pcg_cb",
     "sgf_precond_shard_info", "sgf_precond_shard_set", "sgf_apply_part", "sgf_cell_unknowns",
     "sgf_kernel_launches", "sgf_profile_enable", "sgf_profile_read", "sgf_pcg_ops", "sgf_memcpy",
@@ -108,6 +108,7 @@ def load_library(path=LIB_PATH):
             "sgf_last_error": (C.c_char_p, [vp]),
             "sgf_stream": (vp, [vp]),
             "sgf_sync": (i32, [vp]),
+            "sgf_trim": (i32, [vp]),
             "sgf_factorize": (i32, [vp, C.POINTER(FactorArgs), C.POINTER(vp)]),
             "sgf_precond_free": (i32, [vp]),
             "sgf_precond_n": (i64, [vp]),
@@ -116,6 +117,7 @@ def load_library(path=LIB_PATH):
             "sgf_precond_num_factors": (i32, [vp]),
             "sgf_precond_coupling_bytes": (i32, [vp, vp]),
             "sgf_precond_coupling_bytes_level": (i32, [vp, i32, vp]),
+            "sgf_precond_coupling_bytes_detail": (i32, [vp, i32, vp]),
             "sgf_precond_factor_info": (i32, [vp, i32, vp]),
             "sgf_precond_factor_copy": (i32, [vp, i32, i32, vp, i64]),
             "sgf_apply": (i32, [vp, i32, vp, vp, i32]),
@@ -192,6 +194,17 @@ def context(device=0):
         _ctx[device] = h
         _ctx_device[h.value] = int(device)
     return h
+
+
+def trim_memory():
+    """Return the device memory the library caches for reuse (on every device
+    with a context) to the driver; live factors and matrices are untouched.
+    For a process that shares its GPU with others, e.g. a test session about
+    to launch worker processes on the same device."""
+    with _lock:
+        handles = list(_ctx.values())
+    for h in handles:
+        raise_for(lib().sgf_trim(h), h)
 
 
 def context_device(ctx):

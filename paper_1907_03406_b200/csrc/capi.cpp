@@ -95,6 +95,14 @@ int sgf_sync(sgf_ctx* ctx) {
   return guarded(ctx, [&] { SGF_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
 }
 
+int sgf_trim(sgf_ctx* ctx) {
+  return guarded(ctx, [&] {
+    SGF_CUDA(cudaSetDevice(ctx->c.device));
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    chunk_trim();
+  });
+}
+
 int sgf_factorize(sgf_ctx* ctx, const sgf_factor_args* args, sgf_precond** out) {
   if (!ctx || !args || !out) return SGF_INVALID_ARG;
   *out = nullptr;
@@ -173,6 +181,64 @@ int sgf_precond_coupling_bytes_level(const sgf_precond* p, int level, double* ou
     }
     out[0] = dense;
     out[1] = nz;
+  });
+}
+
+// Diagnostic: bytes of the couplings E of one level (0 = all) as the forward
+// sweeps read them under different skipping granularities:
+//   out[0] dense, out[1] nonzero 32-column tiles, out[2] from the first
+//   nonzero tile to the row's end, out[3] 256-column chunks from the first
+//   nonzero tile (all-zero chunks skipped, last chunk kept), out[4] chunks
+//   trimmed to their first..last nonzero tile, out[5] number of maximal runs
+//   of nonzero tiles (one copy each at tile granularity)
+int sgf_precond_coupling_bytes_detail(const sgf_precond* p, int level, double* out) {
+  if (!p || !out) return SGF_INVALID_ARG;
+  sgf_ctx* ctx = p->ctx;
+  return guarded(ctx, [&] {
+    SGF_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    for (int i = 0; i < 6; ++i) out[i] = 0.0;
+    std::vector<uint32_t> mk;
+    for (const Factor& f : p->p->factors) {
+      if (f.type != SGF_FACTOR_ELIMINATION || !f.E || f.c <= 0 || (level > 0 && f.level != level)) continue;
+      out[0] += 8.0 * f.c * f.m;
+      if (!f.emask) {
+        for (int i = 1; i < 5; ++i) out[i] += 8.0 * f.c * f.m;
+        out[5] += f.c;
+        continue;
+      }
+      mk.resize((size_t)f.c * f.emw);
+      SGF_CUDA(cudaMemcpy(mk.data(), f.emask, mk.size() * 4, cudaMemcpyDeviceToHost));
+      const int nt = (f.m + 31) / 32;
+      for (int r = 0; r < f.c; ++r) {
+        auto bit = [&](int t) { return (mk[(size_t)r * f.emw + (t >> 5)] >> (t & 31)) & 1u; };
+        auto tw = [&](int t) { return std::max(0, std::min(32, f.m - 32 * t)); };
+        int first = -1;
+        bool prev = false;
+        for (int t = 0; t < nt; ++t) {
+          const bool b = bit(t);
+          if (b) {
+            out[1] += 8.0 * tw(t);
+            if (first < 0) first = t;
+            if (!prev) out[5] += 1;
+          }
+          prev = b;
+        }
+        if (first < 0) continue;
+        for (int t = first; t < nt; ++t) out[2] += 8.0 * tw(t);
+        for (int t0 = first; t0 < nt; t0 += 8) {
+          int lo = -1, hi = -1;
+          for (int t = t0; t < std::min(nt, t0 + 8); ++t)
+            if (bit(t)) {
+              if (lo < 0) lo = t;
+              hi = t;
+            }
+          const bool last = t0 + 8 >= nt;
+          if (lo < 0 && !last) continue;
+          for (int t = t0; t < std::min(nt, t0 + 8); ++t) out[3] += 8.0 * tw(t);
+          for (int t = lo; lo >= 0 && t <= hi; ++t) out[4] += 8.0 * tw(t);
+        }
+      }
+    }
   });
 }
 

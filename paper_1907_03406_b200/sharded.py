@@ -463,12 +463,20 @@ def pcg_sharded(A, b, precond, tol=1e-10, maxit=5000, true_residual_every=50):
     import hashlib
 
     # the ownership is the same for every factorization of one problem on one
-    # process group: the plan (owned-row CSR, halo lists) is built once
-    key = (id(Ah), precond.rank, precond.world, hashlib.blake2b(precond.owned.tobytes(), digest_size=16).hexdigest())
-    plan = _PLANS.get(key)
-    if plan is None:
+    # process group: the plan (owned-row CSR, halo lists) is built once.
+    # Building it is a collective, so hit or miss must come out the same on
+    # every rank: the cached entry holds the matrix's arrays themselves and is
+    # matched by object identity (never by id(), which a dead object's
+    # successor can reuse on one rank and not on another).
+    arrays = (Ah.indptr, Ah.indices, Ah.data)
+    key = (precond.rank, precond.world, hashlib.blake2b(precond.owned.tobytes(), digest_size=16).hexdigest())
+    ent = _PLANS.get("plan")
+    if ent is not None and ent[0] == key and all(a is b_ for a, b_ in zip(ent[1], arrays)):
+        plan = ent[2]
+    else:
         _PLANS.clear()
-        plan = _PLANS[key] = _HaloPlan(Ah, precond)
+        plan = _HaloPlan(Ah, precond)
+        _PLANS["plan"] = (key, arrays, plan)
     dev = precond.device
     ctx = precond.pre._ctx
     L = N.lib()

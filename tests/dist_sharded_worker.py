@@ -75,8 +75,13 @@ def solve_mode(args):
         # INT8-emulated products and the recursive Cholesky
         "cfg2": (PB.CONFIGS[2]["make"], dict(scheme="nest-2-2", degree=1, b=9, rank_tol=1e-2)),
     }
+    def note(msg):
+        if args.verbose:
+            print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
+
     for name in args.cases.split(","):
         make, opts = cases[name]
+        note(f"case {name}")
         prob = make()
         n = prob.matrix.shape[0]
         rhs = np.random.default_rng(3).uniform(-1, 1, n)
@@ -85,8 +90,11 @@ def solve_mode(args):
         perms = [np.asarray(f.perm) for f in P1.factors if f.kind == "CompressionFactor"]
         y1 = P1.apply_inverse(rhs)
         x1, rep1 = sgf.pcg(sgf.DeviceCSR(prob.matrix, device=dev), rhs, precond=P1, tol=1e-12)
+        note("single-GPU path done")
         PS = S.factorize_sharded(prob, device=dev, replay_perms=perms, **opts)
+        note("sharded factorization done")
         ys = PS.apply_inverse(rhs)
+        note("sharded apply done")
         xs, reps = S.pcg_sharded(sgf.DeviceCSR(prob.matrix, device=dev), rhs, PS, tol=1e-12)
         r = {
             "n": n,
@@ -154,7 +162,13 @@ def main():
     ap.add_argument("--per-rank-gpu", action="store_true")
     ap.add_argument("--debug", action="store_true")
     ap.add_argument("--free", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--dump-after", type=float, default=0.0,
+                    help="print every thread's Python stack to stderr after this many seconds (hang diagnosis)")
     args = ap.parse_args()
+    if args.dump_after > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.dump_after, exit=False)
     dist.init_process_group(backend=args.backend)
     try:
         out = plan_mode() if args.mode == "plan" else solve_mode(args)

@@ -23,6 +23,7 @@ VARIANTS = {
     "default": {},
     "symv_registers": {"SGF_SYMV": "0"},               # register-staged level-1 symmetric GEMV
     "gemv_no_bulk": {"SGF_GEMV_BULK": "0"},            # 32-lane GEMV for the long rows too
+    "gemv_sparse_ring": {"SGF_GEMV_SPARSE_RING": "1"},  # block-sparse rows through the bulk-copy ring (not tile lists)
     "qr_l2_panel": {"SGF_QR_SMEM": "0"},               # cluster QR with the panel in L2
     "qr_cluster16": {"SGF_QR_SMEM": "16"},             # shared-memory QR forced to 16-CTA clusters
     "l1_dense": {"SGF_NO_L1SPARSE": "1"},              # level-1 E and Schur as dense DMMA GEMMs

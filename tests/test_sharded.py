@@ -29,9 +29,30 @@ def _free_port():
 
 
 def _launch(nproc, *args, timeout=900):
+    if "solve" in args:
+        # the workers share this session's GPU: hand back what earlier tests
+        # left in the allocators' caches (tens of GB after the full-size cases)
+        import gc
+
+        import torch
+
+        from paper_1907_03406_b200 import _native as N
+
+        gc.collect()
+        free0 = torch.cuda.mem_get_info()[0]
+        N.trim_memory()
+        torch.cuda.empty_cache()
+        print(f"[sharded] free HBM before the workers: {free0 / 2**30:.1f} -> "
+              f"{torch.cuda.mem_get_info()[0] / 2**30:.1f} GiB")
+        # a hung rank prints its Python stacks before the timeout kills it
+        args = (*args, "--verbose", "--dump-after", str(max(60, timeout - 120)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", WORKER, *args]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    except subprocess.TimeoutExpired as e:
+        err = e.stderr.decode("utf-8", "replace") if isinstance(e.stderr, bytes) else (e.stderr or "")
+        raise AssertionError(f"sharded workers timed out after {timeout} s; stderr tail:\n{err[-6000:]}") from None
     lines = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")]
     assert out.returncode == 0 and lines, out.stdout[-3000:] + out.stderr[-3000:]
     return json.loads(lines[-1][len("RESULT "):])

@@ -23,3 +23,10 @@ for lev in sorted({f.level for f in P.factors if f.kind == "EliminationFactor"})
     N.raise_for(N.lib().sgf_precond_coupling_bytes_level(P._h, lev, buf.ctypes.data), P._ctx)
     out[lev] = {"E_dense": e_dense, "E_and_masked_Linv_dense": buf[0], "E_and_masked_Linv_nonzero": buf[1]}
 print(json.dumps(out))
+det = {}
+for lev in sorted({f.level for f in P.factors if f.kind == "EliminationFactor"}):
+    buf = np.zeros(6)
+    N.raise_for(N.lib().sgf_precond_coupling_bytes_detail(P._h, lev, buf.ctypes.data), P._ctx)
+    det[lev] = dict(zip(("dense", "nonzero_tiles", "from_first_tile", "chunks256", "chunks256_trimmed", "tile_runs"),
+                        (float(v) for v in buf)))
+print(json.dumps({"forward_sweep_E_bytes": det}))
