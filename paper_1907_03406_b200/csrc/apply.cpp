@@ -10,6 +10,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
+#include <utility>
 
 #include "precond.h"
 
@@ -95,7 +97,9 @@ struct ApplyPlan {
   // CUDA graphs of the sweeps on `work` (index = op), captured on first use
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   unsigned long long graph_launches[3] = {0, 0, 0};
-  explicit ApplyPlan(cudaStream_t s) : mem(s, (size_t)64 << 20) {}
+  // task lists and index arrays are uploaded on the context's upload stream
+  // (the plan worker runs beside the factorization); the sweeps run on `s`
+  ApplyPlan(cudaStream_t s, cudaStream_t upload) : mem(upload, (size_t)64 << 20) { mem.use_plan_pool(s); }
   ~ApplyPlan() {
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
@@ -181,7 +185,7 @@ void plan_extend(Precond* P, size_t begin, size_t end) {
 
 void plan_init(Precond* P) {
   if (P->plan) return;
-  P->plan = new ApplyPlan(P->ctx->stream);
+  P->plan = new ApplyPlan(P->ctx->stream, P->ctx->upload_stream);
   P->plan->n = P->n;
   P->plan->work = P->plan->mem.alloc(std::max<long long>(P->n, 1));
   P->plan->tix.assign(P->n, -1);
@@ -349,28 +353,69 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     g.nred2 = (int)r2.size();
     if (!contrib.empty()) {
       // bucket the contributions per target unknown, keeping factor order
-      // inside a bucket (counting sort; tix is an n-sized scratch map)
-      std::vector<int> tgt;
-      std::vector<long long> ptr, pos(contrib.size());
-      for (auto& c : contrib) {
-        int& ti = tix[c.first];
-        if (ti < 0) {
-          ti = (int)tgt.size();
-          tgt.push_back((int)c.first);
-          ptr.push_back(0);
+      // inside a bucket (counting sort; tix is an n-sized scratch map).  The
+      // passes are bound by random accesses into tix and the fill cursors, so
+      // large levels split the unknowns into ranges, one host thread each: a
+      // thread scans every contribution and handles those of its range (its
+      // slice of tix stays in cache).  The order of the targets differs from
+      // the serial one; the order inside a target -- the summation order of
+      // combine_kernel -- does not.
+      const int nth = contrib.size() > 400000 ? 4 : 1;
+      const int64_t n_all = (int64_t)tix.size();
+      struct Part {
+        std::vector<int> tgt;
+        std::vector<long long> ptr;  // counts, then offsets inside the part
+        long long total = 0;
+      };
+      std::vector<Part> parts(nth);
+      std::vector<long long> pos(contrib.size());
+      auto range = [&](int t) { return std::make_pair(n_all * t / nth, n_all * (t + 1) / nth); };
+      auto count_pass = [&](int t) {
+        Part& pt = parts[t];
+        const auto [lo, hi] = range(t);
+        for (auto& c : contrib) {
+          if (c.first < lo || c.first >= hi) continue;
+          int& ti = tix[c.first];
+          if (ti < 0) {
+            ti = (int)pt.tgt.size();
+            pt.tgt.push_back((int)c.first);
+            pt.ptr.push_back(0);
+          }
+          ++pt.ptr[ti];
         }
-        ++ptr[ti];
+        long long run = 0;
+        for (auto& p : pt.ptr) {
+          const long long k = p;
+          p = run;
+          run += k;
+        }
+        pt.total = run;
+      };
+      auto fill_pass = [&](int t, long long base) {
+        Part& pt = parts[t];
+        const auto [lo, hi] = range(t);
+        std::vector<long long> fillp(pt.ptr);
+        for (auto& c : contrib)
+          if (c.first >= lo && c.first < hi) pos[base + fillp[tix[c.first]]++] = c.second;
+        for (int u : pt.tgt) tix[u] = -1;
+      };
+      auto run_all = [&](auto&& fn) {
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t) th.emplace_back(fn, t);
+        fn(0);
+        for (auto& x : th) x.join();
+      };
+      run_all(count_pass);
+      std::vector<long long> base(nth + 1, 0);
+      for (int t = 0; t < nth; ++t) base[t + 1] = base[t] + parts[t].total;
+      run_all([&](int t) { fill_pass(t, base[t]); });
+      std::vector<int> tgt;
+      std::vector<long long> ptr;
+      for (int t = 0; t < nth; ++t) {
+        tgt.insert(tgt.end(), parts[t].tgt.begin(), parts[t].tgt.end());
+        for (long long p : parts[t].ptr) ptr.push_back(base[t] + p);
       }
-      long long run = 0;
-      for (auto& p : ptr) {
-        const long long k = p;
-        p = run;
-        run += k;
-      }
-      ptr.push_back(run);
-      std::vector<long long> fillp(ptr.begin(), ptr.end() - 1);
-      for (auto& c : contrib) pos[fillp[tix[c.first]]++] = c.second;
-      for (int u : tgt) tix[u] = -1;
+      ptr.push_back(base[nth]);
       g.ntgt = (long long)tgt.size();
       g.tgt = plan->mem.upload(tgt);
       g.tptr = plan->mem.upload(ptr);
@@ -380,13 +425,24 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
   }
 }
 
+// The context stream waits for everything enqueued so far on the upload
+// stream: the plan's task lists are in place before a sweep reads them.
+static void plan_sync_uploads(Precond* P) {
+  Ctx* c = P->ctx;
+  SGF_CUDA(cudaEventRecord(c->upload_ev, c->upload_stream));
+  SGF_CUDA(cudaStreamWaitEvent(c->stream, c->upload_ev, 0));
+}
+
 ApplyPlan* build_plan(Precond* P) {
   plan_extend(P, 0, P->factors.size());
+  plan_sync_uploads(P);
   return P->plan;
 }
 
 void plan_finish(Precond* P) {
-  if (P->plan) std::vector<int>().swap(P->plan->tix);
+  if (!P->plan) return;
+  std::vector<int>().swap(P->plan->tix);
+  plan_sync_uploads(P);
 }
 
 static void gemv(const GemvTask* t, int nt, int mode, double bytes, cudaStream_t st, int lpr = 32) {
@@ -534,6 +590,7 @@ static void prepare_operator(Precond* P) {
     g.bytes_oE = gemv_bytes(te, 0);
     g.bytes_oL = gemv_bytes(tl, 0);
   }
+  plan_sync_uploads(P);
   SGF_CUDA(cudaStreamSynchronize(st));
   pl->op_ready = true;
 }

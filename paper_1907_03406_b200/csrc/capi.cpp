@@ -62,6 +62,8 @@ int sgf_create(sgf_ctx** out, int device) {
     SGF_CUDA(cudaSetDevice(device));
     ctx->c.device = device;
     SGF_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    SGF_CUDA(cudaStreamCreateWithFlags(&ctx->c.upload_stream, cudaStreamNonBlocking));
+    SGF_CUDA(cudaEventCreateWithFlags(&ctx->c.upload_ev, cudaEventDisableTiming));
     cudaMemPool_t pool;
     SGF_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
@@ -83,6 +85,11 @@ int sgf_destroy(sgf_ctx* ctx) {
     cudaStreamDestroy(ctx->c.stream);
   }
   if (ctx->c.order_ev) cudaEventDestroy(ctx->c.order_ev);
+  if (ctx->c.upload_stream) {
+    cudaStreamSynchronize(ctx->c.upload_stream);
+    cudaStreamDestroy(ctx->c.upload_stream);
+  }
+  if (ctx->c.upload_ev) cudaEventDestroy(ctx->c.upload_ev);
   delete ctx;
   return SGF_OK;
 }

@@ -1831,6 +1831,7 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
     plan_pend.clear();
   };
   timeline_begin(S.st);
+  HostTimer::epoch() = std::chrono::steady_clock::now();
   { Phase ph("setup", 0, S.st); setup_level1(S); }
   S.peak = 0;
   std::vector<LevelStats> per_level;
@@ -1917,19 +1918,37 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
              a.trace[3 * S.comp_counter], a.trace[3 * S.comp_counter + 1], a.trace[3 * S.comp_counter + 2]);
     fail(SGF_TRACE, buf);
   }
+  std::unique_ptr<HostTimer> ht_tail(new HostTimer("tail: verify + device drain"));
   S.chk.verify(S.st);
   SGF_CUDA(cudaStreamSynchronize(S.st));
+  ht_tail.reset(new HostTimer("tail: perms, stats"));
   if (S.l1_overflow) {
     int ov = 0;
     SGF_CUDA(cudaMemcpy(&ov, S.l1_overflow, sizeof(int), cudaMemcpyDeviceToHost));
     if (ov) fail(SGF_INVALID_ARG, "internal: level-1 coupling row with more nonzeros than its CSR row");
   }
-  for (auto& f : P->factors)
-    if (f.perm_dev) {
-      f.perm.resize(f.ncols);
-      SGF_CUDA(cudaMemcpy(f.perm.data(), f.perm_dev, f.ncols * sizeof(int), cudaMemcpyDeviceToHost));
-      f.perm_dev = nullptr;
+  {  // QR column permutations: asynchronous copies into one pinned buffer, one synchronisation
+    size_t tot = 0;
+    for (auto& f : P->factors)
+      if (f.perm_dev) tot += f.ncols;
+    if (tot) {
+      int* hp = (int*)S.ctx->pinned(tot * sizeof(int));  // (the setup's staging buffer: idle by now)
+      size_t off = 0;
+      for (auto& f : P->factors)
+        if (f.perm_dev) {
+          SGF_CUDA(cudaMemcpyAsync(hp + off, f.perm_dev, f.ncols * sizeof(int), cudaMemcpyDeviceToHost, S.st));
+          off += f.ncols;
+        }
+      SGF_CUDA(cudaStreamSynchronize(S.st));
+      off = 0;
+      for (auto& f : P->factors)
+        if (f.perm_dev) {
+          f.perm.assign(hp + off, hp + off + f.ncols);
+          off += f.ncols;
+          f.perm_dev = nullptr;
+        }
     }
+  }
   S.scratch.release();
   S.lvl.reset();
   long long fa = S.fa_extra;
@@ -1941,8 +1960,10 @@ Precond* factorize(Ctx& ctx, const sgf_factor_args& a) {
   // stats equal the single-GPU ones; the other ranks' stats cover their local phase
   P->stats = stats_json(a, a.n, per_level, max_after, max_seen, final_size, S.flops, fa, S.peak,
                         (int)P->factors.size() + S.nf_extra, S.warnings);
+  ht_tail.reset(new HostTimer("tail: apply plan finish"));
   planner.finish();
   plan_finish(P.get());
+  ht_tail.reset();
   timeline_end(S.st);
   SGF_CUDA(cudaStreamSynchronize(S.st));
   return P.release();

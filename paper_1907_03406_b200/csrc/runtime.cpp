@@ -95,14 +95,22 @@ void* Arena::alloc_bytes(size_t bytes) {
     }
   }
   size_t cap = std::max(bytes, chunk_);
-  void* p = chunk_get(cap, &cap);
+  auto t0 = std::chrono::steady_clock::now();
+  void* p = plan_pool_ ? plan_chunk_get(cap, &cap, s_) : chunk_get(cap, &cap);
+  if (HostTimer::on()) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 1.0) fprintf(stderr, "[arena] new %s chunk of %.1f MB took %.2f ms\n", plan_pool_ ? "plan" : "cache", cap / 1048576.0, ms);
+  }
   chunks_.push_back(Chunk{(char*)p, cap, bytes});
   used_ += bytes;
   return p;
 }
 
 void Arena::release() {
-  for (auto& c : chunks_) chunk_put(c.base, c.cap);
+  for (auto& c : chunks_) {
+    if (plan_pool_) plan_chunk_put(c.base, c.cap, rel_);
+    else chunk_put(c.base, c.cap);
+  }
   chunks_.clear();
   used_ = 0;
 }
@@ -117,6 +125,12 @@ void Arena::release() {
 namespace {
 std::mutex g_cache_mu;
 std::map<int, std::multimap<size_t, void*>> g_cache;  // device -> (cap -> chunk)
+struct PlanChunk {
+  void* p;
+  cudaEvent_t released;  // recorded after the chunk's last users
+};
+std::map<int, std::multimap<size_t, PlanChunk>> g_plan_cache;  // guarded by g_cache_mu
+std::vector<cudaEvent_t> g_plan_events;                           // spare events (guarded by g_cache_mu)
 
 // The ring is split into NSEG segments used in order; leaving a segment
 // records an event, and re-entering it waits only for that event (work
@@ -129,15 +143,23 @@ struct Stager {
   size_t off = 0;           // offset inside the current segment
   cudaEvent_t ev[STAGE_NSEG] = {};
   bool used[STAGE_NSEG] = {};
+  std::mutex mu;  // one ring per stream: the plan worker's uploads do not hold up the driver's
 };
-std::mutex g_stage_mu;
+std::mutex g_stage_mu;  // guards the map only
 std::map<cudaStream_t, Stager> g_stage;
 }  // namespace
 
 void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
-  std::lock_guard<std::mutex> lk(g_stage_mu);
-  Stager& s = g_stage[st];
+  Stager* sp;
+  {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    sp = &g_stage[st];
+  }
+  Stager& s = *sp;
+  auto tA = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> lk(s.mu);
+  auto tB = std::chrono::steady_clock::now();
   const size_t need = (bytes + 255) & ~(size_t)255;
   if (need > s.seg) {  // (re)allocate a ring whose segments hold this upload
     if (s.buf) {
@@ -177,7 +199,15 @@ void stage_upload(cudaStream_t st, void* dst, const void* src, size_t bytes) {
   } else {
     std::memcpy(p, src, bytes);
   }
+  auto tC = std::chrono::steady_clock::now();
   SGF_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));
+  if (HostTimer::on()) {
+    auto tD = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    if (ms(tA, tD) > 2.0)
+      fprintf(stderr, "[stage] %.1f MB: lock %.2f ms, ring+memcpy %.2f ms, cudaMemcpyAsync %.2f ms\n", bytes / 1048576.0,
+              ms(tA, tB), ms(tB, tC), ms(tC, tD));
+  }
 }
 
 static int cur_device() {
@@ -229,6 +259,71 @@ void chunk_trim() {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (auto& kv : g_cache[dev]) cudaFree(kv.second);
   g_cache[dev].clear();
+  for (auto& kv : g_plan_cache[dev]) {
+    cudaFree(kv.second.p);
+    cudaEventDestroy(kv.second.released);
+  }
+  g_plan_cache[dev].clear();
+}
+
+void* plan_chunk_get(size_t bytes, size_t* cap, cudaStream_t user) {
+  const int dev = cur_device();
+  {
+    std::unique_lock<std::mutex> lk(g_cache_mu);
+    auto& cache = g_plan_cache[dev];
+    auto it = cache.lower_bound(bytes);
+    if (it != cache.end() && it->first <= 2 * bytes + ((size_t)64 << 20)) {
+      const PlanChunk c = it->second;
+      *cap = it->first;
+      cache.erase(it);
+      lk.unlock();
+      // (cudaEventDestroy can block for as long as another thread waits in a
+      // stream synchronisation -- 80 ms in the middle of a factorization --
+      // so events go back to a free list instead)
+      if (cudaEventQuery(c.released) != cudaSuccess) {
+        cudaGetLastError();
+        SGF_CUDA(cudaStreamWaitEvent(user, c.released, 0));
+      }
+      {
+        std::lock_guard<std::mutex> lk2(g_cache_mu);
+        g_plan_events.push_back(c.released);
+      }
+      return c.p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    chunk_trim();
+    e = cudaMalloc(&p, bytes);
+  }
+  SGF_CUDA(e);
+  *cap = bytes;
+  return p;
+}
+
+void plan_chunk_put(void* p, size_t cap, cudaStream_t last_user) {
+  const int dev = cur_device();
+  PlanChunk c{p, nullptr};
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (!g_plan_events.empty()) {
+      c.released = g_plan_events.back();
+      g_plan_events.pop_back();
+    }
+  }
+  if ((!c.released && cudaEventCreateWithFlags(&c.released, cudaEventDisableTiming) != cudaSuccess) ||
+      cudaEventRecord(c.released, last_user) != cudaSuccess) {
+    // no event to order a later user by: wait for the device and free the chunk
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    if (c.released) cudaEventDestroy(c.released);
+    cudaFree(p);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_plan_cache[dev].emplace(cap, c);
 }
 
 // flops the tiles actually multiply (k range per segment after the

@@ -114,10 +114,15 @@ struct HostTimer {
     static bool v = getenv("SGF_TRACE") && atoi(getenv("SGF_TRACE")) == 4;
     return v;
   }
+  static std::chrono::steady_clock::time_point& epoch() {  // reset by the factorization driver
+    static std::chrono::steady_clock::time_point e = std::chrono::steady_clock::now();
+    return e;
+  }
   ~HostTimer() {
     if (on())
-      fprintf(stderr, "[host] %-24s %8.2f ms\n", name,
-              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      fprintf(stderr, "[host] %-24s %8.2f ms  (from %.2f)\n", name,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+              std::chrono::duration<double, std::milli>(t0 - epoch()).count());
   }
 };
 
@@ -125,6 +130,13 @@ struct HostTimer {
 void* chunk_get(size_t bytes, size_t* cap);
 void chunk_put(void* p, size_t cap);
 void chunk_trim();
+// Chunks of the apply plans' arenas.  The plan worker fills them through the
+// context's upload stream while the main stream is still factorizing, so they
+// cannot share the stream-ordered cache above: a released chunk carries an
+// event recorded on the releasing stream (after its last users), and the
+// stream of whoever takes it next waits for that event.
+void* plan_chunk_get(size_t bytes, size_t* cap, cudaStream_t user);
+void plan_chunk_put(void* p, size_t cap, cudaStream_t last_user);
 
 // Asynchronous small host->device upload through a pinned staging ring (a
 // cudaMemcpyAsync from pageable memory would synchronise the stream first
@@ -142,6 +154,12 @@ class Arena {
   Arena(const Arena&) = delete;
   Arena& operator=(const Arena&) = delete;
   void set_stream(cudaStream_t s) { s_ = s; }
+  // chunks from the plan pool (plan_chunk_get/put): uploads run on s_, the
+  // chunk's other users on `release_stream`
+  void use_plan_pool(cudaStream_t release_stream) {
+    plan_pool_ = true;
+    rel_ = release_stream;
+  }
   void* alloc_bytes(size_t bytes);
   double* alloc(size_t n) { return (double*)alloc_bytes(n * sizeof(double)); }
   template <class T>
@@ -162,12 +180,19 @@ class Arena {
   size_t chunk_;
   std::vector<Chunk> chunks_;
   size_t used_ = 0;
+  bool plan_pool_ = false;
+  cudaStream_t rel_ = nullptr;
 };
 
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t order_ev = nullptr;  // sgf_stream_wait: orders the stream after a foreign one
+  // uploads of the apply-plan worker: its own stream, so that its copies never
+  // queue behind (or wait for a launch slot of) the factorization's backlog on
+  // `stream`; `stream` waits for upload_ev before the plan is used (plan_sync_uploads)
+  cudaStream_t upload_stream = nullptr;
+  cudaEvent_t upload_ev = nullptr;
   std::string last_error;
   // grow-only pinned staging buffer for large host->device uploads; callers
   // synchronise the stream before reusing it
