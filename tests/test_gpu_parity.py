@@ -115,6 +115,45 @@ def test_determinism_bitwise():
     assert r1.residual_history == r2.residual_history and np.array_equal(x1, x2)
 
 
+def test_preconditioner_lifetimes_share_the_plan_pool():
+    """Apply plans are uploaded on a second stream into pooled chunks that a
+    freed preconditioner hands on (event-ordered, runtime.cpp plan_chunk_*):
+    preconditioners created, applied and freed in interleaved order keep
+    bitwise the results of a fresh process-order run, and sgf_trim between
+    them changes nothing."""
+    import torch
+
+    from paper_1907_03406_b200 import _native as N
+
+    from paper_1907_03406_b200.problems import CONFIGS
+
+    ga, gb = Golden("cfg2"), Golden("p3d12_b3")
+    proba = CONFIGS[2]["make"]()
+    na = proba.n
+
+    def run_a():
+        return sgf.factorize(proba, **ga.opts)
+
+    xa = np.random.default_rng(5).standard_normal(na)
+    xb = np.random.default_rng(6).standard_normal(gb.n)
+    Pa = run_a()
+    ya = Pa.apply_inverse(xa)
+    Pb = run(gb, replay=False)          # Pa alive: fresh plan chunks
+    yb = Pb.apply_inverse(xb)
+    ta = torch.tensor(xa, device="cuda")
+    ua = Pa.apply_inverse(ta)           # asynchronous apply still queued ...
+    del Pa                              # ... when its plan chunks go back to the pool
+    Pc = run_a()                        # takes them (waits for the release event)
+    assert np.array_equal(ua.cpu().numpy(), ya)
+    assert np.array_equal(Pc.apply_inverse(xa), ya)
+    assert np.array_equal(Pb.apply_inverse(xb), yb)
+    del Pc
+    N.trim_memory()                     # cached chunks back to the driver; live factors untouched
+    assert np.array_equal(Pb.apply_inverse(xb), yb)
+    Pd = run_a()
+    assert np.array_equal(Pd.apply_inverse(xa), ya)
+
+
 def test_lowrank_replay():
     g = Golden("p3d9_gen")
     P = run(g)
