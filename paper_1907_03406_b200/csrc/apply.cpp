@@ -54,6 +54,8 @@ struct Group {
   int lpr1 = 32, lpr2 = 32;                   // mode-N lanes per row (inverse, couplings)
   // level-1 eliminations in apply_inverse: G = A_BB^{-1} with the sparse couplings
   bool sym = false;
+  bool band = false;          // ... through the banded Cholesky factor (launch_l1_band)
+  double bytes_band = 0;
   SymvTask* sym_f = nullptr;  // zb = G xb
   SymvTask* sym_b = nullptr;  // zb = xb - G acc
   int nsym = 0, sym_maxm = 0;
@@ -286,12 +288,21 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
     if (sym) {
       std::vector<SymvTask> tf, tb;
       long long o = 0;
+      static const bool band_ok = !(getenv("SGF_L1_BAND") && atoi(getenv("SGF_L1_BAND")) == 0);
+      g.band = band_ok;
       for (size_t i = rg.first; i < rg.second; ++i) {
         const Factor& f = *fs[i];
+        g.band = g.band && f.bw >= 1 && f.bw <= 64 && f.m <= L1B_MAXM && f.L && f.inv;
+        for (int p = 0; p * 64 < f.m; ++p) {  // entries of X_pp's triangle and of S_p's band, read twice
+          const double rows = std::min(64, f.m - 64 * p);
+          g.bytes_band += 2.0 * 8.0 * (rows * (rows + 1.0) / 2.0 + (p ? rows * 64.0 - rows * (rows - 1.0) / 2.0 : 0.0));
+        }
         // unfused form: x/base/result in the group's gathered buffers; fused
         // form (launch_symv_fused): through idx on the full vector
         tf.push_back(SymvTask{f.G, f.ld, g.xb + o, nullptr, g.zb + o, f.m, 1.0, g.idx + o, 1});
         tb.push_back(SymvTask{f.G, f.ld, g.acc + o, g.xb + o, g.zb + o, f.m, -1.0, g.idx + o, 0});
+        tf.back().L = tb.back().L = f.L;
+        tf.back().X = tb.back().X = f.inv;
         g.sym_maxm = std::max(g.sym_maxm, f.m);
         g.bytes_sym += 4.0 * f.m * (f.m + 1.0);
         o += f.m;
@@ -461,7 +472,10 @@ static void symv(const SymvTask* t, int nt, int maxm, double bytes, cudaStream_t
 // with the fused symv, the gather of x_B and the scatter of the result go
 // through the nodes' index arrays inside the kernel (two launches fewer per sweep)
 static void forward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
-  if (symv_fused_ok(g.sym_maxm)) {
+  if (g.band) {
+    ProfScope ps(st, PROF_GEMV, g.bytes_band);
+    SGF_CUDA(launch_l1_band(g.sym_f, g.nsym, y, st));
+  } else if (symv_fused_ok(g.sym_maxm)) {
     ProfScope ps(st, PROF_GEMV, g.bytes_sym);
     SGF_CUDA(launch_symv_fused(g.sym_f, g.nsym, g.sym_maxm, y, st));
   } else {
@@ -474,7 +488,10 @@ static void forward_group_sym(const L1Couplings& c, const Group& g, double* y, c
 
 static void backward_group_sym(const L1Couplings& c, const Group& g, double* y, cudaStream_t st) {
   SGF_CUDA(launch_sub_spmv(c.nb, nullptr, c.b_rp, c.b_ci, c.b_v, y, g.acc, 1, st));
-  if (symv_fused_ok(g.sym_maxm)) {
+  if (g.band) {
+    ProfScope ps(st, PROF_GEMV, g.bytes_band);
+    SGF_CUDA(launch_l1_band(g.sym_b, g.nsym, y, st));
+  } else if (symv_fused_ok(g.sym_maxm)) {
     ProfScope ps(st, PROF_GEMV, g.bytes_sym);
     SGF_CUDA(launch_symv_fused(g.sym_b, g.nsym, g.sym_maxm, y, st));
   } else {

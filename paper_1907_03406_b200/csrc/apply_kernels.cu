@@ -891,6 +891,152 @@ cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStre
   return cudaErrorInvalidValue;
 }
 
+// ---------------------------------------------------------------------------
+// Level-1 groups through the banded Cholesky factor.  A lexicographic 8^3
+// interior has bandwidth 64, so in 64 x 64 blocks L is block bidiagonal:
+// diagonal blocks L_pp and sub-diagonal blocks S_p = L_{p,p-1}, which hold
+// nonzeros only at column >= row (bandwidth <= 64).  The diagonal blocks of
+// X = L^{-1} are the inverses of the L_pp, so
+//   forward   w_p = X_pp (x_p - S_p w_{p-1}),            p = 0 .. nb-1
+//   backward  v_p = X_pp^T (w_p - S_{p+1}^T v_{p+1}),    p = nb-1 .. 0
+// gives v = L^{-T} L^{-1} x = G x from 2 x 15 block products per 512-unknown
+// node: ~0.6 MB streamed (16-column granularity on the triangles) instead of
+// the 1.05 MB of G's lower triangle.  One CTA per node; the vector lives in
+// shared memory.  Row products: thread (row, quarter) reads 16 entries of its
+// row with 16-byte loads, 4-lane shuffle reduction.  Transposed products:
+// thread (column, row quarter) reads 16 rows of its column (a warp reads 256
+// contiguous bytes per row), partials summed in fixed order through shared
+// memory.  A block's entries are requested before the barrier that publishes
+// the previous product (their addresses do not depend on the solve).
+// ---------------------------------------------------------------------------
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) l1_band_kernel(const SymvTask* __restrict__ tasks, double* __restrict__ v) {
+  __shared__ __align__(16) double xs[L1B_MAXM];
+  __shared__ __align__(16) double tv[64];
+  __shared__ double part[4][64];
+  const SymvTask T = tasks[blockIdx.x];
+  const int m = T.m, tid = threadIdx.x;
+  const long long ld = T.ld;
+  const int nb = (m + 63) >> 6;
+  for (int i = tid; i < 64 * nb; i += 256) xs[i] = i < m ? ((v && T.gather_x) ? v[T.idx[i]] : T.x[i]) : 0.0;
+  __syncthreads();
+  const int r = tid >> 2, qd = tid & 3;   // row products: row, column quarter
+  const int cc = tid & 63, rq = tid >> 6;  // transposed products: column, row quarter
+  double a[16];
+  // thread (r, qd) loads the 16-byte words 4k + qd (k = 0..7) of row r of a
+  // row-major block -- the four threads of a row read 64 contiguous bytes per
+  // instruction and their shared-memory operands do not collide -- and only
+  // the words that touch columns [lo, hi] (zeros elsewhere)
+  auto load_row = [&](const double* B, int lo, int hi) {
+    const double2* src = reinterpret_cast<const double2*>(B + (long long)r * ld) + qd;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c0 = 8 * k + 2 * qd;
+      double2 t = make_double2(0.0, 0.0);
+      if (c0 + 1 >= lo && c0 <= hi) t = __ldcs(src + 4 * k);
+      a[2 * k] = t.x;
+      a[2 * k + 1] = t.y;
+    }
+  };
+  // sum over the thread's words of a[] * vec[columns <= cmax]
+  auto dot_row = [&](const double* vec, int cmax) {
+    const double2* w2 = reinterpret_cast<const double2*>(vec) + qd;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c0 = 8 * k + 2 * qd;
+      const double2 w = w2[4 * k];
+      if (c0 <= cmax) acc = fma(a[2 * k], w.x, acc);
+      if (c0 + 1 <= cmax) acc = fma(a[2 * k + 1], w.y, acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    return acc;
+  };
+  // thread (cc, rq) loads B[16rq .. 16rq+15][cc], rows in [lo, hi] only
+  auto load_col = [&](const double* B, int lo, int hi) {
+    const double* src = B + (long long)(16 * rq) * ld + cc;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int row = 16 * rq + j;
+      a[j] = (row >= lo && row <= hi) ? __ldcs(src) : 0.0;
+      src += ld;
+    }
+  };
+  // ---- forward: L w = x ----
+  for (int p = 0; p < nb; ++p) {
+    const int rows = min(64, m - 64 * p);
+    if (p > 0) {
+      // t = x_p - S_p w_{p-1}: row r of S_p holds nonzeros at columns >= r
+      load_row(T.L + (long long)(64 * p) * ld + 64 * (p - 1), r < rows ? r : 64, 63);
+      const double acc = dot_row(xs + 64 * (p - 1), 63);
+      if (qd == 0 && r < rows) tv[r] = xs[64 * p + r] - acc;
+    } else if (tid < rows) {
+      tv[tid] = xs[tid];
+    }
+    // w_p = X_pp t: lower triangle, row r uses columns <= r
+    load_row(T.X + (long long)(64 * p) * ld + 64 * p, 0, r < rows ? r : -1);
+    __syncthreads();
+    {
+      const double acc = dot_row(tv, r);
+      if (qd == 0 && r < rows) xs[64 * p + r] = acc;
+    }
+    __syncthreads();
+  }
+  // ---- backward: L^T v = w ----
+  for (int p = nb - 1; p >= 0; --p) {
+    const int rows = min(64, m - 64 * p);
+    if (p < nb - 1) {
+      // u = w_p - S_{p+1}^T v_{p+1}: column cc of S_{p+1} holds nonzeros at rows <= cc
+      const int rows1 = min(64, m - 64 * (p + 1));
+      load_col(T.L + (long long)(64 * (p + 1)) * ld + 64 * p, 0, min(cc, rows1 - 1));
+      const double* vv = xs + 64 * (p + 1) + 16 * rq;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc = fma(a[j], vv[j], acc);
+      part[rq][cc] = acc;
+      __syncthreads();
+      if (tid < rows) tv[tid] = xs[64 * p + tid] - (((part[0][tid] + part[1][tid]) + part[2][tid]) + part[3][tid]);
+    } else if (tid < rows) {
+      tv[tid] = xs[64 * p + tid];
+    }
+    // v_p = X_pp^T u: column cc uses rows >= cc (< rows)
+    load_col(T.X + (long long)(64 * p) * ld + 64 * p, cc < rows ? cc : 64, rows - 1);
+    __syncthreads();
+    {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int row = 16 * rq + j;
+        if (row >= cc && row < rows) acc = fma(a[j], tv[row], acc);
+      }
+      part[rq][cc] = acc;
+    }
+    __syncthreads();
+    if (tid < rows) xs[64 * p + tid] = ((part[0][tid] + part[1][tid]) + part[2][tid]) + part[3][tid];
+    __syncthreads();
+  }
+  for (int j = tid; j < m; j += 256) {
+    const double rr = xs[j];
+    if (v) {  // fused: base from and result to the full vector (this node's unknowns only)
+      const int u = T.idx[j];
+      v[u] = T.base ? fma(T.sign, rr, v[u]) : T.sign * rr;
+    } else {
+      T.y[j] = T.base ? fma(T.sign, rr, T.base[j]) : T.sign * rr;
+    }
+  }
+}
+
+cudaError_t launch_l1_band(const SymvTask* d_tasks, int ntasks, double* v, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  count_launch();
+  static const int occ = getenv("SGF_L1_BAND_OCC") ? atoi(getenv("SGF_L1_BAND_OCC")) : 4;
+  if (occ == 6) l1_band_kernel<6><<<ntasks, 256, 0, s>>>(d_tasks, v);
+  else if (occ == 5) l1_band_kernel<5><<<ntasks, 256, 0, s>>>(d_tasks, v);
+  else l1_band_kernel<4><<<ntasks, 256, 0, s>>>(d_tasks, v);
+  return cudaGetLastError();
+}
+
 // short sparse rows (level-1 couplings: 1-3 entries per row), thread per row
 __global__ void sub_spmv_kernel(int nrows, const int* __restrict__ rid, const int* __restrict__ rp,
                                 const int* __restrict__ ci, const double* __restrict__ v, double* __restrict__ x,

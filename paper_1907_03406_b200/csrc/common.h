@@ -223,6 +223,10 @@ struct SymvTask {
   double sign;
   const int* idx = nullptr;  // the node's unknowns in the full vector (fused gather/scatter, see launch_symv)
   int gather_x = 0;          // fused: x = v[idx] (else x as given)
+  // banded form (launch_l1_band): G x = L^{-T} (L^{-1} x) by block substitution with the
+  // Cholesky factor L (bandwidth <= 64) and the inverted diagonal blocks of L^{-1}
+  const double* L = nullptr;
+  const double* X = nullptr;
 };
 
 struct QrFinishTask {
@@ -326,6 +330,9 @@ cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStre
 // task has a base, result written to v[idx]; false when the selected kernel has no fused form
 bool symv_fused_ok(int max_m);
 cudaError_t launch_symv_fused(const SymvTask* d_tasks, int ntasks, int max_m, double* v, cudaStream_t s);
+// the same operation through the banded Cholesky factor (tasks carry L and X; m <= L1B_MAXM)
+constexpr int L1B_MAXM = 1024;
+cudaError_t launch_l1_band(const SymvTask* d_tasks, int ntasks, double* v, cudaStream_t s);
 // sparse rows: mode 0: x[rid[r]] -= sum_e v[e] x[ci[e]];  mode 1: out[r] = sum_e v[e] x[ci[e]]
 cudaError_t launch_sub_spmv(int nrows, const int* rid, const int* rp, const int* ci, const double* v, double* x,
                             double* out, int mode, cudaStream_t s);

@@ -975,6 +975,7 @@ void eliminate_level(State& S, const std::vector<int>& elim, int level) {
       f.xmask = xmk[q];
       f.xmw = xmw[q];
       if (Gall) f.G = Gall + (e.X - Xall);
+      if (level == 1 && !S.l1_bw.empty()) f.bw = std::max(1, S.l1_bw[e.x]);
     }
     // replay the reference sequence for the table and its byte accounting:
     // interior q creates the fills it touches first, then is dropped

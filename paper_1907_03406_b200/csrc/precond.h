@@ -32,6 +32,7 @@ struct Factor {
   double* Tw = nullptr;       // steps x steps compact-WY factor (row-major, upper)
   double* LQ = nullptr;       // compression: L Q (m x m, ld), formed on first apply_operator
   double* G = nullptr;        // level-1 elimination: A_BB^{-1} = L^{-T} L^{-1} (lower triangle, ld)
+  int bw = -1;                // level-1 elimination: lower bandwidth of A_BB (and of L) in the node's order
   std::vector<int32_t> perm;  // compression: QR column permutation (first `steps` meaningful)
   int* perm_dev = nullptr;    // device copy until the end-of-factorization readback
   int ncols = 0;              // compression: columns of the rank basis N
