@@ -4,8 +4,8 @@ environment switch forces) meets the same parity gates as the default path.
 Each variant runs in a subprocess (the switches are read once per process):
 BASELINE config 2 (3-D Poisson 64^3, b = 9) exercises the level-1 sparse
 eliminations, the INT8-emulated level-2 Schur updates and level-3 products,
-the recursive Cholesky, the shared-memory QR and the bulk-copy apply
-kernels, so each switch below replaces a kernel that the default run uses.
+the recursive Cholesky, the shared-memory QR, the banded level-1 sweeps and
+the bulk-copy apply kernels, so each switch below replaces a kernel that the default run uses.
 Gates as in test_gpu_parity.py: stats and rank trace bit-exact, apply
 within 1e-10 of the reference under pivot replay, PCG iterations equal."""
 import json
@@ -21,7 +21,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 VARIANTS = {
     "default": {},
-    "symv_registers": {"SGF_SYMV": "0"},               # register-staged level-1 symmetric GEMV
+    "l1_dense_g": {"SGF_L1_BAND": "0"},                # level-1 sweeps through the dense G = A_BB^-1 (bulk-copy symv)
+    "symv_registers": {"SGF_SYMV": "0", "SGF_L1_BAND": "0"},  # ... with the register-staged symmetric GEMV
     "gemv_no_bulk": {"SGF_GEMV_BULK": "0"},            # 32-lane GEMV for the long rows too
     "gemv_sparse_ring": {"SGF_GEMV_SPARSE_RING": "1"},  # block-sparse rows through the bulk-copy ring (not tile lists)
     "qr_l2_panel": {"SGF_QR_SMEM": "0"},               # cluster QR with the panel in L2
