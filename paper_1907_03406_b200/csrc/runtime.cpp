@@ -130,7 +130,7 @@ struct PlanChunk {
   cudaEvent_t released;  // recorded after the chunk's last users
 };
 std::map<int, std::multimap<size_t, PlanChunk>> g_plan_cache;  // guarded by g_cache_mu
-std::vector<cudaEvent_t> g_plan_events;                           // spare events (guarded by g_cache_mu)
+std::map<int, std::vector<cudaEvent_t>> g_plan_events;            // spare events per device (guarded by g_cache_mu)
 
 // The ring is split into NSEG segments used in order; leaving a segment
 // records an event, and re-entering it waits only for that event (work
@@ -286,7 +286,7 @@ void* plan_chunk_get(size_t bytes, size_t* cap, cudaStream_t user) {
       }
       {
         std::lock_guard<std::mutex> lk2(g_cache_mu);
-        g_plan_events.push_back(c.released);
+        g_plan_events[dev].push_back(c.released);
       }
       return c.p;
     }
@@ -308,9 +308,10 @@ void plan_chunk_put(void* p, size_t cap, cudaStream_t last_user) {
   PlanChunk c{p, nullptr};
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    if (!g_plan_events.empty()) {
-      c.released = g_plan_events.back();
-      g_plan_events.pop_back();
+    auto& spare = g_plan_events[dev];
+    if (!spare.empty()) {
+      c.released = spare.back();
+      spare.pop_back();
     }
   }
   if ((!c.released && cudaEventCreateWithFlags(&c.released, cudaEventDisableTiming) != cudaSuccess) ||
