@@ -193,14 +193,18 @@ def run_reference_subprocess(cfg, threads, timeout_s, n=None):
 # ---------------------------------------------------------------------------
 def run_reference(args, ws, rank):
     """--impl reference: the reference package itself (oracle/_ref) on the full
-    cfg4 problem, one factorize + pcg with one BLAS thread (reference
-    bench.py:157-166 protocol).  One full-size step takes ~15 minutes on one
-    core, so exactly one step is run whatever --steps/--warmup say, and the
-    line reports the steps actually run."""
+    cfg4 problem, one factorize + pcg (reference bench.py:157-166 protocol)
+    with every host core as BLAS threads (--ref-threads 1: the single-thread
+    figure of BASELINE.md section 2).  One full-size step takes 7-10 minutes
+    (measured on the GPU box's 16-core host: 438.7 s with 16 threads, 556.7 s
+    with one; profiles/r02_bench_reference_arm.jsonl), so exactly one step is
+    run whatever --steps/--warmup say, and the line reports the steps
+    actually run."""
     if rank != 0:
         return
     t0 = time.perf_counter()
-    res, err, wall = run_reference_subprocess(CFG, 1, REF_ARM_TIMEOUT_S)
+    threads = args.ref_threads if args.ref_threads > 0 else (os.cpu_count() or 1)
+    res, err, wall = run_reference_subprocess(CFG, threads, REF_ARM_TIMEOUT_S)
     base = {"impl": "reference", "metric": METRIC, "unit": "s", "n_gpus": ws, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
     if res is None:
@@ -212,12 +216,12 @@ def run_reference(args, ws, rank):
         "requested_warmup": args.warmup, "ms_per_step": v * 1e3,
         "config": {"workload": f"cfg{CFG}-aniso-128" if CFG == 4 else f"cfg{CFG}", "grid": res["grid"],
                    "n": res["n"], "b": res["b"], "rank_tol": res["rank_tol"], "scheme": "nest-2-2", "degree": 1,
-                   "pcg_rtol": 1e-12, "parallelism": "cpu, 1 BLAS thread"},
+                   "pcg_rtol": 1e-12, "parallelism": f"cpu, {threads} BLAS thread(s)"},
         "t_factor_s": res["t_factor_s"], "t_solve_s": res["t_solve_s"], "pcg_iterations": res["iterations"],
         "flops_factorize": res["flops_factorize"], "fp64_tflops_factorize": res["flops_factorize"] / res["t_factor_s"] / 1e12,
-        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference",
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "reference",
                          "sample": f"the whole cfg{CFG} workload (n={res['n']}), one factorize + pcg of the reference "
-                                   f"package (oracle/_ref, polyprec {res['polyprec']}), OPENBLAS_NUM_THREADS=1, "
+                                   f"package (oracle/_ref, polyprec {res['polyprec']}), OPENBLAS_NUM_THREADS={threads}, "
                                    f"host {res['cpu_count']} cpus; problem generation {res['t_generate_s']:.1f} s "
                                    f"not timed"},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -573,6 +577,8 @@ def main():
                          "host cores (~15 min; profiles/r02_bench_cpu_full.jsonl); or none.  The full-size "
                          "single-thread reference is the --impl reference arm")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-config and IEEE-FP64 lines")
+    ap.add_argument("--ref-threads", type=int, default=0,
+                    help="--impl reference: BLAS threads of the reference run (0: every host core; 1: single thread)")
     # code-path checks only (numbers from these are not bench values): another
     # config, gloo collectives, every rank on GPU 0
     ap.add_argument("--cfg", type=int, default=4)

@@ -7,6 +7,7 @@
 // matrices, scatters back.  Elimination forward sweeps update shared
 // separator unknowns x_N -= E_N z_B; the plan's combine list applies those
 // in ascending factor order, exactly the reference's sequence.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -332,6 +333,13 @@ void plan_extend_ptrs(Precond* P, size_t begin, const std::vector<const Factor*>
       for (auto& t : tb)
         if (t.rmask) t.tri = 1;
       g.bytes_b2 = gemv_bytes(tb, 1);
+    }
+    {  // masked triangular rows grow with the row index: longest tasks first, so the launch does not end on a
+       // few CTAs holding the longest rows (tasks write disjoint rows: their order is free)
+      bool masked_tri = !f1.empty();
+      for (const auto& t : f1) masked_tri = masked_tri && t.rmask && t.tri == 1;
+      if (masked_tri)
+        std::stable_sort(f1.begin(), f1.end(), [](const GemvTask& a, const GemvTask& b) { return a.r1 > b.r1; });
     }
     g.fwd1 = plan->mem.upload(f1);
     g.nf1 = (int)f1.size();
@@ -746,7 +754,7 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
   // allocates nothing, so it never waits in cudaMalloc / cudaFreeHost
   const long long np = (n + 31) & ~31LL;  // 256-byte aligned vectors
   if (!A->ws) {
-    A->ws = A->mem.alloc(4 * np + 512 + 8);
+    A->ws = A->mem.alloc(4 * np + PCG_PART + 8);
     SGF_CUDA(cudaMallocHost((void**)&A->hsc, 8 * sizeof(double)));
   }
   double* r = A->ws;
@@ -754,7 +762,8 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
   double* p = z + np;
   double* q = p + np;
   double* part = q + np;
-  double* sc = part + 512;  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  double* sc = part + PCG_PART;  // 0 / 2: r'z of this and of the next direction (alternating), 1 pAp, 3 rr, 4 bb
+  SGF_CUDA(cudaMemsetAsync(part + PCG_CNT_OFF, 0, 2 * sizeof(double), st));  // the reductions' arrival counter
   double* hsc = A->hsc;
   // SGF_TRACE=5: host time spent waiting in each readback vs. issuing work
   static const bool trace5 = getenv("SGF_TRACE") && atoi(getenv("SGF_TRACE")) == 5;
@@ -779,6 +788,16 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
       if (b) SGF_CUDA(launch_residual(b, out, n, st));
     } else {
       spmv(A, in, out, b);
+    }
+  };
+  // q = A p and sc[1] = p'q: one launch for the device CSR (the SpMV kernel adds p[row] q[row] as it goes)
+  auto matvec_dot = [&](const double* in, double* out) {
+    if (Aop) {
+      Aop(in, out);
+      SGF_CUDA(launch_dot(in, out, n, part, sc, 1, st));
+    } else {
+      ProfScope ps(A->ctx->stream, PROF_SPMV, 12.0 * A->nnz + (A->rp32 ? 4.0 : 8.0) * (A->n + 1) + 16.0 * A->n);
+      SGF_CUDA(launch_spmv_dot((int)A->n, A->rp, A->rp32, A->ci, A->v, in, out, part, sc, 1, A->ctx->stream));
     }
   };
   auto precond = [&](const double* in, double* out) {
@@ -813,11 +832,11 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
   SGF_CUDA(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   bool converged = false;
   int it = 0;
+  int rz = 0;  // slot of the current r'z; the next one goes to the other of {0, 2} (no scalar copy)
   while (it < maxit) {
     ++it;
-    matvec(p, q, nullptr);
-    SGF_CUDA(launch_dot(p, q, n, part, sc, 1, st));
-    SGF_CUDA(launch_xr_update(d_x, r, p, q, n, sc, part, sc, 3, st));
+    matvec_dot(p, q);
+    SGF_CUDA(launch_xr_update(d_x, r, p, q, n, sc, part, sc, 3, st, rz));
     if (true_every > 0 && it % true_every == 0) {
       matvec(d_x, r, d_b);
       SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
@@ -843,15 +862,16 @@ void pcg(Ctx& ctx, Csr* A, const MatFn& Aop, const PrecFn& M, const double* d_b,
       history[hl++] = rel;
     }
     precond(r, z);
-    SGF_CUDA(launch_dot(r, z, n, part, sc, 2, st));
-    readback(2, 1);
-    if (hsc[2] <= 0.0) {
+    const int rz_new = 2 - rz;
+    SGF_CUDA(launch_dot(r, z, n, part, sc, rz_new, st));
+    readback(rz_new, 1);
+    if (hsc[rz_new] <= 0.0) {
       char buf[96];
-      snprintf(buf, sizeof buf, "r'Mr = %.3e at iteration %d", hsc[2], it);
+      snprintf(buf, sizeof buf, "r'Mr = %.3e at iteration %d", hsc[rz_new], it);
       fail(SGF_INDEFINITE, buf);
     }
-    SGF_CUDA(launch_p_update(p, z, n, sc, st));
-    SGF_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    SGF_CUDA(launch_p_update(p, z, n, sc, st, rz_new, rz));
+    rz = rz_new;
   }
   matvec(d_x, r, d_b);
   SGF_CUDA(launch_dot(r, r, n, part, sc, 3, st));
@@ -878,12 +898,13 @@ void pcg_dist(Ctx& ctx, int64_t n, const MatFn& Aop, const PrecFn& M, const Redu
   auto t0 = std::chrono::steady_clock::now();
   Arena ws(st);
   const long long np = (n + 31) & ~31LL;
-  double* r = ws.alloc(4 * np + 512 + 8);
+  double* r = ws.alloc(4 * np + PCG_PART + 8);
   double* z = r + np;
   double* p = z + np;
   double* q = p + np;
   double* part = q + np;
-  double* sc = part + 512;  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  double* sc = part + PCG_PART;  // 0 rz, 1 pAp, 2 rz_new, 3 rr, 4 bb
+  SGF_CUDA(cudaMemsetAsync(part + PCG_CNT_OFF, 0, 2 * sizeof(double), st));  // the reductions' arrival counter
   double* hsc = nullptr;
   SGF_CUDA(cudaMallocHost((void**)&hsc, 8 * sizeof(double)));
   struct Pin {

@@ -1137,6 +1137,10 @@ cudaError_t launch_combine(double* x, const int* tgt, const long long* ptr, cons
 // a fixed-order final reduction: bitwise reproducible.
 // ---------------------------------------------------------------------------
 constexpr int RED_BLOCKS = 296;
+// Partial buffer of the PCG reductions (PCG_PART doubles, runtime.h): block
+// partials, and at PCG_CNT_OFF the arrival counter of the in-kernel final
+// reduction (zero between launches: the finishing block resets it).
+constexpr int RED_MAX = PCG_CNT_OFF;  // most partials a reducing launch may write
 
 // CSR SpMV y = A x (b == nullptr) or y = b - A x.  One warp per 32
 // consecutive rows: the warp streams the rows' contiguous nonzero range in
@@ -1146,11 +1150,17 @@ constexpr int RED_BLOCKS = 296;
 // CSR product (scipy), so the result does not depend on the launch shape.
 constexpr int SPMV_CH = 256;
 constexpr int SPMV_WARPS = 8;
-template <class RP>
+__device__ void block_partial_finish(double v, double* part, double* out, int slot);
+// DOT: also x.y (p'Ap of PCG) -- every lane adds x[row] * y[row] of its rows,
+// block partials and the final sum in fixed order (block_partial_finish).
+template <class RP, bool DOT = false>
 __global__ void __launch_bounds__(256, 4) spmv_kernel(int n, const RP* __restrict__ rp, const int* __restrict__ ci,
                                                    const double* __restrict__ v, const double* __restrict__ x,
-                                                   double* __restrict__ y, const double* __restrict__ b) {
+                                                   double* __restrict__ y, const double* __restrict__ b,
+                                                   double* __restrict__ part = nullptr, double* __restrict__ out = nullptr,
+                                                   int slot = 0) {
   __shared__ double prod[SPMV_WARPS][SPMV_CH];
+  double dacc = 0.0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* pw = prod[w];
   const long long nwarps = (long long)gridDim.x * SPMV_WARPS;
@@ -1187,8 +1197,12 @@ __global__ void __launch_bounds__(256, 4) spmv_kernel(int n, const RP* __restric
       for (long long e = a; e < z; ++e) s += pw[e - cs];
       __syncwarp();
     }
-    if (row < n) y[row] = b ? b[row] - s : s;
+    if (row < n) {
+      y[row] = b ? b[row] - s : s;
+      if (DOT) dacc = fma(x[row], s, dacc);
+    }
   }
+  if (DOT) block_partial_finish(dacc, part, out, slot);
 }
 
 __global__ void rowptr32_kernel(const long long* __restrict__ rp, int* __restrict__ out, long long n1) {
@@ -1215,50 +1229,73 @@ cudaError_t launch_spmv(int n, const long long* rp, const int* rp32, const int* 
   return cudaGetLastError();
 }
 
+// y = A x and out[slot] = x'y in one launch (the p'Ap of a PCG iteration)
+cudaError_t launch_spmv_dot(int n, const long long* rp, const int* rp32, const int* ci, const double* v,
+                            const double* x, double* y, double* part, double* out, int slot, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long warps = ((long long)n + 31) / 32;
+  long long blocks = (warps + SPMV_WARPS - 1) / SPMV_WARPS;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks > RED_MAX) blocks = RED_MAX;
+  count_launch();
+  if (rp32) spmv_kernel<int, true><<<(unsigned)blocks, 256, 0, s>>>(n, rp32, ci, v, x, y, nullptr, part, out, slot);
+  else spmv_kernel<long long, true><<<(unsigned)blocks, 256, 0, s>>>(n, rp, ci, v, x, y, nullptr, part, out, slot);
+  return cudaGetLastError();
+}
+
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-__device__ void block_partial(double v, double* out) {
+// Block partial to part[blockIdx.x]; the block that arrives last (counter at
+// part + PCG_CNT_OFF) adds all partials in index order into out[slot] and
+// resets the counter -- the sum does not depend on which block that is.  One
+// launch per reduction instead of a partial and a finishing launch.
+__device__ void block_partial_finish(double v, double* part, double* out, int slot) {
   __shared__ double red[8];
+  __shared__ double all[RED_MAX];
+  __shared__ bool last;
+  unsigned* counter = reinterpret_cast<unsigned*>(part + PCG_CNT_OFF);
   v = wsum(v);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < 8; ++w) s += red[w];
-    out[blockIdx.x] = s;
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
-}
-
-// partial dot products; op 0: a.b ; op 1: a.a
-__global__ void __launch_bounds__(256) dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
-                                                  double* __restrict__ part) {
-  double s = 0.0;
-  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) s = fma(a[i], b[i], s);
-  block_partial(s, part);
-}
-
-// final reduction of RED_BLOCKS partials into out[slot]
-__global__ void finish_kernel(const double* __restrict__ part, double* __restrict__ out, int slot) {
-  __shared__ double red[RED_BLOCKS];
-  for (int i = threadIdx.x; i < RED_BLOCKS; i += blockDim.x) red[i] = part[i];
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) all[i] = __ldcg(part + i);
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < RED_BLOCKS; ++i) s += red[i];
+    for (int i = 0; i < (int)gridDim.x; ++i) s += all[i];
     out[slot] = s;
+    *counter = 0u;
   }
 }
 
-// x += alpha p ; r -= alpha q ; partial ||r||^2  with alpha = sc[0]/sc[1]
+// a.b into out[slot]
+__global__ void __launch_bounds__(256) dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                                                  double* __restrict__ part, double* __restrict__ out, int slot) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) s = fma(a[i], b[i], s);
+  block_partial_finish(s, part, out, slot);
+}
+
+// x += alpha p ; r -= alpha q ; ||r||^2 into out[slot]  with alpha = sc[rz]/sc[1]
 __global__ void __launch_bounds__(256) xr_update_kernel(double* __restrict__ x, double* __restrict__ r,
                                                         const double* __restrict__ p, const double* __restrict__ q,
                                                         long long n, const double* __restrict__ sc,
-                                                        double* __restrict__ part) {
-  const double alpha = sc[0] / sc[1];
+                                                        double* __restrict__ part, double* __restrict__ out, int slot,
+                                                        int rz) {
+  const double alpha = sc[rz] / sc[1];
   double s = 0.0;
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
     x[i] += alpha * p[i];
@@ -1266,13 +1303,13 @@ __global__ void __launch_bounds__(256) xr_update_kernel(double* __restrict__ x, 
     r[i] = ri;
     s = fma(ri, ri, s);
   }
-  block_partial(s, part);
+  block_partial_finish(s, part, out, slot);
 }
 
-// p = z + beta p with beta = sc[2]/sc[0]
+// p = z + beta p with beta = sc[num]/sc[den] (the new and the previous r'z)
 __global__ void __launch_bounds__(256) p_update_kernel(double* __restrict__ p, const double* __restrict__ z, long long n,
-                                                       const double* __restrict__ sc) {
-  const double beta = sc[2] / sc[0];
+                                                       const double* __restrict__ sc, int num, int den) {
+  const double beta = sc[num] / sc[den];
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) p[i] = z[i] + beta * p[i];
 }
 
@@ -1289,18 +1326,17 @@ cudaError_t launch_residual(const double* b, double* out, long long n, cudaStrea
 
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s) {
-  count_launch(); dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part);
-  count_launch(); finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+  count_launch(); dot_kernel<<<RED_BLOCKS, 256, 0, s>>>(a, b, n, part, out, slot);
   return cudaGetLastError();
 }
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
-                             double* part, double* out, int slot, cudaStream_t s) {
-  count_launch(); xr_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(x, r, p, q, n, sc, part);
-  count_launch(); finish_kernel<<<1, 256, 0, s>>>(part, out, slot);
+                             double* part, double* out, int slot, cudaStream_t s, int rz) {
+  count_launch(); xr_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(x, r, p, q, n, sc, part, out, slot, rz);
   return cudaGetLastError();
 }
-cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s) {
-  count_launch(); p_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(p, z, n, sc);
+cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s, int num,
+                            int den) {
+  count_launch(); p_update_kernel<<<RED_BLOCKS, 256, 0, s>>>(p, z, n, sc, num, den);
   return cudaGetLastError();
 }
 

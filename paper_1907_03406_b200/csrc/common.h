@@ -209,6 +209,9 @@ struct GemvTask {
   int mwords = 0;                   // (mwords words per row; all-zero tiles are skipped)
 };
 
+// partial buffer of the PCG reductions (doubles) and the offset of its arrival counter (runtime.h launch_dot)
+constexpr int PCG_PART = 1024, PCG_CNT_OFF = 1000;
+
 struct TriTask { double* p; int m; int ld; };
 
 // y = base + sign * G x for a symmetric m x m G whose lower triangle is

@@ -58,11 +58,19 @@ cudaError_t l1_couplings_fill(long long n, const long long* ip, const int* ix, c
                               const int* local, const char* el, const int* bstart, const int* brp, int* bci,
                               double* bv, const int* fscan, const int* fidx, int* frid, int* frp, int* fci,
                               double* fv, int nf, cudaStream_t s);
+// PCG reductions: `part` holds PCG_PART doubles -- block partials and, at
+// PCG_CNT_OFF, the arrival counter of the in-kernel final reduction, which
+// must be zero before the first launch (it is reset by every launch)
 cudaError_t launch_dot(const double* a, const double* b, long long n, double* part, double* out, int slot,
                        cudaStream_t s);
+// x += alpha p, r -= alpha q, out[slot] = r'r with alpha = sc[rz] / sc[1]
 cudaError_t launch_xr_update(double* x, double* r, const double* p, const double* q, long long n, const double* sc,
-                             double* part, double* out, int slot, cudaStream_t s);
-cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s);
+                             double* part, double* out, int slot, cudaStream_t s, int rz = 0);
+// p = z + (sc[num] / sc[den]) p
+cudaError_t launch_p_update(double* p, const double* z, long long n, const double* sc, cudaStream_t s, int num = 2,
+                            int den = 0);
+cudaError_t launch_spmv_dot(int n, const long long* rp, const int* rp32, const int* ci, const double* v,
+                            const double* x, double* y, double* part, double* out, int slot, cudaStream_t s);
 cudaError_t launch_residual(const double* b, double* out, long long n, cudaStream_t s);
 // factor_ops.cu: small dense kernels of the per-factor methods and per-primitive entry points
 cudaError_t launch_dmv(const double* M, long long ld, int rows, int inner, int trans, const double* v, double* y,
