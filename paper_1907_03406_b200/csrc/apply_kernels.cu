@@ -909,8 +909,7 @@ cudaError_t launch_symv(const SymvTask* d_tasks, int ntasks, int max_m, cudaStre
 // memory.  A block's entries are requested before the barrier that publishes
 // the previous product (their addresses do not depend on the solve).
 // ---------------------------------------------------------------------------
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) l1_band_kernel(const SymvTask* __restrict__ tasks, double* __restrict__ v) {
+__global__ void __launch_bounds__(256, 4) l1_band_kernel(const SymvTask* __restrict__ tasks, double* __restrict__ v) {
   __shared__ __align__(16) double xs[L1B_MAXM];
   __shared__ __align__(16) double tv[64];
   __shared__ double part[4][64];
@@ -1030,10 +1029,7 @@ __global__ void __launch_bounds__(256, MINB) l1_band_kernel(const SymvTask* __re
 cudaError_t launch_l1_band(const SymvTask* d_tasks, int ntasks, double* v, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   count_launch();
-  static const int occ = getenv("SGF_L1_BAND_OCC") ? atoi(getenv("SGF_L1_BAND_OCC")) : 4;
-  if (occ == 6) l1_band_kernel<6><<<ntasks, 256, 0, s>>>(d_tasks, v);
-  else if (occ == 5) l1_band_kernel<5><<<ntasks, 256, 0, s>>>(d_tasks, v);
-  else l1_band_kernel<4><<<ntasks, 256, 0, s>>>(d_tasks, v);
+  l1_band_kernel<<<ntasks, 256, 0, s>>>(d_tasks, v);  // (5 or 6 CTAs per SM: no faster; 6 spills)
   return cudaGetLastError();
 }
 
