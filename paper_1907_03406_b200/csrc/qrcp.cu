@@ -225,10 +225,12 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrTask* __restri
 // owner after that barrier.  At the end the columns are put in position order
 // through a scratch panel.  Same arithmetic rules as qrcp_kernel above.
 // ---------------------------------------------------------------------------
-constexpr int QC = 16;            // CTAs per cluster (non-portable size, allowed at launch)
-constexpr int QCT = 256;          // threads per CTA
-constexpr int QCW = QCT / 32;
-
+// QC CTAs per cluster (16: non-portable size, allowed at launch), QCT threads
+// per CTA.  A step's column updates are latency-bound loads from L2 (one warp
+// per column, two passes), so the threads per node set the step time: 1024
+// threads per CTA leave each warp 1-2 columns of a 600-1200 column panel per
+// step (256 threads: 5-10 columns per warp, ~100 us per step at m = 1300).
+template <int QCW>
 __device__ double cblock_sum(double v, double* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -240,8 +242,10 @@ __device__ double cblock_sum(double v, double* red) {
   return s;
 }
 
+template <int QC, int QCT>
 __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     qrcp_cluster_kernel(const QrTask* __restrict__ tasks) {
+  constexpr int QCW = QCT / 32;
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double v[];  // m reflector entries, then c column ids
@@ -365,7 +369,7 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     const double* xk = N + (long long)ck * m;
     double ss = 0.0;
     for (int i = k + tid; i < m; i += QCT) ss = fma(xk[i], xk[i], ss);
-    const double xn = sqrt(cblock_sum(ss, red));
+    const double xn = sqrt(cblock_sum<QCW>(ss, red));
     if (xn <= floor_) break;
     if (k == 0) r00 = xn;
     if (xn > T.tol * r00) ++rank;
@@ -781,14 +785,28 @@ static int qr_active_clusters(int cs, size_t sb) {
   return n;
 }
 
+template <int QC, int QCT>
+static cudaError_t qr_cluster_configure(size_t smem) {
+  static FuncAttrs fa;
+  cudaError_t e = QC > 8 ? ensure_nonportable_cluster(qrcp_cluster_kernel<QC, QCT>, fa) : cudaSuccess;
+  if (e == cudaSuccess) e = ensure_smem(qrcp_cluster_kernel<QC, QCT>, smem, fa);
+  return e;
+}
+
+template <int QC, int QCT>
+static cudaError_t qr_launch_cluster(const QrTask* d_tasks, int ntasks, size_t smem, cudaStream_t s) {
+  cudaError_t e = qr_cluster_configure<QC, QCT>(smem);
+  if (e != cudaSuccess) return e;
+  qrcp_cluster_kernel<QC, QCT><<<ntasks * QC, QCT, smem, s>>>(d_tasks);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream_t s, int max_c) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = (size_t)max_m * sizeof(double) + (size_t)max_c * sizeof(int);
-  static FuncAttrs fa_cluster, fa_single;
+  static FuncAttrs fa_single;
   {
-    cudaError_t e = ensure_nonportable_cluster(qrcp_cluster_kernel, fa_cluster);
-    if (e == cudaSuccess) e = ensure_smem(qrcp_cluster_kernel, smem, fa_cluster);
-    if (e == cudaSuccess) e = ensure_smem(qrcp_kernel, smem, fa_single);
+    cudaError_t e = ensure_smem(qrcp_kernel, smem, fa_single);
     if (e != cudaSuccess) return e;
   }
   static int single = getenv("SGF_QR_SINGLE_CTA") ? 1 : 0;
@@ -824,9 +842,21 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
     if (best_cs == 8) return qr_launch_smem<8>(d_tasks, ntasks, best_sb, max_c, s);
   }
   count_launch();
-  if (single) qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
-  else qrcp_cluster_kernel<<<ntasks * QC, QCT, smem, s>>>(d_tasks);
-  return cudaGetLastError();
+  if (single) {
+    qrcp_kernel<<<ntasks, QR_THREADS, smem, s>>>(d_tasks);
+    return cudaGetLastError();
+  }
+  // panel in global memory / L2: 16-CTA clusters of 1024 threads (cfg5's level-3
+  // waves of 4-12 nodes, m ~ 1300 x 650 columns: 88 ms; 12 / 10 / 8 CTAs per
+  // node 97 / 105 / 122 ms although fewer of the 16-CTA clusters are resident;
+  // 16 x 256 threads 159 ms).  SGF_QR_CL=<size * 10000 + threads>: another variant.
+  static const int cl = getenv("SGF_QR_CL") ? atoi(getenv("SGF_QR_CL")) : 161024;
+  switch (cl) {
+    case 160256: return qr_launch_cluster<16, 256>(d_tasks, ntasks, smem, s);
+    case 160512: return qr_launch_cluster<16, 512>(d_tasks, ntasks, smem, s);
+    case 81024: return qr_launch_cluster<8, 1024>(d_tasks, ntasks, smem, s);
+    default: return qr_launch_cluster<16, 1024>(d_tasks, ntasks, smem, s);
+  }
 }
 
 // ---------------------------------------------------------------------------

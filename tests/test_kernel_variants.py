@@ -26,6 +26,8 @@ VARIANTS = {
     "gemv_no_bulk": {"SGF_GEMV_BULK": "0"},            # 32-lane GEMV for the long rows too
     "gemv_sparse_ring": {"SGF_GEMV_SPARSE_RING": "1"},  # block-sparse rows through the bulk-copy ring (not tile lists)
     "qr_l2_panel": {"SGF_QR_SMEM": "0"},               # cluster QR with the panel in L2
+    "qr_l2_panel_8x1024": {"SGF_QR_SMEM": "0", "SGF_QR_CL": "81024"},  # ... on portable 8-CTA clusters
+    "qr_l2_panel_16x256": {"SGF_QR_SMEM": "0", "SGF_QR_CL": "160256"},  # ... with 256-thread CTAs
     "qr_cluster16": {"SGF_QR_SMEM": "16"},             # shared-memory QR forced to 16-CTA clusters
     "l1_dense": {"SGF_NO_L1SPARSE": "1"},              # level-1 E and Schur as dense DMMA GEMMs
     "l1_e_eager": {"SGF_L1E_EAGER": "1"},              # level-1 couplings E formed during the factorization
