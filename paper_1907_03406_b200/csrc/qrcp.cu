@@ -384,15 +384,52 @@ __global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
     for (int j = k + 1 + ((q - k - 1) % QC + QC) % QC + QC * warp; j < c; j += QC * QCW) {
       const int cj = col_of[j];
       double* col = N + (long long)cj * m + k;
+      // both passes keep 8 loads of the column in flight per lane (the column
+      // comes from L2: one load per trip cost a memory latency per 32 rows);
+      // the accumulation order is the plain loop's
       double s = 0.0;
-      for (int i = lane; i < len; i += 32) s = fma(v[i], col[i], s);
+      int i = lane;
+      for (; i + 224 < len; i += 256) {
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = col[i + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = fma(v[i + 32 * u], cv[u], s);
+      }
+      if (i < len) {  // the last, partial batch
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = (i + 32 * u < len) ? col[i + 32 * u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i + 32 * u < len) s = fma(v[i + 32 * u], cv[u], s);
+      }
       s = warp_sum(s);
       const double ts = tau * s;
       double fresh = 0.0;
-      for (int i = lane; i < len; i += 32) {
-        const double nv = fma(-ts, v[i], col[i]);
-        col[i] = nv;
-        if (i > 0) fresh = fma(nv, nv, fresh);
+      i = lane;
+      for (; i + 224 < len; i += 256) {
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = col[i + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double nv = fma(-ts, v[i + 32 * u], cv[u]);
+          col[i + 32 * u] = nv;
+          if (i + 32 * u > 0) fresh = fma(nv, nv, fresh);
+        }
+      }
+      if (i < len) {
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = (i + 32 * u < len) ? col[i + 32 * u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i + 32 * u < len) {
+            const double nv = fma(-ts, v[i + 32 * u], cv[u]);
+            col[i + 32 * u] = nv;
+            if (i + 32 * u > 0) fresh = fma(nv, nv, fresh);
+          }
       }
       fresh = warp_sum(fresh);
       if (lane == 0) {
@@ -853,7 +890,6 @@ cudaError_t launch_qrcp(const QrTask* d_tasks, int ntasks, int max_m, cudaStream
   static const int cl = getenv("SGF_QR_CL") ? atoi(getenv("SGF_QR_CL")) : 161024;
   switch (cl) {
     case 160256: return qr_launch_cluster<16, 256>(d_tasks, ntasks, smem, s);
-    case 160512: return qr_launch_cluster<16, 512>(d_tasks, ntasks, smem, s);
     case 81024: return qr_launch_cluster<8, 1024>(d_tasks, ntasks, smem, s);
     default: return qr_launch_cluster<16, 1024>(d_tasks, ntasks, smem, s);
   }

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for v in 161024 121024 101024 81024 0; do
+for v in 161024 160512; do
   echo "== SGF_QR_CL=$v" >> gpurun_out/qr_exp.log
   SGF_QR_CL=$v SGF_TRACE=1 timeout 300 python tools/timeline.py 5 1 2>&1 | grep -E "resident|c-wave|L3 compress|L4 compress|factorize wall" | tail -16 >> gpurun_out/qr_exp.log
 done
